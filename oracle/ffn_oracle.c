@@ -1,0 +1,219 @@
+/*
+ * ffn_oracle.c -- TEST INFRASTRUCTURE ONLY.  The plain, slow, fp64 CPU oracle
+ * for the LLaMA fused feed-forward path
+ *
+ *     out = SiLU(RMSNorm(x) . W1^T) (.) (RMSNorm(x) . W3^T)
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_2501_08071_b200/) never links, imports or executes it, and this file
+ * shares no code, header, table or helper with the CUDA path.
+ *
+ * What it follows (citations are PAPER.md lines, "P:L"; BASELINE.json = [BJ]):
+ *   - P:68  "Fused feed-forward is a kernel implementation that fuses multiple
+ *            operators for LLAMA, and root-mean-square layer normalization is a
+ *            popular layer normalization operator" -- the kernel being computed.
+ *   - P:560 Table "Evaluated Kernels": fused_ff inputs B, M, N, K (B folded
+ *            into M = tokens here; reading R10).
+ *   - [BJ] north_star: out = SiLU(RMSNorm(x)W1) (.) (RMSNorm(x)W3), the gain g
+ *            of RMSNorm folded into W1/W3, 1/rms applied as a per-row scale.
+ *   The paper never writes the formula out; the readings taken where it is
+ *   silent are DESIGN.md R1..R12 (eps inside the sqrt, RMS of x not of x*g,
+ *   W1 = SiLU branch, ...).
+ *
+ * Definition computed (mode ORACLE_PLAIN), per row m, all in double, sums in
+ * sequential k order:
+ *     ms      = (sum_k x[m,k]^2) / K
+ *     r       = 1 / sqrt(ms + eps)
+ *     xn[k]   = x[m,k] * r * g[k]
+ *     h1[n]   = sum_k xn[k] * W1[n,k]
+ *     h3[n]   = sum_k xn[k] * W3[n,k]
+ *     out[m,n]= h1[n] / (1 + exp(-h1[n])) * h3[n]          (SiLU(t) = t*sigma(t))
+ *
+ * Fold-aware modes (R4): the method as [BJ] defines it folds g into
+ * the weights *in the storage precision*.  ORACLE_FOLD_BF16 first replaces
+ * W_j[n,k] by RNE_bf16(W_j[n,k]*g[k]) and ORACLE_FOLD_TF32 by
+ * RNE_tf32(RNE_fp32(W_j[n,k]*g[k])), using this file's own bit-level rounding,
+ * then computes h_j = r * sum_k x[m,k]*Wt_j[n,k].  That is the exact value of
+ * what the folded method computes before accumulation/output rounding.
+ *
+ * Inputs are stored values (bf16 bit patterns, fp32 or fp64), widened here
+ * exactly to double.  Output: double, unrounded.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+enum { ORACLE_DT_BF16 = 0, ORACLE_DT_F32 = 1, ORACLE_DT_F64 = 2 };
+enum { ORACLE_PLAIN = 0, ORACLE_FOLD_BF16 = 1, ORACLE_FOLD_TF32 = 2 };
+
+/* ---- storage-format helpers (the oracle's own; not shared with the GPU) ---- */
+
+/* bf16 is the top 16 bits of an IEEE binary32: widening is exact. */
+static double bf16_bits_to_double(uint16_t b) {
+    uint32_t u = ((uint32_t)b) << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+static double load_elem(const void* p, int dtype, int64_t i) {
+    switch (dtype) {
+    case ORACLE_DT_BF16: return bf16_bits_to_double(((const uint16_t*)p)[i]);
+    case ORACLE_DT_F32:  return (double)((const float*)p)[i];
+    default:             return ((const double*)p)[i];
+    }
+}
+
+/* Round-to-nearest-even of a binary32 value to `keep` explicit mantissa bits
+ * (bf16: 7, tf32: 10).  Bit manipulation on the binary32 encoding: add half an
+ * ulp of the target format (minus one if the kept LSB is 0, which realises the
+ * ties-to-even rule) and clear the dropped bits.  NaN passes through quietened;
+ * overflow to inf is the correct RNE result. */
+static uint32_t rne_f32_bits(uint32_t u, int keep) {
+    const int drop = 23 - keep;
+    if ((u & 0x7f800000u) == 0x7f800000u) {           /* inf / nan */
+        if (u & 0x007fffffu) u |= 0x00400000u;
+        return u & ~((1u << drop) - 1u);
+    }
+    uint32_t lsb = (u >> drop) & 1u;
+    uint32_t bias = (1u << (drop - 1)) - 1u + lsb;
+    u += bias;
+    return u & ~((1u << drop) - 1u);
+}
+
+/* Exported for the pins: double -> binary32 (C cast, RNE) -> bf16 bits. */
+uint16_t oracle_round_bf16_bits(double v) {
+    float f = (float)v;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return (uint16_t)(rne_f32_bits(u, 7) >> 16);
+}
+
+double oracle_round_bf16(double v) {
+    return bf16_bits_to_double(oracle_round_bf16_bits(v));
+}
+
+double oracle_round_tf32(double v) {
+    float f = (float)v;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u = rne_f32_bits(u, 10);
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+/* ---- a1: per-row inverse RMS ---------------------------------------------- */
+/* r[m] = 1 / sqrt( (sum_k x[m,k]^2)/K + eps )   ([BJ]; R2, R3) */
+void oracle_rms_inv(const void* x, int dtype, int64_t M, int64_t K, double eps, double* r) {
+    for (int64_t m = 0; m < M; ++m) {
+        double ss = 0.0;
+        for (int64_t k = 0; k < K; ++k) {
+            double v = load_elem(x, dtype, m * K + k);
+            ss += v * v;
+        }
+        r[m] = 1.0 / sqrt(ss / (double)K + eps);
+    }
+}
+
+/* ---- whole path, selected rows ------------------------------------------- */
+/*
+ * rows: the nrows row indices of x to evaluate (NULL = all M rows, nrows = M).
+ * out : [nrows, N] double.
+ * Returns 0 on success, -1 on bad arguments, -2 on allocation failure.
+ */
+int oracle_ffn_rows(const void* x, int x_dtype, const void* g, const void* w1, const void* w3,
+                    int w_dtype, int64_t M, int64_t K, int64_t N, double eps, int mode,
+                    const int64_t* rows, int64_t nrows, double* out) {
+    if (!x || !g || !w1 || !w3 || !out || K <= 0 || N <= 0 || M < 0 || nrows < 0) return -1;
+    if (mode < ORACLE_PLAIN || mode > ORACLE_FOLD_TF32) return -1;
+    if (nrows == 0) return 0;
+
+    /* Widen the weights once to double (row-major [N,K]); apply the fold in
+     * fold-aware modes.  g[k] multiplies column k of both W1 and W3. */
+    double* W1 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)K);
+    double* W3 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)K);
+    double* G = (double*)malloc(sizeof(double) * (size_t)K);
+    if (!W1 || !W3 || !G) { free(W1); free(W3); free(G); return -2; }
+    for (int64_t k = 0; k < K; ++k) G[k] = load_elem(g, w_dtype, k);
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t k = 0; k < K; ++k) {
+            double a = load_elem(w1, w_dtype, n * K + k);
+            double b = load_elem(w3, w_dtype, n * K + k);
+            if (mode == ORACLE_FOLD_BF16) {
+                a = oracle_round_bf16(a * G[k]);
+                b = oracle_round_bf16(b * G[k]);
+            } else if (mode == ORACLE_FOLD_TF32) {
+                a = oracle_round_tf32((double)(float)(a * G[k]));
+                b = oracle_round_tf32((double)(float)(b * G[k]));
+            }
+            W1[n * K + k] = a;
+            W3[n * K + k] = b;
+        }
+    }
+
+    int status = 0;
+    #pragma omp parallel
+    {
+        double* xn = (double*)malloc(sizeof(double) * (size_t)K);
+        if (!xn) {
+            #pragma omp atomic write
+            status = -2;
+        } else {
+            #pragma omp for schedule(dynamic, 1)
+            for (int64_t i = 0; i < nrows; ++i) {
+                int64_t m = rows ? rows[i] : i;
+                if (m < 0 || m >= M) {
+                    for (int64_t n = 0; n < N; ++n) out[i * N + n] = NAN;
+                    continue;
+                }
+                /* a1: r = 1/sqrt(mean(x^2) + eps) */
+                double ss = 0.0;
+                for (int64_t k = 0; k < K; ++k) {
+                    double v = load_elem(x, x_dtype, m * K + k);
+                    ss += v * v;
+                }
+                double r = 1.0 / sqrt(ss / (double)K + eps);
+                /* RMSNorm(x): plain mode applies r and g to x; fold-aware modes
+                 * have g inside the weights and apply r after the contraction. */
+                for (int64_t k = 0; k < K; ++k) {
+                    double v = load_elem(x, x_dtype, m * K + k);
+                    xn[k] = (mode == ORACLE_PLAIN) ? v * r * G[k] : v;
+                }
+                /* a2 + a3 */
+                for (int64_t n = 0; n < N; ++n) {
+                    const double* a = W1 + n * K;
+                    const double* b = W3 + n * K;
+                    double h1 = 0.0, h3 = 0.0;
+                    for (int64_t k = 0; k < K; ++k) {
+                        h1 += xn[k] * a[k];
+                        h3 += xn[k] * b[k];
+                    }
+                    if (mode != ORACLE_PLAIN) { h1 *= r; h3 *= r; }
+                    out[i * N + n] = h1 / (1.0 + exp(-h1)) * h3;
+                }
+            }
+            free(xn);
+        }
+    }
+    free(W1); free(W3); free(G);
+    return status;
+}
+
+int oracle_ffn(const void* x, int x_dtype, const void* g, const void* w1, const void* w3,
+               int w_dtype, int64_t M, int64_t K, int64_t N, double eps, int mode, double* out) {
+    return oracle_ffn_rows(x, x_dtype, g, w1, w3, w_dtype, M, K, N, eps, mode, NULL, M, out);
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,33 @@
+#!/usr/bin/env bash
+# Mutation check of the oracle pins: apply plausible mistakes to
+# oracle/ffn_oracle.c one at a time and require tests/test_oracle.py to fail.
+# Restores the source afterwards.  CPU only.
+set -u
+cd "$(dirname "$0")/.."
+SRC=oracle/ffn_oracle.c
+cp "$SRC" /tmp/ffn_oracle.orig.c
+trap 'cp /tmp/ffn_oracle.orig.c "$SRC"; python -c "import oracle; oracle.build(force=True)"' EXIT
+status=0
+while IFS= read -r mut; do
+  [ -z "$mut" ] && continue
+  cp /tmp/ffn_oracle.orig.c "$SRC"; sed -i "$mut" "$SRC"
+  if cmp -s /tmp/ffn_oracle.orig.c "$SRC"; then echo "NOT APPLIED: $mut"; status=1; continue; fi
+  if timeout 300 python -m pytest tests/test_oracle.py -q >/dev/null 2>&1; then
+    echo "SURVIVED: $mut"; status=1
+  else
+    echo "killed:   $mut"
+  fi
+done <<'MUTS'
+s|r = 1.0 / sqrt(ss / (double)K + eps);|r = 1.0 / (sqrt(ss / (double)K) + eps);|
+s|double r = 1.0 / sqrt(ss / (double)K + eps);|double r = 1.0 / sqrt(ss / (double)(K-1) + eps);|
+s|double r = 1.0 / sqrt(ss / (double)K + eps);|double r = 1.0 / sqrt(ss + eps);|
+s|xn\[k\] = (mode == ORACLE_PLAIN) ? v \* r \* G\[k\] : v;|xn[k] = (mode == ORACLE_PLAIN) ? v * r : v;|
+s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = h3 / (1.0 + exp(-h3)) * h1;|
+s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = h1 / (1.0 + exp(h1)) * h3;|
+s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = 1.0 / (1.0 + exp(-h1)) * h3;|
+s|const double\* a = W1 + n \* K;|const double* a = W1 + (n % 2) * K;|
+s|a = oracle_round_bf16(a \* G\[k\]);|a = a * G[k];|
+s|uint32_t bias = (1u << (drop - 1)) - 1u + lsb;|uint32_t bias = (1u << (drop - 1));|
+s|if (mode != ORACLE_PLAIN) { h1 \*= r; h3 \*= r; }|if (mode != ORACLE_PLAIN) { h1 *= r; }|
+MUTS
+exit $status
