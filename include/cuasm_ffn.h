@@ -1,0 +1,147 @@
+/*
+ * cuasm_ffn.h -- C ABI of the B200-native fused RMSNorm + SwiGLU feed-forward.
+ *
+ *   out = SiLU(RMSNorm(x) . W1^T) (.) (RMSNorm(x) . W3^T),
+ *   RMSNorm(x)[m,k] = x[m,k] * g[k] / sqrt( (sum_k x[m,k]^2)/K + eps )
+ *
+ * The operation is the "fused feed-forward ... for LLAMA" kernel of PAPER.md
+ * P:68 (named fused_ff in Fig. "kernel throughput"; evaluated with
+ * inputs B, M, N, K in Table "Evaluated Kernels", P:560 -- B is folded into
+ * M = tokens here).  The paper never prints the formula; it is BASELINE.json's
+ * north_star, with the readings listed in DESIGN.md (R1 W1 = SiLU branch,
+ * R2 eps inside the sqrt, R3 RMS over x not x*g, R4 fold rounding).
+ *
+ * Design (BASELINE.json north_star): g is folded into W1/W3 once per weight
+ * set (step a0, cached in the handle), a row-wise sum-of-squares pre-pass
+ * produces r[m] = 1/rms (a1), and one persistent tcgen05/TMEM/TMA dual-GEMM
+ * kernel computes both contractions and applies r, SiLU and the gate in its
+ * epilogue (a2 + a3).  Everything runs on the caller's CUDA stream; there is
+ * no CPU fallback: without an sm_100 device every entry point that would
+ * compute returns CUASM_ERR_UNSUPPORTED or CUASM_ERR_CUDA.
+ *
+ * Conventions for every entry point:
+ *   - Pointers named *_dev are CUDA device pointers, *_host are host pointers.
+ *   - All matrices are dense row-major, no padding: x[M,K], w1/w3[N,K]
+ *     (nn.Linear layout, K contiguous), out[M,N]; rms_w = g[K].
+ *   - Element type is the handle's dtype for x, rms_w, w1, w3 AND out
+ *     (CUASM_DTYPE_BF16: bfloat16; CUASM_DTYPE_FP32: float32, contracted on
+ *     the tensor cores as TF32).  Accumulation is fp32.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Errors are return values; no entry point aborts or throws.  Argument
+ *     validation happens before anything is enqueued: on error nothing is
+ *     launched and `out` is untouched.  The message of the last error is
+ *     kept per handle (cuasm_ffn_last_error).
+ *   - A handle is bound to one device and is not thread-safe; use one
+ *     handle per (thread, device).  Multi-GPU runs use one handle per rank.
+ */
+#ifndef CUASM_FFN_H
+#define CUASM_FFN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUASM_FFN_ABI_VERSION 1
+
+typedef struct cuasm_ffn_s* cuasm_ffn_t;
+
+typedef enum {
+    CUASM_OK = 0,
+    CUASM_ERR_INVALID_ARG = 1, /* NULL/misaligned pointer, bad size, eps < 0 or NaN    */
+    CUASM_ERR_UNSUPPORTED = 2, /* device is not compute capability 10.0 (B200, sm_100a) */
+    CUASM_ERR_CUDA = 3,        /* a CUDA runtime/driver call or a launch failed          */
+    CUASM_ERR_OOM = 4          /* device workspace allocation failed                    */
+} cuasm_status_t;
+
+typedef enum { CUASM_DTYPE_BF16 = 0, CUASM_DTYPE_FP32 = 1 } cuasm_dtype_t;
+
+/* Kernel-variant selector (cuasm_ffn_set_option with CUASM_OPT_VARIANT). */
+typedef enum {
+    CUASM_VARIANT_AUTO = 0, /* shape-keyed choice */
+    CUASM_VARIANT_1SM = 1,  /* cta_group::1, 128 x 256 MMA tile per SM            */
+    CUASM_VARIANT_2SM = 2   /* cta_group::2 CTA pair, 256 x 256 MMA tile per TPC  */
+} cuasm_variant_t;
+
+typedef enum {
+    CUASM_OPT_VARIANT = 0, /* value: cuasm_variant_t                                   */
+    CUASM_OPT_PDL = 1,     /* value: 1 = launch the GEMM with programmatic dependent
+                              launch after the pre-pass (default), 0 = plain ordering */
+    CUASM_OPT_GROUP_M = 2  /* value: m-blocks per rasterisation group (0 = auto)       */
+} cuasm_option_t;
+
+/* Create a handle on `device` (CUDA ordinal) for element type `dtype`.
+ * Returns UNSUPPORTED if the device is not CC 10.0, CUDA on any runtime error.
+ * On success *h owns no device memory yet (allocated lazily, on demand). */
+cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* h, int device, cuasm_dtype_t dtype);
+
+/* The whole hot path for one batch of tokens (PAPER.md P:560 inputs M, N, K):
+ *   a0 (only when the weight key (rms_w, w1, w3, K, N) differs from the cached
+ *      one, or after cuasm_ffn_invalidate_weights): fold g into W1/W3 and pack
+ *      them into the handle-owned W13 buffer, on `stream`;
+ *   a1 r[m] = 1/sqrt(sum_k x^2 / K + eps) into a handle-owned fp32 workspace;
+ *   a2+a3 out = bf16( SiLU(r*x.W1g^T) * (r*x.W3g^T) ).
+ * x_dev [M,K], rms_w_dev [K], w1_dev/w3_dev [N,K], out_dev [M,N]: device
+ * pointers, 16-byte aligned, caller-owned; out is fully overwritten.
+ * Preconditions (else INVALID_ARG, nothing launched): pointers non-NULL and
+ * 16-byte aligned, M >= 0, K > 0, N > 0, K % 8 == 0, N % 8 == 0,
+ * M, N < 2^31, eps >= 0 and not NaN.  M == 0 returns OK without launching.
+ * Weights must not change while cached (else call invalidate_weights).
+ * Asynchronous: returns after enqueueing; out is valid once `stream` reaches
+ * this point. */
+cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev, const void* w1_dev,
+                                 const void* w3_dev, void* out_dev, int64_t M, int64_t K, int64_t N, float eps,
+                                 void* stream);
+
+/* End-to-end variant for host-resident activations: copies x_host [M,K]
+ * (ideally pinned) to a handle-owned device buffer, runs cuasm_ffn_forward
+ * with the device-resident weights, and copies the result back into
+ * out_host [M,N].  All on `stream`; synchronous w.r.t. the host only if
+ * `sync` != 0 (otherwise out_host is valid after the stream completes and
+ * must be pinned).  Same preconditions as cuasm_ffn_forward. */
+cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w_dev, const void* w1_dev,
+                                      const void* w3_dev, void* out_host, int64_t M, int64_t K, int64_t N, float eps,
+                                      void* stream, int sync);
+
+/* Step a0 alone: fold g into W1/W3 and pack (one-time weight preparation,
+ * PAPER.md P:434-447's offline/deploy split).  Same weight preconditions. */
+cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w_dev, const void* w1_dev, const void* w3_dev,
+                                 int64_t K, int64_t N, void* stream);
+
+/* Step a1 alone: r_dev[m] = 1/sqrt(sum_k x[m,k]^2/K + eps), fp32, M floats.
+ * r_dev is caller-owned device memory (4-byte aligned). */
+cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x_dev, float* r_dev, int64_t M, int64_t K, float eps,
+                                 void* stream);
+
+/* Copy the packed, g-folded weights (a0's output) to host memory for
+ * inspection: rows = 2*ceil(N/128)*128, row r = (nb, j, rr) holds
+ * RNE(W_j[nb*128+rr, :] * g) (zero for padded rows), K elements each.
+ * *bytes receives the size; pass dst_host = NULL to query it.  Synchronous. */
+cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst_host, int64_t* bytes);
+
+/* Drop the cached packed weights; the next forward re-packs. */
+cuasm_status_t cuasm_ffn_invalidate_weights(cuasm_ffn_t h);
+
+/* Set a tuning option (cuasm_option_t).  INVALID_ARG for unknown keys/values. */
+cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value);
+
+/* Which GEMM variant the last forward launched (cuasm_variant_t), and the
+ * number of kernels it enqueued (0 when M == 0). */
+cuasm_status_t cuasm_ffn_last_launch(cuasm_ffn_t h, int* variant, int* kernels);
+
+/* Free all handle-owned device memory and the handle.  NULL is accepted. */
+cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h);
+
+/* Message of the last error on this handle ("" if none; valid until the next
+ * call on the handle).  h == NULL returns the last init error. */
+const char* cuasm_ffn_last_error(cuasm_ffn_t h);
+
+/* CUASM_FFN_ABI_VERSION of the loaded library. */
+int cuasm_ffn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUASM_FFN_H */

@@ -64,6 +64,10 @@ def _load():
             lib.oracle_round_bf16_bits.restype = ctypes.c_uint16
             lib.oracle_round_tf32.argtypes = [dbl]
             lib.oracle_round_tf32.restype = dbl
+            lib.oracle_fold_bf16.argtypes = [vp, vp, i64, i64, vp]
+            lib.oracle_fold_bf16.restype = None
+            lib.oracle_fold_tf32.argtypes = [vp, vp, i64, i64, vp]
+            lib.oracle_fold_tf32.restype = None
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = ci
             _lib = lib
@@ -158,6 +162,24 @@ def round_bf16_bits(v: float) -> int:
 
 def round_tf32(v: float) -> float:
     return _load().oracle_round_tf32(float(v))
+
+
+def fold(w, g) -> np.ndarray:
+    """Step a0 as the method defines it: RNE(W[n,k]*g[k]) in the storage
+    format (bf16 -> uint16 bit patterns; fp32 -> tf32-rounded float32)."""
+    lib = _load()
+    ws, wdt = _as_storage(w)
+    gs, gdt = _as_storage(g)
+    N, K = ws.shape
+    if wdt == DT_BF16 and gdt == DT_BF16:
+        dst = np.empty((N, K), dtype=np.uint16)
+        lib.oracle_fold_bf16(ws.ctypes.data, gs.ctypes.data, N, K, dst.ctypes.data)
+    elif wdt == DT_F32 and gdt == DT_F32:
+        dst = np.empty((N, K), dtype=np.float32)
+        lib.oracle_fold_tf32(ws.ctypes.data, gs.ctypes.data, N, K, dst.ctypes.data)
+    else:
+        raise TypeError("fold: w and g must both be bf16 or both fp32")
+    return dst
 
 
 def num_threads() -> int:

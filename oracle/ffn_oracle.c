@@ -125,7 +125,14 @@ void oracle_rms_inv(const void* x, int dtype, int64_t M, int64_t K, double eps, 
  * rows: the nrows row indices of x to evaluate (NULL = all M rows, nrows = M).
  * out : [nrows, N] double.
  * Returns 0 on success, -1 on bad arguments, -2 on allocation failure.
+ *
+ * Loop order: the normalised rows are formed first; then the weight rows are
+ * visited in blocks of ORACLE_NB (widened, and folded in fold-aware modes,
+ * once per block) and every selected row is contracted with them.  Each
+ * h1/h3 is still one sequential k-sum exactly as written in the header, so
+ * the blocking changes memory traffic only, never a value.
  */
+#define ORACLE_NB 64
 int oracle_ffn_rows(const void* x, int x_dtype, const void* g, const void* w1, const void* w3,
                     int w_dtype, int64_t M, int64_t K, int64_t N, double eps, int mode,
                     const int64_t* rows, int64_t nrows, double* out) {
@@ -133,76 +140,105 @@ int oracle_ffn_rows(const void* x, int x_dtype, const void* g, const void* w1, c
     if (mode < ORACLE_PLAIN || mode > ORACLE_FOLD_TF32) return -1;
     if (nrows == 0) return 0;
 
-    /* Widen the weights once to double (row-major [N,K]); apply the fold in
-     * fold-aware modes.  g[k] multiplies column k of both W1 and W3. */
-    double* W1 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)K);
-    double* W3 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)K);
     double* G = (double*)malloc(sizeof(double) * (size_t)K);
-    if (!W1 || !W3 || !G) { free(W1); free(W3); free(G); return -2; }
+    double* XN = (double*)malloc(sizeof(double) * (size_t)nrows * (size_t)K);
+    double* R = (double*)malloc(sizeof(double) * (size_t)nrows);
+    char* valid = (char*)malloc((size_t)nrows);
+    if (!G || !XN || !R || !valid) { free(G); free(XN); free(R); free(valid); return -2; }
     for (int64_t k = 0; k < K; ++k) G[k] = load_elem(g, w_dtype, k);
+
+    /* a1 + RMSNorm: r = 1/sqrt(mean(x^2) + eps); plain mode forms
+     * xn = x * r * g, fold-aware modes keep x (g is inside the weights and r
+     * is applied after the contraction). */
     #pragma omp parallel for schedule(static)
-    for (int64_t n = 0; n < N; ++n) {
+    for (int64_t i = 0; i < nrows; ++i) {
+        int64_t m = rows ? rows[i] : i;
+        valid[i] = (m >= 0 && m < M);
+        if (!valid[i]) continue;
+        double ss = 0.0;
         for (int64_t k = 0; k < K; ++k) {
-            double a = load_elem(w1, w_dtype, n * K + k);
-            double b = load_elem(w3, w_dtype, n * K + k);
-            if (mode == ORACLE_FOLD_BF16) {
-                a = oracle_round_bf16(a * G[k]);
-                b = oracle_round_bf16(b * G[k]);
-            } else if (mode == ORACLE_FOLD_TF32) {
-                a = oracle_round_tf32((double)(float)(a * G[k]));
-                b = oracle_round_tf32((double)(float)(b * G[k]));
-            }
-            W1[n * K + k] = a;
-            W3[n * K + k] = b;
+            double v = load_elem(x, x_dtype, m * K + k);
+            ss += v * v;
+        }
+        double r = 1.0 / sqrt(ss / (double)K + eps);
+        R[i] = r;
+        for (int64_t k = 0; k < K; ++k) {
+            double v = load_elem(x, x_dtype, m * K + k);
+            XN[i * K + k] = (mode == ORACLE_PLAIN) ? v * r * G[k] : v;
         }
     }
 
     int status = 0;
+    const int64_t nblocks = (N + ORACLE_NB - 1) / ORACLE_NB;
     #pragma omp parallel
     {
-        double* xn = (double*)malloc(sizeof(double) * (size_t)K);
-        if (!xn) {
+        double* W1 = (double*)malloc(sizeof(double) * ORACLE_NB * (size_t)K);
+        double* W3 = (double*)malloc(sizeof(double) * ORACLE_NB * (size_t)K);
+        if (!W1 || !W3) {
             #pragma omp atomic write
             status = -2;
         } else {
             #pragma omp for schedule(dynamic, 1)
-            for (int64_t i = 0; i < nrows; ++i) {
-                int64_t m = rows ? rows[i] : i;
-                if (m < 0 || m >= M) {
-                    for (int64_t n = 0; n < N; ++n) out[i * N + n] = NAN;
-                    continue;
-                }
-                /* a1: r = 1/sqrt(mean(x^2) + eps) */
-                double ss = 0.0;
-                for (int64_t k = 0; k < K; ++k) {
-                    double v = load_elem(x, x_dtype, m * K + k);
-                    ss += v * v;
-                }
-                double r = 1.0 / sqrt(ss / (double)K + eps);
-                /* RMSNorm(x): plain mode applies r and g to x; fold-aware modes
-                 * have g inside the weights and apply r after the contraction. */
-                for (int64_t k = 0; k < K; ++k) {
-                    double v = load_elem(x, x_dtype, m * K + k);
-                    xn[k] = (mode == ORACLE_PLAIN) ? v * r * G[k] : v;
-                }
-                /* a2 + a3 */
-                for (int64_t n = 0; n < N; ++n) {
-                    const double* a = W1 + n * K;
-                    const double* b = W3 + n * K;
-                    double h1 = 0.0, h3 = 0.0;
+            for (int64_t nb = 0; nb < nblocks; ++nb) {
+                const int64_t n0 = nb * ORACLE_NB;
+                const int64_t nn = (N - n0) < ORACLE_NB ? (N - n0) : ORACLE_NB;
+                /* widen (and in fold-aware modes fold g into) this block of W1/W3 */
+                for (int64_t j = 0; j < nn; ++j) {
                     for (int64_t k = 0; k < K; ++k) {
-                        h1 += xn[k] * a[k];
-                        h3 += xn[k] * b[k];
+                        double a = load_elem(w1, w_dtype, (n0 + j) * K + k);
+                        double b = load_elem(w3, w_dtype, (n0 + j) * K + k);
+                        if (mode == ORACLE_FOLD_BF16) {
+                            a = oracle_round_bf16(a * G[k]);
+                            b = oracle_round_bf16(b * G[k]);
+                        } else if (mode == ORACLE_FOLD_TF32) {
+                            a = oracle_round_tf32((double)(float)(a * G[k]));
+                            b = oracle_round_tf32((double)(float)(b * G[k]));
+                        }
+                        W1[j * K + k] = a;
+                        W3[j * K + k] = b;
                     }
-                    if (mode != ORACLE_PLAIN) { h1 *= r; h3 *= r; }
-                    out[i * N + n] = h1 / (1.0 + exp(-h1)) * h3;
+                }
+                for (int64_t i = 0; i < nrows; ++i) {
+                    const double* xn = XN + i * K;
+                    for (int64_t j = 0; j < nn; ++j) {
+                        if (!valid[i]) { out[i * N + n0 + j] = NAN; continue; }
+                        const double* a = W1 + j * K;
+                        const double* b = W3 + j * K;
+                        /* a2: the two contractions */
+                        double h1 = 0.0, h3 = 0.0;
+                        for (int64_t k = 0; k < K; ++k) {
+                            h1 += xn[k] * a[k];
+                            h3 += xn[k] * b[k];
+                        }
+                        if (mode != ORACLE_PLAIN) { h1 *= R[i]; h3 *= R[i]; }
+                        /* a3: SiLU(h1) * h3, SiLU(t) = t / (1 + e^-t) */
+                        out[i * N + n0 + j] = h1 / (1.0 + exp(-h1)) * h3;
+                    }
                 }
             }
-            free(xn);
         }
+        free(W1); free(W3);
     }
-    free(W1); free(W3); free(G);
+    free(G); free(XN); free(R); free(valid);
     return status;
+}
+
+/* Step a0 as the method defines it, for the bitwise pin of the GPU pack:
+ * dst_bits[n*K+k] = RNE_bf16(W[n,k] * g[k]) for bf16 W, g. */
+void oracle_fold_bf16(const uint16_t* w, const uint16_t* g, int64_t N, int64_t K, uint16_t* dst_bits) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n)
+        for (int64_t k = 0; k < K; ++k)
+            dst_bits[n * K + k] = oracle_round_bf16_bits(bf16_bits_to_double(w[n * K + k]) *
+                                                         bf16_bits_to_double(g[k]));
+}
+
+/* Same for fp32 storage (tf32 MMA path): RNE_tf32(RNE_fp32(W*g)) as fp32. */
+void oracle_fold_tf32(const float* w, const float* g, int64_t N, int64_t K, float* dst) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n)
+        for (int64_t k = 0; k < K; ++k)
+            dst[n * K + k] = (float)oracle_round_tf32((double)(float)((double)w[n * K + k] * (double)g[k]));
 }
 
 int oracle_ffn(const void* x, int x_dtype, const void* g, const void* w1, const void* w3,

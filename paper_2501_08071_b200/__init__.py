@@ -1,0 +1,246 @@
+"""B200-native fused RMSNorm + SwiGLU feed-forward (the LLaMA ``fused_ff``
+kernel of arXiv 2501.08071, PAPER.md P:68 / P:560), as a C-ABI library
+(include/cuasm_ffn.h) plus this thin ctypes binding.
+
+    out = SiLU(RMSNorm(x) @ W1.T) * (RMSNorm(x) @ W3.T)
+
+The binding only marshals arguments (torch tensors -> device pointers, the
+current CUDA stream).  Every step of the path runs in the library's sm_100a
+kernels; there is no CPU or PyTorch fallback -- if libcuasm_ffn.so is missing
+or the device is not a B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import weakref
+
+import torch
+
+__all__ = [
+    "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "CuasmError", "lib_path", "load_library",
+    "VARIANT_AUTO", "VARIANT_1SM", "VARIANT_2SM", "EXPORTED_SYMBOLS",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libcuasm_ffn.so")
+_lib = None
+_lib_lock = threading.Lock()
+
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
+DTYPE_BF16, DTYPE_FP32 = 0, 1
+VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M = 0, 1, 2
+
+# Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
+    "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
+    "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
+)
+
+
+class CuasmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cuasm_ffn status {status}: {msg}")
+        self.status = status
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libcuasm_ffn.so (raises if it has not been built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not found: build it with `python -m paper_2501_08071_b200.build` "
+                              "(or __graft_entry__.build()); there is no fallback path")
+        lib = ctypes.CDLL(_LIB_PATH)
+        vp, i64, f32, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_int
+        lib.cuasm_ffn_init.argtypes = [ctypes.POINTER(vp), ci, ci]
+        lib.cuasm_ffn_forward.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
+        lib.cuasm_ffn_forward_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp, ci]
+        lib.cuasm_ffn_prepare.argtypes = [vp, vp, vp, vp, i64, i64, vp]
+        lib.cuasm_ffn_rms_inv.argtypes = [vp, vp, vp, i64, i64, f32, vp]
+        lib.cuasm_ffn_get_packed.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        lib.cuasm_ffn_invalidate_weights.argtypes = [vp]
+        lib.cuasm_ffn_set_option.argtypes = [vp, ci, i64]
+        lib.cuasm_ffn_last_launch.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+        lib.cuasm_ffn_destroy.argtypes = [vp]
+        lib.cuasm_ffn_last_error.argtypes = [vp]
+        lib.cuasm_ffn_last_error.restype = ctypes.c_char_p
+        lib.cuasm_ffn_abi_version.argtypes = []
+        for name in EXPORTED_SYMBOLS:
+            if name not in ("cuasm_ffn_last_error", "cuasm_ffn_abi_version"):
+                getattr(lib, name).restype = ci
+        lib.cuasm_ffn_abi_version.restype = ci
+        _lib = lib
+        return lib
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.bfloat16:
+        return DTYPE_BF16
+    if dt == torch.float32:
+        return DTYPE_FP32
+    raise TypeError(f"cuasm_ffn supports bfloat16 and float32 tensors, got {dt}")
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class FusedFFN:
+    """One library handle (device + dtype).  Not thread-safe."""
+
+    def __init__(self, device=None, dtype: torch.dtype = torch.bfloat16):
+        self.lib = load_library()
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.type != "cuda":
+            raise ValueError("FusedFFN needs a CUDA device")
+        self.device_index = dev.index if dev.index is not None else torch.cuda.current_device()
+        self.dtype = dtype
+        h = ctypes.c_void_p()
+        st = self.lib.cuasm_ffn_init(ctypes.byref(h), self.device_index, _dtype_code(dtype))
+        if st != OK:
+            raise CuasmError(st, self.lib.cuasm_ffn_last_error(None).decode())
+        self._h = h
+        self._wkey = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.cuasm_ffn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != OK:
+            raise CuasmError(st, self.lib.cuasm_ffn_last_error(self._h).decode())
+
+    def set_option(self, option: int, value: int):
+        self._check(self.lib.cuasm_ffn_set_option(self._h, option, int(value)))
+
+    def set_variant(self, variant: int):
+        self.set_option(OPT_VARIANT, variant)
+
+    def last_launch(self):
+        v, k = ctypes.c_int(), ctypes.c_int()
+        self._check(self.lib.cuasm_ffn_last_launch(self._h, ctypes.byref(v), ctypes.byref(k)))
+        return v.value, k.value
+
+    def _validate(self, *ts):
+        for t in ts:
+            if t.dtype != self.dtype:
+                raise TypeError(f"expected {self.dtype}, got {t.dtype}")
+            if not t.is_cuda or t.device.index != self.device_index:
+                raise ValueError("tensor is not on the handle's device")
+            if not t.is_contiguous():
+                raise ValueError("tensors must be contiguous")
+
+    def _weights_changed(self, rms_w, w1, w3):
+        # The library caches the folded weights keyed by pointer.  A pointer
+        # alone is not an identity (the caching allocator reuses addresses),
+        # so the binding keys on the tensor objects themselves (weak refs) and
+        # their in-place version counters, and invalidates on any change.
+        same = (self._wkey is not None
+                and all(r() is t for r, t in zip(self._wkey[0], (rms_w, w1, w3)))
+                and self._wkey[1] == tuple(t._version for t in (rms_w, w1, w3)))
+        if not same:
+            self._check(self.lib.cuasm_ffn_invalidate_weights(self._h))
+            self._wkey = (tuple(weakref.ref(t) for t in (rms_w, w1, w3)),
+                          tuple(t._version for t in (rms_w, w1, w3)))
+
+    def prepare(self, rms_w, w1, w3):
+        self._validate(rms_w, w1, w3)
+        N, K = w1.shape
+        self._weights_changed(rms_w, w1, w3)
+        self._check(self.lib.cuasm_ffn_prepare(self._h, rms_w.data_ptr(), w1.data_ptr(), w3.data_ptr(), K, N,
+                                               _stream_ptr(w1.device)))
+
+    def forward(self, x, rms_w, w1, w3, eps: float = 1e-6, out=None):
+        self._validate(x, rms_w, w1, w3)
+        if x.dim() != 2 or w1.dim() != 2 or w1.shape != w3.shape:
+            raise ValueError("x must be [M,K] and w1/w3 [N,K]")
+        M, K = x.shape
+        N = w1.shape[0]
+        if w1.shape[1] != K or rms_w.shape != (K,):
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty((M, N), dtype=self.dtype, device=x.device)
+        else:
+            self._validate(out)
+            if out.shape != (M, N):
+                raise ValueError("out must be [M,N]")
+        self._weights_changed(rms_w, w1, w3)
+        self._check(self.lib.cuasm_ffn_forward(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
+                                               w3.data_ptr(), out.data_ptr(), M, K, N, float(eps),
+                                               _stream_ptr(x.device)))
+        return out
+
+    def forward_host(self, x_host, rms_w, w1, w3, eps: float = 1e-6, out_host=None, sync: bool = True):
+        """End-to-end call with host activations: H2D x, forward, D2H out."""
+        self._validate(rms_w, w1, w3)
+        if x_host.is_cuda or x_host.dtype != self.dtype or not x_host.is_contiguous():
+            raise ValueError("x_host must be a contiguous CPU tensor of the handle dtype")
+        M, K = x_host.shape
+        N = w1.shape[0]
+        if out_host is None:
+            out_host = torch.empty((M, N), dtype=self.dtype, pin_memory=True)
+        self._weights_changed(rms_w, w1, w3)
+        self._check(self.lib.cuasm_ffn_forward_host(self._h, x_host.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
+                                                    w3.data_ptr(), out_host.data_ptr(), M, K, N, float(eps),
+                                                    _stream_ptr(w1.device), 1 if sync else 0))
+        return out_host
+
+    def rms_inv(self, x, eps: float = 1e-6, out=None):
+        self._validate(x)
+        M, K = x.shape
+        if out is None:
+            out = torch.empty((M,), dtype=torch.float32, device=x.device)
+        self._check(self.lib.cuasm_ffn_rms_inv(self._h, x.data_ptr(), out.data_ptr(), M, K, float(eps),
+                                               _stream_ptr(x.device)))
+        return out
+
+    def packed_weights(self) -> torch.Tensor:
+        """Host copy of the g-folded, W1/W3-interleaved weights (a0's output)."""
+        n = ctypes.c_int64()
+        self._check(self.lib.cuasm_ffn_get_packed(self._h, None, ctypes.byref(n)))
+        buf = torch.empty((n.value // (2 if self.dtype == torch.bfloat16 else 4),), dtype=self.dtype)
+        self._check(self.lib.cuasm_ffn_get_packed(self._h, buf.data_ptr(), ctypes.byref(n)))
+        return buf
+
+
+_handles: dict = {}
+
+
+def _handle(device, dtype) -> FusedFFN:
+    key = (torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device(),
+           dtype)
+    h = _handles.get(key)
+    if h is None:
+        h = FusedFFN(torch.device("cuda", key[0]), dtype)
+        _handles[key] = h
+    return h
+
+
+def ffn_forward(x, rms_w, w1, w3, eps: float = 1e-6, out=None):
+    """out = SiLU(RMSNorm(x) W1^T) * (RMSNorm(x) W3^T) on the tensors' GPU."""
+    return _handle(x.device, x.dtype).forward(x, rms_w, w1, w3, eps, out)
+
+
+def ffn_forward_host(x_host, rms_w, w1, w3, eps: float = 1e-6, out_host=None, sync: bool = True):
+    return _handle(w1.device, w1.dtype).forward_host(x_host, rms_w, w1, w3, eps, out_host, sync)
+
+
+def rms_inv(x, eps: float = 1e-6):
+    return _handle(x.device, x.dtype).rms_inv(x, eps)

@@ -1,0 +1,495 @@
+// cuasm_ffn.cu -- the C-ABI library (include/cuasm_ffn.h): handle, argument
+// validation, weight-fold cache, TMA tensor-map encoding, kernel selection and
+// launches.  All arithmetic of the path runs in the kernels included below.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <new>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/cuasm_ffn.h"
+#include "dual_gemm.cuh"
+#include "pack.cuh"
+#include "prepass.cuh"
+
+namespace {
+
+using cuasm::FfnGemmParams;
+using cuasm::GemmCfg;
+
+constexpr int kPackBN = 128;  // output block of the W13 interleave (= GemmCfg::BN)
+static_assert(GemmCfg<0, 1>::BN == kPackBN && GemmCfg<0, 2>::BN == kPackBN, "pack/GEMM block mismatch");
+
+thread_local std::string g_init_error;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+struct cuasm_ffn_s {
+    int device = 0;
+    cuasm_dtype_t dtype = CUASM_DTYPE_BF16;
+    int esize = 2;
+    int sm_count = 148;
+    std::string err;
+    // options
+    int variant = CUASM_VARIANT_AUTO;
+    int use_pdl = 1;
+    int group_m = 0;
+    // a1 workspace
+    float* r = nullptr;
+    int64_t r_cap = 0;
+    // a0 cache
+    void* w13 = nullptr;
+    int64_t w13_bytes = 0;
+    int64_t w13_rows = 0;
+    const void* key_g = nullptr;
+    const void* key_w1 = nullptr;
+    const void* key_w3 = nullptr;
+    int64_t key_K = 0, key_N = 0;
+    bool packed = false;
+    CUtensorMap tmap_w;  // over w13, box {BK, B_ROWS}; B_ROWS depends on the variant
+    int tmap_w_rows = 0;
+    // forward_host staging
+    void* x_stage = nullptr;
+    int64_t x_stage_bytes = 0;
+    void* out_stage = nullptr;
+    int64_t out_stage_bytes = 0;
+    // last launch
+    int last_variant = 0;
+    int last_kernels = 0;
+    EncodeTiledFn encode = nullptr;
+};
+
+namespace {
+
+cuasm_status_t fail(cuasm_ffn_t h, cuasm_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (h) h->err = buf; else g_init_error = buf;
+    return st;
+}
+
+cuasm_status_t cuda_fail(cuasm_ffn_t h, cudaError_t e, const char* what) {
+    return fail(h, e == cudaErrorMemoryAllocation ? CUASM_ERR_OOM : CUASM_ERR_CUDA, "%s: %s (%s)", what,
+                cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CUASM_CHECK(h, call, what)                        \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(h, e_, what); \
+    } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cuasm_status_t check_common(cuasm_ffn_t h, int64_t K, int64_t N) {
+    if (K <= 0 || N <= 0) return fail(h, CUASM_ERR_INVALID_ARG, "K and N must be positive (K=%lld N=%lld)",
+                                      (long long)K, (long long)N);
+    if (K % 8 != 0 || N % 8 != 0)
+        return fail(h, CUASM_ERR_INVALID_ARG, "K and N must be multiples of 8 (K=%lld N=%lld)", (long long)K,
+                    (long long)N);
+    if (N >= (int64_t(1) << 31) || K >= (int64_t(1) << 31))
+        return fail(h, CUASM_ERR_INVALID_ARG, "K, N must be < 2^31");
+    return CUASM_OK;
+}
+
+cuasm_status_t check_weights(cuasm_ffn_t h, const void* g, const void* w1, const void* w3) {
+    if (!g || !w1 || !w3) return fail(h, CUASM_ERR_INVALID_ARG, "NULL weight pointer");
+    if (!aligned16(g) || !aligned16(w1) || !aligned16(w3))
+        return fail(h, CUASM_ERR_INVALID_ARG, "weight pointers must be 16-byte aligned");
+    return CUASM_OK;
+}
+
+cuasm_status_t check_eps(cuasm_ffn_t h, float eps) {
+    if (!(eps >= 0.0f)) return fail(h, CUASM_ERR_INVALID_ARG, "eps must be >= 0 and not NaN");
+    return CUASM_OK;
+}
+
+cuasm_status_t set_device(cuasm_ffn_t h) {
+    int cur = -1;
+    CUASM_CHECK(h, cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != h->device) CUASM_CHECK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    return CUASM_OK;
+}
+
+cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint32_t box_inner, uint32_t box_outer) {
+    const CUtensorMapDataType dt =
+        h->dtype == CUASM_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * static_cast<uint64_t>(h->esize)};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = h->encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d, dims %llu x %llu)", (int)r,
+                    (unsigned long long)inner, (unsigned long long)outer);
+    return CUASM_OK;
+}
+
+template <typename T>
+cuasm_status_t launch_pack(cuasm_ffn_t h, const void* g, const void* w1, const void* w3, int64_t K, int64_t N,
+                           cudaStream_t s) {
+    const int64_t n_blocks = (N + kPackBN - 1) / kPackBN;
+    const int64_t rows = n_blocks * 2 * kPackBN;
+    const int64_t bytes = rows * K * h->esize;
+    if (bytes > h->w13_bytes) {
+        if (h->w13) cudaFree(h->w13);
+        h->w13 = nullptr;
+        h->w13_bytes = 0;
+        CUASM_CHECK(h, cudaMalloc(&h->w13, bytes), "cudaMalloc(W13)");
+        h->w13_bytes = bytes;
+    }
+    const int64_t total_vec = rows * (K * h->esize / 16);
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((total_vec + threads - 1) / threads, int64_t(h->sm_count) * 16);
+    cuasm::ffn_pack_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, s>>>(
+        static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(h->w13), N,
+        K, kPackBN, n_blocks);
+    CUASM_CHECK(h, cudaGetLastError(), "ffn_pack_kernel launch");
+    h->w13_rows = rows;
+    h->tmap_w_rows = 0;  // re-encode for the new buffer
+    h->key_g = g;
+    h->key_w1 = w1;
+    h->key_w3 = w3;
+    h->key_K = K;
+    h->key_N = N;
+    h->packed = true;
+    return CUASM_OK;
+}
+
+cuasm_status_t ensure_packed(cuasm_ffn_t h, const void* g, const void* w1, const void* w3, int64_t K, int64_t N,
+                             cudaStream_t s) {
+    if (h->packed && h->key_g == g && h->key_w1 == w1 && h->key_w3 == w3 && h->key_K == K && h->key_N == N)
+        return CUASM_OK;
+    h->packed = false;
+    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, g, w1, w3, K, N, s)
+                                        : launch_pack<float>(h, g, w1, w3, K, N, s);
+}
+
+template <typename T>
+cuasm_status_t launch_prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
+                              cudaStream_t s) {
+    const int64_t blocks = (M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock;
+    cuasm::ffn_rms_prepass_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(static_cast<const T*>(x), r, M, K,
+                                                                                    eps);
+    CUASM_CHECK(h, cudaGetLastError(), "ffn_rms_prepass_kernel launch");
+    return CUASM_OK;
+}
+
+cuasm_status_t prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps, cudaStream_t s) {
+    return h->dtype == CUASM_DTYPE_BF16 ? launch_prepass<__nv_bfloat16>(h, x, r, M, K, eps, s)
+                                        : launch_prepass<float>(h, x, r, M, K, eps, s);
+}
+
+template <int kKind, int kCtaGroup>
+cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, int64_t K, int64_t N,
+                           cudaStream_t s) {
+    using C = GemmCfg<kKind, kCtaGroup>;
+    CUtensorMap tmap_x;
+    cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, C::BM);
+    if (st != CUASM_OK) return st;
+    if (h->tmap_w_rows != C::B_ROWS) {
+        st = encode_2d(h, &h->tmap_w, h->w13, static_cast<uint64_t>(K), static_cast<uint64_t>(h->w13_rows), C::BK,
+                       C::B_ROWS);
+        if (st != CUASM_OK) return st;
+        h->tmap_w_rows = C::B_ROWS;
+    }
+    FfnGemmParams p;
+    p.r = h->r;
+    p.out = out;
+    p.ldo = N;
+    p.M = static_cast<int>(M);
+    p.N = static_cast<int>(N);
+    p.K = static_cast<int>(K);
+    p.num_m_blk = static_cast<int>((M + C::TILE_M - 1) / C::TILE_M);
+    p.num_n_blk = static_cast<int>((N + C::BN - 1) / C::BN);
+    p.num_k_blk = static_cast<int>((K + C::BK - 1) / C::BK);
+    p.group_m = h->group_m > 0 ? h->group_m : std::min(p.num_m_blk, 16);
+    p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
+    p.num_tiles = p.num_m_blk * p.num_n_blk;
+
+    static bool attr_set[2][3] = {};
+    if (!attr_set[kKind][kCtaGroup]) {
+        CUASM_CHECK(h,
+                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
+                    "cudaFuncSetAttribute(smem)");
+        if (kCtaGroup == 2) {
+            CUASM_CHECK(h,
+                        cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>,
+                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 0),
+                        "cudaFuncSetAttribute(cluster)");
+        }
+        attr_set[kKind][kCtaGroup] = true;
+    }
+    const int max_clusters = h->sm_count / kCtaGroup;
+    const int clusters = std::min(p.num_tiles, max_clusters);
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * kCtaGroup), 1, 1);
+    cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    if (kCtaGroup == 2) {
+        attrs[na].id = cudaLaunchAttributeClusterDimension;
+        attrs[na].val.clusterDim.x = 2;
+        attrs[na].val.clusterDim.y = 1;
+        attrs[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (h->use_pdl) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
+    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>, tmap_x, h->tmap_w, p),
+                "ffn_dual_gemm_kernel launch");
+    h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
+    return CUASM_OK;
+}
+
+int choose_variant(cuasm_ffn_t h, int64_t M, int64_t /*K*/, int64_t /*N*/) {
+    if (h->variant != CUASM_VARIANT_AUTO) return h->variant;
+    (void)M;
+    return CUASM_VARIANT_1SM;
+}
+
+cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
+    if (M > h->r_cap) {
+        if (h->r) cudaFree(h->r);
+        h->r = nullptr;
+        h->r_cap = 0;
+        const int64_t cap = std::max<int64_t>(M, 4096);
+        CUASM_CHECK(h, cudaMalloc(&h->r, cap * sizeof(float)), "cudaMalloc(r)");
+        h->r_cap = cap;
+    }
+    return CUASM_OK;
+}
+
+cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3, void* out,
+                            int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
+    cuasm_status_t st;
+    h->last_kernels = 0;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    if ((st = ensure_packed(h, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    if (M == 0) return CUASM_OK;
+    if ((st = ensure_r(h, M)) != CUASM_OK) return st;
+    if ((st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
+    const int v = choose_variant(h, M, K, N);
+    if (h->dtype == CUASM_DTYPE_BF16) {
+        st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, s) : launch_gemm<0, 1>(h, x, out, M, K, N, s);
+    } else {
+        st = v == CUASM_VARIANT_2SM ? launch_gemm<1, 2>(h, x, out, M, K, N, s) : launch_gemm<1, 1>(h, x, out, M, K, N, s);
+    }
+    if (st == CUASM_OK) h->last_kernels = 2;
+    return st;
+}
+
+cuasm_status_t validate_forward(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3,
+                                const void* out, int64_t M, int64_t K, int64_t N, float eps) {
+    cuasm_status_t st;
+    if ((st = check_common(h, K, N)) != CUASM_OK) return st;
+    if ((st = check_weights(h, g, w1, w3)) != CUASM_OK) return st;
+    if ((st = check_eps(h, eps)) != CUASM_OK) return st;
+    if (M < 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31)");
+    if (M > 0 && (!x || !out)) return fail(h, CUASM_ERR_INVALID_ARG, "NULL x or out pointer");
+    if (M > 0 && (!aligned16(x) || !aligned16(out)))
+        return fail(h, CUASM_ERR_INVALID_ARG, "x and out must be 16-byte aligned");
+    return CUASM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cuasm_ffn_abi_version(void) { return CUASM_FFN_ABI_VERSION; }
+
+cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* out, int device, cuasm_dtype_t dtype) {
+    g_init_error.clear();
+    if (!out) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle pointer");
+    *out = nullptr;
+    if (dtype != CUASM_DTYPE_BF16 && dtype != CUASM_DTYPE_FP32)
+        return fail(nullptr, CUASM_ERR_INVALID_ARG, "unknown dtype %d", (int)dtype);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, CUASM_ERR_UNSUPPORTED, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, CUASM_ERR_INVALID_ARG, "device %d out of range", device);
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return fail(nullptr, CUASM_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, CUASM_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only",
+                    device, prop.major, prop.minor);
+    cuasm_ffn_t h = new (std::nothrow) cuasm_ffn_s();
+    if (!h) return fail(nullptr, CUASM_ERR_OOM, "host allocation failed");
+    h->device = device;
+    h->dtype = dtype;
+    h->esize = dtype == CUASM_DTYPE_BF16 ? 2 : 4;
+    h->sm_count = prop.multiProcessorCount;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+        delete h;
+        return fail(nullptr, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    }
+    h->encode = reinterpret_cast<EncodeTiledFn>(fn);
+    *out = h;
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
+                                 void* out, int64_t M, int64_t K, int64_t N, float eps, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    return forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w, const void* w1,
+                                      const void* w3, void* out_host, int64_t M, int64_t K, int64_t N, float eps,
+                                      void* stream, int sync) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    cuasm_status_t st;
+    if ((st = check_common(h, K, N)) != CUASM_OK) return st;
+    if ((st = check_weights(h, rms_w, w1, w3)) != CUASM_OK) return st;
+    if ((st = check_eps(h, eps)) != CUASM_OK) return st;
+    if (M < 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31)");
+    if (M > 0 && (!x_host || !out_host)) return fail(h, CUASM_ERR_INVALID_ARG, "NULL host pointer");
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t xb = M * K * h->esize, ob = M * N * h->esize;
+    if (xb > h->x_stage_bytes) {
+        if (h->x_stage) cudaFree(h->x_stage);
+        h->x_stage = nullptr;
+        h->x_stage_bytes = 0;
+        CUASM_CHECK(h, cudaMalloc(&h->x_stage, xb), "cudaMalloc(x staging)");
+        h->x_stage_bytes = xb;
+    }
+    if (ob > h->out_stage_bytes) {
+        if (h->out_stage) cudaFree(h->out_stage);
+        h->out_stage = nullptr;
+        h->out_stage_bytes = 0;
+        CUASM_CHECK(h, cudaMalloc(&h->out_stage, ob), "cudaMalloc(out staging)");
+        h->out_stage_bytes = ob;
+    }
+    if (M > 0) CUASM_CHECK(h, cudaMemcpyAsync(h->x_stage, x_host, xb, cudaMemcpyHostToDevice, s), "H2D x");
+    st = forward_impl(h, h->x_stage, rms_w, w1, w3, h->out_stage, M, K, N, eps, s);
+    if (st != CUASM_OK) return st;
+    if (M > 0) CUASM_CHECK(h, cudaMemcpyAsync(out_host, h->out_stage, ob, cudaMemcpyDeviceToHost, s), "D2H out");
+    if (sync) CUASM_CHECK(h, cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w, const void* w1, const void* w3, int64_t K,
+                                 int64_t N, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    cuasm_status_t st;
+    if ((st = check_common(h, K, N)) != CUASM_OK) return st;
+    if ((st = check_weights(h, rms_w, w1, w3)) != CUASM_OK) return st;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    h->packed = false;
+    return ensure_packed(h, rms_w, w1, w3, K, N, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
+                                 void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (K <= 0 || K % 8 != 0) return fail(h, CUASM_ERR_INVALID_ARG, "K must be a positive multiple of 8");
+    if (M < 0) return fail(h, CUASM_ERR_INVALID_ARG, "M must be >= 0");
+    cuasm_status_t st;
+    if ((st = check_eps(h, eps)) != CUASM_OK) return st;
+    if (M == 0) return CUASM_OK;
+    if (!x || !r) return fail(h, CUASM_ERR_INVALID_ARG, "NULL pointer");
+    if (!aligned16(x) || (reinterpret_cast<uintptr_t>(r) & 3u))
+        return fail(h, CUASM_ERR_INVALID_ARG, "x must be 16-byte and r 4-byte aligned");
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    return prepass(h, x, r, M, K, eps, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst, int64_t* bytes) {
+    if (!h || !bytes) return fail(h, CUASM_ERR_INVALID_ARG, "NULL argument");
+    if (!h->packed) return fail(h, CUASM_ERR_INVALID_ARG, "no packed weights cached");
+    const int64_t b = h->w13_rows * h->key_K * h->esize;
+    *bytes = b;
+    if (!dst) return CUASM_OK;
+    cuasm_status_t st;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    CUASM_CHECK(h, cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    CUASM_CHECK(h, cudaMemcpy(dst, h->w13, b, cudaMemcpyDeviceToHost), "D2H W13");
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_invalidate_weights(cuasm_ffn_t h) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->packed = false;
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    switch (option) {
+    case CUASM_OPT_VARIANT:
+        if (value < CUASM_VARIANT_AUTO || value > CUASM_VARIANT_2SM)
+            return fail(h, CUASM_ERR_INVALID_ARG, "bad variant %lld", (long long)value);
+        h->variant = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_PDL:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "PDL option is 0 or 1");
+        h->use_pdl = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_GROUP_M:
+        if (value < 0 || value > 1 << 20) return fail(h, CUASM_ERR_INVALID_ARG, "bad group_m");
+        h->group_m = static_cast<int>(value);
+        return CUASM_OK;
+    default:
+        return fail(h, CUASM_ERR_INVALID_ARG, "unknown option %d", option);
+    }
+}
+
+cuasm_status_t cuasm_ffn_last_launch(cuasm_ffn_t h, int* variant, int* kernels) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    if (variant) *variant = h->last_variant;
+    if (kernels) *kernels = h->last_kernels;
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
+    if (!h) return CUASM_OK;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device) cudaSetDevice(h->device);
+    if (h->r) cudaFree(h->r);
+    if (h->w13) cudaFree(h->w13);
+    if (h->x_stage) cudaFree(h->x_stage);
+    if (h->out_stage) cudaFree(h->out_stage);
+    if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
+    delete h;
+    return CUASM_OK;
+}
+
+const char* cuasm_ffn_last_error(cuasm_ffn_t h) { return h ? h->err.c_str() : g_init_error.c_str(); }
+
+}  // extern "C"

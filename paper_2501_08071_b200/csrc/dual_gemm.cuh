@@ -1,0 +1,285 @@
+// dual_gemm.cuh -- steps a2 + a3 of the hot path on the 5th-gen tensor cores.
+//
+//   acc[m, 0:BN]    = sum_k x[m,k] * W1g[n0 + j, k]      (h1 / r)
+//   acc[m, BN:2BN]  = sum_k x[m,k] * W3g[n0 + j, k]      (h3 / r)
+//   out[m, n0 + j]  = RNE( h1 * sigma(h1) * h3 ),  h1 = r[m]*acc1, h3 = r[m]*acc3
+//
+// (BASELINE.json north_star: dual GEMM on tcgen05.mma with TMEM accumulators
+// fed by TMA, 1/rms scale + SiLU + product fused in the epilogue; the paper's
+// fused_ff, PAPER.md P:68 / P:560.)  One MMA of N = 2*BN over the interleaved
+// W13 block (pack.cuh) yields both halves of the gate for the same outputs.
+//
+// Kernel structure (persistent, one CTA per SM, warp-specialised):
+//   warp 0      TMA producer  (one elected lane): x tile [BM x BK] and W13
+//               tile [2BN x BK] per stage, 128-byte swizzle, mbarrier tx-count
+//   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
+//               tcgen05.mma (K=16 bf16 / K=8 tf32) per stage, tcgen05.commit
+//               frees the stage; a final commit hands the accumulator over
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//               32*(w%4)..+31 = tile rows), r-scale, SiLU, gate, bf16 pack,
+//               16-byte global stores
+// TMEM holds two 2*BN-column accumulators (512 columns) so the epilogue of
+// tile i overlaps the mainloop of tile i+1.
+//
+// kCtaGroup == 2 (2-SM variant): a cluster of two CTAs on one TPC computes a
+// 256 x 2BN tile with tcgen05.mma.cta_group::2.  Each CTA TMA-loads its own
+// 128 rows of x and HALF of the W13 block (rank 0: the W1g rows, rank 1: the
+// W3g rows), both crediting the leader's barrier; only the leader issues the
+// MMAs; commits multicast to both CTAs; each CTA's epilogue drains its own
+// 128 accumulator rows (its own TMEM).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace cuasm {
+
+struct FfnGemmParams {
+    const float* r;  // [M] inverse RMS from the pre-pass
+    void* out;       // [M, ldo] row-major, dtype of the handle
+    int64_t ldo;     // leading dimension of out, elements
+    int M, N, K;
+    int num_m_blk;   // ceil(M / tile_m)
+    int num_n_blk;   // ceil(N / BN)
+    int num_k_blk;   // ceil(K / BK)
+    int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
+    int num_tiles;
+};
+
+template <int kKind, int kCtaGroup>
+struct GemmCfg {
+    static constexpr int kEsize = kKind == 0 ? 2 : 4;
+    static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
+    static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
+    static constexpr int BN = 128;                 // outputs per tile; MMA N = 2*BN
+    static constexpr int UMMA_N = 2 * BN;
+    static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
+    static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
+    static constexpr int KSTEPS = BK / UMMA_K;     // 4
+    static constexpr int STAGES = kCtaGroup == 1 ? 4 : 6;
+    static constexpr int A_BYTES = BM * 128;                        // per CTA
+    static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // W13 rows loaded per CTA
+    static constexpr int B_BYTES = B_ROWS * 128;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
+    static constexpr int TMEM_COLS = 512;                           // 2 accumulators x UMMA_N
+    static constexpr int NUM_EPI_WARPS = 4;
+    static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 192
+    static constexpr int BAR_BYTES = 1024;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + align slack
+    static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
+};
+
+__device__ __forceinline__ void tile_coords(int t, const FfnGemmParams& p, int& mb, int& nb) {
+    const int per_group = p.group_m * p.num_n_blk;
+    const int grp = t / per_group;
+    const int first_m = grp * p.group_m;
+    const int gm = min(p.num_m_blk - first_m, p.group_m);
+    const int local = t - grp * per_group;
+    mb = first_m + local % gm;
+    nb = local / gm;
+}
+
+__device__ __forceinline__ float silu_gate(float h1, float h3) {
+    // SiLU(h1) * h3 = h1 / (1 + e^-h1) * h3; e^-h1 -> inf gives exactly -0 / +0.
+    return __fdividef(h1, 1.0f + __expf(-h1)) * h3;
+}
+
+template <int kKind, int kCtaGroup>
+__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
+    ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                         const FfnGemmParams p) {
+    using C = GemmCfg<kKind, kCtaGroup>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzle atoms
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t* full_bar = bars;                       // [STAGES]
+    uint64_t* empty_bar = bars + C::STAGES;          // [STAGES]
+    uint64_t* tfull_bar = bars + 2 * C::STAGES;      // [2]
+    uint64_t* tempty_bar = bars + 2 * C::STAGES + 2; // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+
+    const uint32_t warp = ptx::warp_id_uniform();
+    const uint32_t lane = ptx::lane_id();
+    const uint32_t cta_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;
+    const bool leader = cta_rank == 0;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_x);
+        ptx::prefetch_tmap(&tmap_w);
+        for (int s = 0; s < C::STAGES; ++s) {
+            // 2-SM: only the leader's producer arrives (expect_tx of BOTH
+            // CTAs' bytes); the peer's TMA bytes are credited to it too.
+            ptx::mbar_init(ptx::smem_u32(&full_bar[s]), 1);
+            ptx::mbar_init(ptx::smem_u32(&empty_bar[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(ptx::smem_u32(&tfull_bar[a]), 1);
+            // every epilogue warp of BOTH CTAs releases the leader's accumulator
+            ptx::mbar_init(ptx::smem_u32(&tempty_bar[a]), C::NUM_EPI_WARPS * kCtaGroup);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS, kCtaGroup>(ptx::smem_u32(tmem_slot));
+    ptx::tc_fence_before();
+    if constexpr (kCtaGroup == 2) ptx::cluster_sync(); else __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    // Cluster-level tile id: both CTAs of a pair walk the same tile sequence.
+    const int cluster_id = blockIdx.x / kCtaGroup;
+    const int num_clusters = gridDim.x / kCtaGroup;
+
+    if (warp == 0) {
+        // ========================= TMA producer =========================
+        if (lane == 0) {
+            const uint64_t pol_x = ptx::policy_evict_last();    // x is re-read by every n-block
+            const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+                int mb, nb;
+                tile_coords(t, p, mb, nb);
+                const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
+                const int row_b = nb * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
+                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                    ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
+                    const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
+                    const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
+                    const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+                    if constexpr (kCtaGroup == 1) {
+                        ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                        ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                        ptx::tma_load_2d(sb, &tmap_w, fb, kb * C::BK, row_b, pol_w);
+                    } else {
+                        // both CTAs' bytes land on the leader's barrier
+                        if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::STAGE_BYTES);
+                        ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, kb * C::BK, row_b, pol_w);
+                    }
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ========================= MMA issuer ===========================
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                ptx::mbar_wait(ptx::smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * C::UMMA_N;
+                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                    ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
+                    ptx::tc_fence_after();
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + stage * C::A_BYTES));
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + stage * C::B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < C::KSTEPS; ++k) {
+                        // advance 32 bytes of K inside the 128-byte swizzle row (+2 in 16-byte units)
+                        ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
+                                                   (kb | k) != 0 ? 1u : 0u);
+                    }
+                    if constexpr (kCtaGroup == 1) {
+                        ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
+                    } else {
+                        ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), 0x3);
+                    }
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+                if constexpr (kCtaGroup == 1) {
+                    ptx::mma_commit(ptx::smem_u32(&tfull_bar[acc]));
+                } else {
+                    ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
+                }
+            }
+        }
+    } else {
+        // ========================= epilogue =============================
+        ptx::pdl_wait();  // r[] is produced by the pre-pass kernel (PDL primary)
+        const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const uint32_t row_in_cta = quad * 32 + lane;
+        int it = 0;
+        for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+            int mb, nb;
+            tile_coords(t, p, mb, nb);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM + static_cast<int>(row_in_cta);
+            const bool row_ok = row < p.M;
+            const float rr = row_ok ? __ldg(p.r + row) : 0.f;
+            ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
+#pragma unroll 1
+            for (int c = 0; c < C::BN / 32; ++c) {
+                uint32_t v1[32], v3[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c * 32, v1);
+                ptx::tmem_ld_32x32b_x32(t_row + C::BN + c * 32, v3);
+                ptx::tmem_ld_wait();
+                const int col0 = nb * C::BN + c * 32;
+                if (row_ok) {
+                    if constexpr (kKind == 0) {
+                        uint32_t packed[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float a0 = silu_gate(rr * __uint_as_float(v1[2 * i]), rr * __uint_as_float(v3[2 * i]));
+                            const float a1 =
+                                silu_gate(rr * __uint_as_float(v1[2 * i + 1]), rr * __uint_as_float(v3[2 * i + 1]));
+                            packed[i] = ptx::pack_bf16x2(a0, a1);
+                        }
+                        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (col0 + 8 * q < p.N) {
+                                *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
+                                    make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                            }
+                        }
+                    } else {
+                        float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (col0 + 4 * q < p.N) {
+                                float4 o;
+                                o.x = silu_gate(rr * __uint_as_float(v1[4 * q + 0]), rr * __uint_as_float(v3[4 * q + 0]));
+                                o.y = silu_gate(rr * __uint_as_float(v1[4 * q + 1]), rr * __uint_as_float(v3[4 * q + 1]));
+                                o.z = silu_gate(rr * __uint_as_float(v1[4 * q + 2]), rr * __uint_as_float(v3[4 * q + 2]));
+                                o.w = silu_gate(rr * __uint_as_float(v1[4 * q + 3]), rr * __uint_as_float(v3[4 * q + 3]));
+                                *reinterpret_cast<float4*>(orow + col0 + 4 * q) = o;
+                            }
+                        }
+                    }
+                }
+            }
+            // accumulator drained: hand it back to the MMA issuer (leader CTA)
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (kCtaGroup == 1) {
+                    ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
+                } else {
+                    ptx::mbar_arrive_cluster(ptx::smem_u32(&tempty_bar[acc]), 0);
+                }
+            }
+        }
+    }
+
+    // ----------------------------------------------------------- teardown --
+    ptx::tc_fence_before();
+    if constexpr (kCtaGroup == 2) ptx::cluster_sync(); else __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::TMEM_COLS, kCtaGroup>(tmem_base);
+    }
+}
+
+}  // namespace cuasm

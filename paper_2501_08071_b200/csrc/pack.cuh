@@ -1,0 +1,81 @@
+// pack.cuh -- step a0 (once per weight set): fold the RMSNorm gain into the
+// weights and interleave W1/W3 by output block,
+//
+//   W13[nb][j][rr][k] = RNE( W_j[nb*BN + rr][k] * g[k] ),  j in {1,3}
+//   (rows with nb*BN + rr >= N are zero: the padded tail block)
+//
+// so that ONE tcgen05.mma with N = 2*BN produces h1 and h3 for the same BN
+// outputs side by side in TMEM (BASELINE.json north_star: "the RMSNorm gain g
+// is folded into W1/W3"; R4 on the fold's rounding).  bf16 weights:
+// the product of two bf16 values is exact in fp32, then one RNE to bf16.
+// fp32 weights (tf32 MMA): fp32 product (RNE) then RNE to tf32 so the tensor
+// core consumes the rounded value exactly.
+//
+// Elementwise and HBM-bound: reads 2*N*K*esize + K*esize, writes
+// 2*Npad*K*esize.  16-byte vectors, grid-stride.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace cuasm {
+
+__device__ __forceinline__ uint32_t fold_bf16x2(uint32_t w, uint32_t g) {
+    const float w0 = __uint_as_float(w << 16), w1 = __uint_as_float(w & 0xFFFF0000u);
+    const float g0 = __uint_as_float(g << 16), g1 = __uint_as_float(g & 0xFFFF0000u);
+    const float p0 = w0 * g0, p1 = w1 * g1;  // exact: 8-bit x 8-bit significands
+    uint32_t out;
+    asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(out) : "f"(p0), "f"(p1));
+    return out;
+}
+
+__device__ __forceinline__ uint32_t rne_tf32_bits(uint32_t u) {
+    if ((u & 0x7f800000u) == 0x7f800000u) return (u & 0x007fffffu) ? (u | 0x00400000u) & 0xFFFFE000u : u;
+    const uint32_t lsb = (u >> 13) & 1u;
+    return (u + 0xFFFu + lsb) & 0xFFFFE000u;
+}
+
+__device__ __forceinline__ uint32_t fold_tf32(uint32_t w, uint32_t g) {
+    const float p = __fmul_rn(__uint_as_float(w), __uint_as_float(g));
+    return rne_tf32_bits(__float_as_uint(p));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1, const T* __restrict__ w3,
+                                                       const T* __restrict__ g, T* __restrict__ w13, int64_t N,
+                                                       int64_t K, int BN, int64_t n_blocks) {
+    constexpr int kVec = 16 / sizeof(T);
+    const int64_t kvec = K / kVec;
+    const int64_t rows = n_blocks * 2 * BN;
+    const int64_t total = rows * kvec;
+    const uint4* g4 = reinterpret_cast<const uint4*>(g);
+    uint4* dst = reinterpret_cast<uint4*>(w13);
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t R = idx / kvec;
+        const int64_t kv = idx - R * kvec;
+        const int64_t nb = R / (2 * BN);
+        const int64_t within = R - nb * 2 * BN;
+        const int j = within >= BN ? 1 : 0;
+        const int64_t n = nb * BN + (within - j * BN);
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (n < N) {
+            const T* src = (j == 0 ? w1 : w3) + n * K;
+            const uint4 w = reinterpret_cast<const uint4*>(src)[kv];
+            const uint4 gg = g4[kv];
+            if constexpr (sizeof(T) == 2) {
+                o.x = fold_bf16x2(w.x, gg.x);
+                o.y = fold_bf16x2(w.y, gg.y);
+                o.z = fold_bf16x2(w.z, gg.z);
+                o.w = fold_bf16x2(w.w, gg.w);
+            } else {
+                o.x = fold_tf32(w.x, gg.x);
+                o.y = fold_tf32(w.y, gg.y);
+                o.z = fold_tf32(w.z, gg.z);
+                o.w = fold_tf32(w.w, gg.w);
+            }
+        }
+        dst[idx] = o;
+    }
+}
+
+}  // namespace cuasm

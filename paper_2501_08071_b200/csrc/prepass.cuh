@@ -1,0 +1,79 @@
+// prepass.cuh -- step a1 of the hot path: per-row inverse RMS,
+//     r[m] = 1 / sqrt( (sum_k x[m,k]^2) / K + eps )
+// (BASELINE.json north_star "row-wise sum-of-squares pre-pass (vectorised
+// 128-bit loads, warp-shuffle reductions)"; RMSNorm per PAPER.md P:68, its
+// memory-bound character P:549/P:573; readings R2, R3).
+//
+// HBM-bound: reads M*K*esize bytes once, writes 4*M bytes.  One warp per row,
+// 16-byte ld.global.nc loads, 4 independent loads in flight per lane, fp32
+// accumulation, xor-shuffle tree.  Triggers PDL at entry so the dependent
+// dual-GEMM kernel's prologue and mainloop overlap this kernel (the GEMM only
+// needs r in its epilogue).
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace cuasm {
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ float sumsq_vec(uint4 v, __nv_bfloat16) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float lo = __uint_as_float(w[i] << 16);
+        const float hi = __uint_as_float(w[i] & 0xFFFF0000u);
+        s = fmaf(lo, lo, s);
+        s = fmaf(hi, hi, s);
+    }
+    return s;
+}
+
+__device__ __forceinline__ float sumsq_vec(uint4 v, float) {
+    const float a = __uint_as_float(v.x), b = __uint_as_float(v.y), c = __uint_as_float(v.z),
+                d = __uint_as_float(v.w);
+    return fmaf(a, a, fmaf(b, b, fmaf(c, c, d * d)));
+}
+
+constexpr int kPrepassRowsPerBlock = 8;  // one warp per row, 256 threads
+
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restrict__ x, float* __restrict__ r,
+                                                              int64_t M, int64_t K, float eps) {
+    ptx::pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kPrepassRowsPerBlock + warp;
+    if (row >= M) return;
+    constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte load
+    const int64_t nvec = K / kVec;        // K % 8 == 0 is an API precondition
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * K);
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+    int64_t i = lane;
+    for (; i + 96 < nvec; i += 128) {
+        const uint4 v0 = ld_nc_v4(xr + i);
+        const uint4 v1 = ld_nc_v4(xr + i + 32);
+        const uint4 v2 = ld_nc_v4(xr + i + 64);
+        const uint4 v3 = ld_nc_v4(xr + i + 96);
+        acc0 += sumsq_vec(v0, T{});
+        acc1 += sumsq_vec(v1, T{});
+        acc2 += sumsq_vec(v2, T{});
+        acc3 += sumsq_vec(v3, T{});
+    }
+    for (; i < nvec; i += 32) acc0 += sumsq_vec(ld_nc_v4(xr + i), T{});
+    float s = (acc0 + acc1) + (acc2 + acc3);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) r[row] = 1.0f / sqrtf(s / static_cast<float>(K) + eps);
+}
+
+}  // namespace cuasm

@@ -21,13 +21,14 @@ done <<'MUTS'
 s|r = 1.0 / sqrt(ss / (double)K + eps);|r = 1.0 / (sqrt(ss / (double)K) + eps);|
 s|double r = 1.0 / sqrt(ss / (double)K + eps);|double r = 1.0 / sqrt(ss / (double)(K-1) + eps);|
 s|double r = 1.0 / sqrt(ss / (double)K + eps);|double r = 1.0 / sqrt(ss + eps);|
-s|xn\[k\] = (mode == ORACLE_PLAIN) ? v \* r \* G\[k\] : v;|xn[k] = (mode == ORACLE_PLAIN) ? v * r : v;|
-s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = h3 / (1.0 + exp(-h3)) * h1;|
-s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = h1 / (1.0 + exp(h1)) * h3;|
-s|out\[i \* N + n\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n] = 1.0 / (1.0 + exp(-h1)) * h3;|
-s|const double\* a = W1 + n \* K;|const double* a = W1 + (n % 2) * K;|
+s|XN\[i \* K + k\] = (mode == ORACLE_PLAIN) ? v \* r \* G\[k\] : v;|XN[i * K + k] = (mode == ORACLE_PLAIN) ? v * r : v;|
+s|out\[i \* N + n0 + j\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n0 + j] = h3 / (1.0 + exp(-h3)) * h1;|
+s|out\[i \* N + n0 + j\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n0 + j] = h1 / (1.0 + exp(h1)) * h3;|
+s|out\[i \* N + n0 + j\] = h1 / (1.0 + exp(-h1)) \* h3;|out[i * N + n0 + j] = 1.0 / (1.0 + exp(-h1)) * h3;|
+s|const double\* a = W1 + j \* K;|const double* a = W1 + (j % 2) * K;|
 s|a = oracle_round_bf16(a \* G\[k\]);|a = a * G[k];|
 s|uint32_t bias = (1u << (drop - 1)) - 1u + lsb;|uint32_t bias = (1u << (drop - 1));|
-s|if (mode != ORACLE_PLAIN) { h1 \*= r; h3 \*= r; }|if (mode != ORACLE_PLAIN) { h1 *= r; }|
+s|if (mode != ORACLE_PLAIN) { h1 \*= R\[i\]; h3 \*= R\[i\]; }|if (mode != ORACLE_PLAIN) { h1 *= R[i]; }|
+s|dst_bits\[n \* K + k\] = oracle_round_bf16_bits(bf16_bits_to_double(w\[n \* K + k\]) \*|dst_bits[n * K + k] = oracle_round_bf16_bits(bf16_bits_to_double(w[n * K + k]) + 0 *|
 MUTS
 exit $status

@@ -249,3 +249,19 @@ def test_tiny_config_runs_fast():
     t0 = time.perf_counter()
     oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], eps=1e-6)
     assert time.perf_counter() - t0 < 1.0
+
+
+def test_fold_bf16_matches_torch_bitwise():
+    d = make_inputs(1, 200, 48, family="C", seed=16, dtype="bf16")
+    got = oracle.fold(d["w1"], d["g"])
+    ref = (d["w1"].float() * d["g"].float()).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, ref)
+
+
+def test_fold_tf32_reference():
+    d = make_inputs(1, 64, 16, family="C", seed=17, dtype="fp32")
+    got = oracle.fold(d["w1"], d["g"])
+    prod = (d["w1"].double() * d["g"].double()).float().double().numpy()
+    ref = np.vectorize(lambda v: 0.0 if v == 0 else math.ldexp(round(math.frexp(v)[0] * 2 ** 11) / 2 ** 11,
+                                                               math.frexp(v)[1]))(prod)
+    assert np.array_equal(got.astype(np.float64), ref)

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Acceptance (BASELINE.json north_star): per element
+    |gpu - oracle| <= 2e-2*|oracle| + 1e-3,   NaN fails.
+Reference mode per input family (R4): exact-fold families A/B/T are
+compared with the plain definition; full-entropy family C with the
+fold-aware oracle (g folded into the weights in bf16 first).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2501_08071_b200 as ffn
+from ffn_inputs import CONFIGS, make_inputs, seed_for
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-2, 1e-3
+TORCH_DT = {"bf16": torch.bfloat16, "fp32": torch.float32}
+
+
+def run_gpu(d, eps, dtype, variant=ffn.VARIANT_AUTO, handle=None):
+    dev = torch.device("cuda:0")
+    h = handle or ffn.FusedFFN(dev, TORCH_DT[dtype])
+    h.set_variant(variant)
+    t = {k: v.to(dev) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], eps)
+    torch.cuda.synchronize()
+    return out, h
+
+
+def check(gpu, ref, what):
+    worst, nbad, maxerr = oracle.tolerance_ratio(gpu.double().cpu().numpy(), ref, RTOL, ATOL)
+    assert nbad == 0, f"{what}: {nbad} elements out of tolerance (worst ratio {worst:.3f}, max|err| {maxerr:.3g})"
+    return worst
+
+
+def ref_mode(family, dtype):
+    if family == "C":
+        return "fold_bf16" if dtype == "bf16" else "fold_tf32"
+    return "plain"
+
+
+# ------------------------------------------------------------------ a1 ------
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,K", [(1, 8), (7, 64), (300, 4096), (16, 8192), (33, 1000)])
+def test_prepass_matches_oracle(cuda_device, dtype, M, K):
+    d = make_inputs(M, K, 8, family="C", seed=100 + M, dtype=dtype)
+    h = ffn.FusedFFN(cuda_device, TORCH_DT[dtype])
+    r = h.rms_inv(d["x"].to(cuda_device), 1e-6).cpu().double().numpy()
+    ref = oracle.rms_inv(d["x"], 1e-6)
+    np.testing.assert_allclose(r, ref, rtol=2e-6)
+
+
+# ------------------------------------------------------------------ a0 ------
+@pytest.mark.parametrize("N,K", [(128, 64), (520, 200), (1376, 256)])
+def test_pack_is_bitwise_the_oracle_fold(cuda_device, N, K):
+    d = make_inputs(1, K, N, family="C", seed=200 + N, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h.prepare(t["g"], t["w1"], t["w3"])
+    torch.cuda.synchronize()
+    packed = h.packed_weights().view(torch.int16).numpy().view(np.uint16)
+    nblk = (N + 127) // 128
+    packed = packed.reshape(nblk, 2, 128, K)
+    f1 = oracle.fold(d["w1"], d["g"])
+    f3 = oracle.fold(d["w3"], d["g"])
+    for j, f in ((0, f1), (1, f3)):
+        got = packed[:, j].reshape(nblk * 128, K)
+        assert np.array_equal(got[:N], f)
+        assert np.all(got[N:] == 0)
+
+
+def test_pack_fp32_is_the_oracle_tf32_fold(cuda_device):
+    N, K = 136, 64
+    d = make_inputs(1, K, N, family="C", seed=300, dtype="fp32")
+    h = ffn.FusedFFN(cuda_device, torch.float32)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h.prepare(t["g"], t["w1"], t["w3"])
+    torch.cuda.synchronize()
+    packed = h.packed_weights().numpy().reshape(2, 2, 128, K)
+    got1 = packed[:, 0].reshape(256, K)[:N]
+    assert np.array_equal(got1, oracle.fold(d["w1"], d["g"]))
+
+
+# --------------------------------------------------------- whole path -------
+SMALL_SHAPES = [
+    # (M, K, N): single tile; M/N/K tails; several tiles in every dimension
+    (1, 64, 128),
+    (16, 64, 128),
+    (128, 128, 256),
+    (300, 512, 520),
+    (129, 200, 136),
+    (257, 1024, 1000),
+    (640, 320, 1408),
+]
+
+
+@pytest.mark.parametrize("variant", [ffn.VARIANT_1SM, ffn.VARIANT_2SM])
+@pytest.mark.parametrize("family", ["A", "B", "C", "L"])
+@pytest.mark.parametrize("M,K,N", SMALL_SHAPES)
+def test_parity_small_bf16(cuda_device, M, K, N, family, variant):
+    d = make_inputs(M, K, N, family=family, seed=1000 + M + K + N, dtype="bf16")
+    out, _ = run_gpu(d, 1e-6, "bf16", variant)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode=ref_mode(family, "bf16"))
+    check(out, ref, f"{family} {M}x{K}x{N} v{variant}")
+
+
+@pytest.mark.parametrize("variant", [ffn.VARIANT_1SM, ffn.VARIANT_2SM])
+@pytest.mark.parametrize("M,K,N", [(16, 64, 128), (5, 64, 136), (200, 256, 264)])
+def test_parity_small_fp32(cuda_device, M, K, N, variant):
+    d = make_inputs(M, K, N, family="T", seed=2000 + M, dtype="fp32")
+    out, _ = run_gpu(d, 1e-6, "fp32", variant)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="plain")
+    check(out, ref, f"T {M}x{K}x{N}")
+
+
+def test_tiny_config_fp32(cuda_device):
+    """BASELINE.json configs[0]: M=16 K=64 N=128 fp32 eps=1e-6, full oracle."""
+    c = CONFIGS["tiny"]
+    for run in range(5):
+        d = make_inputs(c["M"], c["K"], c["N"], family="T", seed=seed_for(c["idx"], run), dtype="fp32")
+        out, _ = run_gpu(d, c["eps"], "fp32")
+        ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], c["eps"])
+        check(out, ref, f"tiny run {run}")
+
+
+def _sample_rows(M, n, seed):
+    rng = np.random.default_rng(seed)
+    rows = set([0, M - 1]) | set(rng.choice(M, size=min(n, M), replace=False).tolist())
+    # rows in the last (ragged or full) 128-row tile
+    rows |= set(range(max(0, M - 3), M))
+    return sorted(rows)
+
+
+@pytest.mark.parametrize("name,family", [("llama7b_prefill", "B"), ("llama7b_prefill", "C"),
+                                         ("llama7b_decode", "A"), ("llama7b_decode", "C")])
+def test_full_size_7b(cuda_device, name, family):
+    c = CONFIGS[name]
+    d = make_inputs(c["M"], c["K"], c["N"], family=family, seed=seed_for(c["idx"]), dtype="bf16")
+    out, _ = run_gpu(d, c["eps"], "bf16")
+    rows = _sample_rows(c["M"], 24, 7) if c["M"] > 64 else list(range(c["M"]))
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], c["eps"], mode=ref_mode(family, "bf16"), rows=rows)
+    check(out[rows], ref, name)
+    assert torch.isfinite(out).all()
+
+
+def test_full_size_70b_shard(cuda_device):
+    """70B FFN, rank 0 of an 8-way N-shard (N_l = 3584) at full M, K."""
+    c = CONFIGS["llama70b"]
+    P = 8
+    N_l = c["N"] // P
+    d = make_inputs(c["M"], c["K"], N_l, family="B", seed=seed_for(c["idx"]), dtype="bf16")
+    out, _ = run_gpu(d, c["eps"], "bf16")
+    rows = _sample_rows(c["M"], 6, 8)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], c["eps"], rows=rows)
+    check(out[rows], ref, "70b shard")
+
+
+# ---------------------------------------------------------- invariants ------
+def test_invariants_bitwise(cuda_device):
+    M, K, N = 384, 512, 640
+    d = make_inputs(M, K, N, family="C", seed=3000, dtype="bf16")
+    base, h = run_gpu(d, 0.0, "bf16")
+    again, _ = run_gpu(d, 0.0, "bf16", handle=h)
+    assert torch.equal(base, again), "run-to-run determinism"
+    perm = torch.randperm(M, generator=torch.Generator().manual_seed(0))
+    dp = dict(d, x=d["x"][perm].contiguous())
+    outp, _ = run_gpu(dp, 0.0, "bf16", handle=h)
+    assert torch.equal(outp, base[perm.to(base.device)]), "row permutation equivariance"
+    d2 = dict(d, x=(d["x"].float() * 4.0).to(torch.bfloat16))
+    out2, _ = run_gpu(d2, 0.0, "bf16", handle=h)
+    assert torch.equal(out2, base), "x -> 4x at eps=0 leaves out unchanged"
+    d3 = dict(d, w3=(d["w3"].float() * 2.0).to(torch.bfloat16))
+    out3, _ = run_gpu(d3, 0.0, "bf16", handle=h)
+    assert torch.equal(out3.float(), base.float() * 2.0), "W3 -> 2 W3 doubles out exactly"
+
+
+def test_n_shard_equals_columns(cuda_device):
+    M, K, N = 256, 256, 1024
+    d = make_inputs(M, K, N, family="C", seed=3100, dtype="bf16")
+    full, h = run_gpu(d, 1e-6, "bf16")
+    for n0, n1 in ((0, 512), (512, 1024), (256, 392)):
+        ds = dict(d, w1=d["w1"][n0:n1].contiguous(), w3=d["w3"][n0:n1].contiguous())
+        part, _ = run_gpu(ds, 1e-6, "bf16", handle=h)
+        assert torch.equal(part, full[:, n0:n1]), (n0, n1)
+
+
+def test_variants_agree(cuda_device):
+    M, K, N = 512, 1024, 768
+    d = make_inputs(M, K, N, family="C", seed=3200, dtype="bf16")
+    a, h = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_1SM)
+    b, _ = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_2SM, handle=h)
+    assert torch.equal(a, b)
+
+
+def test_edge_cases(cuda_device):
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    K, N = 64, 128
+    d = {k: v.to(cuda_device) for k, v in make_inputs(4, K, N, family="C", seed=3300, dtype="bf16").items()}
+    # M == 0: OK, nothing launched
+    out = h.forward(d["x"][:0], d["g"], d["w1"], d["w3"])
+    assert out.shape == (0, N)
+    assert h.last_launch()[1] == 0
+    # zero row with eps > 0 -> exactly 0
+    x = d["x"].clone()
+    x[1] = 0
+    out = h.forward(x, d["g"], d["w1"], d["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.all(out[1] == 0)
+    # zero W1 -> SiLU(0) = 0 everywhere
+    out = h.forward(d["x"], d["g"], torch.zeros_like(d["w1"]), d["w3"])
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)
+
+
+def test_contract_errors_do_not_launch(cuda_device):
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    K, N = 64, 128
+    d = {k: v.to(cuda_device) for k, v in make_inputs(4, K, N, family="C", seed=3400, dtype="bf16").items()}
+    out = torch.full((4, N), 7.0, dtype=torch.bfloat16, device=cuda_device)
+    lib = h.lib
+    p = lambda t: t.data_ptr()
+    s = torch.cuda.current_stream().cuda_stream
+    cases = [
+        (p(d["x"]), p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, 60, N, 1e-6),   # K % 8
+        (p(d["x"]), p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, K, 100, 1e-6),  # N % 8
+        (p(d["x"]), p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), -1, K, N, 1e-6),   # M < 0
+        (p(d["x"]), p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, K, N, -1.0),    # eps < 0
+        (p(d["x"]), p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, K, N, float("nan")),
+        (p(d["x"]) + 2, p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, K, N, 1e-6),  # misaligned
+        (0, p(d["g"]), p(d["w1"]), p(d["w3"]), p(out), 4, K, N, 1e-6),             # NULL
+    ]
+    for c in cases:
+        st = lib.cuasm_ffn_forward(h._h, *c, s)
+        assert st == ffn.ERR_INVALID_ARG, c
+        assert lib.cuasm_ffn_last_error(h._h)
+    torch.cuda.synchronize()
+    assert torch.all(out == 7.0)
+
+
+def test_forward_host_matches_device_path(cuda_device):
+    M, K, N = 200, 256, 384
+    d = make_inputs(M, K, N, family="C", seed=3500, dtype="bf16")
+    dev, h = run_gpu(d, 1e-6, "bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    host = h.forward_host(d["x"].pin_memory(), t["g"], t["w1"], t["w3"], 1e-6)
+    assert torch.equal(host, dev.cpu())
