@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""Benchmark of the fused RMSNorm+SwiGLU FFN hot path (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl cuasm|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A step is one pass of the whole hot path -- the row sum-of-squares pre-pass
+(a1) and the fused dual-GEMM + SiLU-gate kernel (a2+a3) -- over one batch of
+M tokens, through the C ABI (cuasm_ffn_forward).  The one-time weight fold
+(a0, the paper's offline/deploy split) runs before the
+timed region and is reported separately as `prep_ms`.
+
+Default workload: LLaMA-7B prefill FFN, M=2048 K=4096 N=11008 bf16
+(BASELINE.json configs[1]).  With N>1 ranks, W1/W3 are column-sharded
+(Megatron, N/P rows each, x replicated; no data-path collective unless
+--gather), so the total problem is fixed: "scaling": "strong".
+
+Timing: W warm-up steps, then exactly K steps between barrier+synchronize
+brackets; each step has its own CUDA-event pair on the launching stream and a
+256 MiB L2 flush (memset) before it, outside the event pair; value = total
+FLOPs of the K steps / max-over-ranks summed device time.  FLOPs = 4*M*K*N
+(the two GEMMs; pre-pass and epilogue excluded).
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 oracle
+(oracle/, the test-only CPU reference) on bounded row samples of the same
+workload instead; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+_ROOT = os.path.dirname(os.path.abspath(__file__))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+
+import torch
+import torch.distributed as dist
+
+METRIC = "fused RMSNorm+SwiGLU FFN TFLOP/s"
+UNIT = "TFLOP/s"
+FLUSH_BYTES = 256 << 20  # > 2x the 126 MB L2
+
+WORKLOADS = {
+    # name: (M, K, N, BASELINE.json configs index)
+    "llama7b_prefill": (2048, 4096, 11008, 1),
+    "llama7b_decode": (16, 4096, 11008, 2),
+    "llama70b": (4096, 8192, 28672, 3),
+}
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["cuasm", "reference"], default="cuasm")
+    ap.add_argument("--workload", default="llama7b_prefill",
+                    help="llama7b_prefill | llama7b_decode | llama70b | sweep:M (K=4096, N=11008)")
+    ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 one-SM, 2 two-SM (CTA pair)")
+    ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0, help="oracle CPU time budget (cpu_baseline)")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0, help="whole --impl reference run budget")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=None)
+    return ap.parse_args(argv)
+
+
+def workload_shape(name: str):
+    if name.startswith("sweep:"):
+        return int(name.split(":")[1]), 4096, 11008, 4
+    if name not in WORKLOADS:
+        raise SystemExit(f"unknown workload {name!r}")
+    return WORKLOADS[name]
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(v: float) -> float:
+    """Max of a float over all ranks (identity without a process group)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return v
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float) -> float:
+    if not (dist.is_available() and dist.is_initialized()):
+        return v
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier():
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and clock-event (throttle) reasons via NVML in a thread."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            props = torch.cuda.get_device_properties(device_index)
+            h = None
+            try:
+                bus = "%08x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.h = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = repr(e)
+
+    def _reasons(self):
+        try:
+            return self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            return self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                self.samples.append((sm, self._reasons()))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mask = 0
+        for _, r in self.samples:
+            mask |= r
+        names = [n for b, n in self.REASONS.items() if mask & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def load_peaks():
+    path = os.path.join(_ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return {"bf16_tflops": float(p["bf16_tflops"]), "bf16_tflops_sustained": float(p["bf16_tflops_sustained"]),
+                "hbm_gbs": float(p["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_traffic(workload: str):
+    """dram bytes per launch of the dual-GEMM kernel from a committed ncu --set full capture."""
+    path = os.path.join(_ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ cpu baseline
+def oracle_sample_time(inputs_cpu, eps, budget_s, rows_hint=None):
+    """Time the fp64 oracle on a bounded sample of rows of the same workload.
+
+    Returns (flops, seconds, rows, threads)."""
+    import oracle
+    x, g, w1, w3 = inputs_cpu["x"], inputs_cpu["g"], inputs_cpu["w1"], inputs_cpu["w3"]
+    M, K = x.shape
+    N = w1.shape[0]
+    threads = oracle.num_threads()
+    if rows_hint is None:
+        t0 = time.perf_counter()
+        oracle.ffn(x, g, w1, w3, eps, mode="fold_bf16", rows=[0])
+        t1 = time.perf_counter() - t0
+        rows_hint = max(1, min(M, int(budget_s / max(t1, 1e-4))))
+    rows = sorted(set((torch.arange(rows_hint) * max(1, M // rows_hint)).clamp(max=M - 1).tolist()))
+    t0 = time.perf_counter()
+    oracle.ffn(x, g, w1, w3, eps, mode="fold_bf16", rows=rows)
+    dt = time.perf_counter() - t0
+    return 4.0 * len(rows) * K * N, dt, len(rows), threads
+
+
+# ------------------------------------------------------------------- cuasm arm
+def run_cuasm(args):
+    import paper_2501_08071_b200 as ffn
+    from ffn_inputs import make_device_inputs, seed_for
+    from paper_2501_08071_b200.tp import shard_bounds
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    M, K, N, cidx = workload_shape(args.workload)
+    n0, n1 = shard_bounds(N, rank, world)
+    N_l = n1 - n0
+    seed = args.seed if args.seed is not None else seed_for(cidx)
+    t = make_device_inputs(M, K, N_l, seed, dev, w_seed=seed + 1 + rank)
+    out = torch.empty((M, N_l), dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    eps = 1e-6
+
+    h = ffn.FusedFFN(dev, torch.bfloat16)
+    h.set_variant(args.variant)
+    if args.no_pdl:
+        h.set_option(ffn.OPT_PDL, 0)
+    stream = torch.cuda.current_stream(dev)
+
+    # a0: one-time weight fold/pack (reported, not part of a step)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h.prepare(t["g"], t["w1"], t["w3"])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    prep_ms = e0.elapsed_time(e1)
+
+    full_out = None
+
+    def step():
+        h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+        if args.gather:
+            from paper_2501_08071_b200.tp import gather_shards
+            return gather_shards(out, N)
+        return None
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------------------------------------------------- timed region
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches = 0
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize(dev)
+    wall0 = time.perf_counter()
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            full_out = step()
+            ends[i].record(stream)
+            launches += h.last_launch()[1]
+        torch.cuda.synchronize(dev)
+        barrier()
+    wall = time.perf_counter() - wall0
+    local_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t_ms = max_over_ranks(local_ms)
+    total_flops = 4.0 * M * K * N * args.steps
+    value = total_flops / (t_ms / 1e3) / 1e12
+    variant_used = h.last_launch()[0]
+    launches_total = int(sum_over_ranks(float(launches)))
+
+    # ------------------------------------------- roofline of the dual-GEMM kernel
+    peaks = load_peaks()
+    prof_steps = min(args.steps, 50)
+    h.set_option(ffn.OPT_PROFILE, 1)
+    h.profile_read()
+    for _ in range(prof_steps):
+        flush.zero_()
+        h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+    pre_ms, gemm_ms, nfw = h.profile_read()
+    h.set_option(ffn.OPT_PROFILE, 0)
+    gemm_avg_ms = gemm_ms / max(nfw, 1)
+    pre_avg_ms = pre_ms / max(nfw, 1)
+    gemm_flops = 4.0 * M * K * N_l
+    achieved = gemm_flops / (gemm_avg_ms / 1e3) / 1e12
+    bound = "tensor"
+    peak = peaks["bf16_tflops"]
+    roof_unit = "TFLOP/s"
+    # decode-like shapes are HBM bound: algorithmic bytes of the GEMM kernel
+    gemm_bytes = 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M
+    if 4.0 * M * K * N_l / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
+        bound, peak, roof_unit = "hbm", peaks["hbm_gbs"], "GB/s"
+        achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
+    traffic = load_traffic(args.workload if world == 1 else f"{args.workload}@tp{world}")
+    roofline = {
+        "kernel": "ffn_dual_gemm_kernel", "bound": bound, "achieved": round(achieved, 2), "peak": peak,
+        "unit": roof_unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+        "peak_source": peaks["source"], "gemm_ms_per_launch": round(gemm_avg_ms, 5),
+        "prepass_ms_per_launch": round(pre_avg_ms, 5),
+        "prepass_GBps": round((2.0 * M * K + 4.0 * M) / (pre_avg_ms / 1e3) / 1e9, 1) if pre_avg_ms > 0 else None,
+        "gemm_share_of_step": round(gemm_avg_ms / (gemm_avg_ms + pre_avg_ms), 4),
+        "flops_per_launch": gemm_flops, "bytes_per_launch": gemm_bytes,
+    }
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.skip_e2e:
+        x_host = t["x"].cpu().pin_memory()
+        out_host = torch.empty((M, N_l), dtype=torch.bfloat16, pin_memory=True)
+        ne = min(args.steps, 20)
+        for _ in range(2):
+            h.forward_host(x_host, t["g"], t["w1"], t["w3"], eps, out_host, sync=True)
+        es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ne)]
+        barrier()
+        torch.cuda.synchronize(dev)
+        for a, b in es:
+            a.record(stream)
+            h.forward_host(x_host, t["g"], t["w1"], t["w3"], eps, out_host, sync=False)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in es))
+        e2e = {"value": round(4.0 * M * K * N * ne / (e_ms / 1e3) / 1e12, 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(float(M * K * 2))),
+               "d2h_bytes_per_step": int(sum_over_ranks(float(M * N_l * 2))),
+               "ms_per_step": round(e_ms / ne, 4), "steps": ne,
+               "api": "cuasm_ffn_forward_host (pinned host x -> H2D, forward, D2H out)"}
+
+    # ------------------------------------------------------ cpu baseline (oracle)
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+        cpu_in = {k: v.cpu() for k, v in t.items()}
+        fl, sec, rows, thr = oracle_sample_time(cpu_in, eps, args.cpu_budget_s)
+        cpu_baseline = {"value": round(fl / sec / 1e12, 6), "unit": UNIT, "cores": thr, "kind": "oracle",
+                        "sample": f"{rows} of {M} rows x all {N_l} columns, K={K}, fp64 fold-aware oracle "
+                                  f"(oracle/ffn_oracle.c), {sec:.2f} s"}
+
+    clocks = sampler.summary()
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded randn x~N(0,1), W~N(0,1/K), g~U(0.5,1.5); bf16)",
+            "config": {
+                "workload": args.workload, "M": M, "K": K, "N": N, "N_per_rank": N_l, "eps": eps,
+                "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else "single GPU",
+                "gather": bool(args.gather), "variant": {1: "1sm", 2: "2sm"}.get(variant_used, str(variant_used)),
+                "pdl": not args.no_pdl,
+                "l2": "flushed before every step (256 MiB memset outside the per-step CUDA-event pair)",
+                "flops_per_step": 4.0 * M * K * N, "prep_ms": round(prep_ms, 4),
+            },
+            "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),
+            "pct_of_nominal_2250": round(value / world / 2250.0, 4),
+            "roofline": roofline,
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": launches_total,
+            "clocks": clocks,
+            "wall_s_timed_region": round(wall, 4),
+            "library": ffn.lib_path(),
+        }
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle as it stands, on the host cores, on bounded row samples."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from ffn_inputs import make_inputs, seed_for
+    import oracle
+
+    M, K, N, cidx = workload_shape(args.workload)
+    n0, n1 = 0, N
+    if world > 1:
+        from paper_2501_08071_b200.tp import shard_bounds  # pure host arithmetic
+        n0, n1 = shard_bounds(N, 0, world)
+    N_l = n1 - n0
+    seed = args.seed if args.seed is not None else seed_for(cidx)
+    # rows of x are independent: generate only what the samples touch
+    M_gen = min(M, 256)
+    d = make_inputs(M_gen, K, N_l, family="C", seed=seed, dtype="bf16")
+    eps = 1e-6
+    nsteps = args.warmup + args.steps
+    t0 = time.perf_counter()
+    oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], eps, mode="fold_bf16", rows=[0])
+    t_row = time.perf_counter() - t0
+    rows_per_step = max(1, min(M_gen, int(args.ref_budget_s / nsteps / max(t_row, 1e-4))))
+    for _ in range(args.warmup):
+        oracle_sample_time(d, eps, 0, rows_hint=rows_per_step)
+    flops = 0.0
+    secs = 0.0
+    for _ in range(args.steps):
+        fl, sec, rows, thr = oracle_sample_time(d, eps, 0, rows_hint=rows_per_step)
+        flops += fl
+        secs += sec
+    # the sample covers rank 0's column block; scale to the whole job (all ranks' columns)
+    value = flops * (N / N_l) / secs / 1e12
+    sample = (f"{rows_per_step} of {M} rows x {N_l} columns per step (K={K}), fp64 fold-aware oracle, "
+              f"{oracle.num_threads()} OpenMP threads")
+    res = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, family C)",
+        "config": {"workload": args.workload, "M": M, "K": K, "N": N, "N_per_rank": N_l},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_cuasm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,15 +95,19 @@ def make_inputs(M: int, K: int, N: int, family: str = "C", seed: int = SEED_BASE
     }
 
 
-def make_device_inputs(M: int, K: int, N: int, seed: int, device, dtype=torch.bfloat16) -> dict:
-    """Family C drawn directly on the GPU (torch's Philox); for timing only,
-    where no oracle comparison is made on the full tensors."""
-    gen = torch.Generator(device=device)
-    gen.manual_seed(seed)
+def make_device_inputs(M: int, K: int, N: int, seed: int, device, dtype=torch.bfloat16,
+                       w_seed: int | None = None) -> dict:
+    """Family C drawn directly on the GPU (torch's Philox); for timing, where
+    no oracle comparison is made on the full tensors.  x depends on `seed`
+    and g on `seed` only (replicated across tensor-parallel ranks); W1/W3 on `w_seed`
+    (default seed + 1), so each rank can draw its own shard."""
     sd = 1.0 / float(np.sqrt(K))
-    f32 = dict(device=device, dtype=torch.float32, generator=gen)
-    x = torch.randn((M, K), **f32).to(dtype)
-    g = (torch.rand((K,), **f32) + 0.5).to(dtype)
-    w1 = (torch.randn((N, K), **f32) * sd).to(dtype)
-    w3 = (torch.randn((N, K), **f32) * sd).to(dtype)
+    gx = torch.Generator(device=device)
+    gx.manual_seed(seed)
+    gw = torch.Generator(device=device)
+    gw.manual_seed(seed + 1 if w_seed is None else w_seed)
+    x = torch.randn((M, K), device=device, dtype=torch.float32, generator=gx).to(dtype)
+    g = (torch.rand((K,), device=device, dtype=torch.float32, generator=gx) + 0.5).to(dtype)
+    w1 = (torch.randn((N, K), device=device, dtype=torch.float32, generator=gw) * sd).to(dtype)
+    w3 = (torch.randn((N, K), device=device, dtype=torch.float32, generator=gw) * sd).to(dtype)
     return {"x": x, "g": g, "w1": w1, "w3": w3}

@@ -68,7 +68,11 @@ typedef enum {
     CUASM_OPT_VARIANT = 0, /* value: cuasm_variant_t                                   */
     CUASM_OPT_PDL = 1,     /* value: 1 = launch the GEMM with programmatic dependent
                               launch after the pre-pass (default), 0 = plain ordering */
-    CUASM_OPT_GROUP_M = 2  /* value: m-blocks per rasterisation group (0 = auto)       */
+    CUASM_OPT_GROUP_M = 2, /* value: m-blocks per rasterisation group (0 = auto)       */
+    CUASM_OPT_PROFILE = 3  /* value: 1 = record CUDA events around each kernel of every
+                              forward on its stream (read with cuasm_ffn_profile_read);
+                              forces plain ordering (no PDL) so each kernel's span is
+                              its own duration.  0 (default) = off                    */
 } cuasm_option_t;
 
 /* Create a handle on `device` (CUDA ordinal) for element type `dtype`.
@@ -129,6 +133,12 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value);
 /* Which GEMM variant the last forward launched (cuasm_variant_t), and the
  * number of kernels it enqueued (0 when M == 0). */
 cuasm_status_t cuasm_ffn_last_launch(cuasm_ffn_t h, int* variant, int* kernels);
+
+/* With CUASM_OPT_PROFILE on: wait for the recorded forwards, return the
+ * summed device time (ms) of the pre-pass kernels and of the dual-GEMM
+ * kernels and the number of forwards recorded, then reset the record.
+ * Synchronous.  Any output pointer may be NULL. */
+cuasm_status_t cuasm_ffn_profile_read(cuasm_ffn_t h, double* prepass_ms, double* gemm_ms, int* forwards);
 
 /* Free all handle-owned device memory and the handle.  NULL is accepted. */
 cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h);

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/cuasm_ffn.h"
 #include "dual_gemm.cuh"
@@ -62,6 +63,10 @@ struct cuasm_ffn_s {
     int64_t x_stage_bytes = 0;
     void* out_stage = nullptr;
     int64_t out_stage_bytes = 0;
+    // profiling (CUASM_OPT_PROFILE)
+    int profile = 0;
+    std::vector<cudaEvent_t> ev_pool;   // 3 events per recorded forward
+    size_t ev_used = 0;
     // last launch
     int last_variant = 0;
     int last_kernels = 0;
@@ -253,7 +258,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
         attrs[na].val.clusterDim.z = 1;
         ++na;
     }
-    if (h->use_pdl) {
+    if (h->use_pdl && !h->profile) {
         attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -266,10 +271,12 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     return CUASM_OK;
 }
 
+// Tile-config table: the CTA-pair kernel halves per-SM smem
+// operand traffic and wins once there are >= 2 row blocks of 128 to pair;
+// below that (decode, M <= 128) the 1-SM kernel wastes no MMA rows on padding.
 int choose_variant(cuasm_ffn_t h, int64_t M, int64_t /*K*/, int64_t /*N*/) {
     if (h->variant != CUASM_VARIANT_AUTO) return h->variant;
-    (void)M;
-    return CUASM_VARIANT_1SM;
+    return M > 128 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM;
 }
 
 cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
@@ -284,6 +291,16 @@ cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
     return CUASM_OK;
 }
 
+cuasm_status_t profile_event(cuasm_ffn_t h, cudaStream_t s) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        CUASM_CHECK(h, cudaEventCreate(&e), "cudaEventCreate");
+        h->ev_pool.push_back(e);
+    }
+    CUASM_CHECK(h, cudaEventRecord(h->ev_pool[h->ev_used++], s), "cudaEventRecord");
+    return CUASM_OK;
+}
+
 cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3, void* out,
                             int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
     cuasm_status_t st;
@@ -292,15 +309,19 @@ cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const v
     if ((st = ensure_packed(h, g, w1, w3, K, N, s)) != CUASM_OK) return st;
     if (M == 0) return CUASM_OK;
     if ((st = ensure_r(h, M)) != CUASM_OK) return st;
+    if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     if ((st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
+    if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     const int v = choose_variant(h, M, K, N);
     if (h->dtype == CUASM_DTYPE_BF16) {
         st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, s) : launch_gemm<0, 1>(h, x, out, M, K, N, s);
     } else {
         st = v == CUASM_VARIANT_2SM ? launch_gemm<1, 2>(h, x, out, M, K, N, s) : launch_gemm<1, 1>(h, x, out, M, K, N, s);
     }
-    if (st == CUASM_OK) h->last_kernels = 2;
-    return st;
+    if (st != CUASM_OK) return st;
+    h->last_kernels = 2;
+    if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
+    return CUASM_OK;
 }
 
 cuasm_status_t validate_forward(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3,
@@ -465,6 +486,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         if (value < 0 || value > 1 << 20) return fail(h, CUASM_ERR_INVALID_ARG, "bad group_m");
         h->group_m = static_cast<int>(value);
         return CUASM_OK;
+    case CUASM_OPT_PROFILE:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "PROFILE option is 0 or 1");
+        h->profile = static_cast<int>(value);
+        return CUASM_OK;
     default:
         return fail(h, CUASM_ERR_INVALID_ARG, "unknown option %d", option);
     }
@@ -477,8 +502,28 @@ cuasm_status_t cuasm_ffn_last_launch(cuasm_ffn_t h, int* variant, int* kernels) 
     return CUASM_OK;
 }
 
+cuasm_status_t cuasm_ffn_profile_read(cuasm_ffn_t h, double* prepass_ms, double* gemm_ms, int* forwards) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    double pre = 0.0, gemm = 0.0;
+    const size_t n = h->ev_used / 3;
+    for (size_t i = 0; i < n; ++i) {
+        float a = 0.f, b = 0.f;
+        CUASM_CHECK(h, cudaEventSynchronize(h->ev_pool[3 * i + 2]), "cudaEventSynchronize");
+        CUASM_CHECK(h, cudaEventElapsedTime(&a, h->ev_pool[3 * i], h->ev_pool[3 * i + 1]), "cudaEventElapsedTime");
+        CUASM_CHECK(h, cudaEventElapsedTime(&b, h->ev_pool[3 * i + 1], h->ev_pool[3 * i + 2]), "cudaEventElapsedTime");
+        pre += a;
+        gemm += b;
+    }
+    h->ev_used = 0;
+    if (prepass_ms) *prepass_ms = pre;
+    if (gemm_ms) *gemm_ms = gemm;
+    if (forwards) *forwards = static_cast<int>(n);
+    return CUASM_OK;
+}
+
 cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     if (!h) return CUASM_OK;
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     int cur = -1;
     if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device) cudaSetDevice(h->device);
     if (h->r) cudaFree(h->r);

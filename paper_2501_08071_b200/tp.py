@@ -1,0 +1,75 @@
+"""Tensor-parallel (Megatron column-parallel) fused FFN across the GPUs of one box.
+
+BASELINE.json north_star (c): "column-sharding the intermediate dimension N of
+W1/W3 (Megatron-style, with no reduction needed), with an NCCL all-gather over
+NVLink only when the full output is requested".  SiLU-gating is elementwise in
+N, so rank p computes out[:, shard p] from its contiguous row block of W1 and
+W3 and the replicated x; there is no data-path collective unless
+``gather=True``.  One process per GPU, ``torch.distributed`` with NCCL for the
+plumbing.  (A later step -- SURVEY §8(f) f1/f2 -- fuses the down projection /
+all-gather into the kernel epilogue over NVSwitch peer memory.)
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import FusedFFN, _handle
+
+
+def shard_bounds(N: int, rank: int, world: int, align: int = 8):
+    """Contiguous [n0, n1) of the N output columns owned by `rank`.
+
+    Shards are as equal as possible in units of `align` columns (the C ABI
+    requires every shard width to be a multiple of 8)."""
+    if N % align != 0:
+        raise ValueError(f"N={N} must be a multiple of {align}")
+    units = N // align
+    base, rem = divmod(units, world)
+    n0 = (rank * base + min(rank, rem)) * align
+    n1 = n0 + (base + (1 if rank < rem else 0)) * align
+    return n0, n1
+
+
+def shard_weights(w1: torch.Tensor, w3: torch.Tensor, rank: int, world: int):
+    """Rank `rank`'s contiguous row block of W1 and W3 ([N,K] nn.Linear layout)."""
+    n0, n1 = shard_bounds(w1.shape[0], rank, world)
+    return w1[n0:n1].contiguous(), w3[n0:n1].contiguous()
+
+
+def gather_shards(out_shard: torch.Tensor, N: int, group=None) -> torch.Tensor:
+    """All-gather the per-rank [M, N_p] output shards into the full [M, N].
+
+    Equal shards use one all_gather_into_tensor into [P, M, N/P] followed by a
+    column interleave; unequal shards fall back to all_gather of padded
+    buffers.  Collective over `group` (NCCL on GPUs, gloo on CPU)."""
+    world = dist.get_world_size(group)
+    M = out_shard.shape[0]
+    widths = [shard_bounds(N, r, world)[1] - shard_bounds(N, r, world)[0] for r in range(world)]
+    wmax = max(widths)
+    if out_shard.shape[1] != widths[dist.get_rank(group)]:
+        raise ValueError("out_shard width does not match this rank's shard")
+    if all(w == wmax for w in widths):
+        buf = torch.empty((world * M, wmax), dtype=out_shard.dtype, device=out_shard.device)
+        dist.all_gather_into_tensor(buf, out_shard.contiguous(), group=group)
+        return buf.view(world, M, wmax).permute(1, 0, 2).reshape(M, N)
+    padded = torch.zeros((M, wmax), dtype=out_shard.dtype, device=out_shard.device)
+    padded[:, :out_shard.shape[1]] = out_shard
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([p[:, :w] for p, w in zip(parts, widths)], dim=1)
+
+
+def ffn_tp_forward(x, rms_w, w1_shard, w3_shard, eps: float = 1e-6, group=None, gather: bool = False,
+                   N: int | None = None, handle: FusedFFN | None = None):
+    """This rank's share of the column-parallel fused FFN.
+
+    x [M,K] (replicated), rms_w [K], w1_shard/w3_shard [N_p,K] -> out [M,N_p],
+    or the full [M,N] when ``gather`` (N = total width, required then)."""
+    h = handle or _handle(x.device, x.dtype)
+    out = h.forward(x, rms_w, w1_shard, w3_shard, eps)
+    if not gather:
+        return out
+    if N is None:
+        raise ValueError("gather=True needs the total N")
+    return gather_shards(out, N, group)

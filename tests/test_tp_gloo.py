@@ -1,0 +1,73 @@
+"""Multi-process host logic of the N-sharded (column-parallel) path, on CPU
+with the gloo backend at world_size 2 (and 3 for ragged shards): shard
+bounds, the all-gather + column interleave that reassembles the output, and
+bench.py's max-over-ranks timing reduction."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2501_08071_b200.tp import gather_shards, shard_bounds, shard_weights
+
+
+@pytest.mark.parametrize("N,world", [(11008, 8), (11008, 2), (28672, 8), (1376, 3), (8, 1), (24, 3), (40, 3)])
+def test_shard_bounds_partition(N, world):
+    spans = [shard_bounds(N, r, world) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == N
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 == b0
+    widths = [b - a for a, b in spans]
+    assert all(w % 8 == 0 for w in widths)
+    assert max(widths) - min(widths) <= 8
+
+
+def test_shard_weights_rows():
+    w1 = torch.arange(48 * 4, dtype=torch.float32).reshape(48, 4)
+    w3 = -w1
+    a1, a3 = shard_weights(w1, w3, 1, 3)
+    n0, n1 = shard_bounds(48, 1, 3)
+    assert torch.equal(a1, w1[n0:n1]) and torch.equal(a3, w3[n0:n1])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, N, M, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = torch.arange(M * N, dtype=torch.float32).reshape(M, N)
+        n0, n1 = shard_bounds(N, rank, world)
+        got = gather_shards(full[:, n0:n1].contiguous(), N)
+        ok_gather = bool(torch.equal(got, full))
+        import bench
+        t = bench.max_over_ranks(float(rank + 1) * 1.5)
+        q.put((rank, ok_gather, t))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N", [(2, 64), (3, 40), (2, 11008)])
+def test_gather_and_max_over_ranks(world, N):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, t in res:
+        assert ok, f"rank {rank}: gathered output differs"
+        assert t == pytest.approx(1.5 * world)
