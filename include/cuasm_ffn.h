@@ -69,11 +69,23 @@ typedef enum {
     CUASM_OPT_PDL = 1,     /* value: 1 = launch the GEMM with programmatic dependent
                               launch after the pre-pass (default), 0 = plain ordering */
     CUASM_OPT_GROUP_M = 2, /* value: m-blocks per rasterisation group (0 = auto)       */
-    CUASM_OPT_PROFILE = 3  /* value: 1 = record CUDA events around each kernel of every
+    CUASM_OPT_PROFILE = 3, /* value: 1 = record CUDA events around each kernel of every
                               forward on its stream (read with cuasm_ffn_profile_read);
                               forces plain ordering (no PDL) so each kernel's span is
                               its own duration.  0 (default) = off                    */
+    CUASM_OPT_SCHEDULE = 4 /* value: cuasm_schedule_t                                  */
 } cuasm_option_t;
+
+/* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
+ * CUASM_OPT_SCHEDULE).  Stream-K splits k-block ranges of the tail tiles
+ * across CTAs (fp32 partials through a handle-owned workspace, fixed
+ * reduction order: results stay bitwise run-to-run deterministic). */
+typedef enum {
+    CUASM_SCHEDULE_AUTO = 0,          /* whole tiles while they fill complete waves, stream-K
+                                         over the last partial wave + one full wave         */
+    CUASM_SCHEDULE_DATA_PARALLEL = 1, /* whole tiles only                                      */
+    CUASM_SCHEDULE_STREAM_K_ALL = 2   /* stream-K over every tile (testing)                     */
+} cuasm_schedule_t;
 
 /* Create a handle on `device` (CUDA ordinal) for element type `dtype`.
  * Returns UNSUPPORTED if the device is not CC 10.0, CUDA on any runtime error.

@@ -31,7 +31,8 @@ _lib_lock = threading.Lock()
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE = 0, 1, 2, 3
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE = 0, 1, 2, 3, 4
+SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL = 0, 1, 2
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (

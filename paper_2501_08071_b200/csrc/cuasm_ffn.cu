@@ -44,6 +44,13 @@ struct cuasm_ffn_s {
     int variant = CUASM_VARIANT_AUTO;
     int use_pdl = 1;
     int group_m = 0;
+    int schedule = 0;  // CUASM_OPT_SCHEDULE
+    // stream-K workspace
+    float* ws = nullptr;
+    int64_t ws_bytes = 0;
+    uint32_t* flags = nullptr;
+    int64_t flags_bytes = 0;
+    uint32_t epoch = 0;
     // a1 workspace
     float* r = nullptr;
     int64_t r_cap = 0;
@@ -242,7 +249,45 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
         attr_set[kKind][kCtaGroup] = true;
     }
     const int max_clusters = h->sm_count / kCtaGroup;
-    const int clusters = std::min(p.num_tiles, max_clusters);
+    // Persistent schedule (DESIGN.md §6 "Stream-K"): whole tiles round-robin
+    // while they fill complete waves; the last partial wave plus one full
+    // wave (or everything, when there are fewer tiles than clusters) is split
+    // into equal contiguous k-block ranges so every cluster finishes together.
+    int clusters = std::min(p.num_tiles, max_clusters);
+    int sk_tiles = 0;
+    const int waves = p.num_tiles / max_clusters, rem = p.num_tiles % max_clusters;
+    if (h->schedule != CUASM_SCHEDULE_DATA_PARALLEL && p.num_k_blk > 1) {
+        if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
+        else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
+        if (sk_tiles > 0) clusters = max_clusters;
+    }
+    p.num_clusters = clusters;
+    p.num_dp_tiles = p.num_tiles - sk_tiles;
+    p.sk_iters = static_cast<int64_t>(sk_tiles) * p.num_k_blk;
+    if (sk_tiles > 0) {
+        const int64_t ws_need = static_cast<int64_t>(clusters) * kCtaGroup * C::BM * C::UMMA_N * 4;
+        const int64_t fl_need = static_cast<int64_t>(clusters) * kCtaGroup * 4 * 4;
+        if (ws_need > h->ws_bytes) {
+            if (h->ws) cudaFree(h->ws);
+            h->ws = nullptr;
+            h->ws_bytes = 0;
+            CUASM_CHECK(h, cudaMalloc(&h->ws, ws_need), "cudaMalloc(stream-K workspace)");
+            h->ws_bytes = ws_need;
+        }
+        if (fl_need > h->flags_bytes) {
+            if (h->flags) cudaFree(h->flags);
+            h->flags = nullptr;
+            h->flags_bytes = 0;
+            CUASM_CHECK(h, cudaMalloc(&h->flags, fl_need), "cudaMalloc(stream-K flags)");
+            CUASM_CHECK(h, cudaMemset(h->flags, 0, fl_need), "cudaMemset(flags)");
+            h->flags_bytes = fl_need;
+            h->epoch = 0;
+        }
+    }
+    p.ws = h->ws;
+    p.flags = h->flags;
+    p.epoch = ++h->epoch;
+    if (p.epoch == 0) p.epoch = ++h->epoch;  // 0 is the flags' initial value
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * kCtaGroup), 1, 1);
@@ -486,6 +531,11 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         if (value < 0 || value > 1 << 20) return fail(h, CUASM_ERR_INVALID_ARG, "bad group_m");
         h->group_m = static_cast<int>(value);
         return CUASM_OK;
+    case CUASM_OPT_SCHEDULE:
+        if (value < CUASM_SCHEDULE_AUTO || value > CUASM_SCHEDULE_STREAM_K_ALL)
+            return fail(h, CUASM_ERR_INVALID_ARG, "bad schedule %lld", (long long)value);
+        h->schedule = static_cast<int>(value);
+        return CUASM_OK;
     case CUASM_OPT_PROFILE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "PROFILE option is 0 or 1");
         h->profile = static_cast<int>(value);
@@ -530,6 +580,8 @@ cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     if (h->w13) cudaFree(h->w13);
     if (h->x_stage) cudaFree(h->x_stage);
     if (h->out_stage) cudaFree(h->out_stage);
+    if (h->ws) cudaFree(h->ws);
+    if (h->flags) cudaFree(h->flags);
     if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
     delete h;
     return CUASM_OK;

@@ -46,7 +46,81 @@ struct FfnGemmParams {
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int num_tiles;
+    // --- persistent schedule: data-parallel tiles, then a stream-K region ---
+    int num_clusters;   // persistent clusters (CTA pairs for the 2-SM variant)
+    int num_dp_tiles;   // tiles [0, num_dp_tiles) round-robin, whole
+    int64_t sk_iters;   // (num_tiles - num_dp_tiles) * num_k_blk k-block iterations,
+                        // split into num_clusters contiguous ranges
+    float* ws;          // stream-K partials: [cluster][cta rank][2BN/32][128][32] fp32
+    uint32_t* flags;    // [cluster][cta rank][4 epilogue warps]: epoch when published
+    uint32_t epoch;     // this launch's flag value (host increments per launch)
 };
+
+// A unit of work: k-blocks [kb0, kb1) of tile `tile`.
+struct Seg {
+    int tile, kb0, kb1;
+};
+
+__device__ __forceinline__ int64_t sk_begin(const FfnGemmParams& p, int c) {
+    return (p.sk_iters * c) / p.num_clusters;
+}
+
+// The cluster whose stream-K range holds iteration i.
+__device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
+    int c = static_cast<int>((i * p.num_clusters) / (p.sk_iters > 0 ? p.sk_iters : 1));
+    while (c + 1 < p.num_clusters && sk_begin(p, c + 1) <= i) ++c;
+    while (c > 0 && sk_begin(p, c) > i) --c;
+    return c;
+}
+
+// Per-cluster walk over its work: first whole data-parallel tiles
+// (cluster, cluster + C, ...), then its contiguous stream-K iteration range
+// cut at tile boundaries.  Every role of the CTA (producer, MMA, epilogue)
+// walks the identical sequence.  In a stream-K range only the first segment
+// can start mid-tile (a "contributor": it publishes an fp32 partial) and only
+// the last can end mid-tile while starting at k-block 0 (the "finisher": it
+// adds the later clusters' partials and runs the epilogue).
+struct Sched {
+    int next_dp, C, KB, T_dp;
+    int64_t cur, end;
+    __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster) {
+        next_dp = cluster;
+        C = p.num_clusters;
+        KB = p.num_k_blk;
+        T_dp = p.num_dp_tiles;
+        cur = sk_begin(p, cluster);
+        end = sk_begin(p, cluster + 1);
+    }
+    __device__ __forceinline__ bool next(Seg& s) {
+        if (next_dp < T_dp) {
+            s.tile = next_dp;
+            s.kb0 = 0;
+            s.kb1 = KB;
+            next_dp += C;
+            return true;
+        }
+        if (cur < end) {
+            const int64_t t = cur / KB;
+            const int kb0 = static_cast<int>(cur - t * KB);
+            const int64_t take = (KB - kb0) < (end - cur) ? (KB - kb0) : (end - cur);
+            s.tile = T_dp + static_cast<int>(t);
+            s.kb0 = kb0;
+            s.kb1 = kb0 + static_cast<int>(take);
+            cur += take;
+            return true;
+        }
+        return false;
+    }
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int kKind, int kCtaGroup>
 struct GemmCfg {
@@ -130,9 +204,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // Cluster-level tile id: both CTAs of a pair walk the same tile sequence.
+    // Cluster-level work: both CTAs of a pair walk the same segment sequence.
     const int cluster_id = blockIdx.x / kCtaGroup;
-    const int num_clusters = gridDim.x / kCtaGroup;
 
     if (warp == 0) {
         // ========================= TMA producer =========================
@@ -141,12 +214,15 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            Sched sch;
+            sch.init(p, cluster_id);
+            Seg sg;
+            while (sch.next(sg)) {
                 int mb, nb;
-                tile_coords(t, p, mb, nb);
+                tile_coords(sg.tile, p, mb, nb);
                 const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
                 const int row_b = nb * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
-                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
                     ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
@@ -171,13 +247,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+            Sched sch;
+            sch.init(p, cluster_id);
+            Seg sg;
+            for (; sch.next(sg); ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 ptx::mbar_wait(ptx::smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C::UMMA_N;
-                for (int kb = 0; kb < p.num_k_blk; ++kb) {
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
                     ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
                     ptx::tc_fence_after();
                     const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + stage * C::A_BYTES));
@@ -186,7 +265,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     for (int k = 0; k < C::KSTEPS; ++k) {
                         // advance 32 bytes of K inside the 128-byte swizzle row (+2 in 16-byte units)
                         ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
-                                                   (kb | k) != 0 ? 1u : 0u);
+                                                   (kb > sg.kb0 || k > 0) ? 1u : 0u);
                     }
                     if constexpr (kCtaGroup == 1) {
                         ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
@@ -208,16 +287,36 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
         const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t row_in_cta = quad * 32 + lane;
         int it = 0;
-        for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+        Sched sch;
+        sch.init(p, cluster_id);
+        Seg sg;
+        for (; sch.next(sg); ++it) {
             int mb, nb;
-            tile_coords(t, p, mb, nb);
+            tile_coords(sg.tile, p, mb, nb);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM + static_cast<int>(row_in_cta);
             const bool row_ok = row < p.M;
+            const bool contributor = sg.kb0 > 0;                       // stream-K: partial, not the tile's start
+            const bool finisher = sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
+            // this CTA's 128 x 2BN fp32 partial slot: [chunk 0..2BN/32)[row 0..127][32]
+            float* my_slot = p.ws + (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N);
+            int c_first = 0, c_last = -1;
+            if (finisher) {
+                // contributors: the clusters whose stream-K ranges cover the rest of this tile
+                const int64_t tile_end = static_cast<int64_t>(sg.tile - p.num_dp_tiles + 1) * p.num_k_blk - 1;
+                c_first = cluster_id + 1;
+                c_last = sk_owner(p, tile_end);
+            }
             const float rr = row_ok ? __ldg(p.r + row) : 0.f;
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
+            for (int cc = c_first; cc <= c_last; ++cc) {
+                // acquire every contributor's per-warp flag for this launch's epoch
+                const uint32_t* f = p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad);
+                while (ld_acquire_u32(f) != p.epoch) {
+                }
+            }
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
             for (int c = 0; c < C::BN / 32; ++c) {
@@ -225,37 +324,68 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, v1);
                 ptx::tmem_ld_32x32b_x32(t_row + C::BN + c * 32, v3);
                 ptx::tmem_ld_wait();
+                if (!row_ok) continue;
+                if (contributor) {
+                    float4* d1 = reinterpret_cast<float4*>(my_slot + (static_cast<int64_t>(c) * C::BM + row_in_cta) * 32);
+                    float4* d3 = reinterpret_cast<float4*>(
+                        my_slot + (static_cast<int64_t>(C::BN / 32 + c) * C::BM + row_in_cta) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        __stcg(d1 + q, make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
+                                                   __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3])));
+                        __stcg(d3 + q, make_float4(__uint_as_float(v3[4 * q]), __uint_as_float(v3[4 * q + 1]),
+                                                   __uint_as_float(v3[4 * q + 2]), __uint_as_float(v3[4 * q + 3])));
+                    }
+                    continue;
+                }
+                for (int cc = c_first; cc <= c_last; ++cc) {
+                    const float* slot = p.ws + (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N);
+                    const float4* s1 = reinterpret_cast<const float4*>(slot + (static_cast<int64_t>(c) * C::BM + row_in_cta) * 32);
+                    const float4* s3 = reinterpret_cast<const float4*>(
+                        slot + (static_cast<int64_t>(C::BN / 32 + c) * C::BM + row_in_cta) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 a = __ldcg(s1 + q);
+                        const float4 b = __ldcg(s3 + q);
+                        v1[4 * q + 0] = __float_as_uint(__uint_as_float(v1[4 * q + 0]) + a.x);
+                        v1[4 * q + 1] = __float_as_uint(__uint_as_float(v1[4 * q + 1]) + a.y);
+                        v1[4 * q + 2] = __float_as_uint(__uint_as_float(v1[4 * q + 2]) + a.z);
+                        v1[4 * q + 3] = __float_as_uint(__uint_as_float(v1[4 * q + 3]) + a.w);
+                        v3[4 * q + 0] = __float_as_uint(__uint_as_float(v3[4 * q + 0]) + b.x);
+                        v3[4 * q + 1] = __float_as_uint(__uint_as_float(v3[4 * q + 1]) + b.y);
+                        v3[4 * q + 2] = __float_as_uint(__uint_as_float(v3[4 * q + 2]) + b.z);
+                        v3[4 * q + 3] = __float_as_uint(__uint_as_float(v3[4 * q + 3]) + b.w);
+                    }
+                }
                 const int col0 = nb * C::BN + c * 32;
-                if (row_ok) {
-                    if constexpr (kKind == 0) {
-                        uint32_t packed[16];
+                if constexpr (kKind == 0) {
+                    uint32_t packed[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float a0 = silu_gate(rr * __uint_as_float(v1[2 * i]), rr * __uint_as_float(v3[2 * i]));
-                            const float a1 =
-                                silu_gate(rr * __uint_as_float(v1[2 * i + 1]), rr * __uint_as_float(v3[2 * i + 1]));
-                            packed[i] = ptx::pack_bf16x2(a0, a1);
+                    for (int i = 0; i < 16; ++i) {
+                        const float a0 = silu_gate(rr * __uint_as_float(v1[2 * i]), rr * __uint_as_float(v3[2 * i]));
+                        const float a1 =
+                            silu_gate(rr * __uint_as_float(v1[2 * i + 1]), rr * __uint_as_float(v3[2 * i + 1]));
+                        packed[i] = ptx::pack_bf16x2(a0, a1);
+                    }
+                    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (col0 + 8 * q < p.N) {
+                            *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
+                                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
                         }
-                        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+                    }
+                } else {
+                    float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            if (col0 + 8 * q < p.N) {
-                                *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
-                                    make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-                            }
-                        }
-                    } else {
-                        float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            if (col0 + 4 * q < p.N) {
-                                float4 o;
-                                o.x = silu_gate(rr * __uint_as_float(v1[4 * q + 0]), rr * __uint_as_float(v3[4 * q + 0]));
-                                o.y = silu_gate(rr * __uint_as_float(v1[4 * q + 1]), rr * __uint_as_float(v3[4 * q + 1]));
-                                o.z = silu_gate(rr * __uint_as_float(v1[4 * q + 2]), rr * __uint_as_float(v3[4 * q + 2]));
-                                o.w = silu_gate(rr * __uint_as_float(v1[4 * q + 3]), rr * __uint_as_float(v3[4 * q + 3]));
-                                *reinterpret_cast<float4*>(orow + col0 + 4 * q) = o;
-                            }
+                    for (int q = 0; q < 8; ++q) {
+                        if (col0 + 4 * q < p.N) {
+                            float4 o;
+                            o.x = silu_gate(rr * __uint_as_float(v1[4 * q + 0]), rr * __uint_as_float(v3[4 * q + 0]));
+                            o.y = silu_gate(rr * __uint_as_float(v1[4 * q + 1]), rr * __uint_as_float(v3[4 * q + 1]));
+                            o.z = silu_gate(rr * __uint_as_float(v1[4 * q + 2]), rr * __uint_as_float(v3[4 * q + 2]));
+                            o.w = silu_gate(rr * __uint_as_float(v1[4 * q + 3]), rr * __uint_as_float(v3[4 * q + 3]));
+                            *reinterpret_cast<float4*>(orow + col0 + 4 * q) = o;
                         }
                     }
                 }
@@ -268,6 +398,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
                 } else {
                     ptx::mbar_arrive_cluster(ptx::smem_u32(&tempty_bar[acc]), 0);
+                }
+            }
+            if (contributor) {
+                // publish this warp's rows of the partial: every lane fences its own
+                // stores, then one release store of the launch epoch
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    st_release_u32(p.flags + ((static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * 4 + quad),
+                                   p.epoch);
                 }
             }
         }

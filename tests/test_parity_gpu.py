@@ -20,10 +20,11 @@ RTOL, ATOL = 2e-2, 1e-3
 TORCH_DT = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
 
-def run_gpu(d, eps, dtype, variant=ffn.VARIANT_AUTO, handle=None):
+def run_gpu(d, eps, dtype, variant=ffn.VARIANT_AUTO, handle=None, schedule=ffn.SCHEDULE_AUTO):
     dev = torch.device("cuda:0")
     h = handle or ffn.FusedFFN(dev, TORCH_DT[dtype])
     h.set_variant(variant)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
     t = {k: v.to(dev) for k, v in d.items()}
     out = h.forward(t["x"], t["g"], t["w1"], t["w3"], eps)
     torch.cuda.synchronize()
@@ -107,8 +108,29 @@ def test_parity_small_bf16(cuda_device, M, K, N, family, variant):
     check(out, ref, f"{family} {M}x{K}x{N} v{variant}")
 
 
+SCHED_SHAPES = [
+    (16, 4096, 512),     # 4-8 tiles over 74-148 clusters: many contributors per tile
+    (300, 1024, 1000),   # ragged M and N, a few tiles
+    (1000, 512, 2056),   # several waves + tail
+    (2048, 4096, 1376),  # 7B prefill, 8-way shard width (88 / 176 tiles)
+]
+
+
+@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL, ffn.SCHEDULE_AUTO])
 @pytest.mark.parametrize("variant", [ffn.VARIANT_1SM, ffn.VARIANT_2SM])
-@pytest.mark.parametrize("M,K,N", [(16, 64, 128), (5, 64, 136), (200, 256, 264)])
+@pytest.mark.parametrize("M,K,N", SCHED_SHAPES)
+def test_parity_schedules(cuda_device, M, K, N, variant, schedule):
+    d = make_inputs(M, K, N, family="C", seed=4000 + M + N, dtype="bf16")
+    out, h = run_gpu(d, 1e-6, "bf16", variant, schedule=schedule)
+    again, _ = run_gpu(d, 1e-6, "bf16", variant, handle=h, schedule=schedule)
+    assert torch.equal(out, again), "bitwise run-to-run determinism"
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 40)))))
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(out[rows], ref, f"sched {schedule} v{variant} {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("variant", [ffn.VARIANT_1SM, ffn.VARIANT_2SM])
+@pytest.mark.parametrize("M,K,N", [(16, 64, 128), (5, 64, 136), (200, 256, 264), (40, 1024, 392)])
 def test_parity_small_fp32(cuda_device, M, K, N, variant):
     d = make_inputs(M, K, N, family="T", seed=2000 + M, dtype="fp32")
     out, _ = run_gpu(d, 1e-6, "fp32", variant)
@@ -180,18 +202,22 @@ def test_invariants_bitwise(cuda_device):
 def test_n_shard_equals_columns(cuda_device):
     M, K, N = 256, 256, 1024
     d = make_inputs(M, K, N, family="C", seed=3100, dtype="bf16")
-    full, h = run_gpu(d, 1e-6, "bf16")
+    # whole-tile schedule: the k-summation of an output then does not depend on
+    # where stream-K cuts fall, which move with the shard width
+    dp = ffn.SCHEDULE_DATA_PARALLEL
+    full, h = run_gpu(d, 1e-6, "bf16", schedule=dp)
     for n0, n1 in ((0, 512), (512, 1024), (256, 392)):
         ds = dict(d, w1=d["w1"][n0:n1].contiguous(), w3=d["w3"][n0:n1].contiguous())
-        part, _ = run_gpu(ds, 1e-6, "bf16", handle=h)
+        part, _ = run_gpu(ds, 1e-6, "bf16", handle=h, schedule=dp)
         assert torch.equal(part, full[:, n0:n1]), (n0, n1)
 
 
 def test_variants_agree(cuda_device):
     M, K, N = 512, 1024, 768
     d = make_inputs(M, K, N, family="C", seed=3200, dtype="bf16")
-    a, h = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_1SM)
-    b, _ = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_2SM, handle=h)
+    dp = ffn.SCHEDULE_DATA_PARALLEL
+    a, h = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_1SM, schedule=dp)
+    b, _ = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_2SM, handle=h, schedule=dp)
     assert torch.equal(a, b)
 
 
