@@ -131,9 +131,12 @@ cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x_dev, float* r_dev,
                                  void* stream);
 
 /* Copy the packed, g-folded weights (a0's output) to host memory for
- * inspection: rows = 2*ceil(N/128)*128, row r = (nb, j, rr) holds
- * RNE(W_j[nb*128+rr, :] * g) (zero for padded rows), K elements each.
- * *bytes receives the size; pass dst_host = NULL to query it.  Synchronous. */
+ * inspection.  Layout (k-block tiled; BK = 128 bytes of K = 64 bf16 / 32 fp32
+ * elements, NB = 128 outputs): element [nb][kb][j*128 + rr][i] =
+ * RNE(W_j[nb*128 + rr, kb*BK + i] * g[kb*BK + i]), j = 0 for W1, 1 for W3,
+ * zero where the row is past N or the column past K; nb < ceil(N/128),
+ * kb < ceil(K/BK).  *bytes receives the size; pass dst_host = NULL to query
+ * it.  Synchronous. */
 cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst_host, int64_t* bytes);
 
 /* Drop the cached packed weights; the next forward re-packs. */

@@ -50,14 +50,14 @@ struct cuasm_ffn_s {
     int64_t ws_bytes = 0;
     uint32_t* flags = nullptr;
     int64_t flags_bytes = 0;
-    uint32_t epoch = 0;
     // a1 workspace
     float* r = nullptr;
     int64_t r_cap = 0;
     // a0 cache
     void* w13 = nullptr;
     int64_t w13_bytes = 0;
-    int64_t w13_rows = 0;
+    int64_t w13_rows = 0;     // rows of 128 bytes in the k-block-tiled W13
+    int64_t w13_kblocks = 0;
     const void* key_g = nullptr;
     const void* key_w1 = nullptr;
     const void* key_w3 = nullptr;
@@ -155,9 +155,11 @@ cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint
 template <typename T>
 cuasm_status_t launch_pack(cuasm_ffn_t h, const void* g, const void* w1, const void* w3, int64_t K, int64_t N,
                            cudaStream_t s) {
+    const int BK = 128 / h->esize;  // one 128-byte swizzle row of K (= GemmCfg::BK)
     const int64_t n_blocks = (N + kPackBN - 1) / kPackBN;
-    const int64_t rows = n_blocks * 2 * kPackBN;
-    const int64_t bytes = rows * K * h->esize;
+    const int64_t k_blocks = (K + BK - 1) / BK;
+    const int64_t rows = n_blocks * k_blocks * 2 * kPackBN;
+    const int64_t bytes = rows * 128;
     if (bytes > h->w13_bytes) {
         if (h->w13) cudaFree(h->w13);
         h->w13 = nullptr;
@@ -165,14 +167,15 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, const void* g, const void* w1, const v
         CUASM_CHECK(h, cudaMalloc(&h->w13, bytes), "cudaMalloc(W13)");
         h->w13_bytes = bytes;
     }
-    const int64_t total_vec = rows * (K * h->esize / 16);
+    const int64_t total_vec = bytes / 16;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>((total_vec + threads - 1) / threads, int64_t(h->sm_count) * 16);
     cuasm::ffn_pack_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, s>>>(
         static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(h->w13), N,
-        K, kPackBN, n_blocks);
+        K, kPackBN, n_blocks, k_blocks, BK);
     CUASM_CHECK(h, cudaGetLastError(), "ffn_pack_kernel launch");
     h->w13_rows = rows;
+    h->w13_kblocks = k_blocks;
     h->tmap_w_rows = 0;  // re-encode for the new buffer
     h->key_g = g;
     h->key_w1 = w1;
@@ -195,6 +198,18 @@ cuasm_status_t ensure_packed(cuasm_ffn_t h, const void* g, const void* w1, const
 template <typename T>
 cuasm_status_t launch_prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
                               cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        // Same L1/smem split as the dual GEMM (max shared): an SM running
+        // pre-pass CTAs can then take the PDL-launched GEMM CTA without a
+        // carveout reconfiguration, so the two kernels actually overlap.
+        CUASM_CHECK(h,
+                    cudaFuncSetAttribute(cuasm::ffn_rms_prepass_kernel<T>,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         static_cast<int>(cudaSharedmemCarveoutMaxShared)),
+                    "cudaFuncSetAttribute(prepass carveout)");
+        attr_set = true;
+    }
     const int64_t blocks = (M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock;
     cuasm::ffn_rms_prepass_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(static_cast<const T*>(x), r, M, K,
                                                                                     eps);
@@ -215,8 +230,8 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, C::BM);
     if (st != CUASM_OK) return st;
     if (h->tmap_w_rows != C::B_ROWS) {
-        st = encode_2d(h, &h->tmap_w, h->w13, static_cast<uint64_t>(K), static_cast<uint64_t>(h->w13_rows), C::BK,
-                       C::B_ROWS);
+        st = encode_2d(h, &h->tmap_w, h->w13, static_cast<uint64_t>(C::BK), static_cast<uint64_t>(h->w13_rows),
+                       C::BK, C::B_ROWS);
         if (st != CUASM_OK) return st;
         h->tmap_w_rows = C::B_ROWS;
     }
@@ -259,7 +274,9 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     if (h->schedule != CUASM_SCHEDULE_DATA_PARALLEL && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
         else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
-        if (sk_tiles > 0) clusters = max_clusters;
+        // every cluster gets a non-empty range (tiny problems: fewer clusters)
+        if (sk_tiles > 0)
+            clusters = static_cast<int>(std::min<int64_t>(max_clusters, static_cast<int64_t>(sk_tiles) * p.num_k_blk));
     }
     p.num_clusters = clusters;
     p.num_dp_tiles = p.num_tiles - sk_tiles;
@@ -281,13 +298,10 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
             CUASM_CHECK(h, cudaMalloc(&h->flags, fl_need), "cudaMalloc(stream-K flags)");
             CUASM_CHECK(h, cudaMemset(h->flags, 0, fl_need), "cudaMemset(flags)");
             h->flags_bytes = fl_need;
-            h->epoch = 0;
         }
     }
     p.ws = h->ws;
     p.flags = h->flags;
-    p.epoch = ++h->epoch;
-    if (p.epoch == 0) p.epoch = ++h->epoch;  // 0 is the flags' initial value
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * kCtaGroup), 1, 1);
@@ -499,7 +513,7 @@ cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t
 cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst, int64_t* bytes) {
     if (!h || !bytes) return fail(h, CUASM_ERR_INVALID_ARG, "NULL argument");
     if (!h->packed) return fail(h, CUASM_ERR_INVALID_ARG, "no packed weights cached");
-    const int64_t b = h->w13_rows * h->key_K * h->esize;
+    const int64_t b = h->w13_rows * 128;
     *bytes = b;
     if (!dst) return CUASM_OK;
     cuasm_status_t st;

@@ -52,8 +52,9 @@ struct FfnGemmParams {
     int64_t sk_iters;   // (num_tiles - num_dp_tiles) * num_k_blk k-block iterations,
                         // split into num_clusters contiguous ranges
     float* ws;          // stream-K partials: [cluster][cta rank][2BN/32][128][32] fp32
-    uint32_t* flags;    // [cluster][cta rank][4 epilogue warps]: epoch when published
-    uint32_t epoch;     // this launch's flag value (host increments per launch)
+    uint32_t* flags;    // [cluster][cta rank][4 epilogue warps]: 1 = partial published;
+                        // the finisher consumes (resets to 0) it, so launches need no
+                        // per-launch state and the kernel can be replayed from a CUDA graph
 };
 
 // A unit of work: k-blocks [kb0, kb1) of tile `tile`.
@@ -120,6 +121,21 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin until a stream-K contributor has published its partial (flag == 1)
+// (watchdog: trap after ~8 s instead of hanging the GPU on a schedule bug).
+__device__ __forceinline__ void wait_flag(const uint32_t* f) {
+    if (ld_acquire_u32(f) == 1u) return;
+#if CUASM_WATCHDOG
+    const long long t0 = clock64();
+#endif
+    while (ld_acquire_u32(f) != 1u) {
+        __nanosleep(64);
+#if CUASM_WATCHDOG
+        if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
+#endif
+    }
 }
 
 template <int kKind, int kCtaGroup>
@@ -221,7 +237,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                 int mb, nb;
                 tile_coords(sg.tile, p, mb, nb);
                 const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
-                const int row_b = nb * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
+                // k-block-tiled W13 (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*2BN
+                const int row_b0 = nb * p.num_k_blk * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
                     ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
@@ -230,12 +247,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     if constexpr (kCtaGroup == 1) {
                         ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
                         ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d(sb, &tmap_w, fb, kb * C::BK, row_b, pol_w);
+                        ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     } else {
                         // both CTAs' bytes land on the leader's barrier
                         if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::STAGE_BYTES);
                         ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, kb * C::BK, row_b, pol_w);
+                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -312,10 +329,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
             for (int cc = c_first; cc <= c_last; ++cc) {
-                // acquire every contributor's per-warp flag for this launch's epoch
-                const uint32_t* f = p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad);
-                while (ld_acquire_u32(f) != p.epoch) {
-                }
+                if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;  // empty range: not a contributor
+                // acquire every contributor's per-warp flag
+                wait_flag(p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad));
             }
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     continue;
                 }
                 for (int cc = c_first; cc <= c_last; ++cc) {
+                    if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
                     const float* slot = p.ws + (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N);
                     const float4* s1 = reinterpret_cast<const float4*>(slot + (static_cast<int64_t>(c) * C::BM + row_in_cta) * 32);
                     const float4* s3 = reinterpret_cast<const float4*>(
@@ -390,6 +407,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     }
                 }
             }
+            if (finisher) {
+                // partials consumed: reset the contributors' flags for the next launch
+                __syncwarp();
+                if (lane == 0) {
+                    for (int cc = c_first; cc <= c_last; ++cc) {
+                        if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
+                        p.flags[(static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad] = 0u;
+                    }
+                }
+            }
             // accumulator drained: hand it back to the MMA issuer (leader CTA)
             ptx::tc_fence_before();
             __syncwarp();
@@ -402,12 +429,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             }
             if (contributor) {
                 // publish this warp's rows of the partial: every lane fences its own
-                // stores, then one release store of the launch epoch
+                // stores, then one release store of the flag
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) {
                     st_release_u32(p.flags + ((static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * 4 + quad),
-                                   p.epoch);
+                                   1u);
                 }
             }
         }

@@ -12,7 +12,7 @@
 // core consumes the rounded value exactly.
 //
 // Elementwise and HBM-bound: reads 2*N*K*esize + K*esize, writes
-// 2*Npad*K*esize.  16-byte vectors, grid-stride.
+// 2*Npad*Kpad*esize.  16-byte vectors, grid-stride.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -39,29 +39,36 @@ __device__ __forceinline__ uint32_t fold_tf32(uint32_t w, uint32_t g) {
     return rne_tf32_bits(__float_as_uint(p));
 }
 
+// Output layout (k-block tiled, so every TMA box the GEMM loads -- 2*BN rows
+// x BK elements of one (n-block, k-block) -- is one contiguous 2*BN*128-byte
+// run in HBM, which the decode-shaped weight stream needs for DRAM locality):
+//   W13t[nb][kb][j*BN + rr][i] = RNE(W_j[nb*BN + rr][kb*BK + i] * g[kb*BK + i])
+// zero where nb*BN + rr >= N (N tail) or kb*BK + i >= K (K tail).
 template <typename T>
 __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1, const T* __restrict__ w3,
                                                        const T* __restrict__ g, T* __restrict__ w13, int64_t N,
-                                                       int64_t K, int BN, int64_t n_blocks) {
+                                                       int64_t K, int BN, int64_t n_blocks, int64_t k_blocks,
+                                                       int BK) {
     constexpr int kVec = 16 / sizeof(T);
-    const int64_t kvec = K / kVec;
-    const int64_t rows = n_blocks * 2 * BN;
-    const int64_t total = rows * kvec;
-    const uint4* g4 = reinterpret_cast<const uint4*>(g);
+    const int vrow = BK / kVec;  // 16-byte vectors per packed row (8)
+    const int64_t total = n_blocks * k_blocks * 2 * BN * vrow;
     uint4* dst = reinterpret_cast<uint4*>(w13);
     for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t R = idx / kvec;
-        const int64_t kv = idx - R * kvec;
-        const int64_t nb = R / (2 * BN);
-        const int64_t within = R - nb * 2 * BN;
-        const int j = within >= BN ? 1 : 0;
-        const int64_t n = nb * BN + (within - j * BN);
+        const int v = static_cast<int>(idx % vrow);
+        const int64_t row = idx / vrow;
+        const int r2 = static_cast<int>(row % (2 * BN));
+        const int64_t rest = row / (2 * BN);
+        const int64_t kb = rest % k_blocks;
+        const int64_t nb = rest / k_blocks;
+        const int j = r2 >= BN ? 1 : 0;
+        const int64_t n = nb * BN + (r2 - j * BN);
+        const int64_t k = kb * BK + static_cast<int64_t>(v) * kVec;  // K % 8 == 0: a vector is all in or all out
         uint4 o = make_uint4(0, 0, 0, 0);
-        if (n < N) {
-            const T* src = (j == 0 ? w1 : w3) + n * K;
-            const uint4 w = reinterpret_cast<const uint4*>(src)[kv];
-            const uint4 gg = g4[kv];
+        if (n < N && k < K) {
+            const T* src = (j == 0 ? w1 : w3) + n * K + k;
+            const uint4 w = *reinterpret_cast<const uint4*>(src);
+            const uint4 gg = *reinterpret_cast<const uint4*>(g + k);
             if constexpr (sizeof(T) == 2) {
                 o.x = fold_bf16x2(w.x, gg.x);
                 o.y = fold_bf16x2(w.y, gg.y);

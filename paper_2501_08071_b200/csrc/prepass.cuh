@@ -5,7 +5,7 @@
 // memory-bound character P:549/P:573; readings R2, R3).
 //
 // HBM-bound: reads M*K*esize bytes once, writes 4*M bytes.  One warp per row,
-// 16-byte ld.global.nc loads, 4 independent loads in flight per lane, fp32
+// 16-byte ld.global.nc loads, 8 independent loads in flight per lane, fp32
 // accumulation, xor-shuffle tree.  Triggers PDL at entry so the dependent
 // dual-GEMM kernel's prologue and mainloop overlap this kernel (the GEMM only
 // needs r in its epilogue).
@@ -57,20 +57,18 @@ __global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restric
     constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte load
     const int64_t nvec = K / kVec;        // K % 8 == 0 is an API precondition
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * K);
-    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+    // 8 independent 16-byte loads in flight per lane (K = 4096 bf16: two rounds)
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int64_t i = lane;
-    for (; i + 96 < nvec; i += 128) {
-        const uint4 v0 = ld_nc_v4(xr + i);
-        const uint4 v1 = ld_nc_v4(xr + i + 32);
-        const uint4 v2 = ld_nc_v4(xr + i + 64);
-        const uint4 v3 = ld_nc_v4(xr + i + 96);
-        acc0 += sumsq_vec(v0, T{});
-        acc1 += sumsq_vec(v1, T{});
-        acc2 += sumsq_vec(v2, T{});
-        acc3 += sumsq_vec(v3, T{});
+    for (; i + 7 * 32 < nvec; i += 8 * 32) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(xr + i + u * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += sumsq_vec(v[u], T{});
     }
-    for (; i < nvec; i += 32) acc0 += sumsq_vec(ld_nc_v4(xr + i), T{});
-    float s = (acc0 + acc1) + (acc2 + acc3);
+    for (; i < nvec; i += 32) acc[0] += sumsq_vec(ld_nc_v4(xr + i), T{});
+    float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) r[row] = 1.0f / sqrtf(s / static_cast<float>(K) + eps);

@@ -55,6 +55,14 @@ def test_prepass_matches_oracle(cuda_device, dtype, M, K):
 
 
 # ------------------------------------------------------------------ a0 ------
+def unpack_w13(packed, N, K, BK):
+    """Invert the k-block-tiled layout of cuasm_ffn_get_packed:
+    [nb][kb][j*128 + rr][i] -> (W1g, W3g) as [N_pad, K_pad] arrays."""
+    nblk, kblk = (N + 127) // 128, (K + BK - 1) // BK
+    a = packed.reshape(nblk, kblk, 2, 128, BK)
+    return [a[:, :, j].transpose(0, 2, 1, 3).reshape(nblk * 128, kblk * BK) for j in (0, 1)]
+
+
 @pytest.mark.parametrize("N,K", [(128, 64), (520, 200), (1376, 256)])
 def test_pack_is_bitwise_the_oracle_fold(cuda_device, N, K):
     d = make_inputs(1, K, N, family="C", seed=200 + N, dtype="bf16")
@@ -63,26 +71,22 @@ def test_pack_is_bitwise_the_oracle_fold(cuda_device, N, K):
     h.prepare(t["g"], t["w1"], t["w3"])
     torch.cuda.synchronize()
     packed = h.packed_weights().view(torch.int16).numpy().view(np.uint16)
-    nblk = (N + 127) // 128
-    packed = packed.reshape(nblk, 2, 128, K)
-    f1 = oracle.fold(d["w1"], d["g"])
-    f3 = oracle.fold(d["w3"], d["g"])
-    for j, f in ((0, f1), (1, f3)):
-        got = packed[:, j].reshape(nblk * 128, K)
-        assert np.array_equal(got[:N], f)
-        assert np.all(got[N:] == 0)
+    for got, w in zip(unpack_w13(packed, N, K, 64), (d["w1"], d["w3"])):
+        assert np.array_equal(got[:N, :K], oracle.fold(w, d["g"]))
+        assert np.all(got[N:] == 0) and np.all(got[:, K:] == 0)
 
 
 def test_pack_fp32_is_the_oracle_tf32_fold(cuda_device):
-    N, K = 136, 64
+    N, K = 136, 72
     d = make_inputs(1, K, N, family="C", seed=300, dtype="fp32")
     h = ffn.FusedFFN(cuda_device, torch.float32)
     t = {k: v.to(cuda_device) for k, v in d.items()}
     h.prepare(t["g"], t["w1"], t["w3"])
     torch.cuda.synchronize()
-    packed = h.packed_weights().numpy().reshape(2, 2, 128, K)
-    got1 = packed[:, 0].reshape(256, K)[:N]
-    assert np.array_equal(got1, oracle.fold(d["w1"], d["g"]))
+    packed = h.packed_weights().numpy()
+    for got, w in zip(unpack_w13(packed, N, K, 32), (d["w1"], d["w3"])):
+        assert np.array_equal(got[:N, :K], oracle.fold(w, d["g"]))
+        assert np.all(got[N:] == 0) and np.all(got[:, K:] == 0)
 
 
 # --------------------------------------------------------- whole path -------
@@ -187,12 +191,17 @@ def test_invariants_bitwise(cuda_device):
     base, h = run_gpu(d, 0.0, "bf16")
     again, _ = run_gpu(d, 0.0, "bf16", handle=h)
     assert torch.equal(base, again), "run-to-run determinism"
+    # row permutation moves rows between tiles; with the whole-tile schedule a
+    # row's k-summation is then independent of its tile, so equivariance is bitwise
+    dps = ffn.SCHEDULE_DATA_PARALLEL
+    base_dp, _ = run_gpu(d, 0.0, "bf16", handle=h, schedule=dps)
     perm = torch.randperm(M, generator=torch.Generator().manual_seed(0))
     dp = dict(d, x=d["x"][perm].contiguous())
-    outp, _ = run_gpu(dp, 0.0, "bf16", handle=h)
-    assert torch.equal(outp, base[perm.to(base.device)]), "row permutation equivariance"
+    outp, _ = run_gpu(dp, 0.0, "bf16", handle=h, schedule=dps)
+    assert torch.equal(outp, base_dp[perm.to(base.device)]), "row permutation equivariance"
+    h.set_option(ffn.OPT_SCHEDULE, ffn.SCHEDULE_AUTO)
     d2 = dict(d, x=(d["x"].float() * 4.0).to(torch.bfloat16))
-    out2, _ = run_gpu(d2, 0.0, "bf16", handle=h)
+    out2, _ = run_gpu(d2, 0.0, "bf16", handle=h)  # same schedule as `base` (auto)
     assert torch.equal(out2, base), "x -> 4x at eps=0 leaves out unchanged"
     d3 = dict(d, w3=(d["w3"].float() * 2.0).to(torch.bfloat16))
     out3, _ = run_gpu(d3, 0.0, "bf16", handle=h)
@@ -264,6 +273,27 @@ def test_contract_errors_do_not_launch(cuda_device):
         assert lib.cuasm_ffn_last_error(h._h)
     torch.cuda.synchronize()
     assert torch.all(out == 7.0)
+
+
+def test_cuda_graph_replay_matches_eager(cuda_device):
+    """The forward (pre-pass + stream-K GEMM) captured in a CUDA graph and
+    replayed: identical to the eager call every time (flags are consumed and
+    reset inside the kernel, so replays need no per-launch host state)."""
+    M, K, N = 1000, 512, 2056
+    d = make_inputs(M, K, N, family="C", seed=3600, dtype="bf16")
+    eager, h = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_2SM, schedule=ffn.SCHEDULE_STREAM_K_ALL)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    out = torch.empty_like(eager)
+    h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)  # warm (weights cached)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, eager)
 
 
 def test_forward_host_matches_device_path(cuda_device):

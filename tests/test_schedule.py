@@ -1,0 +1,108 @@
+"""CPU model of the dual-GEMM persistent schedule (data-parallel tiles + a
+stream-K tail, csrc/dual_gemm.cuh `Sched` / `sk_owner` and the host-side
+split in csrc/cuasm_ffn.cu `launch_gemm`).  Checks, over many shapes, the
+properties the kernel's correctness rests on:
+  * every (tile, k-block) is computed exactly once;
+  * each tile has exactly one owner of k-block 0 (full or finisher);
+  * a finisher's contributor set (non-empty ranges between it and the owner
+    of the tile's last k-block) is exactly the set of clusters that publish a
+    partial of that tile, and each contributing cluster publishes at most once
+    (one workspace slot per cluster);
+  * contributors never wait (so the finisher -> contributor wait graph is
+    acyclic: it only points to higher cluster ids).
+"""
+import itertools
+
+import pytest
+
+
+def plan(T, KB, max_clusters, schedule=0):
+    clusters = min(T, max_clusters)
+    sk_tiles = 0
+    waves, rem = divmod(T, max_clusters)
+    if schedule != 1 and KB > 1:
+        if schedule == 2:
+            sk_tiles = T
+        elif rem != 0:
+            sk_tiles = T if waves == 0 else rem + max_clusters
+        if sk_tiles > 0:
+            clusters = min(max_clusters, sk_tiles * KB)
+    return clusters, T - sk_tiles, sk_tiles * KB
+
+
+def sk_begin(I, C, c):
+    return (I * c) // C
+
+
+def sk_owner(I, C, i):
+    c = (i * C) // max(I, 1)
+    while c + 1 < C and sk_begin(I, C, c + 1) <= i:
+        c += 1
+    while c > 0 and sk_begin(I, C, c) > i:
+        c -= 1
+    return c
+
+
+def segments(cluster, C, KB, T_dp, I):
+    t = cluster
+    while t < T_dp:
+        yield (t, 0, KB)
+        t += C
+    cur, end = sk_begin(I, C, cluster), sk_begin(I, C, cluster + 1)
+    while cur < end:
+        tt, kb0 = divmod(cur, KB)
+        take = min(KB - kb0, end - cur)
+        yield (T_dp + tt, kb0, kb0 + take)
+        cur += take
+
+
+SHAPES = list(itertools.product([1, 2, 5, 8, 16, 22, 86, 88, 96, 148, 176, 512, 688, 700, 3584],
+                                [1, 2, 3, 16, 64, 128], [74, 148], [0, 1, 2]))
+
+
+@pytest.mark.parametrize("T,KB,maxc,sched", SHAPES)
+def test_schedule_properties(T, KB, maxc, sched):
+    C, T_dp, I = plan(T, KB, maxc, sched)
+    assert 1 <= C <= maxc
+    covered = {}
+    publishes = {}
+    finishers = {}
+    for c in range(C):
+        segs = list(segments(c, C, KB, T_dp, I))
+        contrib_segs = [s for s in segs if s[1] > 0]
+        assert len(contrib_segs) <= 1, "a cluster publishes at most one partial"
+        if contrib_segs:
+            # the contributing segment is the first stream-K segment of the cluster
+            first_sk = next(s for s in segs if s[0] >= T_dp)
+            assert contrib_segs[0] == first_sk
+            publishes[contrib_segs[0][0]] = publishes.get(contrib_segs[0][0], set()) | {c}
+        for (t, kb0, kb1) in segs:
+            assert 0 <= kb0 < kb1 <= KB
+            for kb in range(kb0, kb1):
+                assert (t, kb) not in covered, "k-block computed twice"
+                covered[(t, kb)] = c
+            if kb0 == 0 and kb1 < KB:
+                assert t >= T_dp
+                tile_end = (t - T_dp + 1) * KB - 1
+                c_last = sk_owner(I, C, tile_end)
+                waits = {cc for cc in range(c + 1, c_last + 1) if sk_begin(I, C, cc) != sk_begin(I, C, cc + 1)}
+                finishers[t] = (c, waits)
+    assert len(covered) == T * KB
+    for t in range(T):
+        owners0 = covered[(t, 0)]
+        if t in finishers:
+            c, waits = finishers[t]
+            assert owners0 == c
+            assert waits == publishes.get(t, set()), (t, waits, publishes.get(t))
+            assert all(w > c for w in waits)
+        else:
+            assert t not in publishes, "partials published for a tile nobody finishes"
+            assert all(covered[(t, kb)] == owners0 for kb in range(KB))
+
+
+def test_7b_prefill_balance():
+    # 2-SM: 8 m-blocks x 86 n-blocks, 64 k-blocks, 74 CTA pairs
+    C, T_dp, I = plan(688, 64, 74)
+    work = [sum(kb1 - kb0 for _, kb0, kb1 in segments(c, C, 64, T_dp, I)) for c in range(C)]
+    assert max(work) - min(work) <= 1
+    assert max(work) == -(-688 * 64 // 74)   # ceil: 9.30 tile-equivalents per pair, not 10
