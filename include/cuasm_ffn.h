@@ -12,10 +12,11 @@
  * R2 eps inside the sqrt, R3 RMS over x not x*g, R4 fold rounding).
  *
  * Design (BASELINE.json north_star): g is folded into W1/W3 once per weight
- * set (step a0, cached in the handle), a row-wise sum-of-squares pre-pass
+ * set (step a0, cached in the handle), a row-wise sum-of-squares pass
  * produces r[m] = 1/rms (a1), and one persistent tcgen05/TMEM/TMA dual-GEMM
  * kernel computes both contractions and applies r, SiLU and the gate in its
- * epilogue (a2 + a3).  Everything runs on the caller's CUDA stream; there is
+ * epilogue (a2 + a3).  By default a1 runs inside the GEMM kernel (see
+ * CUASM_OPT_FUSED_NORM); the stand-alone pre-pass kernel remains available.  Everything runs on the caller's CUDA stream; there is
  * no CPU fallback: without an sm_100 device every entry point that would
  * compute returns CUASM_ERR_UNSUPPORTED or CUASM_ERR_CUDA.
  *
@@ -73,7 +74,13 @@ typedef enum {
                               forward on its stream (read with cuasm_ffn_profile_read);
                               forces plain ordering (no PDL) so each kernel's span is
                               its own duration.  0 (default) = off                    */
-    CUASM_OPT_SCHEDULE = 4 /* value: cuasm_schedule_t                                  */
+    CUASM_OPT_SCHEDULE = 4, /* value: cuasm_schedule_t                                 */
+    CUASM_OPT_TRACE = 5,    /* value: 1 = every dual-GEMM launch records per-CTA
+                               %globaltimer stamps (read with cuasm_ffn_trace_read)   */
+    CUASM_OPT_FUSED_NORM = 6 /* value: 1 (default) = step a1 runs inside the dual-GEMM
+                               kernel (its epilogue warps compute r while the first
+                               tile's mainloop runs; one launch per forward); 0 = the
+                               separate pre-pass kernel, PDL-overlapped with the GEMM */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -154,6 +161,15 @@ cuasm_status_t cuasm_ffn_last_launch(cuasm_ffn_t h, int* variant, int* kernels);
  * kernels and the number of forwards recorded, then reset the record.
  * Synchronous.  Any output pointer may be NULL. */
 cuasm_status_t cuasm_ffn_profile_read(cuasm_ffn_t h, double* prepass_ms, double* gemm_ms, int* forwards);
+
+/* With CUASM_OPT_TRACE on: copy the last traced dual-GEMM launch's per-CTA
+ * timeline into dst_host[ctas][16] (ns, %globaltimer; slots: 0 entry, 1 first
+ * TMA load issued, 2 last TMA load issued, 3 last MMA issued, 4 epilogue start,
+ * 5 epilogue done, 6 exit, 7 final tile handed to the epilogue, 8 first tile
+ * handed over, 9 first tile's epilogue done, 10 final tile's stream-K
+ * partials acquired, 11 final tile's epilogue done; 0 = not reached).  *ctas receives the CTA count
+ * (pass dst_host = NULL to query it).  Synchronous. */
+cuasm_status_t cuasm_ffn_trace_read(cuasm_ffn_t h, unsigned long long* dst_host, int* ctas);
 
 /* Free all handle-owned device memory and the handle.  NULL is accepted. */
 cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h);

@@ -31,14 +31,14 @@ _lib_lock = threading.Lock()
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE = 0, 1, 2, 3, 4
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM = 0, 1, 2, 3, 4, 5, 6
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL = 0, 1, 2
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
-    "cuasm_ffn_profile_read", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
+    "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
 )
 
 
@@ -74,6 +74,7 @@ def load_library():
         lib.cuasm_ffn_last_launch.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
         lib.cuasm_ffn_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ci)]
+        lib.cuasm_ffn_trace_read.argtypes = [vp, vp, ctypes.POINTER(ci)]
         lib.cuasm_ffn_destroy.argtypes = [vp]
         lib.cuasm_ffn_last_error.argtypes = [vp]
         lib.cuasm_ffn_last_error.restype = ctypes.c_char_p
@@ -146,6 +147,15 @@ class FusedFFN:
         a, b, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
         self._check(self.lib.cuasm_ffn_profile_read(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
         return a.value, b.value, n.value
+
+    def trace_read(self):
+        """Per-CTA %globaltimer stamps [ctas, 16] (ns) of the last traced GEMM launch."""
+        n = ctypes.c_int()
+        self._check(self.lib.cuasm_ffn_trace_read(self._h, None, ctypes.byref(n)))
+        buf = torch.zeros((n.value, 16), dtype=torch.int64)
+        if n.value:
+            self._check(self.lib.cuasm_ffn_trace_read(self._h, buf.data_ptr(), ctypes.byref(n)))
+        return buf
 
     def _validate(self, *ts):
         for t in ts:

@@ -45,6 +45,11 @@ struct cuasm_ffn_s {
     int use_pdl = 1;
     int group_m = 0;
     int schedule = 0;  // CUASM_OPT_SCHEDULE
+    int trace = 0;     // CUASM_OPT_TRACE
+    int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
+    uint32_t* gsync = nullptr;  // grid counters of the fused RMS pass (self-resetting)
+    unsigned long long* trace_buf = nullptr;
+    int trace_ctas = 0;
     // stream-K workspace
     float* ws = nullptr;
     int64_t ws_bytes = 0;
@@ -223,7 +228,7 @@ cuasm_status_t prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_
 }
 
 template <int kKind, int kCtaGroup>
-cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, int64_t K, int64_t N,
+cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, int64_t K, int64_t N, float eps,
                            cudaStream_t s) {
     using C = GemmCfg<kKind, kCtaGroup>;
     CUtensorMap tmap_x;
@@ -236,6 +241,10 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
         h->tmap_w_rows = C::B_ROWS;
     }
     FfnGemmParams p;
+    p.x = x;
+    p.eps = eps;
+    p.fused_norm = h->fused_norm;
+    p.sync = h->gsync;
     p.r = h->r;
     p.out = out;
     p.ldo = N;
@@ -271,7 +280,12 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     int clusters = std::min(p.num_tiles, max_clusters);
     int sk_tiles = 0;
     const int waves = p.num_tiles / max_clusters, rem = p.num_tiles % max_clusters;
-    if (h->schedule != CUASM_SCHEDULE_DATA_PARALLEL && p.num_k_blk > 1) {
+    // Stream-K pays for itself only on tensor-bound shapes: below two row
+    // blocks the weight stream is HBM-bound and whole tiles already saturate
+    // HBM (measured: profiles/r01/trace_decode), so the partial fixup is pure tail.
+    const bool sk_ok = h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
+                       (h->schedule == CUASM_SCHEDULE_AUTO && M > 128);
+    if (sk_ok && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
         else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
         // every cluster gets a non-empty range (tiny problems: fewer clusters)
@@ -283,7 +297,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     p.sk_iters = static_cast<int64_t>(sk_tiles) * p.num_k_blk;
     if (sk_tiles > 0) {
         const int64_t ws_need = static_cast<int64_t>(clusters) * kCtaGroup * C::BM * C::UMMA_N * 4;
-        const int64_t fl_need = static_cast<int64_t>(clusters) * kCtaGroup * 4 * 4;
+        const int64_t fl_need = static_cast<int64_t>(clusters) * kCtaGroup * C::NUM_EPI_WARPS * 4;
         if (ws_need > h->ws_bytes) {
             if (h->ws) cudaFree(h->ws);
             h->ws = nullptr;
@@ -302,6 +316,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     }
     p.ws = h->ws;
     p.flags = h->flags;
+    p.trace = nullptr;
+    if (h->trace) {
+        p.trace = h->trace_buf;
+        h->trace_ctas = clusters * kCtaGroup;
+    }
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * kCtaGroup), 1, 1);
@@ -368,17 +387,32 @@ cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const v
     if ((st = ensure_packed(h, g, w1, w3, K, N, s)) != CUASM_OK) return st;
     if (M == 0) return CUASM_OK;
     if ((st = ensure_r(h, M)) != CUASM_OK) return st;
+    if (h->trace) {
+        // clear the trace before the pre-pass: a memset between the pre-pass
+        // and the GEMM would break their programmatic (PDL) dependency
+        if (!h->trace_buf)
+            CUASM_CHECK(h, cudaMalloc(&h->trace_buf, sizeof(unsigned long long) * 16 * 1024), "cudaMalloc(trace)");
+        CUASM_CHECK(h, cudaMemsetAsync(h->trace_buf, 0, sizeof(unsigned long long) * 16 * 1024, s), "memset(trace)");
+    }
+    if (h->fused_norm && !h->gsync) {
+        CUASM_CHECK(h, cudaMalloc(&h->gsync, 64), "cudaMalloc(grid counters)");
+        CUASM_CHECK(h, cudaMemset(h->gsync, 0, 64), "cudaMemset(grid counters)");
+    }
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
-    if ((st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
+    // a1: fused into the dual GEMM by default; the separate pre-pass kernel
+    // (PDL primary of the GEMM) when CUASM_OPT_FUSED_NORM = 0
+    if (!h->fused_norm && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     const int v = choose_variant(h, M, K, N);
     if (h->dtype == CUASM_DTYPE_BF16) {
-        st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, s) : launch_gemm<0, 1>(h, x, out, M, K, N, s);
+        st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, eps, s)
+                                    : launch_gemm<0, 1>(h, x, out, M, K, N, eps, s);
     } else {
-        st = v == CUASM_VARIANT_2SM ? launch_gemm<1, 2>(h, x, out, M, K, N, s) : launch_gemm<1, 1>(h, x, out, M, K, N, s);
+        st = v == CUASM_VARIANT_2SM ? launch_gemm<1, 2>(h, x, out, M, K, N, eps, s)
+                                    : launch_gemm<1, 1>(h, x, out, M, K, N, eps, s);
     }
     if (st != CUASM_OK) return st;
-    h->last_kernels = 2;
+    h->last_kernels = h->fused_norm ? 1 : 2;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     return CUASM_OK;
 }
@@ -550,6 +584,14 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
             return fail(h, CUASM_ERR_INVALID_ARG, "bad schedule %lld", (long long)value);
         h->schedule = static_cast<int>(value);
         return CUASM_OK;
+    case CUASM_OPT_FUSED_NORM:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "FUSED_NORM option is 0 or 1");
+        h->fused_norm = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_TRACE:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "TRACE option is 0 or 1");
+        h->trace = static_cast<int>(value);
+        return CUASM_OK;
     case CUASM_OPT_PROFILE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "PROFILE option is 0 or 1");
         h->profile = static_cast<int>(value);
@@ -585,8 +627,23 @@ cuasm_status_t cuasm_ffn_profile_read(cuasm_ffn_t h, double* prepass_ms, double*
     return CUASM_OK;
 }
 
+cuasm_status_t cuasm_ffn_trace_read(cuasm_ffn_t h, unsigned long long* dst, int* ctas) {
+    if (!h || !ctas) return fail(h, CUASM_ERR_INVALID_ARG, "NULL argument");
+    *ctas = h->trace_buf ? h->trace_ctas : 0;
+    if (!dst || !h->trace_buf) return CUASM_OK;
+    cuasm_status_t st;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    CUASM_CHECK(h, cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    CUASM_CHECK(h, cudaMemcpy(dst, h->trace_buf, sizeof(unsigned long long) * 16 * h->trace_ctas,
+                              cudaMemcpyDeviceToHost),
+                "D2H trace");
+    return CUASM_OK;
+}
+
 cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     if (!h) return CUASM_OK;
+    if (h->trace_buf) cudaFree(h->trace_buf);
+    if (h->gsync) cudaFree(h->gsync);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     int cur = -1;
     if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device) cudaSetDevice(h->device);

@@ -15,9 +15,9 @@
 //   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
 //               tcgen05.mma (K=16 bf16 / K=8 tf32) per stage, tcgen05.commit
 //               frees the stage; a final commit hands the accumulator over
-//   warps 2..5  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//               32*(w%4)..+31 = tile rows), r-scale, SiLU, gate, bf16 pack,
-//               16-byte global stores
+//   warps 2..9  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//               32*(w%4)..+31 = tile rows, and half of the output columns),
+//               r-scale, SiLU, gate, bf16 pack, 16-byte global stores
 // TMEM holds two 2*BN-column accumulators (512 columns) so the epilogue of
 // tile i overlaps the mainloop of tile i+1.
 //
@@ -31,13 +31,19 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <type_traits>
 
+#include "prepass.cuh"
 #include "ptx.cuh"
 
 namespace cuasm {
 
 struct FfnGemmParams {
-    const float* r;  // [M] inverse RMS from the pre-pass
+    const void* x;   // [M, K] activations (fused RMS pass reads them directly)
+    float eps;
+    int fused_norm;  // 1: this kernel computes r itself (no pre-pass kernel)
+    uint32_t* sync;  // [0] warps done writing r, [1] CTAs exited (self-resetting)
+    float* r;        // [M] inverse RMS (written here when fused_norm, else by the pre-pass)
     void* out;       // [M, ldo] row-major, dtype of the handle
     int64_t ldo;     // leading dimension of out, elements
     int M, N, K;
@@ -52,7 +58,8 @@ struct FfnGemmParams {
     int64_t sk_iters;   // (num_tiles - num_dp_tiles) * num_k_blk k-block iterations,
                         // split into num_clusters contiguous ranges
     float* ws;          // stream-K partials: [cluster][cta rank][2BN/32][128][32] fp32
-    uint32_t* flags;    // [cluster][cta rank][4 epilogue warps]: 1 = partial published;
+    unsigned long long* trace;  // optional [gridDim.x][8] %globaltimer stamps (CUASM_OPT_TRACE), or null
+    uint32_t* flags;    // [cluster][cta rank][8 epilogue warps]: 1 = partial published;
                         // the finisher consumes (resets to 0) it, so launches need no
                         // per-launch state and the kernel can be replayed from a CUDA graph
 };
@@ -114,6 +121,26 @@ struct Sched {
     }
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Trace slots per CTA: 0 entry, 1 first TMA issued, 2 last TMA issued,
+// 3 last MMA issued, 4 epilogue start (after PDL wait), 5 epilogue done, 6 exit,
+// 7 final tile's accumulator handed to the epilogue (tfull wait returned).
+// 8 first tile's accumulator handed over, 9 first tile's epilogue done,
+// 10 final tile: contributor flags acquired, 11 final tile: first chunk stored.
+constexpr int kTraceSlots = 16;
+__device__ __forceinline__ void trace_stamp(const FfnGemmParams& p, int slot) {
+    if (p.trace) p.trace[blockIdx.x * kTraceSlots + slot] = globaltimer();
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -154,8 +181,12 @@ struct GemmCfg {
     static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
     static constexpr int TMEM_COLS = 512;                           // 2 accumulators x UMMA_N
-    static constexpr int NUM_EPI_WARPS = 4;
-    static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 192
+    // Two epilogue warps per TMEM lane quadrant, each owning half of the BN
+    // output columns: two warps per SM sub-partition hide the MUFU/TMEM
+    // latency of the (serially dependent) SiLU-gate math.
+    static constexpr int NUM_EPI_WARPS = 8;
+    static constexpr int EPI_COLS = BN * 4 / NUM_EPI_WARPS;        // 64 outputs per warp
+    static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 320
     static constexpr int BAR_BYTES = 1024;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + align slack
     static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
@@ -171,9 +202,22 @@ __device__ __forceinline__ void tile_coords(int t, const FfnGemmParams& p, int& 
     nb = local / gm;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float silu_gate(float h1, float h3) {
-    // SiLU(h1) * h3 = h1 / (1 + e^-h1) * h3; e^-h1 -> inf gives exactly -0 / +0.
-    return __fdividef(h1, 1.0f + __expf(-h1)) * h3;
+    // SiLU(h1) * h3 = h1 * 1/(1 + 2^(-h1*log2 e)) * h3 (MUFU ex2 + rcp, ~2 ulp each).
+    // h1 -> -inf: 2^(+big) = inf, rcp(inf) = 0, out = -0 (x) h3 -- exact limit;
+    // h1 -> +inf: rcp(1) = 1, out = h1*h3.
+    return h1 * rcp_approx(1.0f + ex2_approx(h1 * -1.4426950408889634f)) * h3;
 }
 
 template <int kKind, int kCtaGroup>
@@ -199,6 +243,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
     const bool leader = cta_rank == 0;
 
     if (warp == 0 && lane == 0) {
+        trace_stamp(p, 0);
         ptx::prefetch_tmap(&tmap_x);
         ptx::prefetch_tmap(&tmap_w);
         for (int s = 0; s < C::STAGES; ++s) {
@@ -226,10 +271,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
     if (warp == 0) {
         // ========================= TMA producer =========================
         if (lane == 0) {
+            ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
             const uint64_t pol_x = ptx::policy_evict_last();    // x is re-read by every n-block
             const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
             int stage = 0;
             uint32_t phase = 0;
+            bool first_load = true;
             Sched sch;
             sch.init(p, cluster_id);
             Seg sg;
@@ -254,9 +301,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                         ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     }
+                    if (first_load) { trace_stamp(p, 1); first_load = false; }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            trace_stamp(p, 2);
         }
     } else if (warp == 1) {
         // ========================= MMA issuer ===========================
@@ -297,11 +346,34 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
                 }
             }
+            trace_stamp(p, 3);
         }
     } else {
         // ========================= epilogue =============================
-        ptx::pdl_wait();  // r[] is produced by the pre-pass kernel (PDL primary)
+        ptx::pdl_wait();  // x / r[] come from the preceding kernel (PDL primary)
+        if (warp == 2 && lane == 0) trace_stamp(p, 4);
+        const uint32_t ewarp0 = warp - 2;
+        if (p.fused_norm) {
+            // Fused step a1: this CTA's epilogue warps compute
+            // r[m] = 1/sqrt(sum_k x^2/K + eps) for a 1/gridDim slice of the rows
+            // while the first tile's mainloop runs (they would idle otherwise),
+            // then publish through a grid-wide counter; every epilogue waits on
+            // it before its first read of r.  All CTAs are co-resident (one
+            // persistent CTA per SM), so the wait cannot deadlock.
+            const int64_t per = (static_cast<int64_t>(p.M) + gridDim.x - 1) / gridDim.x;
+            const int64_t r0 = per * blockIdx.x;
+            const int64_t r1 = min(static_cast<int64_t>(p.M), r0 + per);
+            using T = typename std::conditional<kKind == 0, __nv_bfloat16, float>::type;
+            for (int64_t m = r0 + ewarp0; m < r1; m += C::NUM_EPI_WARPS)
+                rms_row<T>(static_cast<const T*>(p.x), p.r, m, p.K, p.eps, lane);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(p.sync, 1u);
+        }
+        bool r_ready = !p.fused_norm;
         const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const uint32_t ewarp = warp - 2;  // 0..7: flag slot
+        const int col_base = static_cast<int>(ewarp >> 2) * C::EPI_COLS;  // this warp's output columns
         const uint32_t row_in_cta = quad * 32 + lane;
         int it = 0;
         Sched sch;
@@ -316,62 +388,106 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             const bool row_ok = row < p.M;
             const bool contributor = sg.kb0 > 0;                       // stream-K: partial, not the tile's start
             const bool finisher = sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
-            // this CTA's 128 x 2BN fp32 partial slot: [chunk 0..2BN/32)[row 0..127][32]
-            float* my_slot = p.ws + (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N);
+            // this CTA's 128 x 2BN fp32 partial slot, lane-contiguous so every warp
+            // access is 512 contiguous bytes: float4 index ((chunk*4 + quad)*8 + q)*32 + lane
+            // holds columns chunk*32 + 4q..+3 of row quad*32 + lane (chunk < BN/32: h1, else h3)
+            float4* my_slot = reinterpret_cast<float4*>(p.ws) +
+                              (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
             int c_first = 0, c_last = -1;
             if (finisher) {
                 // contributors: the clusters whose stream-K ranges cover the rest of this tile
                 const int64_t tile_end = static_cast<int64_t>(sg.tile - p.num_dp_tiles + 1) * p.num_k_blk - 1;
                 c_first = cluster_id + 1;
                 c_last = sk_owner(p, tile_end);
+                // pull the partials this warp will add into L2 while the accumulator
+                // is still being computed (L2 is the coherence point: safe before the flag)
+                for (int cc = c_first; cc <= c_last; ++cc) {
+                    if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
+                    const char* slot = reinterpret_cast<const char*>(
+                        reinterpret_cast<const float4*>(p.ws) +
+                        (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4));
+#pragma unroll
+                    for (int cc0 = 0; cc0 < C::EPI_COLS / 32; ++cc0) {
+                        const int c = col_base / 32 + cc0;
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {  // h1 chunk, h3 chunk: 4 KB each
+                            const int64_t chunk = c + hh * (C::BN / 32);
+                            prefetch_l2(slot + ((chunk * 4 + quad) * 8 * 32) * 16 + lane * 128);
+                        }
+                    }
+                }
             }
-            const float rr = row_ok ? __ldg(p.r + row) : 0.f;
+            if (!r_ready) {
+                const uint32_t target = gridDim.x * C::NUM_EPI_WARPS;
+                if (ld_acquire_u32(p.sync) < target) {
+#if CUASM_WATCHDOG
+                    const long long t0 = clock64();
+#endif
+                    while (ld_acquire_u32(p.sync) < target) {
+                        __nanosleep(100);
+#if CUASM_WATCHDOG
+                        if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
+#endif
+                    }
+                }
+                r_ready = true;
+            }
+            const float rr = row_ok ? __ldcg(p.r + row) : 0.f;
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
+            if (warp == 2 && lane == 0) {
+                trace_stamp(p, 7);  // (last write wins: the final tile)
+                if (it == 0) trace_stamp(p, 8);
+            }
             for (int cc = c_first; cc <= c_last; ++cc) {
                 if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;  // empty range: not a contributor
                 // acquire every contributor's per-warp flag
-                wait_flag(p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad));
+                wait_flag(p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * C::NUM_EPI_WARPS + ewarp));
             }
+            if (warp == 2 && lane == 0) trace_stamp(p, 10);
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
-            for (int c = 0; c < C::BN / 32; ++c) {
+            for (int cc0 = 0; cc0 < C::EPI_COLS / 32; ++cc0) {
+                const int c = col_base / 32 + cc0;  // 32-column chunk index within BN
                 uint32_t v1[32], v3[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, v1);
                 ptx::tmem_ld_32x32b_x32(t_row + C::BN + c * 32, v3);
                 ptx::tmem_ld_wait();
                 if (!row_ok) continue;
                 if (contributor) {
-                    float4* d1 = reinterpret_cast<float4*>(my_slot + (static_cast<int64_t>(c) * C::BM + row_in_cta) * 32);
-                    float4* d3 = reinterpret_cast<float4*>(
-                        my_slot + (static_cast<int64_t>(C::BN / 32 + c) * C::BM + row_in_cta) * 32);
+                    float4* d1 = my_slot + (static_cast<int64_t>(c) * 4 + quad) * 8 * 32 + lane;
+                    float4* d3 = my_slot + (static_cast<int64_t>(C::BN / 32 + c) * 4 + quad) * 8 * 32 + lane;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        __stcg(d1 + q, make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
-                                                   __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3])));
-                        __stcg(d3 + q, make_float4(__uint_as_float(v3[4 * q]), __uint_as_float(v3[4 * q + 1]),
-                                                   __uint_as_float(v3[4 * q + 2]), __uint_as_float(v3[4 * q + 3])));
+                        __stcg(d1 + q * 32, make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
+                                                        __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3])));
+                        __stcg(d3 + q * 32, make_float4(__uint_as_float(v3[4 * q]), __uint_as_float(v3[4 * q + 1]),
+                                                        __uint_as_float(v3[4 * q + 2]), __uint_as_float(v3[4 * q + 3])));
                     }
                     continue;
                 }
                 for (int cc = c_first; cc <= c_last; ++cc) {
                     if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
-                    const float* slot = p.ws + (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N);
-                    const float4* s1 = reinterpret_cast<const float4*>(slot + (static_cast<int64_t>(c) * C::BM + row_in_cta) * 32);
-                    const float4* s3 = reinterpret_cast<const float4*>(
-                        slot + (static_cast<int64_t>(C::BN / 32 + c) * C::BM + row_in_cta) * 32);
+                    const float4* slot = reinterpret_cast<const float4*>(p.ws) +
+                                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
+                    const float4* s1 = slot + (static_cast<int64_t>(c) * 4 + quad) * 8 * 32 + lane;
+                    const float4* s3 = slot + (static_cast<int64_t>(C::BN / 32 + c) * 4 + quad) * 8 * 32 + lane;
+                    float4 a[8], b[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const float4 a = __ldcg(s1 + q);
-                        const float4 b = __ldcg(s3 + q);
-                        v1[4 * q + 0] = __float_as_uint(__uint_as_float(v1[4 * q + 0]) + a.x);
-                        v1[4 * q + 1] = __float_as_uint(__uint_as_float(v1[4 * q + 1]) + a.y);
-                        v1[4 * q + 2] = __float_as_uint(__uint_as_float(v1[4 * q + 2]) + a.z);
-                        v1[4 * q + 3] = __float_as_uint(__uint_as_float(v1[4 * q + 3]) + a.w);
-                        v3[4 * q + 0] = __float_as_uint(__uint_as_float(v3[4 * q + 0]) + b.x);
-                        v3[4 * q + 1] = __float_as_uint(__uint_as_float(v3[4 * q + 1]) + b.y);
-                        v3[4 * q + 2] = __float_as_uint(__uint_as_float(v3[4 * q + 2]) + b.z);
-                        v3[4 * q + 3] = __float_as_uint(__uint_as_float(v3[4 * q + 3]) + b.w);
+                        a[q] = __ldcg(s1 + q * 32);
+                        b[q] = __ldcg(s3 + q * 32);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        v1[4 * q + 0] = __float_as_uint(__uint_as_float(v1[4 * q + 0]) + a[q].x);
+                        v1[4 * q + 1] = __float_as_uint(__uint_as_float(v1[4 * q + 1]) + a[q].y);
+                        v1[4 * q + 2] = __float_as_uint(__uint_as_float(v1[4 * q + 2]) + a[q].z);
+                        v1[4 * q + 3] = __float_as_uint(__uint_as_float(v1[4 * q + 3]) + a[q].w);
+                        v3[4 * q + 0] = __float_as_uint(__uint_as_float(v3[4 * q + 0]) + b[q].x);
+                        v3[4 * q + 1] = __float_as_uint(__uint_as_float(v3[4 * q + 1]) + b[q].y);
+                        v3[4 * q + 2] = __float_as_uint(__uint_as_float(v3[4 * q + 2]) + b[q].z);
+                        v3[4 * q + 3] = __float_as_uint(__uint_as_float(v3[4 * q + 3]) + b[q].w);
                     }
                 }
                 const int col0 = nb * C::BN + c * 32;
@@ -407,13 +523,17 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     }
                 }
             }
+            if (warp == 2 && lane == 0) {
+                trace_stamp(p, 11);
+                if (it == 0) trace_stamp(p, 9);
+            }
             if (finisher) {
                 // partials consumed: reset the contributors' flags for the next launch
                 __syncwarp();
                 if (lane == 0) {
                     for (int cc = c_first; cc <= c_last; ++cc) {
                         if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
-                        p.flags[(static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * 4 + quad] = 0u;
+                        p.flags[(static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * C::NUM_EPI_WARPS + ewarp] = 0u;
                     }
                 }
             }
@@ -433,19 +553,29 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) {
-                    st_release_u32(p.flags + ((static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * 4 + quad),
+                    st_release_u32(p.flags + ((static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * C::NUM_EPI_WARPS + ewarp),
                                    1u);
                 }
             }
         }
     }
 
+    if (warp >= 2 && lane == 0 && p.trace) atomicMax(p.trace + blockIdx.x * kTraceSlots + 5, globaltimer());
     // ----------------------------------------------------------- teardown --
     ptx::tc_fence_before();
     if constexpr (kCtaGroup == 2) ptx::cluster_sync(); else __syncthreads();
+    if (p.fused_norm && threadIdx.x == 0) {
+        // the last CTA out resets the grid counters for the next launch (graph-safe)
+        if (atomicAdd(p.sync + 1, 1u) == gridDim.x - 1) {
+            p.sync[0] = 0u;
+            p.sync[1] = 0u;
+            __threadfence();
+        }
+    }
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS, kCtaGroup>(tmem_base);
+        if (lane == 0) trace_stamp(p, 6);
     }
 }
 

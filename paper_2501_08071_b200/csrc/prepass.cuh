@@ -46,18 +46,15 @@ __device__ __forceinline__ float sumsq_vec(uint4 v, float) {
 
 constexpr int kPrepassRowsPerBlock = 8;  // one warp per row, 256 threads
 
+// One warp computes r[row]; used by the pre-pass kernel and by the dual GEMM's
+// fused RMS pass.  8 independent 16-byte loads in flight per lane (K = 4096
+// bf16: two rounds), fp32 accumulation, xor-shuffle tree, IEEE 1/sqrt.
 template <typename T>
-__global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restrict__ x, float* __restrict__ r,
-                                                              int64_t M, int64_t K, float eps) {
-    ptx::pdl_launch_dependents();
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kPrepassRowsPerBlock + warp;
-    if (row >= M) return;
+__device__ __forceinline__ void rms_row(const T* __restrict__ x, float* __restrict__ r, int64_t row, int64_t K,
+                                        float eps, int lane) {
     constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte load
     const int64_t nvec = K / kVec;        // K % 8 == 0 is an API precondition
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * K);
-    // 8 independent 16-byte loads in flight per lane (K = 4096 bf16: two rounds)
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int64_t i = lane;
     for (; i + 7 * 32 < nvec; i += 8 * 32) {
@@ -72,6 +69,17 @@ __global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restric
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) r[row] = 1.0f / sqrtf(s / static_cast<float>(K) + eps);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restrict__ x, float* __restrict__ r,
+                                                              int64_t M, int64_t K, float eps) {
+    ptx::pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kPrepassRowsPerBlock + warp;
+    if (row >= M) return;
+    rms_row<T>(x, r, row, K, eps, lane);
 }
 
 }  // namespace cuasm

@@ -1,0 +1,72 @@
+"""Per-CTA timeline of the dual-GEMM kernel (CUASM_OPT_TRACE) for a few shapes.
+
+Prints, relative to the earliest CTA entry of the launch (microseconds):
+entry spread, first TMA issue, last TMA issue, last MMA issue, epilogue start
+(after griddepcontrol.wait, i.e. after the pre-pass finished if PDL overlapped),
+epilogue done and exit -- min / median / max over CTAs.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_2501_08071_b200 as ffn
+from ffn_inputs import make_device_inputs
+
+SLOTS = ["entry", "first_tma", "last_tma", "last_mma", "epi_start", "epi_done", "exit", "last_tfull",
+         "first_tfull", "first_epi_done", "last_flags", "last_epi_done"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shapes", default="2048x4096x11008,16x4096x11008")
+    ap.add_argument("--json", default=None)
+    a = ap.parse_args()
+    dev = torch.device("cuda:0")
+    wbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    rbuf = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+    report = {}
+    for shp in a.shapes.split(","):
+        M, K, N = map(int, shp.split("x"))
+        t = make_device_inputs(M, K, N, 1, dev)
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        for pdl, sched in ((1, 0), (1, 1)):
+            h = ffn.FusedFFN(dev)
+            h.set_option(ffn.OPT_PDL, pdl)
+            h.set_option(ffn.OPT_SCHEDULE, sched)
+            for _ in range(3):
+                h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+            h.set_option(ffn.OPT_TRACE, 1)
+            wbuf.zero_()
+            rbuf.sum()
+            torch.cuda.synchronize()
+            torch.cuda._sleep(int(1e8))
+            h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+            tr = h.trace_read().double()
+            h.close()
+            t0 = tr[:, 0][tr[:, 0] > 0].min()
+            rows = {}
+            for i, name in enumerate(SLOTS):
+                col = tr[:, i]
+                col = col[col > 0]
+                if col.numel() == 0:
+                    continue
+                rel = (col - t0) / 1e3
+                rows[name] = {"min": round(rel.min().item(), 2), "med": round(rel.median().item(), 2),
+                              "max": round(rel.max().item(), 2)}
+            key = f"{shp} pdl={pdl} schedule={'auto' if sched == 0 else 'data-parallel'}"
+            report[key] = rows
+            print(key)
+            for name, r in rows.items():
+                print(f"   {name:10s} min {r['min']:8.2f}  med {r['med']:8.2f}  max {r['max']:8.2f} us")
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(report, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

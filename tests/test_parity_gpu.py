@@ -275,6 +275,22 @@ def test_contract_errors_do_not_launch(cuda_device):
     assert torch.all(out == 7.0)
 
 
+@pytest.mark.parametrize("M,K,N", [(16, 4096, 1024), (1000, 512, 2056), (2048, 1024, 1376)])
+def test_fused_norm_matches_separate_prepass(cuda_device, M, K, N):
+    """a1 inside the GEMM (default) and the stand-alone pre-pass kernel run the
+    same per-row code, so the outputs are bitwise identical."""
+    d = make_inputs(M, K, N, family="C", seed=3700 + M, dtype="bf16")
+    fused, h = run_gpu(d, 1e-6, "bf16")
+    assert h.last_launch()[1] == 1
+    h.set_option(ffn.OPT_FUSED_NORM, 0)
+    sep, _ = run_gpu(d, 1e-6, "bf16", handle=h)
+    assert h.last_launch()[1] == 2
+    assert torch.equal(fused, sep)
+    h.set_option(ffn.OPT_FUSED_NORM, 1)
+    again, _ = run_gpu(d, 1e-6, "bf16", handle=h)  # grid counters were reset by the last launch
+    assert torch.equal(fused, again)
+
+
 def test_cuda_graph_replay_matches_eager(cuda_device):
     """The forward (pre-pass + stream-K GEMM) captured in a CUDA graph and
     replayed: identical to the eager call every time (flags are consumed and
