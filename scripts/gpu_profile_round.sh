@@ -1,0 +1,28 @@
+#!/usr/bin/env bash
+# Full evidence set for profiles/<tag>: tests, bench lines (3 workloads +
+# reference arm), sweep, ncu launch list + full captures, per-CTA trace,
+# compute-sanitizer.  Run under gpurun from the repo root.
+set -u
+TAG=${1:-r01}
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi > $O/nvidia_smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke=$?"
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest=$?"
+timeout 600 python bench.py > $O/bench_llama7b_prefill.json 2> $O/bench.err; echo "bench=$?"
+timeout 600 python bench.py --workload llama7b_decode > $O/bench_llama7b_decode.json 2>> $O/bench.err; echo "bench_decode=$?"
+timeout 600 python bench.py --workload llama70b --skip-cpu-baseline > $O/bench_llama70b.json 2>> $O/bench.err; echo "bench_70b=$?"
+timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference.json 2>> $O/bench.err; echo "bench_ref=$?"
+timeout 900 python scripts/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1; echo "sweep=$?"
+timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,16x4096x11008,4096x8192x3584 --json $O/trace.json > $O/trace.log 2>&1; echo "trace=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_prefill.csv \
+  python bench.py --steps 5 --warmup 2 --skip-cpu-baseline --skip-e2e --no-graph > $O/ncu_launch.log 2>&1; echo "ncu_launches=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_decode.csv \
+  python bench.py --workload llama7b_decode --steps 5 --warmup 2 --skip-cpu-baseline --skip-e2e --no-graph > $O/ncu_launch_d.log 2>&1; echo "ncu_launches_d=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_prefill \
+  python bench.py --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --no-graph > $O/ncu_gemm.log 2>&1; echo "ncu_gemm=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_decode \
+  python bench.py --workload llama7b_decode --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --no-graph > $O/ncu_gemm_d.log 2>&1; echo "ncu_gemm_d=$?"
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_memcheck.log 2>&1; echo "memcheck=$?"
+timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_synccheck.log 2>&1; echo "synccheck=$?"
+timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_racecheck.log 2>&1; echo "racecheck=$?"
