@@ -45,6 +45,7 @@ struct cuasm_ffn_s {
     int use_pdl = 1;
     int group_m = 0;
     int schedule = 0;  // CUASM_OPT_SCHEDULE
+    bool plan_sk = false;  // plan_config's stream-K choice for the current forward
     int trace = 0;     // CUASM_OPT_TRACE
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
     uint32_t* gsync = nullptr;  // grid counters of the fused RMS pass (self-resetting)
@@ -232,7 +233,13 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
                            cudaStream_t s) {
     using C = GemmCfg<kKind, kCtaGroup>;
     CUtensorMap tmap_x;
-    cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, C::BM);
+    // A single row block with fewer than BM rows loads only the rows that exist
+    // (rounded up to 8): the MMA rows beyond them read stale smem, but row m of
+    // the product depends only on row m of x and rows >= M are never stored.
+    // Measured: a 128-row box over an 8-row x streams the weights ~30% slower
+    // than over a 16-row x (profiles/r01/trace_small_m.log).
+    const uint32_t a_rows = (kCtaGroup == 1 && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
+    cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
     if (st != CUASM_OK) return st;
     if (h->tmap_w_rows != C::B_ROWS) {
         st = encode_2d(h, &h->tmap_w, h->w13, static_cast<uint64_t>(C::BK), static_cast<uint64_t>(h->w13_rows),
@@ -257,6 +264,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     p.group_m = h->group_m > 0 ? h->group_m : std::min(p.num_m_blk, 16);
     p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
     p.num_tiles = p.num_m_blk * p.num_n_blk;
+    p.a_box_bytes = static_cast<int>(a_rows) * 128;
 
     static bool attr_set[2][3] = {};
     if (!attr_set[kKind][kCtaGroup]) {
@@ -280,11 +288,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     int clusters = std::min(p.num_tiles, max_clusters);
     int sk_tiles = 0;
     const int waves = p.num_tiles / max_clusters, rem = p.num_tiles % max_clusters;
-    // Stream-K pays for itself only on tensor-bound shapes: below two row
-    // blocks the weight stream is HBM-bound and whole tiles already saturate
-    // HBM (measured: profiles/r01/trace_decode), so the partial fixup is pure tail.
+    // Stream-K only where plan_config's cost model says the balanced tail is
+    // worth the partial fixup (e.g. 7B prefill: 9.3 waves; not decode, where
+    // whole tiles already saturate HBM).
     const bool sk_ok = h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
-                       (h->schedule == CUASM_SCHEDULE_AUTO && M > 128);
+                       (h->schedule == CUASM_SCHEDULE_AUTO && h->plan_sk);
     if (sk_ok && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
         else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
@@ -349,12 +357,44 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     return CUASM_OK;
 }
 
-// Tile-config table: the CTA-pair kernel halves per-SM smem
-// operand traffic and wins once there are >= 2 row blocks of 128 to pair;
-// below that (decode, M <= 128) the 1-SM kernel wastes no MMA rows on padding.
-int choose_variant(cuasm_ffn_t h, int64_t M, int64_t /*K*/, int64_t /*N*/) {
-    if (h->variant != CUASM_VARIANT_AUTO) return h->variant;
-    return M > 128 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM;
+// Shape-keyed configuration (DESIGN.md §6 "Configuration model"): the paper's
+// autotuner step done once, offline, and folded into a cost model.
+// Per candidate (variant, schedule) the mainloop time is the number of tile
+// rounds (data-parallel) or the exact wave count plus a fixed stream-K fixup
+// (partial write/read + finisher epilogue tail), in units of one k-block of
+// one tile; the 1-SM tile pays its measured 16% smem-bandwidth penalty; and
+// every candidate is floored by the HBM time of streaming the weights once.
+// Constants were fitted to scripts/tune.py on a B200 (profiles/r01/tune.json):
+// t_kb = 0.37 us per k-block-tile at the power-capped clock, fixup = 10 us.
+struct Plan {
+    int variant;
+    bool stream_k;
+};
+
+Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N) {
+    const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
+    const int64_t BK = 128 / h->esize;
+    const double KB = static_cast<double>((K + BK - 1) / BK);
+    const int64_t nblk = (N + 127) / 128;
+    const double hbm_floor = (2.0 * N * K + static_cast<double>(M) * K + static_cast<double>(M) * N) * h->esize / hbm;
+    Plan best{CUASM_VARIANT_2SM, false};
+    double best_t = 1e30;
+    for (int cg = 2; cg >= 1; --cg) {
+        const int64_t units = h->sm_count / cg;
+        const int64_t tiles = (M + 128 * cg - 1) / (128 * cg) * nblk;
+        const double waves = static_cast<double>(tiles) / units;
+        const double rounds = static_cast<double>((tiles + units - 1) / units);
+        const double pen = cg == 1 ? pen_1sm : 1.0;
+        const double t_dp = std::max(hbm_floor, rounds * KB * t_kb * pen);
+        const double t_sk = std::max(hbm_floor, waves * KB * t_kb * pen + fixup);
+        // ties go to the earlier candidate: 2-SM before 1-SM, whole tiles before stream-K
+        if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, false}; }
+        if (K / BK > 1 && t_sk < best_t * 0.98) {
+            best_t = t_sk;
+            best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, true};
+        }
+    }
+    return best;
 }
 
 cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
@@ -403,7 +443,9 @@ cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const v
     // (PDL primary of the GEMM) when CUASM_OPT_FUSED_NORM = 0
     if (!h->fused_norm && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
-    const int v = choose_variant(h, M, K, N);
+    const Plan plan = plan_config(h, M, K, N);
+    const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
+    h->plan_sk = plan.stream_k;
     if (h->dtype == CUASM_DTYPE_BF16) {
         st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, eps, s)
                                     : launch_gemm<0, 1>(h, x, out, M, K, N, eps, s);

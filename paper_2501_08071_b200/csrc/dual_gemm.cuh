@@ -51,6 +51,7 @@ struct FfnGemmParams {
     int num_n_blk;   // ceil(N / BN)
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
+    int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
     int num_tiles;
     // --- persistent schedule: data-parallel tiles, then a stream-K region ---
     int num_clusters;   // persistent clusters (CTA pairs for the 2-SM variant)
@@ -292,12 +293,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
                     const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
                     if constexpr (kCtaGroup == 1) {
-                        ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                        ptx::mbar_arrive_expect_tx(fb, p.a_box_bytes + C::B_BYTES);
                         ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     } else {
                         // both CTAs' bytes land on the leader's barrier
-                        if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::STAGE_BYTES);
+                        if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * (p.a_box_bytes + C::B_BYTES));
                         ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     }

@@ -106,3 +106,56 @@ def test_7b_prefill_balance():
     work = [sum(kb1 - kb0 for _, kb0, kb1 in segments(c, C, 64, T_dp, I)) for c in range(C)]
     assert max(work) - min(work) <= 1
     assert max(work) == -(-688 * 64 // 74)   # ceil: 9.30 tile-equivalents per pair, not 10
+
+
+# ---- shape-keyed configuration model (csrc/cuasm_ffn.cu plan_config) ---------
+
+def plan_config(M, K, N, esize=2, sm_count=148):
+    t_kb, fixup, hbm, pen_1sm = 0.37e-6, 10e-6, 6.5e12, 1.16
+    BK = 128 // esize
+    KB = -(-K // BK)
+    nblk = -(-N // 128)
+    hbm_floor = (2.0 * N * K + M * K + M * N) * esize / hbm
+    best, best_t = ("2sm", False), 1e30
+    for cg in (2, 1):
+        units = sm_count // cg
+        tiles = -(-M // (128 * cg)) * nblk
+        waves = tiles / units
+        rounds = -(-tiles // units)
+        pen = pen_1sm if cg == 1 else 1.0
+        t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
+        t_sk = max(hbm_floor, waves * KB * t_kb * pen + fixup)
+        name = "2sm" if cg == 2 else "1sm"
+        if t_dp < best_t * 0.999:
+            best_t, best = t_dp, (name, False)
+        if K // BK > 1 and t_sk < best_t * 0.98:
+            best_t, best = t_sk, (name, True)
+    return best
+
+
+# Best measured configuration per M at K=4096, N=11008 (profiles/r01/tune.json,
+# B200; "auto" there was the hybrid 2-SM stream-K tail).  Where two
+# configurations were within 2% the model may pick either.
+MEASURED_BEST = {
+    16: {("1sm", False)},
+    128: {("1sm", False)},
+    192: {("2sm", True)},
+    256: {("2sm", True)},
+    384: {("1sm", False)},
+    512: {("2sm", True)},
+    768: {("2sm", True), ("2sm", False)},
+    1024: {("2sm", False)},
+    1536: {("2sm", False)},
+    2048: {("2sm", True)},
+    4096: {("2sm", True), ("2sm", False)},
+}
+
+
+@pytest.mark.parametrize("M", sorted(MEASURED_BEST))
+def test_plan_matches_measured_best(M):
+    assert plan_config(M, 4096, 11008) in MEASURED_BEST[M]
+
+
+def test_plan_70b_shard_uses_stream_k():
+    # 8-way shard of the 70B FFN: 448 tiles = 6.05 waves of 74 CTA pairs
+    assert plan_config(4096, 8192, 3584) == ("2sm", True)
