@@ -120,9 +120,13 @@ cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x_dev, const void* r
 /* End-to-end variant for host-resident activations: copies x_host [M,K]
  * (ideally pinned) to a handle-owned device buffer, runs cuasm_ffn_forward
  * with the device-resident weights, and copies the result back into
- * out_host [M,N].  All on `stream`; synchronous w.r.t. the host only if
- * `sync` != 0 (otherwise out_host is valid after the stream completes and
- * must be pinned).  Same preconditions as cuasm_ffn_forward. */
+ * out_host [M,N].  For M >= 1024 the rows are processed in up to 8 chunks
+ * whose H2D copy, forward and D2H copy overlap on two handle-owned copy
+ * streams; `stream` waits for all of it before returning control of its
+ * queue, so work enqueued on `stream` afterwards sees out_host complete.
+ * Synchronous w.r.t. the host only if `sync` != 0 (otherwise out_host is
+ * valid after the stream completes, and both host buffers must be pinned).
+ * Same preconditions as cuasm_ffn_forward. */
 cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w_dev, const void* w1_dev,
                                       const void* w3_dev, void* out_host, int64_t M, int64_t K, int64_t N, float eps,
                                       void* stream, int sync);

@@ -71,7 +71,9 @@ struct cuasm_ffn_s {
     bool packed = false;
     CUtensorMap tmap_w;  // over w13, box {BK, B_ROWS}; B_ROWS depends on the variant
     int tmap_w_rows = 0;
-    // forward_host staging
+    // forward_host staging and its copy pipeline
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    std::vector<cudaEvent_t> copy_events;
     void* x_stage = nullptr;
     int64_t x_stage_bytes = 0;
     void* out_stage = nullptr;
@@ -550,10 +552,51 @@ cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const v
         CUASM_CHECK(h, cudaMalloc(&h->out_stage, ob), "cudaMalloc(out staging)");
         h->out_stage_bytes = ob;
     }
-    if (M > 0) CUASM_CHECK(h, cudaMemcpyAsync(h->x_stage, x_host, xb, cudaMemcpyHostToDevice, s), "H2D x");
-    st = forward_impl(h, h->x_stage, rms_w, w1, w3, h->out_stage, M, K, N, eps, s);
-    if (st != CUASM_OK) return st;
-    if (M > 0) CUASM_CHECK(h, cudaMemcpyAsync(out_host, h->out_stage, ob, cudaMemcpyDeviceToHost, s), "D2H out");
+    if (M == 0) return forward_impl(h, h->x_stage, rms_w, w1, w3, h->out_stage, 0, K, N, eps, s);
+    // Pipelined in row chunks: H2D of chunk i+1 (copy stream 1), the forward of
+    // chunk i (the caller's stream) and D2H of chunk i-1 (copy stream 2) overlap;
+    // PCIe is full duplex, so a step costs ~ the larger transfer plus one chunk.
+    if (!h->h2d_stream) {
+        CUASM_CHECK(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking), "cudaStreamCreate(h2d)");
+        CUASM_CHECK(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking), "cudaStreamCreate(d2h)");
+    }
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, M / 512));
+    const int64_t rows_per = (M + nchunk - 1) / nchunk;
+    const size_t nev = static_cast<size_t>(2 * nchunk + 2);
+    while (h->copy_events.size() < nev) {
+        cudaEvent_t e;
+        CUASM_CHECK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        h->copy_events.push_back(e);
+    }
+    cudaEvent_t ev_start = h->copy_events[0], ev_done = h->copy_events[1];
+    // staging buffers may still be in use by work already on `s`
+    CUASM_CHECK(h, cudaEventRecord(ev_start, s), "cudaEventRecord");
+    CUASM_CHECK(h, cudaStreamWaitEvent(h->h2d_stream, ev_start, 0), "cudaStreamWaitEvent");
+    CUASM_CHECK(h, cudaStreamWaitEvent(h->d2h_stream, ev_start, 0), "cudaStreamWaitEvent");
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t r0 = c * rows_per, rc = std::min(rows_per, M - r0);
+        if (rc <= 0) break;
+        cudaEvent_t ev_in = h->copy_events[2 + 2 * c], ev_out = h->copy_events[3 + 2 * c];
+        char* xs = static_cast<char*>(h->x_stage) + r0 * K * h->esize;
+        char* os = static_cast<char*>(h->out_stage) + r0 * N * h->esize;
+        CUASM_CHECK(h,
+                    cudaMemcpyAsync(xs, static_cast<const char*>(x_host) + r0 * K * h->esize, rc * K * h->esize,
+                                    cudaMemcpyHostToDevice, h->h2d_stream),
+                    "H2D x");
+        CUASM_CHECK(h, cudaEventRecord(ev_in, h->h2d_stream), "cudaEventRecord");
+        CUASM_CHECK(h, cudaStreamWaitEvent(s, ev_in, 0), "cudaStreamWaitEvent");
+        st = forward_impl(h, xs, rms_w, w1, w3, os, rc, K, N, eps, s);
+        if (st != CUASM_OK) return st;
+        CUASM_CHECK(h, cudaEventRecord(ev_out, s), "cudaEventRecord");
+        CUASM_CHECK(h, cudaStreamWaitEvent(h->d2h_stream, ev_out, 0), "cudaStreamWaitEvent");
+        CUASM_CHECK(h,
+                    cudaMemcpyAsync(static_cast<char*>(out_host) + r0 * N * h->esize, os, rc * N * h->esize,
+                                    cudaMemcpyDeviceToHost, h->d2h_stream),
+                    "D2H out");
+    }
+    // the caller's stream covers every copy: work after this call sees out_host
+    CUASM_CHECK(h, cudaEventRecord(ev_done, h->d2h_stream), "cudaEventRecord");
+    CUASM_CHECK(h, cudaStreamWaitEvent(s, ev_done, 0), "cudaStreamWaitEvent");
     if (sync) CUASM_CHECK(h, cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return CUASM_OK;
 }
@@ -687,6 +730,9 @@ cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     if (h->trace_buf) cudaFree(h->trace_buf);
     if (h->gsync) cudaFree(h->gsync);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
+    if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
+    if (h->d2h_stream) cudaStreamDestroy(h->d2h_stream);
     int cur = -1;
     if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device) cudaSetDevice(h->device);
     if (h->r) cudaFree(h->r);

@@ -312,10 +312,24 @@ def test_cuda_graph_replay_matches_eager(cuda_device):
         assert torch.equal(out, eager)
 
 
-def test_forward_host_matches_device_path(cuda_device):
-    M, K, N = 200, 256, 384
-    d = make_inputs(M, K, N, family="C", seed=3500, dtype="bf16")
+@pytest.mark.parametrize("M", [200, 2100])
+def test_forward_host_matches_device_path(cuda_device, M):
+    """forward_host (pinned host in/out; M >= 1024 runs as overlapped row chunks)
+    equals the device path: bitwise when unchunked, within tolerance of the
+    oracle when chunked (a chunk's stream-K cuts differ from the whole's)."""
+    K, N = 256, 384
+    d = make_inputs(M, K, N, family="C", seed=3500 + M, dtype="bf16")
     dev, h = run_gpu(d, 1e-6, "bf16")
     t = {k: v.to(cuda_device) for k, v in d.items()}
     host = h.forward_host(d["x"].pin_memory(), t["g"], t["w1"], t["w3"], 1e-6)
-    assert torch.equal(host, dev.cpu())
+    if M < 1024:
+        assert torch.equal(host, dev.cpu())
+    else:
+        rows = sorted(set([0, M - 1] + list(range(0, M, 37))))
+        ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+        check(host[rows], ref, "forward_host chunked")
+        # async variant: ordered on the caller's stream
+        out2 = torch.empty_like(host).pin_memory()
+        h.forward_host(d["x"].pin_memory(), t["g"], t["w1"], t["w3"], 1e-6, out_host=out2, sync=False)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(out2, host)
