@@ -17,6 +17,10 @@ Parity status per function (DESIGN.md §Oracle pins):
   ffn (fold)   pinned: reduces to plain mode when every g*w is representable,
                round_bf16 pinned against torch's independent bf16 cast
   round_tf32   pinned: hand-derived ties and Python-float reference rounding
+  gemm_act     pinned: numpy float64 matmul, identity weights, exact negative-slope
+               scaling, alpha = 1 reduces to identity
+  ffn_block    pinned: W2 = I reduces to ffn(), torch float64 composition with a
+               down projection, linearity in W2, round_hidden vs torch's bf16 cast
 """
 from __future__ import annotations
 
@@ -68,6 +72,10 @@ def _load():
             lib.oracle_fold_bf16.restype = None
             lib.oracle_fold_tf32.argtypes = [vp, vp, i64, i64, vp]
             lib.oracle_fold_tf32.restype = None
+            lib.oracle_gemm_act.argtypes = [vp, ci, vp, ci, i64, i64, i64, ci, dbl, vp]
+            lib.oracle_gemm_act.restype = ci
+            lib.oracle_ffn_block_rows.argtypes = [vp, ci, vp, vp, vp, vp, ci, i64, i64, i64, dbl, ci, ci, vp, i64, vp]
+            lib.oracle_ffn_block_rows.restype = ci
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = ci
             _lib = lib
@@ -139,6 +147,51 @@ def ffn(x, g, w1, w3, eps: float = 1e-6, mode: str = "plain", rows=None) -> np.n
                              rows_arr.shape[0], out.ctypes.data)
     if st != 0:
         raise RuntimeError(f"oracle_ffn_rows failed with status {st}")
+    return out
+
+
+def gemm_act(x, w, act: str = "identity", alpha: float = 0.01) -> np.ndarray:
+    """out = act(x @ w^T) in fp64; act in {"identity", "leaky_relu"} (slope alpha).
+    The paper's mmLeakyReLu kernel."""
+    lib = _load()
+    xs, xdt = _as_storage(x)
+    ws, wdt = _as_storage(w)
+    M, K = xs.shape
+    N, K2 = ws.shape
+    if K2 != K:
+        raise ValueError("oracle: shape mismatch")
+    out = np.empty((M, N), dtype=np.float64)
+    st = lib.oracle_gemm_act(xs.ctypes.data, xdt, ws.ctypes.data, wdt, M, K, N,
+                             {"identity": 0, "leaky_relu": 1}[act], float(alpha), out.ctypes.data)
+    if st != 0:
+        raise RuntimeError(f"oracle_gemm_act failed with status {st}")
+    return out
+
+
+def ffn_block(x, g, w1, w3, w2, eps: float = 1e-6, mode: str = "plain", round_hidden: bool = False,
+              rows=None) -> np.ndarray:
+    """y[rows] = hidden @ w2^T with hidden = ffn(x, g, w1, w3, eps, mode) (fp64;
+    rounded to bf16 first when round_hidden -- DESIGN.md R13).  w2 [K,N]."""
+    lib = _load()
+    xs, xdt = _as_storage(x)
+    gs, gdt = _as_storage(g)
+    w1s, wdt = _as_storage(w1)
+    w3s, wdt3 = _as_storage(w3)
+    w2s, wdt2 = _as_storage(w2)
+    if not (gdt == wdt == wdt3 == wdt2):
+        gs, w1s, w3s, w2s = (_widen(a, dt) for a, dt in ((gs, gdt), (w1s, wdt), (w3s, wdt3), (w2s, wdt2)))
+        wdt = DT_F64
+    M, K = xs.shape
+    N = w1s.shape[0]
+    if w2s.shape != (K, N):
+        raise ValueError("oracle: w2 must be [K,N]")
+    rows_arr = np.arange(M, dtype=np.int64) if rows is None else np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    out = np.empty((rows_arr.shape[0], K), dtype=np.float64)
+    st = lib.oracle_ffn_block_rows(xs.ctypes.data, xdt, gs.ctypes.data, w1s.ctypes.data, w3s.ctypes.data,
+                                   w2s.ctypes.data, wdt, M, K, N, float(eps), MODES[mode], int(bool(round_hidden)),
+                                   rows_arr.ctypes.data, rows_arr.shape[0], out.ctypes.data)
+    if st != 0:
+        raise RuntimeError(f"oracle_ffn_block_rows failed with status {st}")
     return out
 
 

@@ -253,3 +253,59 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* ---- f3: GEMM + activation (the paper's mmLeakyReLu) ----------------------- */
+/*
+ * PAPER.md P:523 / P:562 ("mmLeakyReLu", inputs B, M, N, K = 1, 512, 512, 2048):
+ * a matrix multiplication whose epilogue applies LeakyReLU.  Definition
+ * (R14: nn.Linear weight layout, negative slope alpha):
+ *     out[m,n] = act( sum_k x[m,k] * w[n,k] ),
+ *     act(t) = t (act = 0)  or  t >= 0 ? t : alpha * t (act = 1).
+ * Sequential k-sums in fp64; out [M,N] double.
+ */
+int oracle_gemm_act(const void* x, int x_dtype, const void* w, int w_dtype, int64_t M, int64_t K, int64_t N,
+                    int act, double alpha, double* out) {
+    if (!x || !w || !out || M < 0 || K <= 0 || N <= 0 || (act != 0 && act != 1)) return -1;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k)
+                acc += load_elem(x, x_dtype, m * K + k) * load_elem(w, w_dtype, n * K + k);
+            out[m * N + n] = (act == 1 && acc < 0.0) ? alpha * acc : acc;
+        }
+    }
+    return 0;
+}
+
+/* ---- f1: the whole feed-forward block -------------------------------------- */
+/*
+ * y[m,j] = sum_n hidden[m,n] * W2[j,n],  hidden = the fused FFN above (rows of
+ * oracle_ffn_rows in `mode`), W2 [K,N] (nn.Linear(N -> K) layout).
+ * round_hidden != 0: hidden is first rounded to bf16 (RNE) -- the method
+ * materialises the hidden activation in the storage precision between its two
+ * GEMMs (R13); 0 keeps it exact.  out [nrows, K] double.
+ */
+int oracle_ffn_block_rows(const void* x, int x_dtype, const void* g, const void* w1, const void* w3, const void* w2,
+                          int w_dtype, int64_t M, int64_t K, int64_t N, double eps, int mode, int round_hidden,
+                          const int64_t* rows, int64_t nrows, double* out) {
+    if (!w2 || !out || nrows < 0) return -1;
+    if (nrows == 0) return 0;
+    double* hid = (double*)malloc(sizeof(double) * (size_t)nrows * (size_t)N);
+    if (!hid) return -2;
+    int st = oracle_ffn_rows(x, x_dtype, g, w1, w3, w_dtype, M, K, N, eps, mode, rows, nrows, hid);
+    if (st != 0) { free(hid); return st; }
+    if (round_hidden) {
+        for (int64_t i = 0; i < nrows * N; ++i) hid[i] = oracle_round_bf16(hid[i]);
+    }
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < nrows; ++i) {
+        for (int64_t j = 0; j < K; ++j) {
+            double acc = 0.0;
+            for (int64_t n = 0; n < N; ++n) acc += hid[i * N + n] * load_elem(w2, w_dtype, j * N + n);
+            out[i * K + j] = acc;
+        }
+    }
+    free(hid);
+    return 0;
+}

@@ -30,5 +30,9 @@ s|a = oracle_round_bf16(a \* G\[k\]);|a = a * G[k];|
 s|uint32_t bias = (1u << (drop - 1)) - 1u + lsb;|uint32_t bias = (1u << (drop - 1));|
 s|if (mode != ORACLE_PLAIN) { h1 \*= R\[i\]; h3 \*= R\[i\]; }|if (mode != ORACLE_PLAIN) { h1 *= R[i]; }|
 s|dst_bits\[n \* K + k\] = oracle_round_bf16_bits(bf16_bits_to_double(w\[n \* K + k\]) \*|dst_bits[n * K + k] = oracle_round_bf16_bits(bf16_bits_to_double(w[n * K + k]) + 0 *|
+s|out\[m \* N + n\] = (act == 1 \&\& acc < 0.0) ? alpha \* acc : acc;|out[m * N + n] = (act == 1 \&\& acc < 0.0) ? 0.01 * acc : acc;|
+s|acc += load_elem(x, x_dtype, m \* K + k) \* load_elem(w, w_dtype, n \* K + k);|acc += load_elem(x, x_dtype, m * K + k) * load_elem(w, w_dtype, k * N + n % K);|
+s|for (int64_t n = 0; n < N; ++n) acc += hid\[i \* N + n\] \* load_elem(w2, w_dtype, j \* N + n);|for (int64_t n = 0; n < N; ++n) acc += hid[i * N + n] * load_elem(w2, w_dtype, n * K + j % N);|
+s|for (int64_t i = 0; i < nrows \* N; ++i) hid\[i\] = oracle_round_bf16(hid\[i\]);|for (int64_t i = 0; i < nrows * N; ++i) hid[i] = (double)(float)hid[i];|
 MUTS
 exit $status

@@ -265,3 +265,69 @@ def test_fold_tf32_reference():
     ref = np.vectorize(lambda v: 0.0 if v == 0 else math.ldexp(round(math.frexp(v)[0] * 2 ** 11) / 2 ** 11,
                                                                math.frexp(v)[1]))(prod)
     assert np.array_equal(got.astype(np.float64), ref)
+
+
+# ---- f3: GEMM + LeakyReLU (the paper's mmLeakyReLu) ------------------------
+
+def test_gemm_act_matches_numpy_and_closed_forms():
+    rng = np.random.default_rng(20)
+    x = rng.standard_normal((7, 40))
+    w = rng.standard_normal((9, 40))
+    ref = x @ w.T
+    np.testing.assert_allclose(oracle.gemm_act(x, w), ref, rtol=1e-12, atol=1e-12)
+    lr = oracle.gemm_act(x, w, "leaky_relu", 0.01)
+    np.testing.assert_allclose(lr, np.where(ref >= 0, ref, 0.01 * ref), rtol=1e-12, atol=1e-12)
+    # negative entries are scaled by exactly alpha (a power of two: bitwise)
+    pos = oracle.gemm_act(x, w)
+    lr2 = oracle.gemm_act(x, w, "leaky_relu", 0.25)
+    assert np.array_equal(lr2, np.where(pos >= 0, pos, 0.25 * pos))
+    # alpha = 1 is the identity; identity weights return act(x)
+    assert np.array_equal(oracle.gemm_act(x, w, "leaky_relu", 1.0), pos)
+    eye = np.eye(40)
+    np.testing.assert_array_equal(oracle.gemm_act(x, eye, "leaky_relu", 0.5), np.where(x >= 0, x, 0.5 * x))
+
+
+def test_gemm_act_paper_shape_bf16_storage():
+    d = make_inputs(512, 2048, 512, family="C", seed=21, dtype="bf16")
+    out = oracle.gemm_act(d["x"][:8], d["w1"], "leaky_relu", 0.01)
+    ref = d["x"][:8].double() @ d["w1"].double().T
+    ref = torch.where(ref >= 0, ref, 0.01 * ref).numpy()
+    np.testing.assert_allclose(out, ref, rtol=1e-11, atol=1e-12)
+
+
+# ---- f1: the feed-forward block with its down projection -------------------------
+
+def test_ffn_block_identity_w2_reduces_to_ffn():
+    K = N = 48
+    d = make_inputs(6, K, N, family="C", seed=22, dtype="bf16")
+    eye = torch.eye(K, dtype=torch.float64)
+    blk = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], eye)
+    np.testing.assert_allclose(blk, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"]), rtol=1e-13, atol=1e-15)
+
+
+def test_ffn_block_matches_torch_composition_and_is_linear_in_w2():
+    M, K, N = 11, 64, 96
+    d = make_inputs(M, K, N, family="C", seed=23, dtype="bf16")
+    w2 = make_inputs(1, N, K, family="C", seed=24, dtype="bf16")["w1"]   # [K, N]
+    x, g, w1, w3 = (d[k].double() for k in ("x", "g", "w1", "w3"))
+    xn = F.rms_norm(x, (K,), g, eps=1e-6)
+    ref = F.linear(F.silu(F.linear(xn, w1)) * F.linear(xn, w3), w2.double()).numpy()
+    blk = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2)
+    np.testing.assert_allclose(blk, ref, rtol=1e-11, atol=1e-13)
+    blk2 = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], (w2.float() * 2).to(torch.bfloat16))
+    assert np.array_equal(blk2, 2 * blk)
+    # rows subset
+    sub = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, rows=[3, 10])
+    assert np.array_equal(sub, blk[[3, 10]])
+
+
+def test_ffn_block_round_hidden_uses_bf16_rne():
+    M, K, N = 5, 64, 32
+    d = make_inputs(M, K, N, family="C", seed=25, dtype="bf16")
+    w2 = torch.zeros(K, N, dtype=torch.float64)
+    w2[torch.arange(N), torch.arange(N)] = 1.0          # picks hidden[:, :N] into out[:, :N]
+    blk = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, round_hidden=True)
+    hid = torch.from_numpy(oracle.ffn(d["x"], d["g"], d["w1"], d["w3"]))
+    # torch's independent RNE; both round fp64 -> fp32 -> bf16 (the oracle's documented path)
+    ref = hid.float().to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(blk[:, :N], ref)
