@@ -58,6 +58,12 @@ typedef enum {
 
 typedef enum { CUASM_DTYPE_BF16 = 0, CUASM_DTYPE_FP32 = 1 } cuasm_dtype_t;
 
+/* Activation of cuasm_gemm_act. */
+typedef enum {
+    CUASM_ACT_IDENTITY = 0,  /* out = acc                                   */
+    CUASM_ACT_LEAKY_RELU = 1 /* out = acc >= 0 ? acc : alpha * acc           */
+} cuasm_act_t;
+
 /* Kernel-variant selector (cuasm_ffn_set_option with CUASM_OPT_VARIANT). */
 typedef enum {
     CUASM_VARIANT_AUTO = 0, /* shape-keyed choice */
@@ -130,6 +136,30 @@ cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x_dev, const void* r
 cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w_dev, const void* w1_dev,
                                       const void* w3_dev, void* out_host, int64_t M, int64_t K, int64_t N, float eps,
                                       void* stream, int sync);
+
+/* GEMM with a fused activation on the same tcgen05/TMA machinery:
+ *   out[m,n] = act( sum_k x[m,k] * w[n,k] ),   act = cuasm_act_t, alpha its slope.
+ * The paper's "mmLeakyReLu" kernel (Table "Evaluated Kernels"
+ * B,M,N,K = 1,512,512,2048; matmul + LeakyReLU epilogue, the kernel of
+ * its Table 3 SASS analysis P:630-652) and, with CUASM_ACT_IDENTITY, the FFN's
+ * down projection.  x [M,K], w [N,K] (nn.Linear layout), out [M,N]: device,
+ * 16-byte aligned, the handle's dtype; w is packed into a handle-owned cache
+ * (slot separate from the W1/W3 cache) on first use.  Same size and error
+ * rules as cuasm_ffn_forward (K % 8 == 0, N % 8 == 0, M == 0 -> no launch). */
+cuasm_status_t cuasm_gemm_act(cuasm_ffn_t h, const void* x_dev, const void* w_dev, void* out_dev, int64_t M,
+                              int64_t K, int64_t N, int act, float alpha, void* stream);
+
+/* The whole LLaMA feed-forward block (PAPER.md P:68's fused
+ * feed-forward followed by its down projection):
+ *   out[m,k] = sum_n hidden[m,n] * w2[k,n],
+ *   hidden   = SiLU(RMSNorm(x) W1^T) (.) (RMSNorm(x) W3^T)   stored in the handle dtype
+ * x [M,K], rms_w [K], w1/w3 [N,K], w2 [K,N] (nn.Linear(N -> K) layout),
+ * out [M,K]; two kernel launches (the fused FFN, then cuasm_gemm_act's GEMM
+ * with identity activation) through a handle-owned hidden buffer.  Same
+ * preconditions as cuasm_ffn_forward; w2 16-byte aligned. */
+cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev, const void* w1_dev,
+                                       const void* w3_dev, const void* w2_dev, void* out_dev, int64_t M, int64_t K,
+                                       int64_t N, float eps, void* stream);
 
 /* Step a0 alone: fold g into W1/W3 and pack (one-time weight preparation,
  * PAPER.md P:434-447's offline/deploy split).  Same weight preconditions. */

@@ -19,7 +19,8 @@ import weakref
 import torch
 
 __all__ = [
-    "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "CuasmError", "lib_path", "load_library",
+    "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "gemm_act", "ffn_block_forward", "CuasmError",
+    "lib_path", "load_library",
     "VARIANT_AUTO", "VARIANT_1SM", "VARIANT_2SM", "EXPORTED_SYMBOLS",
 ]
 
@@ -30,13 +31,15 @@ _lib_lock = threading.Lock()
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
+ACT_IDENTITY, ACT_LEAKY_RELU = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
 OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM = 0, 1, 2, 3, 4, 5, 6
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL = 0, 1, 2
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
-    "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
+    "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_gemm_act", "cuasm_ffn_block_forward",
+    "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
     "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
 )
@@ -66,6 +69,8 @@ def load_library():
         lib.cuasm_ffn_init.argtypes = [ctypes.POINTER(vp), ci, ci]
         lib.cuasm_ffn_forward.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
         lib.cuasm_ffn_forward_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp, ci]
+        lib.cuasm_gemm_act.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, f32, vp]
+        lib.cuasm_ffn_block_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
         lib.cuasm_ffn_prepare.argtypes = [vp, vp, vp, vp, i64, i64, vp]
         lib.cuasm_ffn_rms_inv.argtypes = [vp, vp, vp, i64, i64, f32, vp]
         lib.cuasm_ffn_get_packed.argtypes = [vp, vp, ctypes.POINTER(i64)]
@@ -114,7 +119,7 @@ class FusedFFN:
         if st != OK:
             raise CuasmError(st, self.lib.cuasm_ffn_last_error(None).decode())
         self._h = h
-        self._wkey = None
+        self._wkey = {}
 
     def close(self):
         if getattr(self, "_h", None):
@@ -166,23 +171,29 @@ class FusedFFN:
             if not t.is_contiguous():
                 raise ValueError("tensors must be contiguous")
 
-    def _weights_changed(self, rms_w, w1, w3):
-        # The library caches the folded weights keyed by pointer.  A pointer
-        # alone is not an identity (the caching allocator reuses addresses),
-        # so the binding keys on the tensor objects themselves (weak refs) and
-        # their in-place version counters, and invalidates on any change.
-        same = (self._wkey is not None
-                and all(r() is t for r, t in zip(self._wkey[0], (rms_w, w1, w3)))
-                and self._wkey[1] == tuple(t._version for t in (rms_w, w1, w3)))
+    def _weights_changed(self, *ws, slot: int = 0):
+        # The library caches packed weights keyed by pointer (slot 0: the
+        # folded W1/W3, slot 1: a single GEMM weight).  A pointer alone is not
+        # an identity (the caching allocator reuses addresses), so the binding
+        # keys on the tensor objects themselves (weak refs) and their in-place
+        # version counters, and invalidates the cache on any change.
+        key = self._wkey.get(slot)
+        new = (tuple(weakref.ref(t) for t in ws), tuple(t._version for t in ws))
+        if key is None:
+            # first use in this slot (or after an invalidation): the library's
+            # pointer key decides, and an invalidated slot re-packs anyway
+            self._wkey[slot] = new
+            return
+        same = (len(key[0]) == len(ws) and all(r() is t for r, t in zip(key[0], ws)) and key[1] == new[1])
         if not same:
+            # the library's invalidation drops every cached pack: forget all keys
             self._check(self.lib.cuasm_ffn_invalidate_weights(self._h))
-            self._wkey = (tuple(weakref.ref(t) for t in (rms_w, w1, w3)),
-                          tuple(t._version for t in (rms_w, w1, w3)))
+            self._wkey = {slot: new}
 
     def prepare(self, rms_w, w1, w3):
         self._validate(rms_w, w1, w3)
         N, K = w1.shape
-        self._weights_changed(rms_w, w1, w3)
+        self._weights_changed(rms_w, w1, w3, slot=0)
         self._check(self.lib.cuasm_ffn_prepare(self._h, rms_w.data_ptr(), w1.data_ptr(), w3.data_ptr(), K, N,
                                                _stream_ptr(w1.device)))
 
@@ -200,7 +211,7 @@ class FusedFFN:
             self._validate(out)
             if out.shape != (M, N):
                 raise ValueError("out must be [M,N]")
-        self._weights_changed(rms_w, w1, w3)
+        self._weights_changed(rms_w, w1, w3, slot=0)
         self._check(self.lib.cuasm_ffn_forward(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                w3.data_ptr(), out.data_ptr(), M, K, N, float(eps),
                                                _stream_ptr(x.device)))
@@ -215,11 +226,47 @@ class FusedFFN:
         N = w1.shape[0]
         if out_host is None:
             out_host = torch.empty((M, N), dtype=self.dtype, pin_memory=True)
-        self._weights_changed(rms_w, w1, w3)
+        self._weights_changed(rms_w, w1, w3, slot=0)
         self._check(self.lib.cuasm_ffn_forward_host(self._h, x_host.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                     w3.data_ptr(), out_host.data_ptr(), M, K, N, float(eps),
                                                     _stream_ptr(w1.device), 1 if sync else 0))
         return out_host
+
+    def gemm_act(self, x, w, act: str = "identity", alpha: float = 0.01, out=None):
+        """out = act(x @ w.T) on the tensor cores (the paper's mmLeakyReLu for
+        act="leaky_relu"; a plain GEMM for "identity").  x [M,K], w [N,K]."""
+        self._validate(x, w)
+        M, K = x.shape
+        N = w.shape[0]
+        if w.shape[1] != K:
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty((M, N), dtype=self.dtype, device=x.device)
+        else:
+            self._validate(out)
+        self._weights_changed(w, slot=1)
+        code = {"identity": ACT_IDENTITY, "leaky_relu": ACT_LEAKY_RELU}[act]
+        self._check(self.lib.cuasm_gemm_act(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), M, K, N, code,
+                                            float(alpha), _stream_ptr(x.device)))
+        return out
+
+    def block_forward(self, x, rms_w, w1, w3, w2, eps: float = 1e-6, out=None):
+        """The LLaMA feed-forward block: (SiLU(RMSNorm(x) W1^T) * (RMSNorm(x) W3^T)) W2^T.
+        x [M,K], w1/w3 [N,K], w2 [K,N] -> out [M,K]."""
+        self._validate(x, rms_w, w1, w3, w2)
+        M, K = x.shape
+        N = w1.shape[0]
+        if w2.shape != (K, N) or w1.shape != (N, K) or w3.shape != (N, K):
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty((M, K), dtype=self.dtype, device=x.device)
+        else:
+            self._validate(out)
+        self._weights_changed(rms_w, w1, w3, w2, slot=2)
+        self._check(self.lib.cuasm_ffn_block_forward(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
+                                                     w3.data_ptr(), w2.data_ptr(), out.data_ptr(), M, K, N,
+                                                     float(eps), _stream_ptr(x.device)))
+        return out
 
     def rms_inv(self, x, eps: float = 1e-6, out=None):
         self._validate(x)
@@ -263,3 +310,13 @@ def ffn_forward_host(x_host, rms_w, w1, w3, eps: float = 1e-6, out_host=None, sy
 
 def rms_inv(x, eps: float = 1e-6):
     return _handle(x.device, x.dtype).rms_inv(x, eps)
+
+
+def gemm_act(x, w, act: str = "identity", alpha: float = 0.01, out=None):
+    """act(x @ w.T) on the tensor cores (mmLeakyReLu for act="leaky_relu")."""
+    return _handle(x.device, x.dtype).gemm_act(x, w, act, alpha, out)
+
+
+def ffn_block_forward(x, rms_w, w1, w3, w2, eps: float = 1e-6, out=None):
+    """The whole LLaMA feed-forward block, W2 [K,N] the down projection."""
+    return _handle(x.device, x.dtype).block_forward(x, rms_w, w1, w3, w2, eps, out)

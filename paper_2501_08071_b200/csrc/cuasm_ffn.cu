@@ -32,6 +32,20 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// One packed (k-block tiled, TMA-ready) weight matrix cached in a handle.
+struct PackedWeights {
+    void* buf = nullptr;
+    int64_t bytes = 0;
+    int64_t rows = 0;     // rows of 128 bytes
+    const void* key_g = nullptr;
+    const void* key_w1 = nullptr;
+    const void* key_w3 = nullptr;
+    int64_t key_K = 0, key_N = 0;
+    bool packed = false;
+    CUtensorMap tmap;     // box {BK, tmap_rows}; tmap_rows = B_ROWS of the launched variant
+    int tmap_rows = 0;
+};
+
 }  // namespace
 
 struct cuasm_ffn_s {
@@ -59,18 +73,12 @@ struct cuasm_ffn_s {
     // a1 workspace
     float* r = nullptr;
     int64_t r_cap = 0;
-    // a0 cache
-    void* w13 = nullptr;
-    int64_t w13_bytes = 0;
-    int64_t w13_rows = 0;     // rows of 128 bytes in the k-block-tiled W13
-    int64_t w13_kblocks = 0;
-    const void* key_g = nullptr;
-    const void* key_w1 = nullptr;
-    const void* key_w3 = nullptr;
-    int64_t key_K = 0, key_N = 0;
-    bool packed = false;
-    CUtensorMap tmap_w;  // over w13, box {BK, B_ROWS}; B_ROWS depends on the variant
-    int tmap_w_rows = 0;
+    // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN;
+    // slot 1 = a single packed weight (GEMM + activation / down projection)
+    PackedWeights pw[2];
+    // FFN block: the hidden activation between the two GEMMs
+    void* hidden = nullptr;
+    int64_t hidden_bytes = 0;
     // forward_host staging and its copy pipeline
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     std::vector<cudaEvent_t> copy_events;
@@ -160,47 +168,52 @@ cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint
     return CUASM_OK;
 }
 
+// a0: fold g (optional) into the weights and write the k-block tiled layout
+// (pack.cuh) into cache slot `slot`.  w3 != null: the interleaved W13 of the
+// fused FFN (128-output blocks); w3 == null: one weight, 256-row blocks.
 template <typename T>
-cuasm_status_t launch_pack(cuasm_ffn_t h, const void* g, const void* w1, const void* w3, int64_t K, int64_t N,
-                           cudaStream_t s) {
+cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
+                           int64_t N, cudaStream_t s) {
+    PackedWeights& w = h->pw[slot];
     const int BK = 128 / h->esize;  // one 128-byte swizzle row of K (= GemmCfg::BK)
-    const int64_t n_blocks = (N + kPackBN - 1) / kPackBN;
+    const int64_t rows_per_block = 2 * kPackBN;
+    const int64_t n_blocks = w3 ? (N + kPackBN - 1) / kPackBN : (N + rows_per_block - 1) / rows_per_block;
     const int64_t k_blocks = (K + BK - 1) / BK;
-    const int64_t rows = n_blocks * k_blocks * 2 * kPackBN;
+    const int64_t rows = n_blocks * k_blocks * rows_per_block;
     const int64_t bytes = rows * 128;
-    if (bytes > h->w13_bytes) {
-        if (h->w13) cudaFree(h->w13);
-        h->w13 = nullptr;
-        h->w13_bytes = 0;
-        CUASM_CHECK(h, cudaMalloc(&h->w13, bytes), "cudaMalloc(W13)");
-        h->w13_bytes = bytes;
+    if (bytes > w.bytes) {
+        if (w.buf) cudaFree(w.buf);
+        w.buf = nullptr;
+        w.bytes = 0;
+        CUASM_CHECK(h, cudaMalloc(&w.buf, bytes), "cudaMalloc(packed weights)");
+        w.bytes = bytes;
     }
     const int64_t total_vec = bytes / 16;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>((total_vec + threads - 1) / threads, int64_t(h->sm_count) * 16);
     cuasm::ffn_pack_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, s>>>(
-        static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(h->w13), N,
-        K, kPackBN, n_blocks, k_blocks, BK);
+        static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(w.buf), N, K,
+        kPackBN, n_blocks, k_blocks, BK);
     CUASM_CHECK(h, cudaGetLastError(), "ffn_pack_kernel launch");
-    h->w13_rows = rows;
-    h->w13_kblocks = k_blocks;
-    h->tmap_w_rows = 0;  // re-encode for the new buffer
-    h->key_g = g;
-    h->key_w1 = w1;
-    h->key_w3 = w3;
-    h->key_K = K;
-    h->key_N = N;
-    h->packed = true;
+    w.rows = rows;
+    w.tmap_rows = 0;  // re-encode for the new buffer
+    w.key_g = g;
+    w.key_w1 = w1;
+    w.key_w3 = w3;
+    w.key_K = K;
+    w.key_N = N;
+    w.packed = true;
     return CUASM_OK;
 }
 
-cuasm_status_t ensure_packed(cuasm_ffn_t h, const void* g, const void* w1, const void* w3, int64_t K, int64_t N,
-                             cudaStream_t s) {
-    if (h->packed && h->key_g == g && h->key_w1 == w1 && h->key_w3 == w3 && h->key_K == K && h->key_N == N)
+cuasm_status_t ensure_packed(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
+                             int64_t N, cudaStream_t s) {
+    PackedWeights& w = h->pw[slot];
+    if (w.packed && w.key_g == g && w.key_w1 == w1 && w.key_w3 == w3 && w.key_K == K && w.key_N == N)
         return CUASM_OK;
-    h->packed = false;
-    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, g, w1, w3, K, N, s)
-                                        : launch_pack<float>(h, g, w1, w3, K, N, s);
+    w.packed = false;
+    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, slot, g, w1, w3, K, N, s)
+                                        : launch_pack<float>(h, slot, g, w1, w3, K, N, s);
 }
 
 template <typename T>
@@ -230,10 +243,20 @@ cuasm_status_t prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_
                                         : launch_prepass<float>(h, x, r, M, K, eps, s);
 }
 
-template <int kKind, int kCtaGroup>
-cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, int64_t K, int64_t N, float eps,
-                           cudaStream_t s) {
-    using C = GemmCfg<kKind, kCtaGroup>;
+// What one dual-GEMM launch computes (FfnGemmParams fields the host sets).
+struct EpiSpec {
+    int slot;        // packed-weight cache slot (0: W13, 1: single weight)
+    int fused_norm;  // compute r in-kernel
+    int use_r;       // scale by r
+    int act;         // kEpi == 1: 0 identity, 1 LeakyReLU
+    float alpha;
+};
+
+template <int kKind, int kCtaGroup, int kEpi>
+cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
+                           int64_t N, float eps, cudaStream_t s) {
+    using C = GemmCfg<kKind, kCtaGroup, kEpi>;
+    PackedWeights& w = h->pw[e.slot];
     CUtensorMap tmap_x;
     // A single row block with fewer than BM rows loads only the rows that exist
     // (rounded up to 8): the MMA rows beyond them read stale smem, but row m of
@@ -243,16 +266,19 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     const uint32_t a_rows = (kCtaGroup == 1 && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
     if (st != CUASM_OK) return st;
-    if (h->tmap_w_rows != C::B_ROWS) {
-        st = encode_2d(h, &h->tmap_w, h->w13, static_cast<uint64_t>(C::BK), static_cast<uint64_t>(h->w13_rows),
-                       C::BK, C::B_ROWS);
+    if (w.tmap_rows != C::B_ROWS) {
+        st = encode_2d(h, &w.tmap, w.buf, static_cast<uint64_t>(C::BK), static_cast<uint64_t>(w.rows), C::BK,
+                       C::B_ROWS);
         if (st != CUASM_OK) return st;
-        h->tmap_w_rows = C::B_ROWS;
+        w.tmap_rows = C::B_ROWS;
     }
     FfnGemmParams p;
     p.x = x;
     p.eps = eps;
-    p.fused_norm = h->fused_norm;
+    p.fused_norm = e.fused_norm;
+    p.use_r = e.use_r;
+    p.act = e.act;
+    p.alpha = e.alpha;
     p.sync = h->gsync;
     p.r = h->r;
     p.out = out;
@@ -261,26 +287,20 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     p.N = static_cast<int>(N);
     p.K = static_cast<int>(K);
     p.num_m_blk = static_cast<int>((M + C::TILE_M - 1) / C::TILE_M);
-    p.num_n_blk = static_cast<int>((N + C::BN - 1) / C::BN);
+    p.num_n_blk = static_cast<int>((N + C::OUT_COLS - 1) / C::OUT_COLS);
     p.num_k_blk = static_cast<int>((K + C::BK - 1) / C::BK);
     p.group_m = h->group_m > 0 ? h->group_m : std::min(p.num_m_blk, 16);
     p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
     p.num_tiles = p.num_m_blk * p.num_n_blk;
     p.a_box_bytes = static_cast<int>(a_rows) * 128;
 
-    static bool attr_set[2][3] = {};
-    if (!attr_set[kKind][kCtaGroup]) {
+    static bool attr_set = false;  // one per template instance
+    if (!attr_set) {
         CUASM_CHECK(h,
-                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>,
+                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
                     "cudaFuncSetAttribute(smem)");
-        if (kCtaGroup == 2) {
-            CUASM_CHECK(h,
-                        cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>,
-                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 0),
-                        "cudaFuncSetAttribute(cluster)");
-        }
-        attr_set[kKind][kCtaGroup] = true;
+        attr_set = true;
     }
     const int max_clusters = h->sm_count / kCtaGroup;
     // Persistent schedule (DESIGN.md §6 "Stream-K"): whole tiles round-robin
@@ -353,7 +373,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const void* x, void* out, int64_t M, i
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
-    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup>, tmap_x, h->tmap_w, p),
+    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi>, tmap_x, w.tmap, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
     return CUASM_OK;
@@ -373,12 +393,13 @@ struct Plan {
     bool stream_k;
 };
 
-Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N) {
+Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
     const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
     const int64_t BK = 128 / h->esize;
     const double KB = static_cast<double>((K + BK - 1) / BK);
-    const int64_t nblk = (N + 127) / 128;
-    const double hbm_floor = (2.0 * N * K + static_cast<double>(M) * K + static_cast<double>(M) * N) * h->esize / hbm;
+    const int64_t nblk = (N + out_cols - 1) / out_cols;
+    const double w_elems = out_cols == 128 ? 2.0 * N * K : 1.0 * N * K;  // W1+W3, or one weight
+    const double hbm_floor = (w_elems + static_cast<double>(M) * K + static_cast<double>(M) * N) * h->esize / hbm;
     Plan best{CUASM_VARIANT_2SM, false};
     double best_t = 1e30;
     for (int cg = 2; cg >= 1; --cg) {
@@ -421,14 +442,24 @@ cuasm_status_t profile_event(cuasm_ffn_t h, cudaStream_t s) {
     return CUASM_OK;
 }
 
-cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3, void* out,
-                            int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
+template <int kEpi>
+cuasm_status_t dispatch_gemm(cuasm_ffn_t h, const EpiSpec& e, int v, const void* x, void* out, int64_t M, int64_t K,
+                             int64_t N, float eps, cudaStream_t s) {
+    if (h->dtype == CUASM_DTYPE_BF16) {
+        return v == CUASM_VARIANT_2SM ? launch_gemm<0, 2, kEpi>(h, e, x, out, M, K, N, eps, s)
+                                      : launch_gemm<0, 1, kEpi>(h, e, x, out, M, K, N, eps, s);
+    }
+    return v == CUASM_VARIANT_2SM ? launch_gemm<1, 2, kEpi>(h, e, x, out, M, K, N, eps, s)
+                                  : launch_gemm<1, 1, kEpi>(h, e, x, out, M, K, N, eps, s);
+}
+
+// Launch one dual-GEMM kernel (plus the stand-alone pre-pass when a1 is not
+// fused) on the already packed weights of slot e.slot.
+cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
+                        int64_t N, float eps, cudaStream_t s) {
     cuasm_status_t st;
-    h->last_kernels = 0;
-    if ((st = set_device(h)) != CUASM_OK) return st;
-    if ((st = ensure_packed(h, g, w1, w3, K, N, s)) != CUASM_OK) return st;
     if (M == 0) return CUASM_OK;
-    if ((st = ensure_r(h, M)) != CUASM_OK) return st;
+    if (e.use_r && (st = ensure_r(h, M)) != CUASM_OK) return st;
     if (h->trace) {
         // clear the trace before the pre-pass: a memset between the pre-pass
         // and the GEMM would break their programmatic (PDL) dependency
@@ -436,29 +467,46 @@ cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const v
             CUASM_CHECK(h, cudaMalloc(&h->trace_buf, sizeof(unsigned long long) * 16 * 1024), "cudaMalloc(trace)");
         CUASM_CHECK(h, cudaMemsetAsync(h->trace_buf, 0, sizeof(unsigned long long) * 16 * 1024, s), "memset(trace)");
     }
-    if (h->fused_norm && !h->gsync) {
+    if (e.fused_norm && !h->gsync) {
         CUASM_CHECK(h, cudaMalloc(&h->gsync, 64), "cudaMalloc(grid counters)");
         CUASM_CHECK(h, cudaMemset(h->gsync, 0, 64), "cudaMemset(grid counters)");
     }
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     // a1: fused into the dual GEMM by default; the separate pre-pass kernel
     // (PDL primary of the GEMM) when CUASM_OPT_FUSED_NORM = 0
-    if (!h->fused_norm && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
+    const bool separate_prepass = e.use_r && !e.fused_norm;
+    if (separate_prepass && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
-    const Plan plan = plan_config(h, M, K, N);
+    const Plan plan = plan_config(h, M, K, N, kepi == 0 ? 128 : 256);
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
-    if (h->dtype == CUASM_DTYPE_BF16) {
-        st = v == CUASM_VARIANT_2SM ? launch_gemm<0, 2>(h, x, out, M, K, N, eps, s)
-                                    : launch_gemm<0, 1>(h, x, out, M, K, N, eps, s);
-    } else {
-        st = v == CUASM_VARIANT_2SM ? launch_gemm<1, 2>(h, x, out, M, K, N, eps, s)
-                                    : launch_gemm<1, 1>(h, x, out, M, K, N, eps, s);
-    }
+    st = kepi == 0 ? dispatch_gemm<0>(h, e, v, x, out, M, K, N, eps, s) : dispatch_gemm<1>(h, e, v, x, out, M, K, N, eps, s);
     if (st != CUASM_OK) return st;
-    h->last_kernels = h->fused_norm ? 1 : 2;
+    h->last_kernels += separate_prepass ? 2 : 1;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     return CUASM_OK;
+}
+
+// The fused FFN (a0 if needed, then a1-a3).
+cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3, void* out,
+                            int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
+    cuasm_status_t st;
+    h->last_kernels = 0;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    const EpiSpec e{0, h->fused_norm, 1, 0, 0.f};
+    return run_gemm(h, 0, e, x, out, M, K, N, eps, s);
+}
+
+// out = act(x . w^T): the single-weight GEMM + activation path.
+cuasm_status_t gemm_act_impl(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K, int64_t N,
+                             int act, float alpha, cudaStream_t s) {
+    cuasm_status_t st;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    if ((st = ensure_packed(h, 1, nullptr, w, nullptr, K, N, s)) != CUASM_OK) return st;
+    h->last_kernels = 0;
+    const EpiSpec e{1, 0, 0, act, alpha};
+    return run_gemm(h, 1, e, x, out, M, K, N, 0.f, s);
 }
 
 cuasm_status_t validate_forward(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3,
@@ -601,6 +649,51 @@ cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const v
     return CUASM_OK;
 }
 
+cuasm_status_t cuasm_gemm_act(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K, int64_t N,
+                              int act, float alpha, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    h->last_kernels = 0;
+    cuasm_status_t st;
+    if ((st = check_common(h, K, N)) != CUASM_OK) return st;
+    if (act != CUASM_ACT_IDENTITY && act != CUASM_ACT_LEAKY_RELU)
+        return fail(h, CUASM_ERR_INVALID_ARG, "unknown activation %d", act);
+    if (!(alpha == alpha)) return fail(h, CUASM_ERR_INVALID_ARG, "alpha is NaN");
+    if (!w || !aligned16(w)) return fail(h, CUASM_ERR_INVALID_ARG, "w must be non-NULL and 16-byte aligned");
+    if (M < 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31)");
+    if (M > 0 && (!x || !out || !aligned16(x) || !aligned16(out)))
+        return fail(h, CUASM_ERR_INVALID_ARG, "x and out must be non-NULL and 16-byte aligned");
+    return gemm_act_impl(h, x, w, out, M, K, N, act, alpha, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
+                                       const void* w3, const void* w2, void* out, int64_t M, int64_t K, int64_t N,
+                                       float eps, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    if (!w2 || !aligned16(w2)) return fail(h, CUASM_ERR_INVALID_ARG, "w2 must be non-NULL and 16-byte aligned");
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t hb = M * N * h->esize;
+    if (hb > h->hidden_bytes) {
+        if (h->hidden) cudaFree(h->hidden);
+        h->hidden = nullptr;
+        h->hidden_bytes = 0;
+        CUASM_CHECK(h, cudaMalloc(&h->hidden, hb), "cudaMalloc(hidden)");
+        h->hidden_bytes = hb;
+    }
+    // hidden [M,N] = SiLU(RMSNorm(x) W1^T) * (RMSNorm(x) W3^T), stored in the handle dtype
+    if ((st = forward_impl(h, x, rms_w, w1, w3, h->hidden, M, K, N, eps, s)) != CUASM_OK) return st;
+    const int k1 = h->last_kernels;
+    // out [M,K] = hidden . W2^T  (W2 [K,N], nn.Linear(N -> K) layout)
+    if ((st = ensure_packed(h, 1, nullptr, w2, nullptr, N, K, s)) != CUASM_OK) return st;
+    h->last_kernels = k1;
+    const EpiSpec e{1, 0, 0, CUASM_ACT_IDENTITY, 0.f};
+    return run_gemm(h, 1, e, h->hidden, out, M, N, K, 0.f, s);
+}
+
 cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w, const void* w1, const void* w3, int64_t K,
                                  int64_t N, void* stream) {
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
@@ -609,8 +702,8 @@ cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w, const void* w
     if ((st = check_common(h, K, N)) != CUASM_OK) return st;
     if ((st = check_weights(h, rms_w, w1, w3)) != CUASM_OK) return st;
     if ((st = set_device(h)) != CUASM_OK) return st;
-    h->packed = false;
-    return ensure_packed(h, rms_w, w1, w3, K, N, static_cast<cudaStream_t>(stream));
+    h->pw[0].packed = false;
+    return ensure_packed(h, 0, rms_w, w1, w3, K, N, static_cast<cudaStream_t>(stream));
 }
 
 cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
@@ -631,20 +724,21 @@ cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t
 
 cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst, int64_t* bytes) {
     if (!h || !bytes) return fail(h, CUASM_ERR_INVALID_ARG, "NULL argument");
-    if (!h->packed) return fail(h, CUASM_ERR_INVALID_ARG, "no packed weights cached");
-    const int64_t b = h->w13_rows * 128;
+    if (!h->pw[0].packed) return fail(h, CUASM_ERR_INVALID_ARG, "no packed weights cached");
+    const int64_t b = h->pw[0].rows * 128;
     *bytes = b;
     if (!dst) return CUASM_OK;
     cuasm_status_t st;
     if ((st = set_device(h)) != CUASM_OK) return st;
     CUASM_CHECK(h, cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-    CUASM_CHECK(h, cudaMemcpy(dst, h->w13, b, cudaMemcpyDeviceToHost), "D2H W13");
+    CUASM_CHECK(h, cudaMemcpy(dst, h->pw[0].buf, b, cudaMemcpyDeviceToHost), "D2H W13");
     return CUASM_OK;
 }
 
 cuasm_status_t cuasm_ffn_invalidate_weights(cuasm_ffn_t h) {
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
-    h->packed = false;
+    h->pw[0].packed = false;
+    h->pw[1].packed = false;
     return CUASM_OK;
 }
 
@@ -736,7 +830,9 @@ cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     int cur = -1;
     if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device) cudaSetDevice(h->device);
     if (h->r) cudaFree(h->r);
-    if (h->w13) cudaFree(h->w13);
+    for (PackedWeights& w : h->pw)
+        if (w.buf) cudaFree(w.buf);
+    if (h->hidden) cudaFree(h->hidden);
     if (h->x_stage) cudaFree(h->x_stage);
     if (h->out_stage) cudaFree(h->out_stage);
     if (h->ws) cudaFree(h->ws);

@@ -42,13 +42,16 @@ struct FfnGemmParams {
     const void* x;   // [M, K] activations (fused RMS pass reads them directly)
     float eps;
     int fused_norm;  // 1: this kernel computes r itself (no pre-pass kernel)
+    int use_r;       // 1: scale the accumulators by r[m] (RMSNorm); 0: r = 1 (plain GEMM)
+    int act;         // kEpi == 1 only: 0 identity, 1 LeakyReLU with negative slope `alpha`
+    float alpha;
     uint32_t* sync;  // [0] warps done writing r, [1] CTAs exited (self-resetting)
     float* r;        // [M] inverse RMS (written here when fused_norm, else by the pre-pass)
     void* out;       // [M, ldo] row-major, dtype of the handle
     int64_t ldo;     // leading dimension of out, elements
     int M, N, K;
     int num_m_blk;   // ceil(M / tile_m)
-    int num_n_blk;   // ceil(N / BN)
+    int num_n_blk;   // ceil(N / OUT_COLS)
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
@@ -166,31 +169,41 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
     }
 }
 
-template <int kKind, int kCtaGroup>
+// kEpi: the epilogue / B-operand layout.
+//   0 (SwiGLU) B = the interleaved W13 block [128 W1g rows | 128 W3g rows];
+//     out[m, n0+j] = SiLU(r*acc[j]) * (r*acc[128+j]), 128 outputs per tile.
+//   1 (GEMM + activation) B = 256 rows of one weight matrix;
+//     out[m, n0+j] = act(r*acc[j]), 256 outputs per tile (r = 1 unless use_r).
+template <int kKind, int kCtaGroup, int kEpi = 0>
 struct GemmCfg {
     static constexpr int kEsize = kKind == 0 ? 2 : 4;
     static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
     static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
-    static constexpr int BN = 128;                 // outputs per tile; MMA N = 2*BN
+    static constexpr int BN = 128;                 // half of the MMA N
     static constexpr int UMMA_N = 2 * BN;
+    static constexpr int OUT_COLS = kEpi == 0 ? BN : UMMA_N;  // output columns per tile
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
     static constexpr int STAGES = kCtaGroup == 1 ? 4 : 6;
     static constexpr int A_BYTES = BM * 128;                        // per CTA
-    static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // W13 rows loaded per CTA
+    static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // packed-weight rows loaded per CTA
     static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
     static constexpr int TMEM_COLS = 512;                           // 2 accumulators x UMMA_N
-    // Two epilogue warps per TMEM lane quadrant, each owning half of the BN
-    // output columns: two warps per SM sub-partition hide the MUFU/TMEM
-    // latency of the (serially dependent) SiLU-gate math.
+    // Two epilogue warps per TMEM lane quadrant, each owning half of the
+    // accumulator columns (two pairs of 32-column chunks): two warps per SM
+    // sub-partition hide the MUFU/TMEM latency of the epilogue math.
     static constexpr int NUM_EPI_WARPS = 8;
-    static constexpr int EPI_COLS = BN * 4 / NUM_EPI_WARPS;        // 64 outputs per warp
     static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 320
     static constexpr int BAR_BYTES = 1024;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + align slack
     static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
+    // Accumulator chunks (32 columns) of epilogue pair `i` of a warp in column half `half`.
+    __device__ static constexpr int chunk_a(int half, int i) { return kEpi == 0 ? half * 2 + i : half * 4 + 2 * i; }
+    __device__ static constexpr int chunk_b(int half, int i) {
+        return kEpi == 0 ? half * 2 + i + BN / 32 : half * 4 + 2 * i + 1;
+    }
 };
 
 __device__ __forceinline__ void tile_coords(int t, const FfnGemmParams& p, int& mb, int& nb) {
@@ -214,6 +227,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ float apply_act(float v, int act, float alpha) {
+    return (act == 1 && v < 0.f) ? v * alpha : v;
+}
+
 __device__ __forceinline__ float silu_gate(float h1, float h3) {
     // SiLU(h1) * h3 = h1 * 1/(1 + 2^(-h1*log2 e)) * h3 (MUFU ex2 + rcp, ~2 ulp each).
     // h1 -> -inf: 2^(+big) = inf, rcp(inf) = 0, out = -0 (x) h3 -- exact limit;
@@ -221,11 +238,36 @@ __device__ __forceinline__ float silu_gate(float h1, float h3) {
     return h1 * rcp_approx(1.0f + ex2_approx(h1 * -1.4426950408889634f)) * h3;
 }
 
-template <int kKind, int kCtaGroup>
-__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
+// 32 consecutive outputs of one row -> global (bf16 pairs packed with RNE, or
+// fp32), 16-byte stores, columns >= N dropped in groups of 8 (N % 8 == 0).
+template <int kKind>
+__device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int col0, const float (&o)[32]) {
+    if constexpr (kKind == 0) {
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (col0 + 8 * q < p.N) {
+                *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
+                    make_uint4(ptx::pack_bf16x2(o[8 * q + 0], o[8 * q + 1]), ptx::pack_bf16x2(o[8 * q + 2], o[8 * q + 3]),
+                               ptx::pack_bf16x2(o[8 * q + 4], o[8 * q + 5]), ptx::pack_bf16x2(o[8 * q + 6], o[8 * q + 7]));
+            }
+        }
+    } else {
+        float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (col0 + 4 * q < p.N)
+                *reinterpret_cast<float4*>(orow + col0 + 4 * q) =
+                    make_float4(o[4 * q + 0], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+    }
+}
+
+template <int kKind, int kCtaGroup, int kEpi>
+__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                          const FfnGemmParams p) {
-    using C = GemmCfg<kKind, kCtaGroup>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -374,7 +416,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
         bool r_ready = !p.fused_norm;
         const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t ewarp = warp - 2;  // 0..7: flag slot
-        const int col_base = static_cast<int>(ewarp >> 2) * C::EPI_COLS;  // this warp's output columns
+        const int half = static_cast<int>(ewarp >> 2);  // this warp's half of the accumulator columns
         const uint32_t row_in_cta = quad * 32 + lane;
         int it = 0;
         Sched sch;
@@ -408,11 +450,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                         reinterpret_cast<const float4*>(p.ws) +
                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4));
 #pragma unroll
-                    for (int cc0 = 0; cc0 < C::EPI_COLS / 32; ++cc0) {
-                        const int c = col_base / 32 + cc0;
+                    for (int i = 0; i < 2; ++i) {
 #pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {  // h1 chunk, h3 chunk: 4 KB each
-                            const int64_t chunk = c + hh * (C::BN / 32);
+                        for (int hh = 0; hh < 2; ++hh) {  // chunk a, chunk b: 4 KB each
+                            const int64_t chunk = hh == 0 ? C::chunk_a(half, i) : C::chunk_b(half, i);
                             prefetch_l2(slot + ((chunk * 4 + quad) * 8 * 32) * 16 + lane * 128);
                         }
                     }
@@ -433,7 +474,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                 }
                 r_ready = true;
             }
-            const float rr = row_ok ? __ldcg(p.r + row) : 0.f;
+            const float rr = !row_ok ? 0.f : (p.use_r ? __ldcg(p.r + row) : 1.f);
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
             if (warp == 2 && lane == 0) {
@@ -448,16 +489,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
             if (warp == 2 && lane == 0) trace_stamp(p, 10);
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
-            for (int cc0 = 0; cc0 < C::EPI_COLS / 32; ++cc0) {
-                const int c = col_base / 32 + cc0;  // 32-column chunk index within BN
+            for (int i = 0; i < 2; ++i) {
+                const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
                 uint32_t v1[32], v3[32];
-                ptx::tmem_ld_32x32b_x32(t_row + c * 32, v1);
-                ptx::tmem_ld_32x32b_x32(t_row + C::BN + c * 32, v3);
+                ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
+                ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
                 ptx::tmem_ld_wait();
                 if (!row_ok) continue;
                 if (contributor) {
-                    float4* d1 = my_slot + (static_cast<int64_t>(c) * 4 + quad) * 8 * 32 + lane;
-                    float4* d3 = my_slot + (static_cast<int64_t>(C::BN / 32 + c) * 4 + quad) * 8 * 32 + lane;
+                    float4* d1 = my_slot + (static_cast<int64_t>(ca) * 4 + quad) * 8 * 32 + lane;
+                    float4* d3 = my_slot + (static_cast<int64_t>(cb) * 4 + quad) * 8 * 32 + lane;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         __stcg(d1 + q * 32, make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
@@ -471,8 +512,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                     if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
                     const float4* slot = reinterpret_cast<const float4*>(p.ws) +
                                          (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
-                    const float4* s1 = slot + (static_cast<int64_t>(c) * 4 + quad) * 8 * 32 + lane;
-                    const float4* s3 = slot + (static_cast<int64_t>(C::BN / 32 + c) * 4 + quad) * 8 * 32 + lane;
+                    const float4* s1 = slot + (static_cast<int64_t>(ca) * 4 + quad) * 8 * 32 + lane;
+                    const float4* s3 = slot + (static_cast<int64_t>(cb) * 4 + quad) * 8 * 32 + lane;
                     float4 a[8], b[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -491,37 +532,19 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup>::NUM_THREADS, 1)
                         v3[4 * q + 3] = __float_as_uint(__uint_as_float(v3[4 * q + 3]) + b[q].w);
                     }
                 }
-                const int col0 = nb * C::BN + c * 32;
-                if constexpr (kKind == 0) {
-                    uint32_t packed[16];
+                if constexpr (kEpi == 0) {
+                    float o[32];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float a0 = silu_gate(rr * __uint_as_float(v1[2 * i]), rr * __uint_as_float(v3[2 * i]));
-                        const float a1 =
-                            silu_gate(rr * __uint_as_float(v1[2 * i + 1]), rr * __uint_as_float(v3[2 * i + 1]));
-                        packed[i] = ptx::pack_bf16x2(a0, a1);
-                    }
-                    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (col0 + 8 * q < p.N) {
-                            *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
-                                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-                        }
-                    }
+                    for (int j = 0; j < 32; ++j) o[j] = silu_gate(rr * __uint_as_float(v1[j]), rr * __uint_as_float(v3[j]));
+                    store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
                 } else {
-                    float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
+                    float o[32];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        if (col0 + 4 * q < p.N) {
-                            float4 o;
-                            o.x = silu_gate(rr * __uint_as_float(v1[4 * q + 0]), rr * __uint_as_float(v3[4 * q + 0]));
-                            o.y = silu_gate(rr * __uint_as_float(v1[4 * q + 1]), rr * __uint_as_float(v3[4 * q + 1]));
-                            o.z = silu_gate(rr * __uint_as_float(v1[4 * q + 2]), rr * __uint_as_float(v3[4 * q + 2]));
-                            o.w = silu_gate(rr * __uint_as_float(v1[4 * q + 3]), rr * __uint_as_float(v3[4 * q + 3]));
-                            *reinterpret_cast<float4*>(orow + col0 + 4 * q) = o;
-                        }
-                    }
+                    for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);
+                    store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v3[j]), p.act, p.alpha);
+                    store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
                 }
             }
             if (warp == 2 && lane == 0) {

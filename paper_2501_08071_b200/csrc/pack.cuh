@@ -44,6 +44,8 @@ __device__ __forceinline__ uint32_t fold_tf32(uint32_t w, uint32_t g) {
 // run in HBM, which the decode-shaped weight stream needs for DRAM locality):
 //   W13t[nb][kb][j*BN + rr][i] = RNE(W_j[nb*BN + rr][kb*BK + i] * g[kb*BK + i])
 // zero where nb*BN + rr >= N (N tail) or kb*BK + i >= K (K tail).
+// Single-source mode (w3 == nullptr, the plain GEMM + activation path):
+//   Wt[nb][kb][r][i] = RNE(W[nb*2BN + r][kb*BK + i] * g[kb*BK + i])  (g == nullptr: g = 1)
 template <typename T>
 __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1, const T* __restrict__ w3,
                                                        const T* __restrict__ g, T* __restrict__ w13, int64_t N,
@@ -61,14 +63,19 @@ __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1,
         const int64_t rest = row / (2 * BN);
         const int64_t kb = rest % k_blocks;
         const int64_t nb = rest / k_blocks;
-        const int j = r2 >= BN ? 1 : 0;
-        const int64_t n = nb * BN + (r2 - j * BN);
+        // interleaved (w3 != null): rows j*BN + rr of the block come from W_j;
+        // single source (w3 == null): the block's 2*BN rows are W rows nb*2BN + r2
+        const int j = (w3 != nullptr && r2 >= BN) ? 1 : 0;
+        const int64_t n = w3 != nullptr ? nb * BN + (r2 - j * BN) : nb * 2 * BN + r2;
         const int64_t k = kb * BK + static_cast<int64_t>(v) * kVec;  // K % 8 == 0: a vector is all in or all out
         uint4 o = make_uint4(0, 0, 0, 0);
         if (n < N && k < K) {
             const T* src = (j == 0 ? w1 : w3) + n * K + k;
             const uint4 w = *reinterpret_cast<const uint4*>(src);
-            const uint4 gg = *reinterpret_cast<const uint4*>(g + k);
+            // no gain (plain GEMM weights): fold by 1.0, i.e. keep bf16 / round fp32 to tf32
+            const uint4 gg = g != nullptr ? *reinterpret_cast<const uint4*>(g + k)
+                                          : (sizeof(T) == 2 ? make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u)
+                                                            : make_uint4(0x3F800000u, 0x3F800000u, 0x3F800000u, 0x3F800000u));
             if constexpr (sizeof(T) == 2) {
                 o.x = fold_bf16x2(w.x, gg.x);
                 o.y = fold_bf16x2(w.y, gg.y);

@@ -73,3 +73,22 @@ def ffn_tp_forward(x, rms_w, w1_shard, w3_shard, eps: float = 1e-6, group=None, 
     if N is None:
         raise ValueError("gather=True needs the total N")
     return gather_shards(out, N, group)
+
+
+def shard_w2(w2: torch.Tensor, rank: int, world: int):
+    """Rank `rank`'s columns of the down projection W2 [K,N] (row-parallel:
+    the same N range as its W1/W3 rows)."""
+    n0, n1 = shard_bounds(w2.shape[1], rank, world)
+    return w2[:, n0:n1].contiguous()
+
+
+def ffn_block_tp_forward(x, rms_w, w1_shard, w3_shard, w2_shard, eps: float = 1e-6, group=None,
+                         handle: FusedFFN | None = None):
+    """Megatron tensor-parallel LLaMA feed-forward block: column-parallel W1/W3
+    (this rank's N-shard of the hidden), row-parallel W2, one all-reduce of
+    the [M,K] partial outputs (NCCL over NVLink on GPUs)."""
+    h = handle or _handle(x.device, x.dtype)
+    y = h.block_forward(x, rms_w, w1_shard, w3_shard, w2_shard, eps)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(y, group=group)
+    return y

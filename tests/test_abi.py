@@ -24,7 +24,7 @@ def lib():
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(cuasm_ffn_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(cuasm_[a-z_]+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_entry_points():
@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
     names = header_functions()
     assert sorted(ffn.EXPORTED_SYMBOLS) == names
     out = subprocess.run(["nm", "-D", "--defined-only", ffn.lib_path()], capture_output=True, text=True).stdout
-    exported = set(re.findall(r"\bT (cuasm_ffn_\w+)", out))
+    exported = set(re.findall(r"\bT (cuasm_\w+)", out))
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     for n in names:

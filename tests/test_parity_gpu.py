@@ -333,3 +333,52 @@ def test_forward_host_matches_device_path(cuda_device, M):
         h.forward_host(d["x"].pin_memory(), t["g"], t["w1"], t["w3"], 1e-6, out_host=out2, sync=False)
         torch.cuda.current_stream().synchronize()
         assert torch.equal(out2, host)
+
+
+# --------------------------------------------- f3: mmLeakyReLu, f1: FFN block ----
+@pytest.mark.parametrize("variant", [ffn.VARIANT_AUTO, ffn.VARIANT_1SM, ffn.VARIANT_2SM])
+@pytest.mark.parametrize("M,K,N", [(512, 2048, 512), (300, 520, 776), (1, 64, 256), (1000, 1024, 2056)])
+@pytest.mark.parametrize("act,alpha", [("leaky_relu", 0.01), ("identity", 0.0)])
+def test_gemm_act_parity(cuda_device, M, K, N, act, alpha, variant):
+    """The paper's mmLeakyReLu (B,M,N,K = 1,512,512,2048) and plain GEMM."""
+    d = make_inputs(M, K, N, family="C", seed=5000 + M + N, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_variant(variant)
+    x, w = d["x"].to(cuda_device), d["w1"].to(cuda_device)
+    out = h.gemm_act(x, w, act, alpha)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_act(d["x"], d["w1"], act, alpha)
+    check(out, ref, f"gemm_act {act} {M}x{K}x{N} v{variant}")
+    again = h.gemm_act(x, w, act, alpha)
+    torch.cuda.synchronize()
+    assert torch.equal(out, again)
+
+
+def test_gemm_act_fp32_tf32_exact_inputs(cuda_device):
+    d = make_inputs(64, 96, 264, family="T", seed=5100, dtype="fp32")
+    h = ffn.FusedFFN(cuda_device, torch.float32)
+    out = h.gemm_act(d["x"].to(cuda_device), d["w1"].to(cuda_device), "leaky_relu", 0.25)
+    torch.cuda.synchronize()
+    check(out, oracle.gemm_act(d["x"], d["w1"], "leaky_relu", 0.25), "gemm_act fp32")
+
+
+@pytest.mark.parametrize("M,K,N", [(16, 512, 1024), (300, 256, 648), (2048, 1024, 2816)])
+def test_ffn_block_parity(cuda_device, M, K, N):
+    """out = (SiLU(xn W1^T) * (xn W3^T)) W2^T against the oracle with the hidden
+    rounded to bf16 (reading R13) and g folded into bf16 weights (R4)."""
+    d = make_inputs(M, K, N, family="C", seed=5200 + M, dtype="bf16")
+    w2 = make_inputs(1, N, K, family="C", seed=5300 + M, dtype="bf16")["w1"]   # [K, N]
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    y = h.block_forward(t["x"], t["g"], t["w1"], t["w3"], w2.to(cuda_device), 1e-6)
+    torch.cuda.synchronize()
+    assert y.shape == (M, K)
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 24)))))
+    ref = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, 1e-6, mode="fold_bf16", round_hidden=True,
+                           rows=rows)
+    check(y[rows], ref, f"ffn block {M}x{K}x{N}")
+    # the hidden it used is exactly the fused FFN's output
+    hid = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    y2 = h.gemm_act(hid, w2.to(cuda_device), "identity")
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
