@@ -53,6 +53,14 @@ WORKLOADS = {
     "llama7b_decode": (16, 4096, 11008, 2),
     "llama70b": (4096, 8192, 28672, 3),
 }
+# Operations beyond the headline fused FFN: name -> (op, M, K, N)
+#   block: the whole LLaMA FFN block (fused FFN + down projection W2), FLOPs 6*M*K*N
+#   gemm_lrelu: the paper's mmLeakyReLu (B,M,N,K = 1,512,512,2048), FLOPs 2*M*K*N
+EXTRA = {
+    "llama7b_block": ("block", 2048, 4096, 11008),
+    "mmleakyrelu_paper": ("gemm_lrelu", 512, 2048, 512),
+    "mmleakyrelu_large": ("gemm_lrelu", 4096, 4096, 4096),
+}
 
 
 def parse_args(argv=None):
@@ -75,7 +83,14 @@ def parse_args(argv=None):
     return ap.parse_args(argv)
 
 
+def workload_op(name: str):
+    return EXTRA[name][0] if name in EXTRA else "ffn"
+
+
 def workload_shape(name: str):
+    if name in EXTRA:
+        _, M, K, N = EXTRA[name]
+        return M, K, N, 1
     if name.startswith("sweep:"):
         return int(name.split(":")[1]), 4096, 11008, 4
     if name not in WORKLOADS:
@@ -263,8 +278,17 @@ def run_cuasm(args):
     n0, n1 = shard_bounds(N, rank, world)
     N_l = n1 - n0
     seed = args.seed if args.seed is not None else seed_for(cidx)
+    op = workload_op(args.workload)
     t = make_device_inputs(M, K, N_l, seed, dev, w_seed=seed + 1 + rank)
-    out = torch.empty((M, N_l), dtype=torch.bfloat16, device=dev)
+    if op == "block":
+        # down projection W2 [K, N_l] (row-parallel shard), ~N(0, 1/N)
+        gw = torch.Generator(device=dev)
+        gw.manual_seed(seed + 101 + rank)
+        t["w2"] = (torch.randn((K, N_l), device=dev, generator=gw) / float(N) ** 0.5).to(torch.bfloat16)
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    else:
+        out = torch.empty((M, N_l), dtype=torch.bfloat16, device=dev)
+    flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0}[op] * M * K * N
     flush = L2Flush(dev)
     eps = 1e-6
 
@@ -276,8 +300,20 @@ def run_cuasm(args):
 
     # a0: one-time weight fold/pack (reported, not part of a step)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def fwd():
+        if op == "ffn":
+            return h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+        if op == "block":
+            return h.block_forward(t["x"], t["g"], t["w1"], t["w3"], t["w2"], eps, out=out)
+        return h.gemm_act(t["x"], t["w1"], "leaky_relu", 0.01, out=out)
+
     e0.record(stream)
-    h.prepare(t["g"], t["w1"], t["w3"])
+    if op == "gemm_lrelu":
+        fwd()  # the first call packs the weight
+    else:
+        h.prepare(t["g"], t["w1"], t["w3"])
+        if op == "block":
+            fwd()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     prep_ms = e0.elapsed_time(e1)
@@ -285,7 +321,7 @@ def run_cuasm(args):
     full_out = None
 
     def step():
-        h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+        fwd()
         if args.gather:
             from paper_2501_08071_b200.tp import gather_shards
             return gather_shards(out, N)
@@ -304,7 +340,7 @@ def run_cuasm(args):
     if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+            fwd()
         graph.replay()
         torch.cuda.synchronize(dev)
 
@@ -339,7 +375,7 @@ def run_cuasm(args):
     wall = time.perf_counter() - wall0
     local_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t_ms = max_over_ranks(local_ms)
-    total_flops = 4.0 * M * K * N * args.steps
+    total_flops = flops_per_step * args.steps
     value = total_flops / (t_ms / 1e3) / 1e12
     variant_used = h.last_launch()[0]
     launches_total = int(sum_over_ranks(float(launches)))
@@ -353,24 +389,28 @@ def run_cuasm(args):
     torch.cuda._sleep(int(4e8))  # host runs ahead: no launch gap inside the per-kernel spans
     for _ in range(prof_steps):
         flush.zero_()
-        h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
+        fwd()
     pre_ms, gemm_ms, nfw = h.profile_read()
     h.set_option(ffn.OPT_PROFILE, 0)
-    gemm_avg_ms = gemm_ms / max(nfw, 1)
-    pre_avg_ms = pre_ms / max(nfw, 1)
-    gemm_flops = 4.0 * M * K * N_l
+    # per step (the block launches two GEMMs; their spans are summed)
+    gemm_avg_ms = gemm_ms / prof_steps
+    pre_avg_ms = pre_ms / prof_steps
+    gemm_flops = flops_per_step / world
     achieved = gemm_flops / (gemm_avg_ms / 1e3) / 1e12
     bound = "tensor"
     peak = peaks["bf16_tflops"]
     roof_unit = "TFLOP/s"
     # decode-like shapes are HBM bound: algorithmic bytes of the GEMM kernel
-    gemm_bytes = 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M
-    if 4.0 * M * K * N_l / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
+    gemm_bytes = {"ffn": 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M,
+                  "block": 2.0 * (M * K + 3 * K * N_l + 2 * M * N_l + M * K) + 4.0 * M,
+                  "gemm_lrelu": 2.0 * (M * K + K * N_l + M * N_l)}[op]
+    if gemm_flops / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
         bound, peak, roof_unit = "hbm", peaks["hbm_gbs"], "GB/s"
         achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
     traffic = load_traffic(args.workload if world == 1 else f"{args.workload}@tp{world}")
     roofline = {
-        "kernel": "ffn_dual_gemm_kernel", "bound": bound, "achieved": round(achieved, 2), "peak": peak,
+        "kernel": {"ffn": "ffn_dual_gemm_kernel", "block": "ffn_dual_gemm_kernel x2 (fused FFN + W2 GEMM)",
+                   "gemm_lrelu": "ffn_dual_gemm_kernel<GEMM + LeakyReLU epilogue>"}[op], "bound": bound, "achieved": round(achieved, 2), "peak": peak,
         "unit": roof_unit, "frac": round(achieved / peak, 4), "traffic": traffic,
         "peak_source": peaks["source"], "gemm_ms_per_launch": round(gemm_avg_ms, 5),
         "prepass_ms_per_launch": round(pre_avg_ms, 5),
@@ -381,7 +421,7 @@ def run_cuasm(args):
 
     # ---------------------------------------------------------------- e2e
     e2e = None
-    if not args.skip_e2e:
+    if not args.skip_e2e and op == "ffn":
         x_host = t["x"].cpu().pin_memory()
         out_host = torch.empty((M, N_l), dtype=torch.bfloat16, pin_memory=True)
         ne = min(args.steps, 20)
@@ -404,7 +444,7 @@ def run_cuasm(args):
 
     # ------------------------------------------------------ cpu baseline (oracle)
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline and op == "ffn":
         cpu_in = {k: v.cpu() for k, v in t.items()}
         fl, sec, rows, thr = oracle_sample_time(cpu_in, eps, args.cpu_budget_s)
         cpu_baseline = {"value": round(fl / sec / 1e12, 6), "unit": UNIT, "cores": thr, "kind": "oracle",
@@ -425,7 +465,7 @@ def run_cuasm(args):
                 "pdl": not args.no_pdl, "cuda_graph": graph is not None,
                 "l2": "flushed before every step outside the per-step CUDA-event pair: 256 MiB memset, then a "
                       "256 MiB read so the flush's dirty lines are written back before the step",
-                "flops_per_step": 4.0 * M * K * N, "prep_ms": round(prep_ms, 4),
+                "op": op, "flops_per_step": flops_per_step, "prep_ms": round(prep_ms, 4),
             },
             "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),
             "pct_of_nominal_2250": round(value / world / 2250.0, 4),
