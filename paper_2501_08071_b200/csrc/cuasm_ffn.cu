@@ -387,7 +387,8 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
 // one tile; the 1-SM tile pays its measured 16% smem-bandwidth penalty; and
 // every candidate is floored by the HBM time of streaming the weights once.
 // Constants were fitted to scripts/tune.py on a B200 (profiles/r01/tune.json):
-// t_kb = 0.37 us per k-block-tile at the power-capped clock, fixup = 10 us.
+// t_kb = 0.37 us per k-block-tile at the power-capped clock, fixup = 10 us,
+// stream-K L2-overflow slowdown 1.32x (profiles/r01/trace_gemm.log).
 struct Plan {
     int variant;
     bool stream_k;
@@ -404,12 +405,24 @@ Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_col
     double best_t = 1e30;
     for (int cg = 2; cg >= 1; --cg) {
         const int64_t units = h->sm_count / cg;
-        const int64_t tiles = (M + 128 * cg - 1) / (128 * cg) * nblk;
+        const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
+        const int64_t tiles = mblk * nblk;
         const double waves = static_cast<double>(tiles) / units;
         const double rounds = static_cast<double>((tiles + units - 1) / units);
         const double pen = cg == 1 ? pen_1sm : 1.0;
         const double t_dp = std::max(hbm_floor, rounds * KB * t_kb * pen);
-        const double t_sk = std::max(hbm_floor, waves * KB * t_kb * pen + fixup);
+        // Stream-K keeps its whole region in flight at once (every cluster
+        // holds a slice of it), so when the region's operands overflow L2 the
+        // k-block rate drops (measured 0.49 vs 0.37 us on 2048x11008x4096,
+        // profiles/r01/trace_gemm.log): charge that as a 1.32x slowdown.
+        const int64_t rem = tiles % units;
+        const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
+        const int64_t gm = std::min<int64_t>(mblk, h->group_m > 0 ? h->group_m : 16);
+        const double region_bytes =
+            static_cast<double>((sk_tiles + gm - 1) / gm + 1) * 256.0 * K * h->esize +
+            static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * h->esize;
+        const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
+        const double t_sk = std::max(hbm_floor, waves * KB * t_kb * pen * l2_pen + fixup);
         // ties go to the earlier candidate: 2-SM before 1-SM, whole tiles before stream-K
         if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, false}; }
         if (K / BK > 1 && t_sk < best_t * 0.98) {

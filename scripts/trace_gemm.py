@@ -25,6 +25,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="2048x4096x11008,16x4096x11008")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--op", default="ffn", choices=["ffn", "gemm"], help="gemm: cuasm_gemm_act (identity)")
+    ap.add_argument("--scheds", default="0,1")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     wbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -34,18 +36,24 @@ def main():
         M, K, N = map(int, shp.split("x"))
         t = make_device_inputs(M, K, N, 1, dev)
         out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        for pdl, sched in ((1, 0), (1, 1)):
+        for sched in map(int, a.scheds.split(",")):
+            pdl = 1
             h = ffn.FusedFFN(dev)
             h.set_option(ffn.OPT_PDL, pdl)
             h.set_option(ffn.OPT_SCHEDULE, sched)
+            def run():
+                if a.op == "ffn":
+                    h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+                else:
+                    h.gemm_act(t["x"], t["w1"], "identity", 0.0, out=out)
             for _ in range(3):
-                h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+                run()
             h.set_option(ffn.OPT_TRACE, 1)
             wbuf.zero_()
             rbuf.sum()
             torch.cuda.synchronize()
             torch.cuda._sleep(int(1e8))
-            h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+            run()
             tr = h.trace_read().double()
             h.close()
             t0 = tr[:, 0][tr[:, 0] > 0].min()
@@ -58,7 +66,7 @@ def main():
                 rel = (col - t0) / 1e3
                 rows[name] = {"min": round(rel.min().item(), 2), "med": round(rel.median().item(), 2),
                               "max": round(rel.max().item(), 2)}
-            key = f"{shp} pdl={pdl} schedule={'auto' if sched == 0 else 'data-parallel'}"
+            key = f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all'][sched]}"
             report[key] = rows
             print(key)
             for name, r in rows.items():

@@ -110,21 +110,27 @@ def test_7b_prefill_balance():
 
 # ---- shape-keyed configuration model (csrc/cuasm_ffn.cu plan_config) ---------
 
-def plan_config(M, K, N, esize=2, sm_count=148):
+def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     t_kb, fixup, hbm, pen_1sm = 0.37e-6, 10e-6, 6.5e12, 1.16
     BK = 128 // esize
     KB = -(-K // BK)
-    nblk = -(-N // 128)
-    hbm_floor = (2.0 * N * K + M * K + M * N) * esize / hbm
+    nblk = -(-N // out_cols)
+    hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     best, best_t = ("2sm", False), 1e30
     for cg in (2, 1):
         units = sm_count // cg
-        tiles = -(-M // (128 * cg)) * nblk
+        mblk = -(-M // (128 * cg))
+        tiles = mblk * nblk
         waves = tiles / units
         rounds = -(-tiles // units)
         pen = pen_1sm if cg == 1 else 1.0
         t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
-        t_sk = max(hbm_floor, waves * KB * t_kb * pen + fixup)
+        rem = tiles % units
+        sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
+        gm = min(mblk, 16)
+        region = (-(-sk_tiles // gm) + 1) * 256.0 * K * esize + min(M, gm * 128 * cg) * K * esize
+        l2_pen = 1.32 if region > 120e6 else 1.0
+        t_sk = max(hbm_floor, waves * KB * t_kb * pen * l2_pen + fixup)
         name = "2sm" if cg == 2 else "1sm"
         if t_dp < best_t * 0.999:
             best_t, best = t_dp, (name, False)
@@ -159,3 +165,8 @@ def test_plan_matches_measured_best(M):
 def test_plan_70b_shard_uses_stream_k():
     # 8-way shard of the 70B FFN: 448 tiles = 6.05 waves of 74 CTA pairs
     assert plan_config(4096, 8192, 3584) == ("2sm", True)
+
+
+def test_plan_w2_down_projection_avoids_l2_thrashing_stream_k():
+    # hidden [2048, 11008] x W2 [4096, 11008]: whole tiles 128 us vs stream-K 158 us measured
+    assert plan_config(2048, 11008, 4096, out_cols=256) == ("2sm", False)
