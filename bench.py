@@ -60,6 +60,8 @@ EXTRA = {
     "llama7b_block": ("block", 2048, 4096, 11008),
     "mmleakyrelu_paper": ("gemm_lrelu", 512, 2048, 512),
     "mmleakyrelu_large": ("gemm_lrelu", 4096, 4096, 4096),
+    # the paper's stand-alone rmsnorm: 4096 rows x 2048 features; N unused
+    "rmsnorm_paper": ("rmsnorm", 4096, 2048, 8),
 }
 
 
@@ -286,9 +288,11 @@ def run_cuasm(args):
         gw.manual_seed(seed + 101 + rank)
         t["w2"] = (torch.randn((K, N_l), device=dev, generator=gw) / float(N) ** 0.5).to(torch.bfloat16)
         out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    elif op == "rmsnorm":
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
     else:
         out = torch.empty((M, N_l), dtype=torch.bfloat16, device=dev)
-    flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0}[op] * M * K * N
+    flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0, "rmsnorm": 0.0}[op] * M * K * N
     flush = L2Flush(dev)
     eps = 1e-6
 
@@ -305,11 +309,13 @@ def run_cuasm(args):
             return h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
         if op == "block":
             return h.block_forward(t["x"], t["g"], t["w1"], t["w3"], t["w2"], eps, out=out)
+        if op == "rmsnorm":
+            return h.rmsnorm(t["x"], t["g"], eps, out=out)
         return h.gemm_act(t["x"], t["w1"], "leaky_relu", 0.01, out=out)
 
     e0.record(stream)
-    if op == "gemm_lrelu":
-        fwd()  # the first call packs the weight
+    if op in ("gemm_lrelu", "rmsnorm"):
+        fwd()  # the first call packs the weight (gemm)
     else:
         h.prepare(t["g"], t["w1"], t["w3"])
         if op == "block":
@@ -377,6 +383,10 @@ def run_cuasm(args):
     t_ms = max_over_ranks(local_ms)
     total_flops = flops_per_step * args.steps
     value = total_flops / (t_ms / 1e3) / 1e12
+    metric, unit = METRIC, UNIT
+    if op == "rmsnorm":  # memory-bound: report algorithmic GB/s (read x once, write out once)
+        metric, unit = "RMSNorm GB/s", "GB/s"
+        value = (4.0 * M * K + 2.0 * K) * args.steps / (t_ms / 1e3) / 1e9
     variant_used = h.last_launch()[0]
     launches_total = int(sum_over_ranks(float(launches)))
 
@@ -392,6 +402,8 @@ def run_cuasm(args):
         fwd()
     pre_ms, gemm_ms, nfw = h.profile_read()
     h.set_option(ffn.OPT_PROFILE, 0)
+    if op == "rmsnorm":  # not a GEMM launch: the step is the kernel
+        gemm_ms = t_ms
     # per step (the block launches two GEMMs; their spans are summed)
     gemm_avg_ms = gemm_ms / prof_steps
     pre_avg_ms = pre_ms / prof_steps
@@ -401,15 +413,18 @@ def run_cuasm(args):
     peak = peaks["bf16_tflops"]
     roof_unit = "TFLOP/s"
     # decode-like shapes are HBM bound: algorithmic bytes of the GEMM kernel
-    gemm_bytes = {"ffn": 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M,
+    if op == "rmsnorm":
+        gemm_avg_ms = t_ms / args.steps
+    gemm_bytes = {"ffn": 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M, "rmsnorm": 4.0 * M * K + 2.0 * K,
                   "block": 2.0 * (M * K + 3 * K * N_l + 2 * M * N_l + M * K) + 4.0 * M,
                   "gemm_lrelu": 2.0 * (M * K + K * N_l + M * N_l)}[op]
-    if gemm_flops / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
+    if op == "rmsnorm" or gemm_flops / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
         bound, peak, roof_unit = "hbm", peaks["hbm_gbs"], "GB/s"
         achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
     traffic = load_traffic(args.workload if world == 1 else f"{args.workload}@tp{world}")
     roofline = {
         "kernel": {"ffn": "ffn_dual_gemm_kernel", "block": "ffn_dual_gemm_kernel x2 (fused FFN + W2 GEMM)",
+                   "rmsnorm": "ffn_rmsnorm_kernel",
                    "gemm_lrelu": "ffn_dual_gemm_kernel<GEMM + LeakyReLU epilogue>"}[op], "bound": bound, "achieved": round(achieved, 2), "peak": peak,
         "unit": roof_unit, "frac": round(achieved / peak, 4), "traffic": traffic,
         "peak_source": peaks["source"], "gemm_ms_per_launch": round(gemm_avg_ms, 5),
@@ -454,7 +469,7 @@ def run_cuasm(args):
     clocks = sampler.summary()
     if rank == 0:
         res = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded randn x~N(0,1), W~N(0,1/K), g~U(0.5,1.5); bf16)",

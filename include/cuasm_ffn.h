@@ -161,6 +161,15 @@ cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x_dev, const v
                                        const void* w3_dev, const void* w2_dev, void* out_dev, int64_t M, int64_t K,
                                        int64_t N, float eps, void* stream);
 
+/* Stand-alone RMSNorm (the paper's memory-bound "rmsnorm"
+ * kernel, PAPER.md P:68 / P:523 / P:573):
+ *   out[m,k] = x[m,k] * g[k] / sqrt( (sum_k x[m,k]^2)/K + eps )
+ * x, out [M,K], rms_w = g [K]: device, 16-byte aligned, the handle's dtype
+ * (bf16 out is RNE of the fp32 product).  K % 8 == 0; M == 0 -> no launch;
+ * eps >= 0.  One kernel, x read from HBM once for K <= 4096 (bf16). */
+cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev, void* out_dev, int64_t M,
+                             int64_t K, float eps, void* stream);
+
 /* Step a0 alone: fold g into W1/W3 and pack (one-time weight preparation,
  * PAPER.md P:434-447's offline/deploy split).  Same weight preconditions. */
 cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w_dev, const void* w1_dev, const void* w3_dev,

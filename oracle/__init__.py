@@ -17,6 +17,7 @@ Parity status per function (DESIGN.md §Oracle pins):
   ffn (fold)   pinned: reduces to plain mode when every g*w is representable,
                round_bf16 pinned against torch's independent bf16 cast
   round_tf32   pinned: hand-derived ties and Python-float reference rounding
+  rmsnorm      pinned: torch float64 F.rms_norm, constant-row closed form, E2
   gemm_act     pinned: numpy float64 matmul, identity weights, exact negative-slope
                scaling, alpha = 1 reduces to identity
   ffn_block    pinned: W2 = I reduces to ffn(), torch float64 composition with a
@@ -76,6 +77,8 @@ def _load():
             lib.oracle_gemm_act.restype = ci
             lib.oracle_ffn_block_rows.argtypes = [vp, ci, vp, vp, vp, vp, ci, i64, i64, i64, dbl, ci, ci, vp, i64, vp]
             lib.oracle_ffn_block_rows.restype = ci
+            lib.oracle_rmsnorm.argtypes = [vp, ci, vp, ci, i64, i64, dbl, vp]
+            lib.oracle_rmsnorm.restype = ci
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = ci
             _lib = lib
@@ -192,6 +195,19 @@ def ffn_block(x, g, w1, w3, w2, eps: float = 1e-6, mode: str = "plain", round_hi
                                    rows_arr.ctypes.data, rows_arr.shape[0], out.ctypes.data)
     if st != 0:
         raise RuntimeError(f"oracle_ffn_block_rows failed with status {st}")
+    return out
+
+
+def rmsnorm(x, g, eps: float = 1e-6) -> np.ndarray:
+    """RMSNorm(x) = x * g / sqrt(mean(x^2) + eps), fp64 (PAPER.md P:573's kernel)."""
+    lib = _load()
+    xs, xdt = _as_storage(x)
+    gs, gdt = _as_storage(g)
+    M, K = xs.shape
+    out = np.empty((M, K), dtype=np.float64)
+    st = lib.oracle_rmsnorm(xs.ctypes.data, xdt, gs.ctypes.data, gdt, M, K, float(eps), out.ctypes.data)
+    if st != 0:
+        raise RuntimeError(f"oracle_rmsnorm failed with status {st}")
     return out
 
 

@@ -309,3 +309,28 @@ int oracle_ffn_block_rows(const void* x, int x_dtype, const void* g, const void*
     free(hid);
     return 0;
 }
+
+/* ---- f3: stand-alone RMSNorm (the paper's "rmsnorm" kernel) ----------------- */
+/*
+ * PAPER.md P:68 ("root-mean-square layer normalization"), Table
+ * "Evaluated Kernels" P:573 (memory-bound; B, n_head, seq_len, d_head =
+ * 1, 32, 4096, 64, read as 4096 rows of 32*64 = 2048 features, R10):
+ *     out[m,k] = x[m,k] * g[k] / sqrt( (sum_k x[m,k]^2)/K + eps )
+ * fp64, sequential k-sums; out [M,K] double.
+ */
+int oracle_rmsnorm(const void* x, int x_dtype, const void* g, int g_dtype, int64_t M, int64_t K, double eps,
+                   double* out) {
+    if (!x || !g || !out || M < 0 || K <= 0) return -1;
+    #pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        double ss = 0.0;
+        for (int64_t k = 0; k < K; ++k) {
+            double v = load_elem(x, x_dtype, m * K + k);
+            ss += v * v;
+        }
+        double r = 1.0 / sqrt(ss / (double)K + eps);
+        for (int64_t k = 0; k < K; ++k)
+            out[m * K + k] = load_elem(x, x_dtype, m * K + k) * r * load_elem(g, g_dtype, k);
+    }
+    return 0;
+}

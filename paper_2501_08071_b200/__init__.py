@@ -19,7 +19,7 @@ import weakref
 import torch
 
 __all__ = [
-    "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "gemm_act", "ffn_block_forward", "CuasmError",
+    "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "rmsnorm", "gemm_act", "ffn_block_forward", "CuasmError",
     "lib_path", "load_library",
     "VARIANT_AUTO", "VARIANT_1SM", "VARIANT_2SM", "EXPORTED_SYMBOLS",
 ]
@@ -39,6 +39,7 @@ SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL = 0, 1, 2
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_gemm_act", "cuasm_ffn_block_forward",
+    "cuasm_rmsnorm",
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
     "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
@@ -71,6 +72,7 @@ def load_library():
         lib.cuasm_ffn_forward_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp, ci]
         lib.cuasm_gemm_act.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, f32, vp]
         lib.cuasm_ffn_block_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
+        lib.cuasm_rmsnorm.argtypes = [vp, vp, vp, vp, i64, i64, f32, vp]
         lib.cuasm_ffn_prepare.argtypes = [vp, vp, vp, vp, i64, i64, vp]
         lib.cuasm_ffn_rms_inv.argtypes = [vp, vp, vp, i64, i64, f32, vp]
         lib.cuasm_ffn_get_packed.argtypes = [vp, vp, ctypes.POINTER(i64)]
@@ -268,6 +270,20 @@ class FusedFFN:
                                                      float(eps), _stream_ptr(x.device)))
         return out
 
+    def rmsnorm(self, x, rms_w, eps: float = 1e-6, out=None):
+        """RMSNorm(x) = x * g / sqrt(mean(x^2) + eps) (the paper's rmsnorm kernel)."""
+        self._validate(x, rms_w)
+        M, K = x.shape
+        if rms_w.shape != (K,):
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty_like(x)
+        else:
+            self._validate(out)
+        self._check(self.lib.cuasm_rmsnorm(self._h, x.data_ptr(), rms_w.data_ptr(), out.data_ptr(), M, K, float(eps),
+                                           _stream_ptr(x.device)))
+        return out
+
     def rms_inv(self, x, eps: float = 1e-6, out=None):
         self._validate(x)
         M, K = x.shape
@@ -310,6 +326,11 @@ def ffn_forward_host(x_host, rms_w, w1, w3, eps: float = 1e-6, out_host=None, sy
 
 def rms_inv(x, eps: float = 1e-6):
     return _handle(x.device, x.dtype).rms_inv(x, eps)
+
+
+def rmsnorm(x, rms_w, eps: float = 1e-6, out=None):
+    """RMSNorm(x) on the GPU (stand-alone kernel)."""
+    return _handle(x.device, x.dtype).rmsnorm(x, rms_w, eps, out)
 
 
 def gemm_act(x, w, act: str = "identity", alpha: float = 0.01, out=None):

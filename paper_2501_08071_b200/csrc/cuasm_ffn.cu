@@ -707,6 +707,36 @@ cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void*
     return run_gemm(h, 1, e, h->hidden, out, M, N, K, 0.f, s);
 }
 
+cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x, const void* rms_w, void* out, int64_t M, int64_t K,
+                             float eps, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    h->last_kernels = 0;
+    cuasm_status_t st;
+    if (K <= 0 || K % 8 != 0) return fail(h, CUASM_ERR_INVALID_ARG, "K must be a positive multiple of 8");
+    if (M < 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31)");
+    if ((st = check_eps(h, eps)) != CUASM_OK) return st;
+    if (!rms_w || !aligned16(rms_w)) return fail(h, CUASM_ERR_INVALID_ARG, "rms_w must be non-NULL, 16-byte aligned");
+    if (M == 0) return CUASM_OK;
+    if (!x || !out || !aligned16(x) || !aligned16(out))
+        return fail(h, CUASM_ERR_INVALID_ARG, "x and out must be non-NULL and 16-byte aligned");
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned blocks = static_cast<unsigned>((M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock);
+    if (h->dtype == CUASM_DTYPE_BF16) {
+        cuasm::ffn_rmsnorm_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(rms_w),
+            static_cast<__nv_bfloat16*>(out), M, K, eps);
+    } else {
+        cuasm::ffn_rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x),
+                                                                 static_cast<const float*>(rms_w),
+                                                                 static_cast<float*>(out), M, K, eps);
+    }
+    CUASM_CHECK(h, cudaGetLastError(), "ffn_rmsnorm_kernel launch");
+    h->last_kernels = 1;
+    return CUASM_OK;
+}
+
 cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w, const void* w1, const void* w3, int64_t K,
                                  int64_t N, void* stream) {
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");

@@ -82,4 +82,65 @@ __global__ void __launch_bounds__(256) ffn_rms_prepass_kernel(const T* __restric
     rms_row<T>(x, r, row, K, eps, lane);
 }
 
+// ---- f3: stand-alone RMSNorm (PAPER.md P:68, P:573's memory-bound rmsnorm) --
+//   out[m,k] = RNE( x[m,k] * r[m] * g[k] ),  r[m] = 1/sqrt(sum_k x^2/K + eps)
+// One warp per row.  The first kCache*32 16-byte vectors of the row stay in
+// registers between the reduction and the scaled write (the whole row for
+// K <= 4096 bf16 / 2048 fp32), so x is read from HBM once; longer rows re-read
+// their tail from L2.  HBM-bound: 2*M*K*esize bytes.
+__device__ __forceinline__ uint4 scale_vec(uint4 v, uint4 g, float r, __nv_bfloat16) {
+    const uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {g.x, g.y, g.z, g.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float lo = __uint_as_float(a[i] << 16) * r * __uint_as_float(b[i] << 16);
+        const float hi = __uint_as_float(a[i] & 0xFFFF0000u) * r * __uint_as_float(b[i] & 0xFFFF0000u);
+        o[i] = ptx::pack_bf16x2(lo, hi);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ __forceinline__ uint4 scale_vec(uint4 v, uint4 g, float r, float) {
+    return make_uint4(__float_as_uint(__uint_as_float(v.x) * r * __uint_as_float(g.x)),
+                      __float_as_uint(__uint_as_float(v.y) * r * __uint_as_float(g.y)),
+                      __float_as_uint(__uint_as_float(v.z) * r * __uint_as_float(g.z)),
+                      __float_as_uint(__uint_as_float(v.w) * r * __uint_as_float(g.w)));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_rmsnorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                          T* __restrict__ out, int64_t M, int64_t K, float eps) {
+    constexpr int kCache = 16;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kPrepassRowsPerBlock + warp;
+    if (row >= M) return;
+    constexpr int kVec = 16 / sizeof(T);
+    const int64_t nvec = K / kVec;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * K);
+    const uint4* g4 = reinterpret_cast<const uint4*>(g);
+    uint4* orow = reinterpret_cast<uint4*>(out + row * K);
+    uint4 c[kCache];
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int u = 0; u < kCache; ++u) {
+        const int64_t i = lane + u * 32;
+        if (i < nvec) {
+            c[u] = ld_nc_v4(xr + i);
+            acc[u & 3] += sumsq_vec(c[u], T{});
+        }
+    }
+    for (int64_t i = lane + kCache * 32; i < nvec; i += 32) acc[0] += sumsq_vec(__ldcg(xr + i), T{});
+    float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float r = 1.0f / sqrtf(s / static_cast<float>(K) + eps);
+#pragma unroll
+    for (int u = 0; u < kCache; ++u) {
+        const int64_t i = lane + u * 32;
+        if (i < nvec) orow[i] = scale_vec(c[u], __ldg(g4 + i), r, T{});
+    }
+    for (int64_t i = lane + kCache * 32; i < nvec; i += 32) orow[i] = scale_vec(__ldcg(xr + i), __ldg(g4 + i), r, T{});
+}
+
 }  // namespace cuasm

@@ -331,3 +331,19 @@ def test_ffn_block_round_hidden_uses_bf16_rne():
     # torch's independent RNE; both round fp64 -> fp32 -> bf16 (the oracle's documented path)
     ref = hid.float().to(torch.bfloat16).double().numpy()
     np.testing.assert_array_equal(blk[:, :N], ref)
+
+
+# ---- f3: stand-alone RMSNorm (the paper's rmsnorm kernel) ------------------
+
+def test_rmsnorm_matches_torch_and_closed_forms():
+    d = make_inputs(13, 2048, 8, family="L", seed=26, dtype="bf16")
+    out = oracle.rmsnorm(d["x"], d["g"], 1e-6)
+    ref = F.rms_norm(d["x"].double(), (2048,), d["g"].double(), eps=1e-6).numpy()
+    np.testing.assert_allclose(out, ref, rtol=1e-13, atol=1e-300)
+    # E2: rms = 1 exactly, so RMSNorm(x) = x * g
+    x = torch.tensor([[1.0, -1.0, 1.0, -1.0]], dtype=torch.float64)
+    g = torch.tensor([1.0, 2.0, 0.5, 1.0], dtype=torch.float64)
+    assert np.array_equal(oracle.rmsnorm(x, g, 0.0), np.array([[1.0, -2.0, 0.5, -1.0]]))
+    # constant row c: RMSNorm = g * c / sqrt(c^2 + eps)
+    x = torch.full((1, 8), 3.0, dtype=torch.float64)
+    np.testing.assert_allclose(oracle.rmsnorm(x, torch.ones(8, dtype=torch.float64), 7.0), 3.0 / 4.0, rtol=1e-15)

@@ -382,3 +382,16 @@ def test_ffn_block_parity(cuda_device, M, K, N):
     y2 = h.gemm_act(hid, w2.to(cuda_device), "identity")
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,K", [(4096, 2048), (7, 64), (33, 8192), (300, 1000)])
+def test_rmsnorm_parity(cuda_device, dtype, M, K):
+    """The paper's stand-alone rmsnorm (4096 rows x 2048 features)."""
+    d = make_inputs(M, K, 8, family="L", seed=5400 + M, dtype=dtype)
+    h = ffn.FusedFFN(cuda_device, TORCH_DT[dtype])
+    out = h.rmsnorm(d["x"].to(cuda_device), d["g"].to(cuda_device), 1e-6)
+    torch.cuda.synchronize()
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 64)))))
+    ref = oracle.rmsnorm(d["x"][rows], d["g"], 1e-6)
+    check(out[rows], ref, f"rmsnorm {dtype} {M}x{K}")
