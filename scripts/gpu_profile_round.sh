@@ -13,6 +13,12 @@ timeout 600 python bench.py > $O/bench_llama7b_prefill.json 2> $O/bench.err; ech
 timeout 600 python bench.py --workload llama7b_decode > $O/bench_llama7b_decode.json 2>> $O/bench.err; echo "bench_decode=$?"
 timeout 600 python bench.py --workload llama70b --skip-cpu-baseline > $O/bench_llama70b.json 2>> $O/bench.err; echo "bench_70b=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference.json 2>> $O/bench.err; echo "bench_ref=$?"
+for w in llama7b_block mmleakyrelu_paper mmleakyrelu_large rmsnorm_paper; do
+  timeout 600 python bench.py --workload $w --skip-cpu-baseline --skip-e2e > $O/bench_$w.json 2>> $O/bench.err; echo "bench_$w=$?"
+done
+timeout 600 python scripts/tune.py --out $O/tune.json > $O/tune.log 2>&1; echo "tune=$?"
+timeout 300 python scripts/launch_floor.py > $O/launch_floor.log 2>&1; echo "launch_floor=$?"
+timeout 300 python scripts/trace_gemm.py --op gemm --shapes 2048x11008x4096,4096x4096x4096 --scheds 0,1,2 > $O/trace_gemm.log 2>&1; echo "trace_gemm=$?"
 timeout 900 python scripts/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1; echo "sweep=$?"
 timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,16x4096x11008,4096x8192x3584 --json $O/trace.json > $O/trace.log 2>&1; echo "trace=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_prefill.csv \

@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2501_08071_b200.tp import gather_shards, shard_bounds, shard_weights
+from paper_2501_08071_b200.tp import gather_shards, shard_bounds, shard_w2, shard_weights
 
 
 @pytest.mark.parametrize("N,world", [(11008, 8), (11008, 2), (28672, 8), (1376, 3), (8, 1), (24, 3), (40, 3)])
@@ -71,3 +71,45 @@ def test_gather_and_max_over_ranks(world, N):
     for rank, ok, t in res:
         assert ok, f"rank {rank}: gathered output differs"
         assert t == pytest.approx(1.5 * world)
+
+
+def test_shard_w2_columns_match_w1_rows():
+    K, N = 16, 48
+    w2 = torch.arange(K * N, dtype=torch.float32).reshape(K, N)
+    for world in (1, 2, 3):
+        cols = torch.cat([shard_w2(w2, r, world) for r in range(world)], dim=1)
+        assert torch.equal(cols, w2)
+
+
+def _block_worker(rank, world, port, q):
+    """Row-parallel W2: each rank's partial y_p = h_p @ W2_p^T, all-reduced,
+    equals the unsharded h @ W2^T (the host logic of ffn_block_tp_forward)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(0)
+        M, K, N = 5, 16, 48
+        hid = torch.randn(M, N, generator=g, dtype=torch.float64)
+        w2 = torch.randn(K, N, generator=g, dtype=torch.float64)
+        n0, n1 = shard_bounds(N, rank, world)
+        y = hid[:, n0:n1] @ shard_w2(w2, rank, world).T
+        dist.all_reduce(y)
+        q.put((rank, bool(torch.allclose(y, hid @ w2.T, rtol=1e-12, atol=1e-12))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_parallel_w2_all_reduce(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)
