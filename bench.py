@@ -271,10 +271,17 @@ def run_cuasm(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # CUASM_BENCH_SHARED_GPU=1: ranks share the visible GPU(s) over gloo -- a
+    # functional check of the N>1 path on a 1-GPU box (timings meaningless)
+    shared = os.environ.get("CUASM_BENCH_SHARED_GPU") == "1"
+    local_dev = local % torch.cuda.device_count() if shared else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     M, K, N, cidx = workload_shape(args.workload)
     n0, n1 = shard_bounds(N, rank, world)
@@ -363,7 +370,7 @@ def run_cuasm(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches = 0
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local_dev)
     barrier()
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()

@@ -395,3 +395,74 @@ def test_rmsnorm_parity(cuda_device, dtype, M, K):
     rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 64)))))
     ref = oracle.rmsnorm(d["x"][rows], d["g"], 1e-6)
     check(out[rows], ref, f"rmsnorm {dtype} {M}x{K}")
+
+
+# ------------------------------------------------------------ shape fuzzing ---
+def _fuzz_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        M = int(rng.choice([rng.integers(1, 130), rng.integers(129, 700), rng.integers(700, 3000)]))
+        K = 8 * int(rng.integers(1, 520))
+        N = 8 * int(rng.integers(1, 700))
+        cases.append((i, M, K, N, int(rng.integers(0, 3)), int(rng.integers(0, 3))))
+    return cases
+
+
+@pytest.mark.parametrize("i,M,K,N,variant,schedule", _fuzz_cases(24, 777))
+def test_fuzz_ffn_shapes(cuda_device, i, M, K, N, variant, schedule):
+    """Random (M, K, N) incl. K not a multiple of 64, N not of 128, M tails,
+    every variant x schedule: parity on sampled rows + run-to-run determinism."""
+    d = make_inputs(M, K, N, family="C", seed=9000 + i, dtype="bf16")
+    out, h = run_gpu(d, 1e-6, "bf16", variant, schedule=schedule)
+    again, _ = run_gpu(d, 1e-6, "bf16", variant, handle=h, schedule=schedule)
+    assert torch.equal(out, again)
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 16)))))
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(out[rows], ref, f"fuzz {i}: {M}x{K}x{N} v{variant} s{schedule}")
+
+
+@pytest.mark.parametrize("i,M,K,N,variant,schedule", _fuzz_cases(12, 778))
+def test_fuzz_gemm_act_shapes(cuda_device, i, M, K, N, variant, schedule):
+    d = make_inputs(M, K, N, family="C", seed=9100 + i, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_variant(variant)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
+    out = h.gemm_act(d["x"].to(cuda_device), d["w1"].to(cuda_device), "leaky_relu", 0.125)
+    torch.cuda.synchronize()
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 16)))))
+    ref = oracle.gemm_act(d["x"][rows], d["w1"], "leaky_relu", 0.125)
+    check(out[rows], ref, f"fuzz gemm {i}: {M}x{K}x{N} v{variant} s{schedule}")
+
+
+def test_block_forward_fp32(cuda_device):
+    M, K, N = 40, 64, 136
+    d = make_inputs(M, K, N, family="T", seed=9200, dtype="fp32")
+    w2 = make_inputs(1, N, K, family="T", seed=9201, dtype="fp32")["w1"]
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.float32)
+    y = h.block_forward(t["x"], t["g"], t["w1"], t["w3"], w2.to(cuda_device), 1e-6)
+    torch.cuda.synchronize()
+    # fp32 hidden: the MMA reads it as tf32 (truncated), so compare with a tf32-rounded
+    # hidden only loosely: the tolerance covers 2^-11 relative per term
+    ref = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, 1e-6, mode="plain")
+    check(y, ref, "block fp32")
+
+
+def test_new_entry_points_validate_arguments(cuda_device):
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    lib, s = h.lib, torch.cuda.current_stream().cuda_stream
+    x = torch.zeros((4, 64), dtype=torch.bfloat16, device=cuda_device)
+    w = torch.zeros((128, 64), dtype=torch.bfloat16, device=cuda_device)
+    out = torch.full((4, 128), 3.0, dtype=torch.bfloat16, device=cuda_device)
+    p = lambda t: t.data_ptr()
+    assert lib.cuasm_gemm_act(h._h, p(x), p(w), p(out), 4, 60, 128, 0, 0.0, s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_gemm_act(h._h, p(x), p(w), p(out), 4, 64, 128, 7, 0.0, s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_gemm_act(h._h, p(x), 0, p(out), 4, 64, 128, 0, 0.0, s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_gemm_act(h._h, p(x), p(w), p(out), 4, 64, 128, 1, float("nan"), s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_rmsnorm(h._h, p(x), p(w), p(out), 4, 60, 1e-6, s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_rmsnorm(h._h, p(x), p(w), p(out), 4, 64, -1.0, s) == ffn.ERR_INVALID_ARG
+    assert lib.cuasm_ffn_block_forward(h._h, p(x), p(w), p(w), p(w), 0, p(out), 4, 64, 128, 1e-6, s) == \
+        ffn.ERR_INVALID_ARG
+    torch.cuda.synchronize()
+    assert torch.all(out == 3.0)
