@@ -240,12 +240,22 @@ class L2Flush:
         self.sink = self.r.sum()
 
 
+def host_cores() -> int:
+    """Cores this process may run on (torchrun's OMP_NUM_THREADS=1 must not
+    shrink the CPU baseline to one core)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 # ------------------------------------------------------------------ cpu baseline
 def oracle_sample_time(inputs_cpu, eps, budget_s, rows_hint=None):
     """Time the fp64 oracle on a bounded sample of rows of the same workload.
 
     Returns (flops, seconds, rows, threads)."""
     import oracle
+    oracle.set_threads(host_cores())
     x, g, w1, w3 = inputs_cpu["x"], inputs_cpu["g"], inputs_cpu["w1"], inputs_cpu["w3"]
     M, K = x.shape
     N = w1.shape[0]
@@ -522,6 +532,7 @@ def run_reference(args):
     seed = args.seed if args.seed is not None else seed_for(cidx)
     # rows of x are independent: generate only what the samples touch
     M_gen = min(M, 256)
+    oracle.set_threads(host_cores())
     d = make_inputs(M_gen, K, N_l, family="C", seed=seed, dtype="bf16")
     eps = 1e-6
     nsteps = args.warmup + args.steps

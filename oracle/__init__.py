@@ -79,6 +79,8 @@ def _load():
             lib.oracle_ffn_block_rows.restype = ci
             lib.oracle_rmsnorm.argtypes = [vp, ci, vp, ci, i64, i64, dbl, vp]
             lib.oracle_rmsnorm.restype = ci
+            lib.oracle_set_threads.argtypes = [ci]
+            lib.oracle_set_threads.restype = None
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = ci
             _lib = lib
@@ -249,6 +251,10 @@ def fold(w, g) -> np.ndarray:
     else:
         raise TypeError("fold: w and g must both be bf16 or both fp32")
     return dst
+
+
+def set_threads(n: int) -> None:
+    _load().oracle_set_threads(int(n))
 
 
 def num_threads() -> int:

@@ -334,3 +334,13 @@ int oracle_rmsnorm(const void* x, int x_dtype, const void* g, int g_dtype, int64
     }
     return 0;
 }
+
+/* Thread count for the OpenMP loops (bench.py pins it to the host's cores:
+ * torchrun exports OMP_NUM_THREADS=1 to every rank). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
