@@ -349,6 +349,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
                 }
             }
             trace_stamp(p, 2);
+            // all of this CTA's loads are issued: let the next PDL kernel in the
+            // stream get scheduled as SMs free up (it griddepcontrol.waits for
+            // this grid's completion before reading anything we write)
+            ptx::pdl_launch_dependents();
         }
     } else if (warp == 1) {
         // ========================= MMA issuer ===========================
