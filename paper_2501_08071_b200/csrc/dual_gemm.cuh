@@ -356,44 +356,79 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
         }
     } else if (warp == 1) {
         // ========================= MMA issuer ===========================
-        if (leader && lane == 0) {
+        // The whole warp walks the loop (barrier waits included) and one
+        // elected lane issues: the descriptors then live in uniform registers
+        // and ptxas emits no per-instruction uniformity loop around UTCHMMA.
+        // The issue loop is on the critical path (the tensor core only runs
+        // ahead of it by a few instructions), so it is kept short.
+        if (leader) {
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            long long kblocks = 0, clk0 = 0, wait_full = 0, wait_tempty = 0;
+            // smem descriptors of stage 0; stage s adds s*bytes >> 4 to the address field
+            const uint64_t adesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a));
+            const uint64_t bdesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b));
             Sched sch;
             sch.init(p, cluster_id);
             Seg sg;
             for (; sch.next(sg); ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
-                ptx::mbar_wait(ptx::smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                {
+                    const long long w0 = p.trace ? clock64() : 0;
+                    ptx::mbar_wait(ptx::smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                    if (p.trace && kblocks > 0) wait_tempty += clock64() - w0;
+                }
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C::UMMA_N;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
-                    ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
+                    {
+                        const long long w0 = p.trace ? clock64() : 0;
+                        ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
+                        if (p.trace && kblocks > 0) wait_full += clock64() - w0;
+                    }
                     ptx::tc_fence_after();
-                    const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + stage * C::A_BYTES));
-                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + stage * C::B_BYTES));
+                    const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * C::A_BYTES) >> 4);
+                    const uint64_t bdesc = bdesc0 + static_cast<uint64_t>((stage * C::B_BYTES) >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < C::KSTEPS; ++k) {
-                        // advance 32 bytes of K inside the 128-byte swizzle row (+2 in 16-byte units)
-                        ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
-                                                   (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < C::KSTEPS; ++k) {
+                            // advance 32 bytes of K inside the 128-byte swizzle row (+2 in 16-byte units)
+                            ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
+                                                       (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                        }
+                        if constexpr (kCtaGroup == 1) {
+                            ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
+                        } else {
+                            ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), 0x3);
+                        }
                     }
-                    if constexpr (kCtaGroup == 1) {
-                        ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
-                    } else {
-                        ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), 0x3);
-                    }
+                    __syncwarp();
+                    if (p.trace && kblocks++ == 0) clk0 = clock64();
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
-                if constexpr (kCtaGroup == 1) {
-                    ptx::mma_commit(ptx::smem_u32(&tfull_bar[acc]));
-                } else {
-                    ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
+                if (ptx::elect_one()) {
+                    if constexpr (kCtaGroup == 1) {
+                        ptx::mma_commit(ptx::smem_u32(&tfull_bar[acc]));
+                    } else {
+                        ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                trace_stamp(p, 3);
+                if (p.trace) {
+                    // SM cycles from the first to the last MMA issue, k-blocks issued and
+                    // cycles spent waiting: (cycles / (k-blocks - 1)) vs the tcgen05 floor
+                    // (4 x 128 cycles) tells a starved tensor pipe from a slow clock
+                    p.trace[blockIdx.x * kTraceSlots + 12] = static_cast<unsigned long long>(clock64() - clk0);
+                    p.trace[blockIdx.x * kTraceSlots + 13] = static_cast<unsigned long long>(kblocks);
+                    p.trace[blockIdx.x * kTraceSlots + 14] = static_cast<unsigned long long>(wait_full);
+                    p.trace[blockIdx.x * kTraceSlots + 15] = static_cast<unsigned long long>(wait_tempty);
                 }
             }
-            trace_stamp(p, 3);
         }
     } else {
         // ========================= epilogue =============================

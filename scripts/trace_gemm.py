@@ -58,6 +58,21 @@ def main():
             h.close()
             t0 = tr[:, 0][tr[:, 0] > 0].min()
             rows = {}
+            cyc, kbs = tr[:, 12], tr[:, 13]
+            sel = kbs > 1
+            if sel.any():
+                cpk = cyc[sel] / (kbs[sel] - 1)
+                span_ns = (tr[:, 3] - tr[:, 1])[sel]
+                ghz = cyc[sel] / span_ns.clamp(min=1)
+                print(f"   cycles per k-block (MMA issue, leader CTAs): min {cpk.min():.0f} med {cpk.median():.0f} "
+                      f"max {cpk.max():.0f}  (tcgen05 floor: 512); implied SM clock med {ghz.median():.3f} GHz")
+                wf = tr[:, 14][sel] / (kbs[sel] - 1)
+                wt = tr[:, 15][sel] / (kbs[sel] - 1)
+                print(f"   MMA-thread wait per k-block: full (data) med {wf.median():.0f} cyc, "
+                      f"tempty (accumulator) med {wt.median():.0f} cyc")
+                rows["wait_full_per_kblock_med"] = round(wf.median().item(), 1)
+                rows["cycles_per_kblock_med"] = round(cpk.median().item(), 1)
+                rows["sm_ghz_med"] = round(ghz.median().item(), 3)
             for i, name in enumerate(SLOTS):
                 col = tr[:, i]
                 col = col[col > 0]
@@ -70,7 +85,8 @@ def main():
             report[key] = rows
             print(key)
             for name, r in rows.items():
-                print(f"   {name:10s} min {r['min']:8.2f}  med {r['med']:8.2f}  max {r['max']:8.2f} us")
+                if isinstance(r, dict):
+                    print(f"   {name:10s} min {r['min']:8.2f}  med {r['med']:8.2f}  max {r['max']:8.2f} us")
     if a.json:
         with open(a.json, "w") as f:
             json.dump(report, f, indent=1)
