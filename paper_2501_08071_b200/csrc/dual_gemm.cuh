@@ -185,7 +185,7 @@ struct GemmCfg {
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
-    static constexpr int STAGES = kCtaGroup == 1 ? 4 : 6;
+    static constexpr int STAGES = kCtaGroup == 1 ? 4 : 7;  // 2-SM: 7 x 32 KB + barriers = 226 KB of 227
     static constexpr int A_BYTES = BM * 128;                        // per CTA
     static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // packed-weight rows loaded per CTA
     static constexpr int B_BYTES = B_ROWS * 128;
@@ -313,27 +313,29 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
 
     if (warp == 0) {
         // ========================= TMA producer =========================
-        if (lane == 0) {
-            ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
-            const uint64_t pol_x = ptx::policy_evict_last();    // x is re-read by every n-block
-            const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
-            int stage = 0;
-            uint32_t phase = 0;
-            bool first_load = true;
-            Sched sch;
-            sch.init(p, cluster_id);
-            Seg sg;
-            while (sch.next(sg)) {
-                int mb, nb;
-                tile_coords(sg.tile, p, mb, nb);
-                const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
-                // k-block-tiled W13 (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*2BN
-                const int row_b0 = nb * p.num_k_blk * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
-                for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
-                    ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
-                    const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
-                    const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
-                    const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+        // Whole warp walks the loop, one elected lane issues (uniform operands,
+        // no per-instruction uniformity loops around UTMALDG).
+        ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
+        const uint64_t pol_x = ptx::policy_evict_last();    // x is re-read by every n-block
+        const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
+        int stage = 0;
+        uint32_t phase = 0;
+        bool first_load = true;
+        Sched sch;
+        sch.init(p, cluster_id);
+        Seg sg;
+        while (sch.next(sg)) {
+            int mb, nb;
+            tile_coords(sg.tile, p, mb, nb);
+            const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
+            // k-block-tiled weights (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*UMMA_N
+            const int row_b0 = nb * p.num_k_blk * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
+            for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
+                ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
+                const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
+                const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
+                const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+                if (ptx::elect_one()) {
                     if constexpr (kCtaGroup == 1) {
                         ptx::mbar_arrive_expect_tx(fb, p.a_box_bytes + C::B_BYTES);
                         ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
@@ -344,10 +346,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
                         ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
                     }
-                    if (first_load) { trace_stamp(p, 1); first_load = false; }
-                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
+                __syncwarp();
+                if (first_load && lane == 0) trace_stamp(p, 1);
+                first_load = false;
+                if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             }
+        }
+        if (lane == 0) {
             trace_stamp(p, 2);
             // all of this CTA's loads are issued: let the next PDL kernel in the
             // stream get scheduled as SMs free up (it griddepcontrol.waits for
