@@ -221,6 +221,14 @@ cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h);
  * call on the handle).  h == NULL returns the last init error. */
 const char* cuasm_ffn_last_error(cuasm_ffn_t h);
 
+/* The shape-keyed configuration model the AUTO variant and
+ * schedule use, without a handle or a device: for `sm_count` SMs, element
+ * type `dtype`, problem M x K x N and op (0: fused FFN, 128 outputs per tile;
+ * 1: GEMM + activation, 256 outputs per tile) it returns the chosen
+ * cuasm_variant_t and whether the stream-K tail is used.  Pure host code. */
+cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
+                                 int* stream_k);
+
 /* CUASM_FFN_ABI_VERSION of the loaded library. */
 int cuasm_ffn_abi_version(void);
 

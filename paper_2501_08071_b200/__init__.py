@@ -42,8 +42,19 @@ EXPORTED_SYMBOLS = (
     "cuasm_rmsnorm",
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
-    "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
+    "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_plan_config", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
 )
+
+
+def plan_config(M: int, K: int, N: int, op: str = "ffn", dtype=torch.bfloat16, sm_count: int = 148):
+    """The library's configuration model: ("1sm" | "2sm", stream_k: bool) for a shape."""
+    lib = load_library()
+    v, sk = ctypes.c_int(), ctypes.c_int()
+    st = lib.cuasm_plan_config(sm_count, _dtype_code(dtype), M, K, N, {"ffn": 0, "gemm": 1}[op], ctypes.byref(v),
+                               ctypes.byref(sk))
+    if st != OK:
+        raise CuasmError(st, "cuasm_plan_config: invalid arguments")
+    return ("1sm" if v.value == VARIANT_1SM else "2sm"), bool(sk.value)
 
 
 class CuasmError(RuntimeError):
@@ -82,6 +93,7 @@ def load_library():
         lib.cuasm_ffn_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ci)]
         lib.cuasm_ffn_trace_read.argtypes = [vp, vp, ctypes.POINTER(ci)]
+        lib.cuasm_plan_config.argtypes = [ci, ci, i64, i64, i64, ci, ctypes.POINTER(ci), ctypes.POINTER(ci)]
         lib.cuasm_ffn_destroy.argtypes = [vp]
         lib.cuasm_ffn_last_error.argtypes = [vp]
         lib.cuasm_ffn_last_error.restype = ctypes.c_char_p

@@ -394,17 +394,17 @@ struct Plan {
     bool stream_k;
 };
 
-Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
+Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
     const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
-    const int64_t BK = 128 / h->esize;
+    const int64_t BK = 128 / esize;
     const double KB = static_cast<double>((K + BK - 1) / BK);
     const int64_t nblk = (N + out_cols - 1) / out_cols;
     const double w_elems = out_cols == 128 ? 2.0 * N * K : 1.0 * N * K;  // W1+W3, or one weight
-    const double hbm_floor = (w_elems + static_cast<double>(M) * K + static_cast<double>(M) * N) * h->esize / hbm;
+    const double hbm_floor = (w_elems + static_cast<double>(M) * K + static_cast<double>(M) * N) * esize / hbm;
     Plan best{CUASM_VARIANT_2SM, false};
     double best_t = 1e30;
     for (int cg = 2; cg >= 1; --cg) {
-        const int64_t units = h->sm_count / cg;
+        const int64_t units = sm_count / cg;
         const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
         const int64_t tiles = mblk * nblk;
         const double waves = static_cast<double>(tiles) / units;
@@ -417,10 +417,10 @@ Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_col
         // profiles/r01/trace_gemm.log): charge that as a 1.32x slowdown.
         const int64_t rem = tiles % units;
         const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
-        const int64_t gm = std::min<int64_t>(mblk, h->group_m > 0 ? h->group_m : 16);
+        const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : 16);
         const double region_bytes =
-            static_cast<double>((sk_tiles + gm - 1) / gm + 1) * 256.0 * K * h->esize +
-            static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * h->esize;
+            static_cast<double>((sk_tiles + gm - 1) / gm + 1) * 256.0 * K * esize +
+            static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
         const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
         const double t_sk = std::max(hbm_floor, waves * KB * t_kb * pen * l2_pen + fixup);
         // ties go to the earlier candidate: 2-SM before 1-SM, whole tiles before stream-K
@@ -431,6 +431,10 @@ Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_col
         }
     }
     return best;
+}
+
+Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
+    return plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols);
 }
 
 cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
@@ -540,6 +544,17 @@ cuasm_status_t validate_forward(cuasm_ffn_t h, const void* x, const void* g, con
 extern "C" {
 
 int cuasm_ffn_abi_version(void) { return CUASM_FFN_ABI_VERSION; }
+
+cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
+                                 int* stream_k) {
+    if (sm_count <= 1 || (dtype != CUASM_DTYPE_BF16 && dtype != CUASM_DTYPE_FP32) || M < 0 || K <= 0 || N <= 0 ||
+        (op != 0 && op != 1) || !variant || !stream_k)
+        return CUASM_ERR_INVALID_ARG;
+    const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
+    *variant = pl.variant;
+    *stream_k = pl.stream_k ? 1 : 0;
+    return CUASM_OK;
+}
 
 cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* out, int device, cuasm_dtype_t dtype) {
     g_init_error.clear();

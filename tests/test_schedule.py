@@ -170,3 +170,29 @@ def test_plan_70b_shard_uses_stream_k():
 def test_plan_w2_down_projection_avoids_l2_thrashing_stream_k():
     # hidden [2048, 11008] x W2 [4096, 11008]: whole tiles 128 us vs stream-K 158 us measured
     assert plan_config(2048, 11008, 4096, out_cols=256) == ("2sm", False)
+
+
+# ---- the library's own implementation agrees with the model above -------------------
+@pytest.fixture(scope="module")
+def lib_plan():
+    from paper_2501_08071_b200 import build as ffn_build
+    ffn_build.build()
+    import paper_2501_08071_b200 as ffn
+    return ffn.plan_config
+
+
+@pytest.mark.parametrize("M", sorted(MEASURED_BEST))
+def test_library_plan_matches_measured_best(lib_plan, M):
+    assert lib_plan(M, 4096, 11008) in MEASURED_BEST[M]
+
+
+@pytest.mark.parametrize("M,K,N,op", [(m, k, n, op) for m in (1, 16, 200, 512, 1000, 2048, 4096, 16384)
+                                      for k, n in ((4096, 11008), (8192, 3584), (11008, 4096), (2048, 512))
+                                      for op in ("ffn", "gemm")])
+def test_library_plan_equals_python_mirror(lib_plan, M, K, N, op):
+    assert lib_plan(M, K, N, op) == plan_config(M, K, N, out_cols=128 if op == "ffn" else 256)
+
+
+def test_library_plan_w2_and_70b(lib_plan):
+    assert lib_plan(2048, 11008, 4096, "gemm") == ("2sm", False)
+    assert lib_plan(4096, 8192, 3584) == ("2sm", True)
