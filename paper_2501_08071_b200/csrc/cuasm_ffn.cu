@@ -318,9 +318,14 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     if (sk_ok && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
         else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
-        // every cluster gets a non-empty range (tiny problems: fewer clusters)
-        if (sk_tiles > 0)
-            clusters = static_cast<int>(std::min<int64_t>(max_clusters, static_cast<int64_t>(sk_tiles) * p.num_k_blk));
+        // every cluster gets a non-empty range (tiny problems: fewer clusters); in
+        // auto mode a tile is split at most in two when there are fewer tiles
+        // than clusters (each finisher then adds a single partial)
+        if (sk_tiles > 0) {
+            int64_t c = std::min<int64_t>(max_clusters, static_cast<int64_t>(sk_tiles) * p.num_k_blk);
+            if (h->schedule == CUASM_SCHEDULE_AUTO && waves == 0) c = std::min<int64_t>(c, 2 * sk_tiles);
+            clusters = static_cast<int>(c);
+        }
     }
     p.num_clusters = clusters;
     p.num_dp_tiles = p.num_tiles - sk_tiles;
@@ -422,7 +427,12 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             static_cast<double>((sk_tiles + gm - 1) / gm + 1) * 256.0 * K * esize +
             static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
         const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
-        const double t_sk = std::max(hbm_floor, waves * KB * t_kb * pen * l2_pen + fixup);
+        // fewer tiles than clusters: auto stream-K splits each tile at most in two
+        // (launch_gemm), so only 2*tiles clusters work and each finisher adds one
+        // partial (more splits make the finisher read many partials: the paper's
+        // 512x2048x512 mmLeakyReLu took 65 us with 18 segments per tile)
+        const double sk_units = tiles < units ? static_cast<double>(std::min<int64_t>(units, 2 * tiles)) : units;
+        const double t_sk = std::max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup);
         // ties go to the earlier candidate: 2-SM before 1-SM, whole tiles before stream-K
         if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, false}; }
         if (K / BK > 1 && t_sk < best_t * 0.98) {

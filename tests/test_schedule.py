@@ -27,6 +27,8 @@ def plan(T, KB, max_clusters, schedule=0):
             sk_tiles = T if waves == 0 else rem + max_clusters
         if sk_tiles > 0:
             clusters = min(max_clusters, sk_tiles * KB)
+            if schedule == 0 and waves == 0:
+                clusters = min(clusters, 2 * sk_tiles)
     return clusters, T - sk_tiles, sk_tiles * KB
 
 
@@ -130,7 +132,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
         gm = min(mblk, 16)
         region = (-(-sk_tiles // gm) + 1) * 256.0 * K * esize + min(M, gm * 128 * cg) * K * esize
         l2_pen = 1.32 if region > 120e6 else 1.0
-        t_sk = max(hbm_floor, waves * KB * t_kb * pen * l2_pen + fixup)
+        sk_units = min(units, 2 * tiles) if tiles < units else units
+        t_sk = max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup)
         name = "2sm" if cg == 2 else "1sm"
         if t_dp < best_t * 0.999:
             best_t, best = t_dp, (name, False)
@@ -191,6 +194,11 @@ def test_library_plan_matches_measured_best(lib_plan, M):
                                       for op in ("ffn", "gemm")])
 def test_library_plan_equals_python_mirror(lib_plan, M, K, N, op):
     assert lib_plan(M, K, N, op) == plan_config(M, K, N, out_cols=128 if op == "ffn" else 256)
+
+
+def test_plan_paper_mmleakyrelu_is_whole_tiles(lib_plan):
+    # 512 x 2048 x 512: 4 tiles of 2-SM; stream-K would split each tile many ways
+    assert lib_plan(512, 2048, 512, "gemm")[1] is False
 
 
 def test_library_plan_w2_and_70b(lib_plan):
