@@ -62,6 +62,8 @@ EXTRA = {
     "mmleakyrelu_large": ("gemm_lrelu", 4096, 4096, 4096),
     # the paper's stand-alone rmsnorm: 4096 rows x 2048 features; N unused
     "rmsnorm_paper": ("rmsnorm", 4096, 2048, 8),
+    # BASELINE.json configs[0]: tiny fp32 fused FFN (tf32 tensor cores), latency-bound
+    "tiny_fp32": ("ffn", 16, 64, 128),
 }
 
 
@@ -307,7 +309,8 @@ def run_cuasm(args):
     N_l = n1 - n0
     seed = args.seed if args.seed is not None else seed_for(cidx)
     op = workload_op(args.workload)
-    t = make_device_inputs(M, K, N_l, seed, dev, w_seed=seed + 1 + rank)
+    wdtype = torch.float32 if args.workload == "tiny_fp32" else torch.bfloat16
+    t = make_device_inputs(M, K, N_l, seed, dev, dtype=wdtype, w_seed=seed + 1 + rank)
     if op == "block":
         # down projection W2 [K, N_l] (row-parallel shard), ~N(0, 1/N)
         gw = torch.Generator(device=dev)
@@ -317,12 +320,12 @@ def run_cuasm(args):
     elif op == "rmsnorm":
         out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
     else:
-        out = torch.empty((M, N_l), dtype=torch.bfloat16, device=dev)
+        out = torch.empty((M, N_l), dtype=wdtype, device=dev)
     flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0, "rmsnorm": 0.0}[op] * M * K * N
     flush = L2Flush(dev)
     eps = 1e-6
 
-    h = ffn.FusedFFN(dev, torch.bfloat16)
+    h = ffn.FusedFFN(dev, wdtype)
     h.set_variant(args.variant)
     if args.no_pdl:
         h.set_option(ffn.OPT_PDL, 0)
@@ -464,7 +467,7 @@ def run_cuasm(args):
     e2e = None
     if not args.skip_e2e and op == "ffn":
         x_host = t["x"].cpu().pin_memory()
-        out_host = torch.empty((M, N_l), dtype=torch.bfloat16, pin_memory=True)
+        out_host = torch.empty((M, N_l), dtype=wdtype, pin_memory=True)
         ne = min(args.steps, 20)
         for _ in range(2):
             h.forward_host(x_host, t["g"], t["w1"], t["w3"], eps, out_host, sync=True)
@@ -497,7 +500,7 @@ def run_cuasm(args):
         res = {
             "metric": metric, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (tf32 tensor cores)" if wdtype == torch.float32 else "bf16",
             "data": "synthetic (seeded randn x~N(0,1), W~N(0,1/K), g~U(0.5,1.5); bf16)",
             "config": {
                 "workload": args.workload, "M": M, "K": K, "N": N, "N_per_rank": N_l, "eps": eps,

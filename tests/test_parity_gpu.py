@@ -466,3 +466,15 @@ def test_new_entry_points_validate_arguments(cuda_device):
         ffn.ERR_INVALID_ARG
     torch.cuda.synchronize()
     assert torch.all(out == 3.0)
+
+
+def test_full_size_70b_unsharded(cuda_device):
+    """BASELINE.json configs[3] at P=1: M=4096 K=8192 N=28672 (0.94 GB of folded
+    weights), sampled rows incl. the first/last row block, vs the oracle."""
+    c = CONFIGS["llama70b"]
+    d = make_inputs(c["M"], c["K"], c["N"], family="A", seed=seed_for(c["idx"], 1), dtype="bf16")
+    out, _ = run_gpu(d, c["eps"], "bf16")
+    rows = [0, 1, 255, 256, 2047, 4095]
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], c["eps"], rows=rows)
+    check(out[rows], ref, "70b P=1")
+    assert torch.isfinite(out).all()
