@@ -83,10 +83,12 @@ typedef enum {
     CUASM_OPT_SCHEDULE = 4, /* value: cuasm_schedule_t                                 */
     CUASM_OPT_TRACE = 5,    /* value: 1 = every dual-GEMM launch records per-CTA
                                %globaltimer stamps (read with cuasm_ffn_trace_read)   */
-    CUASM_OPT_FUSED_NORM = 6 /* value: 1 (default) = step a1 runs inside the dual-GEMM
+    CUASM_OPT_FUSED_NORM = 6, /* value: 1 (default) = step a1 runs inside the dual-GEMM
                                kernel (its epilogue warps compute r while the first
                                tile's mainloop runs; one launch per forward); 0 = the
                                separate pre-pass kernel, PDL-overlapped with the GEMM */
+    CUASM_OPT_TILE_N = 7      /* cuasm_gemm_act / down projection only: MMA N of a tile,
+                               0 = auto (configuration model), 128 or 256              */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -224,8 +226,9 @@ const char* cuasm_ffn_last_error(cuasm_ffn_t h);
 /* The shape-keyed configuration model the AUTO variant and
  * schedule use, without a handle or a device: for `sm_count` SMs, element
  * type `dtype`, problem M x K x N and op (0: fused FFN, 128 outputs per tile;
- * 1: GEMM + activation, 256 outputs per tile) it returns the chosen
- * cuasm_variant_t and whether the stream-K tail is used.  Pure host code. */
+ * 1: GEMM + activation, 256- or 128-output tiles) it returns the chosen
+ * cuasm_variant_t and in *stream_k bit 0 = stream-K tail used, bit 1 = the
+ * 128-wide tile.  Pure host code. */
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k);
 

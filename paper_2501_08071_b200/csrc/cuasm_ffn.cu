@@ -61,6 +61,8 @@ struct cuasm_ffn_s {
     int schedule = 0;  // CUASM_OPT_SCHEDULE
     bool plan_sk = false;  // plan_config's stream-K choice for the current forward
     int trace = 0;     // CUASM_OPT_TRACE
+    int tile_n = 0;    // CUASM_OPT_TILE_N (GEMM + activation): 0 auto, 128, 256
+    int last_tile_n = 256;
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
     uint32_t* gsync = nullptr;  // grid counters of the fused RMS pass (self-resetting)
     unsigned long long* trace_buf = nullptr;
@@ -252,10 +254,10 @@ struct EpiSpec {
     float alpha;
 };
 
-template <int kKind, int kCtaGroup, int kEpi>
+template <int kKind, int kCtaGroup, int kEpi, int kN>
 cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
                            int64_t N, float eps, cudaStream_t s) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
     PackedWeights& w = h->pw[e.slot];
     CUtensorMap tmap_x;
     // A single row block with fewer than BM rows loads only the rows that exist
@@ -297,7 +299,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     static bool attr_set = false;  // one per template instance
     if (!attr_set) {
         CUASM_CHECK(h,
-                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi>,
+                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
                     "cudaFuncSetAttribute(smem)");
         attr_set = true;
@@ -378,7 +380,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
-    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi>, tmap_x, w.tmap, p),
+    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, tmap_x, w.tmap, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
     return CUASM_OK;
@@ -397,54 +399,64 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
 struct Plan {
     int variant;
     bool stream_k;
+    int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
 };
 
-Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
+Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,
+                     int tile_n_force = 0) {
     const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
     const int64_t BK = 128 / esize;
     const double KB = static_cast<double>((K + BK - 1) / BK);
     const int64_t nblk = (N + out_cols - 1) / out_cols;
     const double w_elems = out_cols == 128 ? 2.0 * N * K : 1.0 * N * K;  // W1+W3, or one weight
     const double hbm_floor = (w_elems + static_cast<double>(M) * K + static_cast<double>(M) * N) * esize / hbm;
-    Plan best{CUASM_VARIANT_2SM, false};
+    Plan best{CUASM_VARIANT_2SM, false, 256};
     double best_t = 1e30;
-    for (int cg = 2; cg >= 1; --cg) {
-        const int64_t units = sm_count / cg;
-        const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
-        const int64_t tiles = mblk * nblk;
-        const double waves = static_cast<double>(tiles) / units;
-        const double rounds = static_cast<double>((tiles + units - 1) / units);
-        const double pen = cg == 1 ? pen_1sm : 1.0;
-        const double t_dp = std::max(hbm_floor, rounds * KB * t_kb * pen);
-        // Stream-K keeps its whole region in flight at once (every cluster
-        // holds a slice of it), so when the region's operands overflow L2 the
-        // k-block rate drops (measured 0.49 vs 0.37 us on 2048x11008x4096,
-        // profiles/r01/trace_gemm.log): charge that as a 1.32x slowdown.
-        const int64_t rem = tiles % units;
-        const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
-        const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : 16);
-        const double region_bytes =
-            static_cast<double>((sk_tiles + gm - 1) / gm + 1) * 256.0 * K * esize +
-            static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
-        const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
-        // fewer tiles than clusters: auto stream-K splits each tile at most in two
-        // (launch_gemm), so only 2*tiles clusters work and each finisher adds one
-        // partial (more splits make the finisher read many partials: the paper's
-        // 512x2048x512 mmLeakyReLu took 65 us with 18 segments per tile)
-        const double sk_units = tiles < units ? static_cast<double>(std::min<int64_t>(units, 2 * tiles)) : units;
-        const double t_sk = std::max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup);
-        // ties go to the earlier candidate: 2-SM before 1-SM, whole tiles before stream-K
-        if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, false}; }
-        if (K / BK > 1 && t_sk < best_t * 0.98) {
-            best_t = t_sk;
-            best = Plan{cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM, true};
+    // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM
+    // mode may also use 128 (128 outputs, half the k-block time per tile)
+    const int widths[2] = {256, 128};
+    for (int wi = 0; wi < (out_cols == 128 ? 1 : 2); ++wi) {
+        const int tn = widths[wi];
+        if (tile_n_force && tn != tile_n_force) continue;
+        const int64_t oc = out_cols == 128 ? 128 : tn;   // output columns per tile
+        const double tile_frac = tn / 256.0;            // k-block time relative to N = 256
+        const int64_t nblk_w = (N + oc - 1) / oc;
+        for (int cg = 2; cg >= 1; --cg) {
+            const int64_t units = sm_count / cg;
+            const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
+            const int64_t tiles = mblk * nblk_w;
+            const double rounds = static_cast<double>((tiles + units - 1) / units);
+            const double pen = (cg == 1 ? pen_1sm : 1.0) * tile_frac;
+            const double t_dp = std::max(hbm_floor, rounds * KB * t_kb * pen);
+            // Stream-K keeps its whole region in flight at once (every cluster
+            // holds a slice of it), so when the region's operands overflow L2 the
+            // k-block rate drops (measured 0.49 vs 0.37 us on 2048x11008x4096,
+            // profiles/r01/trace_gemm.log): charge that as a 1.32x slowdown.
+            const int64_t rem = tiles % units;
+            const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
+            const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : 16);
+            const double region_bytes =
+                static_cast<double>((sk_tiles + gm - 1) / gm + 1) * tn * K * esize +
+                static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
+            const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
+            // fewer tiles than clusters: auto stream-K splits each tile at most in two
+            // (launch_gemm), so only 2*tiles clusters work and each finisher adds one
+            // partial (more splits make the finisher read many partials: the paper's
+            // 512x2048x512 mmLeakyReLu took 65 us with 18 segments per tile)
+            const double sk_units = tiles < units ? static_cast<double>(std::min<int64_t>(units, 2 * tiles)) : units;
+            const double t_sk = std::max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup);
+            const int v = cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM;
+            // ties go to the earlier candidate: N=256 before 128, 2-SM before 1-SM,
+            // whole tiles before stream-K
+            if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{v, false, tn}; }
+            if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn}; }
         }
     }
     return best;
 }
 
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
-    return plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols);
+    return plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n);
 }
 
 cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
@@ -469,15 +481,15 @@ cuasm_status_t profile_event(cuasm_ffn_t h, cudaStream_t s) {
     return CUASM_OK;
 }
 
-template <int kEpi>
+template <int kEpi, int kN>
 cuasm_status_t dispatch_gemm(cuasm_ffn_t h, const EpiSpec& e, int v, const void* x, void* out, int64_t M, int64_t K,
                              int64_t N, float eps, cudaStream_t s) {
     if (h->dtype == CUASM_DTYPE_BF16) {
-        return v == CUASM_VARIANT_2SM ? launch_gemm<0, 2, kEpi>(h, e, x, out, M, K, N, eps, s)
-                                      : launch_gemm<0, 1, kEpi>(h, e, x, out, M, K, N, eps, s);
+        return v == CUASM_VARIANT_2SM ? launch_gemm<0, 2, kEpi, kN>(h, e, x, out, M, K, N, eps, s)
+                                      : launch_gemm<0, 1, kEpi, kN>(h, e, x, out, M, K, N, eps, s);
     }
-    return v == CUASM_VARIANT_2SM ? launch_gemm<1, 2, kEpi>(h, e, x, out, M, K, N, eps, s)
-                                  : launch_gemm<1, 1, kEpi>(h, e, x, out, M, K, N, eps, s);
+    return v == CUASM_VARIANT_2SM ? launch_gemm<1, 2, kEpi, kN>(h, e, x, out, M, K, N, eps, s)
+                                  : launch_gemm<1, 1, kEpi, kN>(h, e, x, out, M, K, N, eps, s);
 }
 
 // Launch one dual-GEMM kernel (plus the stand-alone pre-pass when a1 is not
@@ -507,7 +519,10 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     const Plan plan = plan_config(h, M, K, N, kepi == 0 ? 128 : 256);
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
-    st = kepi == 0 ? dispatch_gemm<0>(h, e, v, x, out, M, K, N, eps, s) : dispatch_gemm<1>(h, e, v, x, out, M, K, N, eps, s);
+    if (kepi == 0) st = dispatch_gemm<0, 256>(h, e, v, x, out, M, K, N, eps, s);
+    else if (plan.tile_n == 128) st = dispatch_gemm<1, 128>(h, e, v, x, out, M, K, N, eps, s);
+    else st = dispatch_gemm<1, 256>(h, e, v, x, out, M, K, N, eps, s);
+    h->last_tile_n = kepi == 0 ? 256 : plan.tile_n;
     if (st != CUASM_OK) return st;
     h->last_kernels += separate_prepass ? 2 : 1;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
@@ -562,7 +577,7 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
         return CUASM_ERR_INVALID_ARG;
     const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
     *variant = pl.variant;
-    *stream_k = pl.stream_k ? 1 : 0;
+    *stream_k = pl.stream_k ? (pl.tile_n == 128 ? 3 : 1) : (pl.tile_n == 128 ? 2 : 0);
     return CUASM_OK;
 }
 
@@ -834,6 +849,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
     case CUASM_OPT_FUSED_NORM:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "FUSED_NORM option is 0 or 1");
         h->fused_norm = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_TILE_N:
+        if (value != 0 && value != 128 && value != 256) return fail(h, CUASM_ERR_INVALID_ARG, "TILE_N is 0, 128 or 256");
+        h->tile_n = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_TRACE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "TRACE option is 0 or 1");

@@ -174,35 +174,51 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 //     out[m, n0+j] = SiLU(r*acc[j]) * (r*acc[128+j]), 128 outputs per tile.
 //   1 (GEMM + activation) B = 256 rows of one weight matrix;
 //     out[m, n0+j] = act(r*acc[j]), 256 outputs per tile (r = 1 unless use_r).
-template <int kKind, int kCtaGroup, int kEpi = 0>
+// kN: the MMA N.  kEpi 0 uses 256 (128 W1g + 128 W3g rows); kEpi 1 uses 256
+// or 128 (a 128-output tile reads half of a packed 256-row block) -- the
+// narrower tile halves the wave-quantisation step of square-ish GEMMs.
+template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256>
 struct GemmCfg {
+    static_assert(kN == 256 || (kEpi == 1 && kN == 128), "SwiGLU tiles are 256 wide");
     static constexpr int kEsize = kKind == 0 ? 2 : 4;
     static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
     static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
-    static constexpr int BN = 128;                 // half of the MMA N
-    static constexpr int UMMA_N = 2 * BN;
+    static constexpr int UMMA_N = kN;
+    static constexpr int BN = kN / 2;              // SwiGLU: outputs per tile (h1 | h3 halves)
     static constexpr int OUT_COLS = kEpi == 0 ? BN : UMMA_N;  // output columns per tile
+    static constexpr int PACK_ROWS = 256;          // rows of one packed (n-block, k-block) box run
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
-    static constexpr int STAGES = kCtaGroup == 1 ? 4 : 7;  // 2-SM: 7 x 32 KB + barriers = 226 KB of 227
     static constexpr int A_BYTES = BM * 128;                        // per CTA
     static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // packed-weight rows loaded per CTA
     static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
-    static constexpr int TMEM_COLS = 512;                           // 2 accumulators x UMMA_N
+    static constexpr int BAR_BYTES = 1024;
+    // as many pipeline stages as fit in 227 KB (4 x 48 KB 1-SM/256, 7 x 32 KB 2-SM/256,
+    // 7 x 32 KB 1-SM/128, 9 x 24 KB 2-SM/128)
+    static constexpr int STAGES_FIT = (232448 - BAR_BYTES - 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT < 9 ? STAGES_FIT : 9;
+    static constexpr int TMEM_COLS = 2 * UMMA_N;                    // 2 accumulators (power of 2)
     // Two epilogue warps per TMEM lane quadrant, each owning half of the
-    // accumulator columns (two pairs of 32-column chunks): two warps per SM
+    // accumulator columns (PAIRS pairs of 32-column chunks): two warps per SM
     // sub-partition hide the MUFU/TMEM latency of the epilogue math.
     static constexpr int NUM_EPI_WARPS = 8;
+    static constexpr int PAIRS = UMMA_N / 128;
     static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 320
-    static constexpr int BAR_BYTES = 1024;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + align slack
     static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
     // Accumulator chunks (32 columns) of epilogue pair `i` of a warp in column half `half`.
-    __device__ static constexpr int chunk_a(int half, int i) { return kEpi == 0 ? half * 2 + i : half * 4 + 2 * i; }
+    __device__ static constexpr int chunk_a(int half, int i) {
+        return kEpi == 0 ? half * 2 + i : half * (UMMA_N / 64) + 2 * i;
+    }
     __device__ static constexpr int chunk_b(int half, int i) {
-        return kEpi == 0 ? half * 2 + i + BN / 32 : half * 4 + 2 * i + 1;
+        return kEpi == 0 ? half * 2 + i + BN / 32 : half * (UMMA_N / 64) + 2 * i + 1;
+    }
+    // First packed row of n-block nb's (or its half's) box for k-block 0; k-block kb adds kb * PACK_ROWS.
+    __device__ static constexpr int b_row0(int nb, int KB) {
+        return kEpi == 0 ? nb * KB * PACK_ROWS
+                         : (nb * OUT_COLS / PACK_ROWS) * KB * PACK_ROWS + (nb * OUT_COLS) % PACK_ROWS;
     }
 };
 
@@ -263,11 +279,11 @@ __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int
     }
 }
 
-template <int kKind, int kCtaGroup, int kEpi>
-__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 1)
+template <int kKind, int kCtaGroup, int kEpi, int kN>
+__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                          const FfnGemmParams p) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
             tile_coords(sg.tile, p, mb, nb);
             const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
             // k-block-tiled weights (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*UMMA_N
-            const int row_b0 = nb * p.num_k_blk * C::UMMA_N + static_cast<int>(cta_rank) * C::B_ROWS;
+            const int row_b0 = C::b_row0(nb, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
             for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
                 ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
                 const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
@@ -339,12 +355,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
                     if constexpr (kCtaGroup == 1) {
                         ptx::mbar_arrive_expect_tx(fb, p.a_box_bytes + C::B_BYTES);
                         ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
+                        ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     } else {
                         // both CTAs' bytes land on the leader's barrier
                         if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * (p.a_box_bytes + C::B_BYTES));
                         ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::UMMA_N, pol_w);
+                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     }
                 }
                 __syncwarp();
@@ -495,7 +511,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
                         reinterpret_cast<const float4*>(p.ws) +
                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4));
 #pragma unroll
-                    for (int i = 0; i < 2; ++i) {
+                    for (int i = 0; i < C::PAIRS; ++i) {
 #pragma unroll
                         for (int hh = 0; hh < 2; ++hh) {  // chunk a, chunk b: 4 KB each
                             const int64_t chunk = hh == 0 ? C::chunk_a(half, i) : C::chunk_b(half, i);
@@ -534,7 +550,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi>::NUM_THREADS, 
             if (warp == 2 && lane == 0) trace_stamp(p, 10);
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < C::PAIRS; ++i) {
                 const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
                 uint32_t v1[32], v3[32];
                 ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);

@@ -19,14 +19,21 @@ import paper_2501_08071_b200 as ffn
 from ffn_inputs import make_device_inputs
 
 CONFIGS = [(1, 1, "1sm-dp"), (1, 2, "1sm-sk"), (2, 1, "2sm-dp"), (2, 2, "2sm-sk")]
+GEMM_CONFIGS = [(v, sch, tn, f"{'1sm' if v == 1 else '2sm'}-{'dp' if sch == 1 else 'sk'}-n{tn}")
+                for v in (1, 2) for sch in (1, 2) for tn in (256, 128)]
 
 
-def time_cfg(h, x, t, out, steps, flush):
+def time_cfg(h, x, t, out, steps, flush, op="ffn"):
+    def run():
+        if op == "ffn":
+            h.forward(x, t["g"], t["w1"], t["w3"], 1e-6, out=out)
+        else:
+            h.gemm_act(x, t["w1"], "leaky_relu", 0.01, out=out)
     for _ in range(2):
-        h.forward(x, t["g"], t["w1"], t["w3"], 1e-6, out=out)
+        run()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        h.forward(x, t["g"], t["w1"], t["w3"], 1e-6, out=out)
+        run()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     torch.cuda.synchronize()
     torch.cuda._sleep(int(1e8))
@@ -47,28 +54,34 @@ def main():
     ap.add_argument("--N", type=int, default=11008)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--op", default="ffn", choices=["ffn", "gemm"])
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     flush = bench.L2Flush(dev)
     Ms = [int(m) for m in a.ms.split(",")]
     t = make_device_inputs(max(Ms), a.K, a.N, 11, dev)
     handles = {}
-    for v, sch, name in CONFIGS:
+    cfgs = CONFIGS if a.op == "ffn" else GEMM_CONFIGS
+    for c in cfgs:
         h = ffn.FusedFFN(dev)
-        h.set_variant(v)
-        h.set_option(ffn.OPT_SCHEDULE, sch)
-        h.prepare(t["g"], t["w1"], t["w3"])
-        handles[name] = h
+        h.set_variant(c[0])
+        h.set_option(ffn.OPT_SCHEDULE, c[1])
+        if a.op == "gemm":
+            h.set_option(ffn.OPT_TILE_N, c[2])
+        else:
+            h.prepare(t["g"], t["w1"], t["w3"])
+        handles[c[-1]] = h
     rows = []
     for M in Ms:
         x = t["x"][:M].contiguous()
         out = torch.empty((M, a.N), dtype=torch.bfloat16, device=dev)
         r = {"M": M}
-        for _, _, name in CONFIGS:
-            r[name] = round(time_cfg(handles[name], x, t, out, a.steps, flush), 2)
+        for c in cfgs:
+            r[c[-1]] = round(time_cfg(handles[c[-1]], x, t, out, a.steps, flush, a.op), 2)
         hauto = handles.setdefault("auto", ffn.FusedFFN(dev))
-        r["auto"] = round(time_cfg(hauto, x, t, out, a.steps, flush), 2)
-        r["best"] = min((k for k in r if k not in ("M", "best")), key=lambda k: r[k])
+        r["auto"] = round(time_cfg(hauto, x, t, out, a.steps, flush, a.op), 2)
+        r["auto_plan"] = ffn.plan_config(M, a.K, a.N, a.op)
+        r["best"] = min((k for k in r if k not in ("M", "best", "auto_plan")), key=lambda k: r[k])
         rows.append(r)
         print(json.dumps(r), flush=True)
     if a.out:

@@ -336,14 +336,17 @@ def test_forward_host_matches_device_path(cuda_device, M):
 
 
 # --------------------------------------------- f3: mmLeakyReLu, f1: FFN block ----
+@pytest.mark.parametrize("tile_n", [0, 128, 256])
 @pytest.mark.parametrize("variant", [ffn.VARIANT_AUTO, ffn.VARIANT_1SM, ffn.VARIANT_2SM])
 @pytest.mark.parametrize("M,K,N", [(512, 2048, 512), (300, 520, 776), (1, 64, 256), (1000, 1024, 2056)])
 @pytest.mark.parametrize("act,alpha", [("leaky_relu", 0.01), ("identity", 0.0)])
-def test_gemm_act_parity(cuda_device, M, K, N, act, alpha, variant):
-    """The paper's mmLeakyReLu (B,M,N,K = 1,512,512,2048) and plain GEMM."""
+def test_gemm_act_parity(cuda_device, M, K, N, act, alpha, variant, tile_n):
+    """The paper's mmLeakyReLu (B,M,N,K = 1,512,512,2048) and plain GEMM,
+    256- and 128-wide tiles."""
     d = make_inputs(M, K, N, family="C", seed=5000 + M + N, dtype="bf16")
     h = ffn.FusedFFN(cuda_device, torch.bfloat16)
     h.set_variant(variant)
+    h.set_option(ffn.OPT_TILE_N, tile_n)
     x, w = d["x"].to(cuda_device), d["w1"].to(cuda_device)
     out = h.gemm_act(x, w, act, alpha)
     torch.cuda.synchronize()
@@ -422,12 +425,13 @@ def test_fuzz_ffn_shapes(cuda_device, i, M, K, N, variant, schedule):
     check(out[rows], ref, f"fuzz {i}: {M}x{K}x{N} v{variant} s{schedule}")
 
 
-@pytest.mark.parametrize("i,M,K,N,variant,schedule", _fuzz_cases(12, 778))
+@pytest.mark.parametrize("i,M,K,N,variant,schedule", _fuzz_cases(16, 778))
 def test_fuzz_gemm_act_shapes(cuda_device, i, M, K, N, variant, schedule):
     d = make_inputs(M, K, N, family="C", seed=9100 + i, dtype="bf16")
     h = ffn.FusedFFN(cuda_device, torch.bfloat16)
     h.set_variant(variant)
     h.set_option(ffn.OPT_SCHEDULE, schedule)
+    h.set_option(ffn.OPT_TILE_N, (0, 128, 256)[i % 3])
     out = h.gemm_act(d["x"].to(cuda_device), d["w1"].to(cuda_device), "leaky_relu", 0.125)
     torch.cuda.synchronize()
     rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 16)))))

@@ -116,29 +116,30 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     t_kb, fixup, hbm, pen_1sm = 0.37e-6, 10e-6, 6.5e12, 1.16
     BK = 128 // esize
     KB = -(-K // BK)
-    nblk = -(-N // out_cols)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
-    best, best_t = ("2sm", False), 1e30
-    for cg in (2, 1):
-        units = sm_count // cg
-        mblk = -(-M // (128 * cg))
-        tiles = mblk * nblk
-        waves = tiles / units
-        rounds = -(-tiles // units)
-        pen = pen_1sm if cg == 1 else 1.0
-        t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
-        rem = tiles % units
-        sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
-        gm = min(mblk, 16)
-        region = (-(-sk_tiles // gm) + 1) * 256.0 * K * esize + min(M, gm * 128 * cg) * K * esize
-        l2_pen = 1.32 if region > 120e6 else 1.0
-        sk_units = min(units, 2 * tiles) if tiles < units else units
-        t_sk = max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup)
-        name = "2sm" if cg == 2 else "1sm"
-        if t_dp < best_t * 0.999:
-            best_t, best = t_dp, (name, False)
-        if K // BK > 1 and t_sk < best_t * 0.98:
-            best_t, best = t_sk, (name, True)
+    best, best_t = ("2sm", False, 256), 1e30
+    for tn in ((256,) if out_cols == 128 else (256, 128)):
+        oc = 128 if out_cols == 128 else tn
+        nblk = -(-N // oc)
+        for cg in (2, 1):
+            units = sm_count // cg
+            mblk = -(-M // (128 * cg))
+            tiles = mblk * nblk
+            rounds = -(-tiles // units)
+            pen = (pen_1sm if cg == 1 else 1.0) * tn / 256.0
+            t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
+            rem = tiles % units
+            sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
+            gm = min(mblk, 16)
+            region = (-(-sk_tiles // gm) + 1) * tn * K * esize + min(M, gm * 128 * cg) * K * esize
+            l2_pen = 1.32 if region > 120e6 else 1.0
+            sk_units = min(units, 2 * tiles) if tiles < units else units
+            t_sk = max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup)
+            name = "2sm" if cg == 2 else "1sm"
+            if t_dp < best_t * 0.999:
+                best_t, best = t_dp, (name, False, tn)
+            if K // BK > 1 and t_sk < best_t * 0.98:
+                best_t, best = t_sk, (name, True, tn)
     return best
 
 
@@ -162,17 +163,18 @@ MEASURED_BEST = {
 
 @pytest.mark.parametrize("M", sorted(MEASURED_BEST))
 def test_plan_matches_measured_best(M):
-    assert plan_config(M, 4096, 11008) in MEASURED_BEST[M]
+    assert plan_config(M, 4096, 11008)[:2] in MEASURED_BEST[M]
 
 
 def test_plan_70b_shard_uses_stream_k():
     # 8-way shard of the 70B FFN: 448 tiles = 6.05 waves of 74 CTA pairs
-    assert plan_config(4096, 8192, 3584) == ("2sm", True)
+    assert plan_config(4096, 8192, 3584)[:2] == ("2sm", True)
 
 
 def test_plan_w2_down_projection_avoids_l2_thrashing_stream_k():
     # hidden [2048, 11008] x W2 [4096, 11008]: whole tiles 128 us vs stream-K 158 us measured
-    assert plan_config(2048, 11008, 4096, out_cols=256) == ("2sm", False)
+    # (256-wide stream-K would thrash L2: 128 us whole tiles vs 158 us measured)
+    assert plan_config(2048, 11008, 4096, out_cols=256) != ("2sm", True, 256)
 
 
 # ---- the library's own implementation agrees with the model above -------------------
@@ -186,7 +188,7 @@ def lib_plan():
 
 @pytest.mark.parametrize("M", sorted(MEASURED_BEST))
 def test_library_plan_matches_measured_best(lib_plan, M):
-    assert lib_plan(M, 4096, 11008) in MEASURED_BEST[M]
+    assert lib_plan(M, 4096, 11008)[:2] in MEASURED_BEST[M]
 
 
 @pytest.mark.parametrize("M,K,N,op", [(m, k, n, op) for m in (1, 16, 200, 512, 1000, 2048, 4096, 16384)
@@ -201,6 +203,11 @@ def test_plan_paper_mmleakyrelu_is_whole_tiles(lib_plan):
     assert lib_plan(512, 2048, 512, "gemm")[1] is False
 
 
+def test_plan_square_gemm_prefers_narrow_tiles(lib_plan):
+    # 4096^3: 256 tiles of 256 wide = 3.46 waves vs 512 tiles of 128 wide = 6.92 waves
+    assert lib_plan(4096, 4096, 4096, "gemm")[2] == 128
+
+
 def test_library_plan_w2_and_70b(lib_plan):
-    assert lib_plan(2048, 11008, 4096, "gemm") == ("2sm", False)
-    assert lib_plan(4096, 8192, 3584) == ("2sm", True)
+    assert lib_plan(2048, 11008, 4096, "gemm") != ("2sm", True, 256)
+    assert lib_plan(4096, 8192, 3584)[:2] == ("2sm", True)
