@@ -419,7 +419,10 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
         const int tn = widths[wi];
         if (tile_n_force && tn != tile_n_force) continue;
         const int64_t oc = out_cols == 128 ? 128 : tn;   // output columns per tile
-        const double tile_frac = tn / 256.0;            // k-block time relative to N = 256
+        // k-block time relative to N = 256: a 128-wide k-block costs 0.72 of a 256-wide one,
+        // not 0.5 -- its fixed per-k-block issue/TMA overheads do not halve
+        // (scripts/tune.py --op gemm, profiles/r01/tune_gemm*.log)
+        const double tile_frac = tn == 256 ? 1.0 : 0.72;
         const int64_t nblk_w = (N + oc - 1) / oc;
         for (int cg = 2; cg >= 1; --cg) {
             const int64_t units = sm_count / cg;

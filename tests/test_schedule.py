@@ -126,7 +126,7 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
             mblk = -(-M // (128 * cg))
             tiles = mblk * nblk
             rounds = -(-tiles // units)
-            pen = (pen_1sm if cg == 1 else 1.0) * tn / 256.0
+            pen = (pen_1sm if cg == 1 else 1.0) * (1.0 if tn == 256 else 0.72)
             t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
             rem = tiles % units
             sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
@@ -203,9 +203,24 @@ def test_plan_paper_mmleakyrelu_is_whole_tiles(lib_plan):
     assert lib_plan(512, 2048, 512, "gemm")[1] is False
 
 
-def test_plan_square_gemm_prefers_narrow_tiles(lib_plan):
-    # 4096^3: 256 tiles of 256 wide = 3.46 waves vs 512 tiles of 128 wide = 6.92 waves
-    assert lib_plan(4096, 4096, 4096, "gemm")[2] == 128
+# measured best of {1-SM, 2-SM} x {whole tiles, stream-K} x {256, 128 wide} for the
+# GEMM + activation mode (profiles/r01/tune_gemm*.log); near-ties (<= 3%) accept either
+GEMM_MEASURED = {
+    (512, 4096, 4096): {("2sm", False, 128)},
+    (2048, 4096, 4096): {("2sm", False, 256)},
+    (4096, 4096, 4096): {("2sm", False, 256), ("2sm", True, 256)},
+    (8192, 4096, 4096): {("2sm", False, 256)},
+    (2048, 11008, 4096): {("2sm", False, 256)},
+    (4096, 11008, 4096): {("2sm", False, 256)},
+    (512, 2048, 512): {("2sm", False, 128), ("1sm", False, 128)},
+    (512, 11008, 4096): {("2sm", True, 256), ("1sm", True, 256)},
+}
+
+
+@pytest.mark.parametrize("shape", sorted(GEMM_MEASURED))
+def test_library_gemm_plan_matches_measured_best(lib_plan, shape):
+    M, K, N = shape
+    assert lib_plan(M, K, N, "gemm") in GEMM_MEASURED[shape]
 
 
 def test_library_plan_w2_and_70b(lib_plan):
