@@ -1,31 +1,38 @@
-// dual_gemm.cuh -- steps a2 + a3 of the hot path on the 5th-gen tensor cores.
+// dual_gemm.cuh -- the persistent tcgen05 kernel behind every GEMM of the
+// library: steps a1 (fused row inverse-RMS), a2 and a3 of the fused FFN, and
+// the GEMM + activation mode (mmLeakyReLu, the FFN block's down projection).
 //
-//   acc[m, 0:BN]    = sum_k x[m,k] * W1g[n0 + j, k]      (h1 / r)
-//   acc[m, BN:2BN]  = sum_k x[m,k] * W3g[n0 + j, k]      (h3 / r)
-//   out[m, n0 + j]  = RNE( h1 * sigma(h1) * h3 ),  h1 = r[m]*acc1, h3 = r[m]*acc3
+//   FFN (kEpi 0):  acc[m, 0:128]   = sum_k x[m,k] * W1g[n0 + j, k]   (h1 / r)
+//                  acc[m, 128:256] = sum_k x[m,k] * W3g[n0 + j, k]   (h3 / r)
+//                  out[m, n0 + j]  = RNE( h1 * sigma(h1) * h3 ),  h1 = r[m]*acc1, h3 = r[m]*acc3
+//   GEMM (kEpi 1): out[m, n0 + j]  = RNE( act( acc[m, j] ) )
 //
 // (BASELINE.json north_star: dual GEMM on tcgen05.mma with TMEM accumulators
 // fed by TMA, 1/rms scale + SiLU + product fused in the epilogue; the paper's
-// fused_ff, PAPER.md P:68 / P:560.)  One MMA of N = 2*BN over the interleaved
+// fused_ff, PAPER.md P:68 / P:560.)  One MMA of N = 256 over the interleaved
 // W13 block (pack.cuh) yields both halves of the gate for the same outputs.
 //
-// Kernel structure (persistent, one CTA per SM, warp-specialised):
-//   warp 0      TMA producer  (one elected lane): x tile [BM x BK] and W13
-//               tile [2BN x BK] per stage, 128-byte swizzle, mbarrier tx-count
-//   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
-//               tcgen05.mma (K=16 bf16 / K=8 tf32) per stage, tcgen05.commit
-//               frees the stage; a final commit hands the accumulator over
-//   warps 2..9  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//               32*(w%4)..+31 = tile rows, and half of the output columns),
-//               r-scale, SiLU, gate, bf16 pack, 16-byte global stores
-// TMEM holds two 2*BN-column accumulators (512 columns) so the epilogue of
-// tile i overlaps the mainloop of tile i+1.
+// Kernel structure (persistent, one CTA per SM, warp-specialised, 320 threads):
+//   warp 0      TMA producer: the warp walks the k-block loop, an elected lane
+//               issues the x tile [BM x BK] and weight tile [B_ROWS x BK] loads
+//               per stage (128-byte swizzle, mbarrier transaction counts)
+//   warp 1      TMEM allocator + MMA issuer: the warp walks the loop, an elected
+//               lane issues 4 x tcgen05.mma (K=16 bf16 / K=8 tf32) per stage and
+//               the tcgen05.commit that frees it; a final commit per tile hands
+//               the accumulator to the epilogue
+//   warps 2..9  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32*(w%4)..+31
+//               = tile rows, and half of the accumulator columns), r-scale,
+//               activation / SiLU gate, bf16 pack, 16-byte global stores; at
+//               kernel entry they also compute r for a 1/grid slice of the rows
+// TMEM holds two UMMA_N-column accumulators so the epilogue of tile i overlaps
+// the mainloop of tile i+1.  The schedule (Sched) is whole tiles, optionally
+// followed by a stream-K tail whose partials go through a global workspace.
 //
 // kCtaGroup == 2 (2-SM variant): a cluster of two CTAs on one TPC computes a
-// 256 x 2BN tile with tcgen05.mma.cta_group::2.  Each CTA TMA-loads its own
-// 128 rows of x and HALF of the W13 block (rank 0: the W1g rows, rank 1: the
-// W3g rows), both crediting the leader's barrier; only the leader issues the
-// MMAs; commits multicast to both CTAs; each CTA's epilogue drains its own
+// 256 x UMMA_N tile with tcgen05.mma.cta_group::2.  Each CTA TMA-loads its own
+// 128 rows of x and HALF of the weight block (FFN: rank 0 the W1g rows, rank 1
+// the W3g rows), both crediting the leader's barrier; only the leader issues
+// the MMAs; commits multicast to both CTAs; each CTA's epilogue drains its own
 // 128 accumulator rows (its own TMEM).
 #pragma once
 #include <cuda.h>
@@ -61,8 +68,9 @@ struct FfnGemmParams {
     int num_dp_tiles;   // tiles [0, num_dp_tiles) round-robin, whole
     int64_t sk_iters;   // (num_tiles - num_dp_tiles) * num_k_blk k-block iterations,
                         // split into num_clusters contiguous ranges
-    float* ws;          // stream-K partials: [cluster][cta rank][2BN/32][128][32] fp32
-    unsigned long long* trace;  // optional [gridDim.x][8] %globaltimer stamps (CUASM_OPT_TRACE), or null
+    float* ws;          // stream-K partials: per (cluster, cta rank) a BM x UMMA_N fp32 slot in the
+                        // lane-contiguous layout [chunk][quad][8 float4][32 lanes] (see the epilogue)
+    unsigned long long* trace;  // optional [gridDim.x][16] stamps / counters (CUASM_OPT_TRACE), or null
     uint32_t* flags;    // [cluster][cta rank][8 epilogue warps]: 1 = partial published;
                         // the finisher consumes (resets to 0) it, so launches need no
                         // per-launch state and the kernel can be replayed from a CUDA graph
@@ -135,11 +143,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Trace slots per CTA: 0 entry, 1 first TMA issued, 2 last TMA issued,
-// 3 last MMA issued, 4 epilogue start (after PDL wait), 5 epilogue done, 6 exit,
-// 7 final tile's accumulator handed to the epilogue (tfull wait returned).
-// 8 first tile's accumulator handed over, 9 first tile's epilogue done,
-// 10 final tile: contributor flags acquired, 11 final tile: first chunk stored.
+// Trace slots per CTA (%globaltimer ns unless noted): 0 entry, 1 first TMA
+// issued, 2 last TMA issued, 3 last MMA issued, 4 epilogue start (after the PDL
+// wait), 5 epilogue done (max over warps), 6 exit, 7 final tile's accumulator
+// handed to the epilogue, 8 first tile's accumulator handed over, 9 first
+// tile's epilogue done, 10 final tile: contributor flags acquired, 11 final
+// tile's epilogue done; leader CTAs also store 12 SM cycles from the first to
+// the last MMA issue, 13 k-blocks issued, 14 / 15 issuer cycles spent waiting
+// for data (full barriers) / for a free accumulator.
 constexpr int kTraceSlots = 16;
 __device__ __forceinline__ void trace_stamp(const FfnGemmParams& p, int slot) {
     if (p.trace) p.trace[blockIdx.x * kTraceSlots + slot] = globaltimer();
