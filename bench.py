@@ -16,11 +16,17 @@ Default workload: LLaMA-7B prefill FFN, M=2048 K=4096 N=11008 bf16
 (Megatron, N/P rows each, x replicated; no data-path collective unless
 --gather), so the total problem is fixed: "scaling": "strong".
 
-Timing: W warm-up steps, then exactly K steps between barrier+synchronize
-brackets; each step has its own CUDA-event pair on the launching stream and a
-L2 flush before it (256 MiB memset + 256 MiB read), outside the event pair; value = total
-FLOPs of the K steps / max-over-ranks summed device time.  FLOPs = 4*M*K*N
-(the two GEMMs; pre-pass and epilogue excluded).
+Timing (the paper's protocol P:384): W warm-up steps,
+then exactly K steps between barrier+synchronize brackets; each step has its
+own CUDA-event pair on the launching stream and a L2 flush before it (256 MiB
+memset + 256 MiB read), outside the event pair; value = total FLOPs of the K
+steps / max-over-ranks summed device time.  FLOPs = 4*M*K*N (the two GEMMs;
+pre-pass and epilogue excluded).  `back_to_back` adds the sustained number:
+the step's data (x, W1/W3, out) in R "layer" copies with their own handles, R
+chosen so >= 2x L2 of other data passes through L2 between two uses of a copy
+("inputs larger than L2"), K steps cycling the copies back to back in one CUDA
+graph (PDL between steps) between one event pair -- no per-step event/launch
+cost, and the power draw of a long step.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 oracle
 (oracle/, the test-only CPU reference) on bounded row samples of the same
@@ -46,6 +52,7 @@ import torch.distributed as dist
 METRIC = "fused RMSNorm+SwiGLU FFN TFLOP/s"
 UNIT = "TFLOP/s"
 FLUSH_BYTES = 256 << 20  # > 2x the 126 MB L2
+MAX_LAYER_COPIES = 16    # back_to_back: at most this many copies of a step's data
 
 WORKLOADS = {
     # name: (M, K, N, BASELINE.json configs index)
@@ -79,6 +86,9 @@ def parse_args(argv=None):
     ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of a CUDA graph")
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="projection: time rank 0's column shard of a P-way split on this one GPU")
+    ap.add_argument("--skip-b2b", action="store_true", help="skip the back-to-back (layer copies) measurement")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0, help="oracle CPU time budget (cpu_baseline)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0, help="whole --impl reference run budget")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
@@ -261,6 +271,26 @@ def host_cores() -> int:
 
 
 # ------------------------------------------------------------------ cpu baseline
+def calibrate_rows(inputs_cpu, eps, budget_s):
+    """Rows of the oracle that take about `budget_s` on the host cores.
+
+    The oracle is row-blocked (a weight row is streamed once per block of
+    rows), so one row costs far more than 1/M of the whole: time a 32-row
+    probe, then one more probe sized from it, and extrapolate from the larger."""
+    import oracle
+    x, g, w1, w3 = inputs_cpu["x"], inputs_cpu["g"], inputs_cpu["w1"], inputs_cpu["w3"]
+    M = x.shape[0]
+    n = min(M, 32)
+    while True:
+        t0 = time.perf_counter()
+        oracle.ffn(x, g, w1, w3, eps, mode="fold_bf16", rows=list(range(n)))
+        dt = max(time.perf_counter() - t0, 1e-4)
+        if n >= M or dt >= 0.1 * budget_s:
+            break
+        n = min(M, max(2 * n, int(n * 0.1 * budget_s / dt)))
+    return max(1, min(M, int(n * budget_s / dt)))
+
+
 def oracle_sample_time(inputs_cpu, eps, budget_s, rows_hint=None):
     """Time the fp64 oracle on a bounded sample of rows of the same workload.
 
@@ -272,10 +302,7 @@ def oracle_sample_time(inputs_cpu, eps, budget_s, rows_hint=None):
     N = w1.shape[0]
     threads = oracle.num_threads()
     if rows_hint is None:
-        t0 = time.perf_counter()
-        oracle.ffn(x, g, w1, w3, eps, mode="fold_bf16", rows=[0])
-        t1 = time.perf_counter() - t0
-        rows_hint = max(1, min(M, int(budget_s / max(t1, 1e-4))))
+        rows_hint = calibrate_rows(inputs_cpu, eps, budget_s)
     rows = sorted(set((torch.arange(rows_hint) * max(1, M // rows_hint)).clamp(max=M - 1).tolist()))
     t0 = time.perf_counter()
     oracle.ffn(x, g, w1, w3, eps, mode="fold_bf16", rows=rows)
@@ -306,6 +333,11 @@ def run_cuasm(args):
 
     M, K, N, cidx = workload_shape(args.workload)
     n0, n1 = shard_bounds(N, rank, world)
+    if args.shard_of > 1:
+        # projection on one GPU: run rank 0's shard of a P-way column split alone
+        if world != 1:
+            raise SystemExit("--shard-of is a single-process projection")
+        n0, n1 = shard_bounds(N, 0, args.shard_of)
     N_l = n1 - n0
     seed = args.seed if args.seed is not None else seed_for(cidx)
     op = workload_op(args.workload)
@@ -321,45 +353,71 @@ def run_cuasm(args):
         out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
     else:
         out = torch.empty((M, N_l), dtype=wdtype, device=dev)
-    flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0, "rmsnorm": 0.0}[op] * M * K * N
+    # whole-job FLOPs per step (with --shard-of P: P equal shards, each as fast as rank 0's)
+    flops_per_step = {"ffn": 4.0, "block": 6.0, "gemm_lrelu": 2.0, "rmsnorm": 0.0}[op] * M * K * (
+        N_l * args.shard_of if args.shard_of > 1 else N)
     flush = L2Flush(dev)
     eps = 1e-6
 
-    h = ffn.FusedFFN(dev, wdtype)
-    h.set_variant(args.variant)
-    if args.no_pdl:
-        h.set_option(ffn.OPT_PDL, 0)
+    # Step footprint in HBM (x, weights, out), for the back-to-back measurement:
+    # R "layer" copies of (x, weights, out), each with its own handle (own folded
+    # weights), cycled step by step so that >= 2x L2 of other data streams through
+    # L2 between two uses of a copy -- every step reads its operands from HBM, as
+    # consecutive layers of a model do -- and run back to back (one CUDA graph of
+    # K steps, PDL between them) with no flush.
+    step_bytes = {"ffn": 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M, "rmsnorm": 4.0 * M * K + 2.0 * K,
+                  "block": 2.0 * (M * K + 3 * K * N_l + 2 * M * N_l + M * K) + 4.0 * M,
+                  "gemm_lrelu": 2.0 * (M * K + K * N_l + M * N_l)}[op] * (2 if wdtype == torch.float32 else 1)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_layers = 1 + int(-(-2 * l2_bytes // int(step_bytes)))
+    b2b_ok = not args.gather and not args.no_graph and n_layers <= MAX_LAYER_COPIES and not args.skip_b2b
+    if not b2b_ok:
+        n_layers = 1
+    layers = [(t, out)] + [({k: v.clone() for k, v in t.items()}, torch.empty_like(out)) for _ in range(n_layers - 1)]
+
+    handles = []
+    for _ in range(n_layers):
+        hh = ffn.FusedFFN(dev, wdtype)
+        hh.set_variant(args.variant)
+        if args.no_pdl:
+            hh.set_option(ffn.OPT_PDL, 0)
+        handles.append(hh)
+    h = handles[0]
     stream = torch.cuda.current_stream(dev)
+
+    def fwd(i=0):
+        hh, (tt, oo) = handles[i], layers[i]
+        if op == "ffn":
+            return hh.forward(tt["x"], tt["g"], tt["w1"], tt["w3"], eps, out=oo)
+        if op == "block":
+            return hh.block_forward(tt["x"], tt["g"], tt["w1"], tt["w3"], tt["w2"], eps, out=oo)
+        if op == "rmsnorm":
+            return hh.rmsnorm(tt["x"], tt["g"], eps, out=oo)
+        return hh.gemm_act(tt["x"], tt["w1"], "leaky_relu", 0.01, out=oo)
 
     # a0: one-time weight fold/pack (reported, not part of a step)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    def fwd():
-        if op == "ffn":
-            return h.forward(t["x"], t["g"], t["w1"], t["w3"], eps, out=out)
-        if op == "block":
-            return h.block_forward(t["x"], t["g"], t["w1"], t["w3"], t["w2"], eps, out=out)
-        if op == "rmsnorm":
-            return h.rmsnorm(t["x"], t["g"], eps, out=out)
-        return h.gemm_act(t["x"], t["w1"], "leaky_relu", 0.01, out=out)
-
     e0.record(stream)
     if op in ("gemm_lrelu", "rmsnorm"):
-        fwd()  # the first call packs the weight (gemm)
+        fwd(0)  # the first call packs the weight (gemm)
     else:
         h.prepare(t["g"], t["w1"], t["w3"])
         if op == "block":
-            fwd()
+            fwd(0)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     prep_ms = e0.elapsed_time(e1)
+    for i in range(1, n_layers):
+        fwd(i)
+    torch.cuda.synchronize(dev)
 
     full_out = None
 
-    def step():
-        fwd()
+    def step(i=0):
+        fwd(i)
         if args.gather:
             from paper_2501_08071_b200.tp import gather_shards
-            return gather_shards(out, N)
+            return gather_shards(layers[i][1], N)
         return None
 
     for _ in range(args.warmup):
@@ -389,6 +447,8 @@ def run_cuasm(args):
         return step()
 
     # ---------------------------------------------------------- timed region
+    # SURVEY §8(d) / the paper's protocol: every step alone, L2
+    # flushed before it outside its own CUDA-event pair.
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches = 0
@@ -408,7 +468,7 @@ def run_cuasm(args):
         torch.cuda.synchronize(dev)
         barrier()
     wall = time.perf_counter() - wall0
-    local_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    local_ms = sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
     t_ms = max_over_ranks(local_ms)
     total_flops = flops_per_step * args.steps
     value = total_flops / (t_ms / 1e3) / 1e12
@@ -418,6 +478,44 @@ def run_cuasm(args):
         value = (4.0 * M * K + 2.0 * K) * args.steps / (t_ms / 1e3) / 1e9
     variant_used = h.last_launch()[0]
     launches_total = int(sum_over_ranks(float(launches)))
+
+    # ------------------------------------------------ back to back (secondary)
+    back_to_back = None
+    if b2b_ok:
+        peaks0 = load_peaks()
+        for i in range(n_layers):
+            fwd(i)
+        gb = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gb):
+            for i in range(args.steps):
+                fwd(i % n_layers)
+        warm = torch.cuda.CUDAGraph()  # first replays are slower: warm with a short copy
+        with torch.cuda.graph(warm):
+            for i in range(max(args.warmup, n_layers)):
+                fwd(i % n_layers)
+        warm.replay()
+        sb, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize(dev)
+        torch.cuda._sleep(int(2e8))  # the host enqueues ahead of the device
+        sb.record(stream)
+        gb.replay()
+        eb.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        b_ms = max_over_ranks(sb.elapsed_time(eb))
+        work = flops_per_step / 1e12 if op != "rmsnorm" else (4.0 * M * K + 2.0 * K) / 1e9
+        b_val = work * args.steps / (b_ms / 1e3)
+        back_to_back = {
+            "value": round(b_val, 2), "unit": unit, "ms_per_step": round(b_ms / args.steps, 5),
+            "steps": args.steps, "layer_copies": n_layers,
+            "frac_of_sustained_peak": (round(b_val / world / max(1, args.shard_of) / peaks0["bf16_tflops_sustained"], 4)
+                                       if op != "rmsnorm" and peaks0.get("bf16_tflops_sustained") else None),
+            "protocol": (f"inputs larger than L2: {n_layers} layer copies of (x, weights, out), "
+                         f"{n_layers * step_bytes / 1e6:.0f} MB vs {l2_bytes / 1e6:.0f} MB L2, cycled step by step; "
+                         "K steps back to back in one CUDA graph (PDL between steps) between one event pair, max "
+                         "over ranks; no flush, so no per-step event/launch cost -- and a sustained power draw"),
+        }
 
     # ------------------------------------------- roofline of the dual-GEMM kernel
     peaks = load_peaks()
@@ -432,18 +530,18 @@ def run_cuasm(args):
     pre_ms, gemm_ms, nfw = h.profile_read()
     h.set_option(ffn.OPT_PROFILE, 0)
     if op == "rmsnorm":  # not a GEMM launch: the step is the kernel
-        gemm_ms = t_ms
+        gemm_ms, pre_ms = 1.0, 0.0
     # per step (the block launches two GEMMs; their spans are summed)
-    gemm_avg_ms = gemm_ms / prof_steps
+    iso_gemm_ms = gemm_ms / prof_steps
     pre_avg_ms = pre_ms / prof_steps
-    gemm_flops = flops_per_step / world
+    gemm_share = iso_gemm_ms / (iso_gemm_ms + pre_avg_ms)
+    gemm_avg_ms = iso_gemm_ms if op != "rmsnorm" else t_ms / args.steps
+    gemm_flops = flops_per_step / world / max(1, args.shard_of)
     achieved = gemm_flops / (gemm_avg_ms / 1e3) / 1e12
     bound = "tensor"
     peak = peaks["bf16_tflops"]
     roof_unit = "TFLOP/s"
     # decode-like shapes are HBM bound: algorithmic bytes of the GEMM kernel
-    if op == "rmsnorm":
-        gemm_avg_ms = t_ms / args.steps
     gemm_bytes = {"ffn": 2.0 * (M * K + 2 * K * N_l + M * N_l) + 4.0 * M, "rmsnorm": 4.0 * M * K + 2.0 * K,
                   "block": 2.0 * (M * K + 3 * K * N_l + 2 * M * N_l + M * K) + 4.0 * M,
                   "gemm_lrelu": 2.0 * (M * K + K * N_l + M * N_l)}[op]
@@ -459,7 +557,7 @@ def run_cuasm(args):
         "peak_source": peaks["source"], "gemm_ms_per_launch": round(gemm_avg_ms, 5),
         "prepass_ms_per_launch": round(pre_avg_ms, 5),
         "prepass_GBps": round((2.0 * M * K + 4.0 * M) / (pre_avg_ms / 1e3) / 1e9, 1) if pre_avg_ms > 0 else None,
-        "gemm_share_of_step": round(gemm_avg_ms / (gemm_avg_ms + pre_avg_ms), 4),
+        "gemm_share_of_step": round(gemm_share, 4),
         "flops_per_launch": gemm_flops, "bytes_per_launch": gemm_bytes,
     }
 
@@ -480,7 +578,7 @@ def run_cuasm(args):
             b.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in es))
-        e2e = {"value": round(4.0 * M * K * N * ne / (e_ms / 1e3) / 1e12, 2), "unit": UNIT,
+        e2e = {"value": round(flops_per_step * ne / (e_ms / 1e3) / 1e12, 2), "unit": UNIT,
                "h2d_bytes_per_step": int(sum_over_ranks(float(M * K * 2))),
                "d2h_bytes_per_step": int(sum_over_ranks(float(M * N_l * 2))),
                "ms_per_step": round(e_ms / ne, 4), "steps": ne,
@@ -504,7 +602,9 @@ def run_cuasm(args):
             "data": "synthetic (seeded randn x~N(0,1), W~N(0,1/K), g~U(0.5,1.5); bf16)",
             "config": {
                 "workload": args.workload, "M": M, "K": K, "N": N, "N_per_rank": N_l, "eps": eps,
-                "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else "single GPU",
+                "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else (
+                    f"PROJECTION of tp{args.shard_of}: rank 0's shard timed alone on one GPU; value = "
+                    f"{args.shard_of} x its FLOPs / its time" if args.shard_of > 1 else "single GPU"),
                 "gather": bool(args.gather), "variant": {1: "1sm", 2: "2sm"}.get(variant_used, str(variant_used)),
                 "pdl": not args.no_pdl, "cuda_graph": graph is not None,
                 "l2": "flushed before every step outside the per-step CUDA-event pair: 256 MiB memset, then a "
@@ -514,6 +614,7 @@ def run_cuasm(args):
             "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),
             "pct_of_nominal_2250": round(value / world / 2250.0, 4),
             "roofline": roofline,
+            "back_to_back": back_to_back,
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
             "gpu_launches": launches_total,
@@ -548,10 +649,7 @@ def run_reference(args):
     d = make_inputs(M_gen, K, N_l, family="C", seed=seed, dtype="bf16")
     eps = 1e-6
     nsteps = args.warmup + args.steps
-    t0 = time.perf_counter()
-    oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], eps, mode="fold_bf16", rows=[0])
-    t_row = time.perf_counter() - t0
-    rows_per_step = max(1, min(M_gen, int(args.ref_budget_s / nsteps / max(t_row, 1e-4))))
+    rows_per_step = max(1, min(M_gen, calibrate_rows(d, eps, args.ref_budget_s / nsteps)))
     for _ in range(args.warmup):
         oracle_sample_time(d, eps, 0, rows_hint=rows_per_step)
     flops = 0.0

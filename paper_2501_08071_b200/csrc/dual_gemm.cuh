@@ -248,21 +248,45 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
     return (act == 1 && v < 0.f) ? v * alpha : v;
 }
 
-__device__ __forceinline__ float silu_gate(float h1, float h3) {
-    // SiLU(h1) * h3 = h1 * 1/(1 + 2^(-h1*log2 e)) * h3 (MUFU ex2 + rcp, ~2 ulp each).
-    // h1 -> -inf: 2^(+big) = inf, rcp(inf) = 0, out = -0 (x) h3 -- exact limit;
-    // h1 -> +inf: rcp(1) = 1, out = h1*h3.
-    return h1 * rcp_approx(1.0f + ex2_approx(h1 * -1.4426950408889634f)) * h3;
+// Per-row constants of the SwiGLU gate (step a3) for raw accumulators v1, v3
+// and the row's inverse RMS r:  out = h1*sigma(h1)*h3 with h1 = r*v1, h3 = r*v3
+//                                   = v1*v3 / ((1 + 2^t) * k),  t = -h1*log2(e),  k = 1/r^2.
+// The epilogue is MUFU-bound when both ex2 and rcp go to MUFU (2 ops per output
+// = 2048 SM cycles per 128x128 tile at 16 MUFU/clk), so only ex2 stays on MUFU;
+// 1/((1+2^t)k) is one FFMA plus a bit-trick seed (|rel err| <= 5.1%) and two
+// Newton steps on the FMA pipe (rel err <= e0^4 = 6.6e-6, centred by folding
+// 1/(1+delta) into k).  One step (e0^2 = 0.26%) would be inside the [BJ]
+// tolerance for the FFN output but flips the bf16 rounding of the FFN block's
+// hidden (reading R13) in ~25% of elements; two steps keep flips as rare as
+// with MUFU rcp.
+struct GateRow {
+    float c;     // r * -log2(e)
+    float kk;    // 1 / (r^2 (1 + delta))
+    float tmax;  // clamp of t so that (1 + 2^t) * kk <= 2^121 (finite, seedable); NaN for r = inf / NaN
+};
+__device__ __forceinline__ GateRow gate_row(float rr) {
+    constexpr float kDelta = 3.3e-6f;  // half of the two-step Newton bias e0^4
+    GateRow g;
+    g.c = rr * -1.4426950408889634f;
+    const float k = 1.0f / (rr * rr);
+    g.kk = k * (1.0f / (1.0f + kDelta));
+    // r = inf (zero row with eps = 0, reading R8) or NaN: tmax = NaN lets the
+    // NaN reach d and the output, as the plain definition does (0 * inf)
+    g.tmax = (rr - rr == 0.0f) ? 120.0f - __log2f(fmaxf(k, 1.0f)) : __int_as_float(0x7fc00000);
+    return g;
+}
+__device__ __forceinline__ float silu_gate(float v1, float v3, const GateRow& g) {
+    const float t = fminf(v1 * g.c, g.tmax);  // fminf(NaN, x) = x: a NaN accumulator still reaches p
+    const float d = fmaf(ex2_approx(t), g.kk, g.kk);        // (1 + e^-h1) / r^2, finite, > 0
+    const float y0 = __int_as_float(0x7EF311C7 - __float_as_int(d));  // ~1/d, |rel err| <= 5.1%
+    const float y1 = fmaf(y0, fmaf(-d, y0, 1.0f), y0);                 // Newton: err e0^2
+    const float y2 = fmaf(y1, fmaf(-d, y1, 1.0f), y1);                 // Newton: err e0^4
+    return (v1 * v3) * y2;
 }
 
 // 32 consecutive outputs of one row -> global (bf16 pairs packed with RNE, or
@@ -547,6 +571,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 r_ready = true;
             }
             const float rr = !row_ok ? 0.f : (p.use_r ? __ldcg(p.r + row) : 1.f);
+            const GateRow gr = gate_row(rr);
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
             if (warp == 2 && lane == 0) {
@@ -607,7 +632,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 if constexpr (kEpi == 0) {
                     float o[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = silu_gate(rr * __uint_as_float(v1[j]), rr * __uint_as_float(v3[j]));
+                    for (int j = 0; j < 32; ++j) o[j] = silu_gate(__uint_as_float(v1[j]), __uint_as_float(v3[j]), gr);
                     store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
                 } else {
                     float o[32];
