@@ -83,7 +83,11 @@ def parse_args(argv=None):
     ap.add_argument("--workload", default="llama7b_prefill",
                     help="llama7b_prefill | llama7b_decode | llama70b | sweep:M (K=4096, N=11008)")
     ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 one-SM, 2 two-SM (CTA pair)")
-    ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step")
+    ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step (NCCL)")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="a4 fused into the epilogue (cuasm_ffn_forward_gather): every rank's full [M,N] "
+                         "symmetric-memory buffer written by every kernel; with --shard-of P on one GPU, P "
+                         "simulated peer buffers on this device (store fan-out cost only, no NVLink)")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of a CUDA graph")
     ap.add_argument("--shard-of", type=int, default=1,
@@ -370,7 +374,8 @@ def run_cuasm(args):
                   "gemm_lrelu": 2.0 * (M * K + K * N_l + M * N_l)}[op] * (2 if wdtype == torch.float32 else 1)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     n_layers = 1 + int(-(-2 * l2_bytes // int(step_bytes)))
-    b2b_ok = not args.gather and not args.no_graph and n_layers <= MAX_LAYER_COPIES and not args.skip_b2b
+    fused_gather = args.fused_gather and op == "ffn"
+    b2b_ok = not args.gather and not fused_gather and not args.no_graph and n_layers <= MAX_LAYER_COPIES and not args.skip_b2b
     if not b2b_ok:
         n_layers = 1
     layers = [(t, out)] + [({k: v.clone() for k, v in t.items()}, torch.empty_like(out)) for _ in range(n_layers - 1)]
@@ -385,8 +390,27 @@ def run_cuasm(args):
     h = handles[0]
     stream = torch.cuda.current_stream(dev)
 
+    # a4 fused (f2): destinations of this rank's stores -- every rank's symmetric
+    # buffer (world > 1), or P simulated peer buffers on this GPU (--shard-of P)
+    fg, gather_dst, gather_mc, sim_bufs = None, None, False, None
+    if fused_gather:
+        from paper_2501_08071_b200.tp import FusedGather, gather_destinations
+        if world > 1:
+            fg = FusedGather(M, N, wdtype, dev)
+            gather_dst, gather_mc = fg.destinations(n0)
+        else:
+            P_sim = max(1, args.shard_of)
+            sim_bufs = [torch.empty((M, N_l * P_sim), dtype=wdtype, device=dev) for _ in range(P_sim)]
+            gather_dst, gather_mc = gather_destinations([b.data_ptr() for b in sim_bufs], 0, out.element_size())
+
     def fwd(i=0):
         hh, (tt, oo) = handles[i], layers[i]
+        if fused_gather:
+            hh.forward_gather(tt["x"], tt["g"], tt["w1"], tt["w3"], gather_dst,
+                              N if world > 1 else N_l * max(1, args.shard_of), eps, multicast=gather_mc)
+            if fg is not None:
+                fg.barrier()
+            return None
         if op == "ffn":
             return hh.forward(tt["x"], tt["g"], tt["w1"], tt["w3"], eps, out=oo)
         if op == "block":
@@ -430,7 +454,7 @@ def run_cuasm(args):
     # enqueues) is captured once in a CUDA graph and replayed per step, so
     # host-side launch latency never leaks into the device-timed spans.
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and fg is None:  # (the symmetric-memory barrier runs eagerly)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             fwd()
@@ -605,7 +629,10 @@ def run_cuasm(args):
                 "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else (
                     f"PROJECTION of tp{args.shard_of}: rank 0's shard timed alone on one GPU; value = "
                     f"{args.shard_of} x its FLOPs / its time" if args.shard_of > 1 else "single GPU"),
-                "gather": bool(args.gather), "variant": {1: "1sm", 2: "2sm"}.get(variant_used, str(variant_used)),
+                "gather": ("fused: kernel epilogue stores into " + (
+                    f"every rank's symmetric buffer ({'NVLS multicast' if gather_mc else 'P2P peer pointers'})"
+                    if world > 1 else f"{max(1, args.shard_of)} simulated peer buffers on this GPU")
+                           ) if fused_gather else ("nccl all-gather" if args.gather else False), "variant": {1: "1sm", 2: "2sm"}.get(variant_used, str(variant_used)),
                 "pdl": not args.no_pdl, "cuda_graph": graph is not None,
                 "l2": "flushed before every step outside the per-step CUDA-event pair: 256 MiB memset, then a "
                       "256 MiB read so the flush's dirty lines are written back before the step",

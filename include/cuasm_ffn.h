@@ -87,8 +87,12 @@ typedef enum {
                                kernel (its epilogue warps compute r while the first
                                tile's mainloop runs; one launch per forward); 0 = the
                                separate pre-pass kernel, PDL-overlapped with the GEMM */
-    CUASM_OPT_TILE_N = 7      /* cuasm_gemm_act / down projection only: MMA N of a tile,
+    CUASM_OPT_TILE_N = 7,     /* cuasm_gemm_act / down projection only: MMA N of a tile,
                                0 = auto (configuration model), 128 or 256              */
+    CUASM_OPT_SK_SPLIT = 8    /* auto schedule, fewer tiles than CTAs (pairs): at most
+                               this many stream-K ranges per tile, 2..16 (0 = 2, the
+                               default; each extra range is one more partial for the
+                               tile's finisher to add)                                 */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -124,6 +128,32 @@ cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* h, int device, cuasm_dtype_t dtype);
 cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev, const void* w1_dev,
                                  const void* w3_dev, void* out_dev, int64_t M, int64_t K, int64_t N, float eps,
                                  void* stream);
+
+/* Tensor-parallel forward with step a4 (the all-gather of the column shards,
+ * SURVEY §8(e)/(f) f2) fused into the epilogue: the same computation as
+ * cuasm_ffn_forward on this rank's shard (w1_dev/w3_dev = rows [n0, n0+N) of
+ * the full W1/W3, N = the shard width), but every 16-byte output store is
+ * written to each destination instead of one local buffer, tile by tile while
+ * the next tile's mainloop runs -- the gather overlaps the math and no
+ * separate collective or interleave pass runs.
+ *   dst[q] (q < num_dst <= 8): device address of THIS shard's column 0 inside
+ *     rank q's full row-major [M, ldo] output, i.e. base_q + n0 * elemsize;
+ *     base_q mapped into this device's address space (CUDA IPC / symmetric
+ *     memory peer pointers; stores travel over NVLink).  num_dst = 1 with a
+ *     local pointer is the plain forward with an output stride.
+ *   multicast = 1: num_dst must be 1 and dst[0] is an NVLS multicast address
+ *     (+ n0 * elemsize) bound to every rank's output buffer; each store is
+ *     issued once as multimem.st.relaxed.sys and NVSwitch replicates it.
+ *   ldo: row stride of every destination, elements, >= N, multiple of 16 bytes.
+ * Visibility: a rank's full output is complete once EVERY rank's launch has
+ * completed and a cross-rank barrier ordered after those launches has
+ * returned on the reading rank (e.g. the symmetric-memory barrier on the same
+ * stream); this call issues no cross-rank synchronisation itself.
+ * Other preconditions and errors as cuasm_ffn_forward (destinations 16-byte
+ * aligned, non-NULL; INVALID_ARG before any launch). */
+cuasm_status_t cuasm_ffn_forward_gather(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev, const void* w1_dev,
+                                        const void* w3_dev, void* const* dst, int num_dst, int multicast,
+                                        int64_t ldo, int64_t M, int64_t K, int64_t N, float eps, void* stream);
 
 /* End-to-end variant for host-resident activations: copies x_host [M,K]
  * (ideally pinned) to a handle-owned device buffer, runs cuasm_ffn_forward

@@ -33,12 +33,13 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 ACT_IDENTITY, ACT_LEAKY_RELU = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N = range(8)
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT = range(9)
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL = 0, 1, 2
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
-    "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_host", "cuasm_gemm_act", "cuasm_ffn_block_forward",
+    "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_gather", "cuasm_ffn_forward_host", "cuasm_gemm_act",
+    "cuasm_ffn_block_forward",
     "cuasm_rmsnorm",
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
@@ -81,6 +82,8 @@ def load_library():
         lib.cuasm_ffn_init.argtypes = [ctypes.POINTER(vp), ci, ci]
         lib.cuasm_ffn_forward.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
         lib.cuasm_ffn_forward_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp, ci]
+        lib.cuasm_ffn_forward_gather.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(vp), ci, ci, i64, i64, i64, i64,
+                                                 f32, vp]
         lib.cuasm_gemm_act.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, f32, vp]
         lib.cuasm_ffn_block_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
         lib.cuasm_rmsnorm.argtypes = [vp, vp, vp, vp, i64, i64, f32, vp]
@@ -230,6 +233,27 @@ class FusedFFN:
                                                w3.data_ptr(), out.data_ptr(), M, K, N, float(eps),
                                                _stream_ptr(x.device)))
         return out
+
+    def forward_gather(self, x, rms_w, w1, w3, dst_ptrs, ldo: int, eps: float = 1e-6, multicast: bool = False,
+                       keepalive=None):
+        """Tensor-parallel forward of this rank's column shard (w1/w3 = its rows of
+        W1/W3) with the all-gather fused into the epilogue (cuasm_ffn_forward_gather):
+        every output store goes to each address in `dst_ptrs` -- this shard's column 0
+        inside every rank's full [M, ldo] output (peer pointers) -- or, with
+        `multicast`, once to the single NVLS multicast address dst_ptrs[0].
+        `keepalive`: tensors owning the destinations (validated when given)."""
+        self._validate(x, rms_w, w1, w3)
+        if keepalive is not None:
+            self._validate(*keepalive)
+        M, K = x.shape
+        N = w1.shape[0]
+        if w1.shape != w3.shape or w1.shape[1] != K or rms_w.shape != (K,):
+            raise ValueError("shape mismatch")
+        dst = (ctypes.c_void_p * len(dst_ptrs))(*[int(p_) for p_ in dst_ptrs])
+        self._weights_changed(rms_w, w1, w3, slot=0)
+        self._check(self.lib.cuasm_ffn_forward_gather(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
+                                                      w3.data_ptr(), dst, len(dst_ptrs), 1 if multicast else 0,
+                                                      int(ldo), M, K, N, float(eps), _stream_ptr(x.device)))
 
     def forward_host(self, x_host, rms_w, w1, w3, eps: float = 1e-6, out_host=None, sync: bool = True):
         """End-to-end call with host activations: H2D x, forward, D2H out."""

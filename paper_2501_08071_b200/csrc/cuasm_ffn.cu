@@ -62,6 +62,7 @@ struct cuasm_ffn_s {
     bool plan_sk = false;  // plan_config's stream-K choice for the current forward
     int trace = 0;     // CUASM_OPT_TRACE
     int tile_n = 0;    // CUASM_OPT_TILE_N (GEMM + activation): 0 auto, 128, 256
+    int sk_split = 0;  // CUASM_OPT_SK_SPLIT: max stream-K ranges per tile when tiles < clusters (0: 2)
     int last_tile_n = 256;
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
     uint32_t* gsync = nullptr;  // grid counters of the fused RMS pass (self-resetting)
@@ -252,6 +253,11 @@ struct EpiSpec {
     int use_r;       // scale by r
     int act;         // kEpi == 1: 0 identity, 1 LeakyReLU
     float alpha;
+    // a4 fused gather (cuasm_ffn_forward_gather): null = the plain output `out`, ldo = N
+    void* const* dst = nullptr;
+    int num_dst = 0;
+    int dst_mc = 0;
+    int64_t ldo = 0;
 };
 
 template <int kKind, int kCtaGroup, int kEpi, int kN>
@@ -285,6 +291,16 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.r = h->r;
     p.out = out;
     p.ldo = N;
+    p.num_dst = 1;
+    p.dst_mc = 0;
+    for (int q = 0; q < 8; ++q) p.dst[q] = nullptr;
+    p.dst[0] = out;
+    if (e.dst) {
+        p.ldo = e.ldo;
+        p.num_dst = e.num_dst;
+        p.dst_mc = e.dst_mc;
+        for (int q = 0; q < e.num_dst; ++q) p.dst[q] = e.dst[q];
+    }
     p.M = static_cast<int>(M);
     p.N = static_cast<int>(N);
     p.K = static_cast<int>(K);
@@ -325,7 +341,8 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         // than clusters (each finisher then adds a single partial)
         if (sk_tiles > 0) {
             int64_t c = std::min<int64_t>(max_clusters, static_cast<int64_t>(sk_tiles) * p.num_k_blk);
-            if (h->schedule == CUASM_SCHEDULE_AUTO && waves == 0) c = std::min<int64_t>(c, 2 * sk_tiles);
+            if (waves == 0 && (h->schedule == CUASM_SCHEDULE_AUTO || h->sk_split > 0))
+                c = std::min<int64_t>(c, static_cast<int64_t>(h->sk_split > 0 ? h->sk_split : 2) * sk_tiles);
             clusters = static_cast<int>(c);
         }
     }
@@ -543,6 +560,23 @@ cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const v
     return run_gemm(h, 0, e, x, out, M, K, N, eps, s);
 }
 
+// The fused FFN with step a4 in its epilogue: every output store goes to each
+// of `dst` (P2P) or once to the multicast address dst[0].
+cuasm_status_t forward_gather_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3,
+                                   void* const* dst, int num_dst, int mc, int64_t ldo, int64_t M, int64_t K,
+                                   int64_t N, float eps, cudaStream_t s) {
+    cuasm_status_t st;
+    h->last_kernels = 0;
+    if ((st = set_device(h)) != CUASM_OK) return st;
+    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    EpiSpec e{0, h->fused_norm, 1, 0, 0.f};
+    e.dst = dst;
+    e.num_dst = num_dst;
+    e.dst_mc = mc;
+    e.ldo = ldo;
+    return run_gemm(h, 0, e, x, mc ? nullptr : dst[0], M, K, N, eps, s);
+}
+
 // out = act(x . w^T): the single-weight GEMM + activation path.
 cuasm_status_t gemm_act_impl(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K, int64_t N,
                              int act, float alpha, cudaStream_t s) {
@@ -626,6 +660,27 @@ cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x, const void* rms_w
     cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
     if (st != CUASM_OK) return st;
     return forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_ffn_forward_gather(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
+                                        const void* w3, void* const* dst, int num_dst, int multicast, int64_t ldo,
+                                        int64_t M, int64_t K, int64_t N, float eps, void* stream) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (!dst || num_dst < 1 || num_dst > 8) return fail(h, CUASM_ERR_INVALID_ARG, "num_dst must be in [1, 8]");
+    if (multicast != 0 && multicast != 1) return fail(h, CUASM_ERR_INVALID_ARG, "multicast is 0 or 1");
+    if (multicast && num_dst != 1)
+        return fail(h, CUASM_ERR_INVALID_ARG, "a multicast destination is one address (num_dst = 1)");
+    for (int q = 0; q < num_dst; ++q) {
+        if (!dst[q] && M > 0) return fail(h, CUASM_ERR_INVALID_ARG, "NULL destination %d", q);
+        if (!aligned16(dst[q])) return fail(h, CUASM_ERR_INVALID_ARG, "destination %d is not 16-byte aligned", q);
+    }
+    if (ldo < N || ldo % (16 / h->esize) != 0)
+        return fail(h, CUASM_ERR_INVALID_ARG, "ldo must be >= N and a multiple of %d elements", 16 / h->esize);
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, dst[0], M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    return forward_gather_impl(h, x, rms_w, w1, w3, dst, num_dst, multicast, ldo, M, K, N, eps,
+                               static_cast<cudaStream_t>(stream));
 }
 
 cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w, const void* w1,
@@ -856,6 +911,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
     case CUASM_OPT_TILE_N:
         if (value != 0 && value != 128 && value != 256) return fail(h, CUASM_ERR_INVALID_ARG, "TILE_N is 0, 128 or 256");
         h->tile_n = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_SK_SPLIT:
+        if (value != 0 && (value < 2 || value > 16)) return fail(h, CUASM_ERR_INVALID_ARG, "SK_SPLIT is 0 or 2..16");
+        h->sk_split = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_TRACE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "TRACE option is 0 or 1");

@@ -54,8 +54,15 @@ struct FfnGemmParams {
     float alpha;
     uint32_t* sync;  // [0] warps done writing r, [1] CTAs exited (self-resetting)
     float* r;        // [M] inverse RMS (written here when fused_norm, else by the pre-pass)
-    void* out;       // [M, ldo] row-major, dtype of the handle
-    int64_t ldo;     // leading dimension of out, elements
+    void* out;       // [M, ldo] row-major, dtype of the handle (== dst[0] unless multicast)
+    int64_t ldo;     // leading dimension of out / every dst, elements
+    // Step a4 fused into the epilogue: every output store goes to
+    // dst[0..num_dst) -- this shard's column 0 inside each rank's full [M, ldo]
+    // output (peer pointers: P2P stores over NVLink) -- or, with dst_mc, once to
+    // the NVLS multicast address dst[0] (multimem.st: the switch replicates it).
+    void* dst[8];
+    int num_dst;     // 1..8 (1 = plain local output)
+    int dst_mc;      // 1: dst[0] is a multicast address
     int M, N, K;
     int num_m_blk;   // ceil(M / tile_m)
     int num_n_blk;   // ceil(N / OUT_COLS)
@@ -289,27 +296,46 @@ __device__ __forceinline__ float silu_gate(float v1, float v3, const GateRow& g)
     return (v1 * v3) * y2;
 }
 
+// One 16-byte output store to every destination (DESIGN.md §8 "fused gather").
+template <int kKind>
+__device__ __forceinline__ void store16(const FfnGemmParams& p, int64_t off_bytes, uint4 v) {
+    if (p.dst_mc) {
+        char* a = static_cast<char*>(p.dst[0]) + off_bytes;
+        if constexpr (kKind == 0)
+            asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};"
+                         ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        else
+            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                         ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (q < p.num_dst) *reinterpret_cast<uint4*>(static_cast<char*>(p.dst[q]) + off_bytes) = v;
+}
+
 // 32 consecutive outputs of one row -> global (bf16 pairs packed with RNE, or
 // fp32), 16-byte stores, columns >= N dropped in groups of 8 (N % 8 == 0).
 template <int kKind>
 __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int col0, const float (&o)[32]) {
+    constexpr int kEs = kKind == 0 ? 2 : 4;
+    const int64_t rbase = static_cast<int64_t>(row) * p.ldo;
     if constexpr (kKind == 0) {
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (col0 + 8 * q < p.N) {
-                *reinterpret_cast<uint4*>(orow + col0 + 8 * q) =
-                    make_uint4(ptx::pack_bf16x2(o[8 * q + 0], o[8 * q + 1]), ptx::pack_bf16x2(o[8 * q + 2], o[8 * q + 3]),
-                               ptx::pack_bf16x2(o[8 * q + 4], o[8 * q + 5]), ptx::pack_bf16x2(o[8 * q + 6], o[8 * q + 7]));
+                store16<kKind>(p, (rbase + col0 + 8 * q) * kEs,
+                               make_uint4(ptx::pack_bf16x2(o[8 * q + 0], o[8 * q + 1]), ptx::pack_bf16x2(o[8 * q + 2], o[8 * q + 3]),
+                                          ptx::pack_bf16x2(o[8 * q + 4], o[8 * q + 5]), ptx::pack_bf16x2(o[8 * q + 6], o[8 * q + 7])));
             }
         }
     } else {
-        float* orow = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             if (col0 + 4 * q < p.N)
-                *reinterpret_cast<float4*>(orow + col0 + 4 * q) =
-                    make_float4(o[4 * q + 0], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                store16<kKind>(p, (rbase + col0 + 4 * q) * kEs,
+                               make_uint4(__float_as_uint(o[4 * q + 0]), __float_as_uint(o[4 * q + 1]),
+                                          __float_as_uint(o[4 * q + 2]), __float_as_uint(o[4 * q + 3])));
         }
     }
 }

@@ -6,8 +6,11 @@ NVLink only when the full output is requested".  SiLU-gating is elementwise in
 N, so rank p computes out[:, shard p] from its contiguous row block of W1 and
 W3 and the replicated x; there is no data-path collective unless
 ``gather=True``.  One process per GPU, ``torch.distributed`` with NCCL for the
-plumbing.  (A later step -- SURVEY §8(f) f1/f2 -- fuses the down projection /
-all-gather into the kernel epilogue over NVSwitch peer memory.)
+plumbing.  ``gather="fused"`` instead writes every output
+tile straight into every rank's full [M, N] buffer from the kernel epilogue
+(symmetric-memory peer pointers over NVLink, or one NVLS multicast store per
+tile when the switch supports it), so the gather overlaps the GEMM and no
+separate collective or interleave pass runs.
 """
 from __future__ import annotations
 
@@ -60,13 +63,68 @@ def gather_shards(out_shard: torch.Tensor, N: int, group=None) -> torch.Tensor:
     return torch.cat([p[:, :w] for p, w in zip(parts, widths)], dim=1)
 
 
-def ffn_tp_forward(x, rms_w, w1_shard, w3_shard, eps: float = 1e-6, group=None, gather: bool = False,
-                   N: int | None = None, handle: FusedFFN | None = None):
+def gather_destinations(buffer_ptrs, col0: int, elem_size: int, multicast_ptr: int = 0):
+    """Destination list of cuasm_ffn_forward_gather for one rank: this shard's
+    column 0 (byte offset col0 * elem_size) inside every rank's full output
+    buffer, or inside the multicast mapping when one exists.  Returns
+    (dst_ptrs, multicast)."""
+    off = int(col0) * int(elem_size)
+    if multicast_ptr:
+        return [int(multicast_ptr) + off], True
+    if not 1 <= len(buffer_ptrs) <= 8:
+        raise ValueError("the fused gather addresses 1..8 ranks (one NVLink domain of one box)")
+    return [int(p) + off for p in buffer_ptrs], False
+
+
+class FusedGather:
+    """Symmetric-memory full-output buffer [M, N] of one process group, for
+    ffn_tp_forward(gather="fused").  Every rank allocates it through torch's
+    symmetric memory (one collective rendezvous), so each rank holds the peer
+    pointers of all ranks' buffers (and a multicast mapping when NVLS is
+    available)."""
+
+    def __init__(self, M: int, N: int, dtype, device, group=None, use_multicast: bool = True):
+        import torch.distributed._symmetric_memory as symm_mem
+        grp = group or dist.group.WORLD
+        self.buf = symm_mem.empty((M, N), dtype=dtype, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, grp)
+        self.M, self.N = M, N
+        self.rank, self.world = self.hdl.rank, self.hdl.world_size
+        # multicast_ptr is 0 when torch could not set up an NVLS multicast object
+        # (no NVSwitch fabric / single device): the P2P stores are used then
+        self.multicast_ptr = int(self.hdl.multicast_ptr or 0) if use_multicast else 0
+
+    def destinations(self, col0: int):
+        return gather_destinations(self.hdl.buffer_ptrs, col0, self.buf.element_size(), self.multicast_ptr)
+
+    def barrier(self):
+        """Stream-ordered cross-rank barrier: after it, every rank's stores are in."""
+        self.hdl.barrier(channel=0)
+
+
+def ffn_tp_forward(x, rms_w, w1_shard, w3_shard, eps: float = 1e-6, group=None, gather=False,
+                   N: int | None = None, handle: FusedFFN | None = None, fused: FusedGather | None = None):
     """This rank's share of the column-parallel fused FFN.
 
     x [M,K] (replicated), rms_w [K], w1_shard/w3_shard [N_p,K] -> out [M,N_p],
-    or the full [M,N] when ``gather`` (N = total width, required then)."""
+    or the full [M,N] when ``gather`` (N = total width, required then):
+    gather=True / "nccl": NCCL all-gather + interleave after the kernel;
+    gather="fused": the kernel epilogue writes into every rank's symmetric
+    buffer (`fused`, a FusedGather of this group; created when None)."""
     h = handle or _handle(x.device, x.dtype)
+    if gather == "fused":
+        if N is None:
+            raise ValueError("gather='fused' needs the total N")
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        fg = fused or FusedGather(x.shape[0], N, x.dtype, x.device, group)
+        n0, n1 = shard_bounds(N, rank, world)
+        if w1_shard.shape[0] != n1 - n0:
+            raise ValueError("w1_shard width does not match this rank's shard")
+        dst, mc = fg.destinations(n0)
+        h.forward_gather(x, rms_w, w1_shard, w3_shard, dst, N, eps, multicast=mc)
+        fg.barrier()
+        return fg.buf
     out = h.forward(x, rms_w, w1_shard, w3_shard, eps)
     if not gather:
         return out

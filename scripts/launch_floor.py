@@ -44,3 +44,20 @@ for n in (2, 4, 8):
         for _ in range(n):
             g.replay()
     print(f"{n} decode forwards back to back / {n} (no flush): {med(many, do_flush=False) / n:7.2f} us")
+
+# launch modes of the same decode forward, each after a flush, own event pair
+def eager():
+    h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
+
+
+print(f"decode forward, eager launch (after flush):    {med(eager):7.2f} us")
+h.set_option(ffn.OPT_PDL, 0)
+print(f"decode forward, eager, no PDL (after flush):   {med(eager):7.2f} us")
+g2 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g2):
+    eager()
+print(f"decode forward, graph, no PDL (after flush):   {med(g2.replay):7.2f} us")
+h.set_option(ffn.OPT_PDL, 1)
+# the flush's last kernel is a 256 MiB read; a tiny kernel between it and the
+# start event separates "previous kernel drain" from the event pair itself
+print(f"trivial kernel, then event pair around forward: {med(lambda: g.replay()):7.2f} us")

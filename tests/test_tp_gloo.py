@@ -113,3 +113,57 @@ def test_row_parallel_w2_all_reduce(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok in res)
+
+
+# ---- fused gather (f2): the destination arithmetic, emulated across processes ----
+_VBASE = 1 << 40  # virtual "peer pointer" of rank q's buffer: q * _VBASE
+
+
+def _fused_gather_worker(rank, world, port, M, N, bufs, q):
+    """Each rank writes its shard into EVERY rank's full buffer at the addresses
+    gather_destinations gives (what the kernel epilogue stores do over NVLink),
+    then a barrier; afterwards every rank's buffer must hold the full output."""
+    from paper_2501_08071_b200.tp import gather_destinations
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n0, n1 = shard_bounds(N, rank, world)
+        shard = (torch.arange(M * (n1 - n0), dtype=torch.float32).reshape(M, n1 - n0) + 1000.0 * rank)
+        dst, mc = gather_destinations([p * _VBASE for p in range(world)], n0, 4)
+        assert mc is False and len(dst) == world
+        for d in dst:
+            peer, off = divmod(d, _VBASE)
+            col0 = off // 4
+            assert col0 == n0
+            flat = bufs[peer].view(M, N)
+            flat[:, col0:col0 + (n1 - n0)] = shard   # row stride ldo = N
+        dist.barrier()
+        full = torch.cat([torch.arange(M * (b - a), dtype=torch.float32).reshape(M, b - a) + 1000.0 * r
+                          for r, (a, b) in enumerate(shard_bounds(N, r, world) for r in range(world))], dim=1)
+        q.put((rank, bool(torch.equal(bufs[rank].view(M, N), full))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N", [(2, 64), (3, 40), (4, 11008 // 4)])
+def test_fused_gather_destinations_fill_every_buffer(world, N):
+    M = 5
+    bufs = [torch.full((M * N,), -1.0).share_memory_() for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_gather_worker, args=(r, world, port, M, N, bufs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}
+
+
+def test_gather_destinations_multicast_and_limits():
+    from paper_2501_08071_b200.tp import gather_destinations
+    assert gather_destinations([100, 200], 8, 2, multicast_ptr=5000) == ([5016], True)
+    assert gather_destinations([100, 200], 8, 2) == ([116, 216], False)
+    with pytest.raises(ValueError):
+        gather_destinations(list(range(9)), 0, 2)
