@@ -482,3 +482,41 @@ def test_full_size_70b_unsharded(cuda_device):
     ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], c["eps"], rows=rows)
     check(out[rows], ref, "70b P=1")
     assert torch.isfinite(out).all()
+
+
+# ---------------------------------------------- epilogue gate at the extremes ---
+@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL])
+def test_gate_extremes(cuda_device, schedule):
+    """The gate's one-MUFU form (dual_gemm.cuh silu_gate: ex2 + bit-trick seed +
+    two Newton steps, t clamped per row) against the fp64 oracle where it is
+    most fragile: |h1| up to ~10^3 (exp overflow / full saturation), rows of
+    magnitude 1e4 (k = ms + eps ~ 1e8 moves the clamp), and the NaN cases of
+    reading R8 (zero row with eps = 0) and of a NaN input."""
+    M, K, N = 8, 256, 256
+    d = make_inputs(M, K, N, family="C", seed=3400, dtype="bf16")
+    x = d["x"].clone()
+    x[2] *= 1e4                      # large row: clamp at 120 - log2(k)
+    w1 = d["w1"].clone()
+    w1[:64] *= 512.0                 # |h1| ~ 10^2..10^3 for the first 64 outputs
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
+    dv = {"x": x.to(cuda_device), "g": d["g"].to(cuda_device), "w1": w1.to(cuda_device), "w3": d["w3"].to(cuda_device)}
+    out = h.forward(dv["x"], dv["g"], dv["w1"], dv["w3"], 1e-6)
+    torch.cuda.synchronize()
+    ref = oracle.ffn(x, d["g"], w1, d["w3"], 1e-6, mode="fold_bf16")
+    assert not torch.isnan(out).any()
+    check(out, ref, f"gate extremes (schedule {schedule})")
+    # reading R8: a zero row with eps = 0 is 0 * inf = NaN in the plain definition
+    x0 = dv["x"].clone()
+    x0[5] = 0
+    out0 = h.forward(x0, dv["g"], dv["w1"], dv["w3"], 0.0)
+    torch.cuda.synchronize()
+    assert bool(torch.isnan(out0[5]).all())
+    assert not torch.isnan(out0[torch.arange(M, device=cuda_device) != 5]).any()
+    # a NaN input element poisons its row only
+    xn = dv["x"].clone()
+    xn[3, 7] = float("nan")
+    outn = h.forward(xn, dv["g"], dv["w1"], dv["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert bool(torch.isnan(outn[3]).all())
+    assert not torch.isnan(outn[torch.arange(M, device=cuda_device) != 3]).any()
