@@ -311,6 +311,9 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
     p.num_tiles = p.num_m_blk * p.num_n_blk;
     p.a_box_bytes = static_cast<int>(a_rows) * 128;
+    // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
+    // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
+    p.rep = (kCtaGroup == 1 && kEpi == 0 && M <= 32) ? 1 : 0;
 
     static bool attr_set = false;  // one per template instance
     if (!attr_set) {

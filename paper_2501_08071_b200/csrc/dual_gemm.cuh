@@ -69,6 +69,11 @@ struct FfnGemmParams {
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
+    int rep;         // 1 (SwiGLU, 1-SM, M <= 32): the x rows are loaded into all four 32-row
+                     // quarters of the A tile, so every TMEM lane quadrant holds every row and
+                     // the epilogue spreads the columns over the four SM sub-partitions (warp
+                     // w may only read quadrant w%4: without this a decode tile's whole
+                     // epilogue runs on sub-partition 0)
     int num_tiles;
     // --- persistent schedule: data-parallel tiles, then a stream-K region ---
     int num_clusters;   // persistent clusters (CTA pairs for the 2-SM variant)
@@ -299,6 +304,10 @@ __device__ __forceinline__ float silu_gate(float v1, float v3, const GateRow& g)
 // One 16-byte output store to every destination (DESIGN.md §8 "fused gather").
 template <int kKind>
 __device__ __forceinline__ void store16(const FfnGemmParams& p, int64_t off_bytes, uint4 v) {
+    if (p.num_dst == 1 && !p.dst_mc) {  // the plain forward: one local store
+        *reinterpret_cast<uint4*>(static_cast<char*>(p.dst[0]) + off_bytes) = v;
+        return;
+    }
     if (p.dst_mc) {
         char* a = static_cast<char*>(p.dst[0]) + off_bytes;
         if constexpr (kKind == 0)
@@ -414,8 +423,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
                 if (ptx::elect_one()) {
                     if constexpr (kCtaGroup == 1) {
-                        ptx::mbar_arrive_expect_tx(fb, p.a_box_bytes + C::B_BYTES);
-                        ptx::tma_load_2d(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                        const int nrep = p.rep ? 4 : 1;
+                        ptx::mbar_arrive_expect_tx(fb, nrep * p.a_box_bytes + C::B_BYTES);
+                        for (int q = 0; q < nrep; ++q)  // quarter q of the A tile: smem rows 32q.. (4 KB aligned)
+                            ptx::tma_load_2d(sa + q * 32 * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     } else {
                         // both CTAs' bytes land on the leader's barrier
@@ -549,7 +560,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             tile_coords(sg.tile, p, mb, nb);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM + static_cast<int>(row_in_cta);
+            // rep: quadrant `quad` holds rows 0..31 of the tile (lane = row), and only its
+            // own column pair is drained by it (below)
+            const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
+                            static_cast<int>(p.rep ? lane : row_in_cta);
             const bool row_ok = row < p.M;
             const bool contributor = sg.kb0 > 0;                       // stream-K: partial, not the tile's start
             const bool finisher = sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
@@ -613,7 +627,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
             for (int i = 0; i < C::PAIRS; ++i) {
-                const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+                int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+                if (kEpi == 0 && p.rep) {
+                    // quadrant q drains column pair q (h1 chunk q, h3 chunk q + BN/32); the
+                    // second warp of each quadrant idles
+                    if (half != 0 || i != 0) continue;
+                    ca = static_cast<int>(quad);
+                    cb = static_cast<int>(quad) + C::BN / 32;
+                }
                 uint32_t v1[32], v3[32];
                 ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
                 ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
