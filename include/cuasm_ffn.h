@@ -89,10 +89,13 @@ typedef enum {
                                separate pre-pass kernel, PDL-overlapped with the GEMM */
     CUASM_OPT_TILE_N = 7,     /* cuasm_gemm_act / down projection only: MMA N of a tile,
                                0 = auto (configuration model), 128 or 256              */
-    CUASM_OPT_SK_SPLIT = 8    /* auto schedule, fewer tiles than CTAs (pairs): at most
+    CUASM_OPT_SK_SPLIT = 8,   /* auto schedule, fewer tiles than CTAs (pairs): at most
                                this many stream-K ranges per tile, 2..16 (0 = 2, the
                                default; each extra range is one more partial for the
                                tile's finisher to add)                                 */
+    CUASM_OPT_L2_POLICY = 9   /* L2 eviction policy of the TMA loads, 2 bits each: bits 0-1
+                               x, bits 2-3 packed W13; 0 evict_normal, 1 evict_first,
+                               2 evict_last.  Default 2 (x evict_last, W13 normal)    */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -103,7 +106,9 @@ typedef enum {
     CUASM_SCHEDULE_AUTO = 0,          /* whole tiles while they fill complete waves, stream-K
                                          over the last partial wave + one full wave         */
     CUASM_SCHEDULE_DATA_PARALLEL = 1, /* whole tiles only                                      */
-    CUASM_SCHEDULE_STREAM_K_ALL = 2   /* stream-K over every tile (testing)                     */
+    CUASM_SCHEDULE_STREAM_K_ALL = 2,  /* stream-K over every tile (testing)                     */
+    CUASM_SCHEDULE_STREAM_K_TAIL = 3  /* whole tiles for every complete wave, stream-K over the
+                                         last partial wave only                                */
 } cuasm_schedule_t;
 
 /* Create a handle on `device` (CUDA ordinal) for element type `dtype`.

@@ -62,6 +62,7 @@ struct cuasm_ffn_s {
     bool plan_sk = false;  // plan_config's stream-K choice for the current forward
     int trace = 0;     // CUASM_OPT_TRACE
     int tile_n = 0;    // CUASM_OPT_TILE_N (GEMM + activation): 0 auto, 128, 256
+    int l2pol = 2;     // CUASM_OPT_L2_POLICY (x evict_last, W13 evict_normal)
     int sk_split = 0;  // CUASM_OPT_SK_SPLIT: max stream-K ranges per tile when tiles < clusters (0: 2)
     int last_tile_n = 256;
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
@@ -260,6 +261,17 @@ struct EpiSpec {
     int64_t ldo = 0;
 };
 
+// Rasterisation group (m-blocks whose tiles run before the next W13 column
+// block): as many as keep the group's rows of x within ~32 MB of L2, at most
+// 16.  x of a group is re-read once per n-block and must stay L2-resident; a
+// 70B group of 16 (64 MB of x) measured 2.6% slower than 8 (32 MB), ncu
+// showing 6.6 GB of DRAM reads per launch for 1.0 GB of operands
+// (scripts/tune_group.py, profiles/r01/tune_group.log).
+inline int auto_group_m(int64_t K, int esize, int cta_group) {
+    const int64_t per_mblk = static_cast<int64_t>(128) * cta_group * K * esize;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(32) << 20) / per_mblk)));
+}
+
 template <int kKind, int kCtaGroup, int kEpi, int kN>
 cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
                            int64_t N, float eps, cudaStream_t s) {
@@ -307,10 +319,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.num_m_blk = static_cast<int>((M + C::TILE_M - 1) / C::TILE_M);
     p.num_n_blk = static_cast<int>((N + C::OUT_COLS - 1) / C::OUT_COLS);
     p.num_k_blk = static_cast<int>((K + C::BK - 1) / C::BK);
-    p.group_m = h->group_m > 0 ? h->group_m : std::min(p.num_m_blk, 16);
+    p.group_m = h->group_m > 0 ? h->group_m : auto_group_m(K, h->esize, kCtaGroup);
     p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
     p.num_tiles = p.num_m_blk * p.num_n_blk;
     p.a_box_bytes = static_cast<int>(a_rows) * 128;
+    p.l2pol = h->l2pol;
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
     p.rep = (kCtaGroup == 1 && kEpi == 0 && M <= 32) ? 1 : 0;
@@ -334,10 +347,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // Stream-K only where plan_config's cost model says the balanced tail is
     // worth the partial fixup (e.g. 7B prefill: 9.3 waves; not decode, where
     // whole tiles already saturate HBM).
-    const bool sk_ok = h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
+    const bool sk_ok = h->schedule == CUASM_SCHEDULE_STREAM_K_ALL || h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL ||
                        (h->schedule == CUASM_SCHEDULE_AUTO && h->plan_sk);
     if (sk_ok && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
+        else if (rem != 0 && h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL) sk_tiles = waves == 0 ? p.num_tiles : rem;
         else if (rem != 0) sk_tiles = waves == 0 ? p.num_tiles : rem + max_clusters;
         // every cluster gets a non-empty range (tiny problems: fewer clusters); in
         // auto mode a tile is split at most in two when there are fewer tiles
@@ -457,7 +471,7 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             // profiles/r01/trace_gemm.log): charge that as a 1.32x slowdown.
             const int64_t rem = tiles % units;
             const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
-            const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : 16);
+            const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : auto_group_m(K, esize, cg));
             const double region_bytes =
                 static_cast<double>((sk_tiles + gm - 1) / gm + 1) * tn * K * esize +
                 static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
@@ -903,7 +917,7 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         h->group_m = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_SCHEDULE:
-        if (value < CUASM_SCHEDULE_AUTO || value > CUASM_SCHEDULE_STREAM_K_ALL)
+        if (value < CUASM_SCHEDULE_AUTO || value > CUASM_SCHEDULE_STREAM_K_TAIL)
             return fail(h, CUASM_ERR_INVALID_ARG, "bad schedule %lld", (long long)value);
         h->schedule = static_cast<int>(value);
         return CUASM_OK;
@@ -914,6 +928,11 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
     case CUASM_OPT_TILE_N:
         if (value != 0 && value != 128 && value != 256) return fail(h, CUASM_ERR_INVALID_ARG, "TILE_N is 0, 128 or 256");
         h->tile_n = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_L2_POLICY:
+        if (value < 0 || value > 15 || (value & 3) == 3 || ((value >> 2) & 3) == 3)
+            return fail(h, CUASM_ERR_INVALID_ARG, "L2_POLICY: 2-bit codes 0..2 for x (bits 0-1) and W13 (bits 2-3)");
+        h->l2pol = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_SK_SPLIT:
         if (value != 0 && (value < 2 || value > 16)) return fail(h, CUASM_ERR_INVALID_ARG, "SK_SPLIT is 0 or 2..16");

@@ -69,6 +69,7 @@ struct FfnGemmParams {
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
+    int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
     int rep;         // 1 (SwiGLU, 1-SM, M <= 32): the x rows are loaded into all four 32-row
                      // quarters of the A tile, so every TMEM lane quadrant holds every row and
                      // the epilogue spreads the columns over the four SM sub-partitions (warp
@@ -402,8 +403,13 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         // Whole warp walks the loop, one elected lane issues (uniform operands,
         // no per-instruction uniformity loops around UTMALDG).
         ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
-        const uint64_t pol_x = ptx::policy_evict_last();    // x is re-read by every n-block
-        const uint64_t pol_w = ptx::policy_evict_normal();  // W13 block shared by group_m tiles
+        // default: x evict_last (re-read by every n-block), W13 evict_normal (shared by the
+        // group's tiles); CUASM_OPT_L2_POLICY overrides (2 bits each: 0 normal, 1 first, 2 last)
+        auto pol = [](int c) {
+            return c == 1 ? ptx::policy_evict_first() : c == 2 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+        };
+        const uint64_t pol_x = pol(p.l2pol & 3);
+        const uint64_t pol_w = pol((p.l2pol >> 2) & 3);
         int stage = 0;
         uint32_t phase = 0;
         bool first_load = true;

@@ -1,8 +1,7 @@
-O=gpurun_out/e4; mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > $O/pytest.log 2>&1; echo pytest=$?
-timeout 600 python scripts/tune.py --out $O/tune.json > $O/tune.log 2>&1; echo tune=$?
-timeout 600 python scripts/tune.py --N 1376 --ms 1,16,64,128,256,512,1024,2048,4096 --out $O/tune_n1376.json > $O/tune_n1376.log 2>&1; echo tune8=$?
-timeout 600 python scripts/tune.py --op gemm --ms 512,2048,4096 --K 4096 --N 4096 > $O/tune_gemm.log 2>&1; echo tg=$?
-timeout 600 python scripts/tune.py --op gemm --ms 2048 --K 11008 --N 4096 >> $O/tune_gemm.log 2>&1; echo tg2=$?
-timeout 600 python scripts/tune.py --op gemm --ms 512 --K 2048 --N 512 >> $O/tune_gemm.log 2>&1; echo tg3=$?
-timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,2048x4096x1376,16x4096x1376,16x4096x11008,256x4096x11008 --scheds 0,2 > $O/trace.log 2>&1; echo tr=$?
+O=gpurun_out/e10; mkdir -p $O
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -p no:cacheprovider -k "schedules" > $O/pytest.log 2>&1; echo p=$?
+timeout 900 python scripts/tune.py --out $O/tune.json > $O/tune.log 2>&1; echo tune=$?
+timeout 600 python scripts/tune.py --N 1376 --ms 16,128,256,512,1024,2048,4096 --out $O/tune_n1376.json > $O/tune_n1376.log 2>&1; echo t8=$?
+timeout 600 python scripts/tune.py --K 8192 --N 3584 --ms 4096 > $O/tune_70b8.log 2>&1; echo t70=$?
+timeout 600 python bench.py --workload llama70b --skip-cpu-baseline --skip-e2e > $O/bench_70b.json 2>>$O/err; echo b70=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_70b python bench.py --workload llama70b --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu70.log 2>&1; echo ncu=$?

@@ -18,7 +18,11 @@ import bench
 import paper_2501_08071_b200 as ffn
 from ffn_inputs import make_device_inputs
 
-CONFIGS = [(1, 1, "1sm-dp"), (1, 2, "1sm-sk"), (2, 1, "2sm-dp"), (2, 2, "2sm-sk")]
+# (variant, schedule, name): schedule 1 whole tiles, 2 stream-K over every tile, 3 stream-K over the
+# last partial wave only ("auto" is the library's choice: stream-K over the last partial wave + one
+# full wave where its model says so)
+CONFIGS = [(1, 1, "1sm-dp"), (1, 2, "1sm-sk"), (1, 3, "1sm-skt"), (2, 1, "2sm-dp"), (2, 2, "2sm-sk"),
+           (2, 3, "2sm-skt")]
 GEMM_CONFIGS = [(v, sch, tn, f"{'1sm' if v == 1 else '2sm'}-{'dp' if sch == 1 else 'sk'}-n{tn}")
                 for v in (1, 2) for sch in (1, 2) for tn in (256, 128)]
 

@@ -120,7 +120,8 @@ SCHED_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL, ffn.SCHEDULE_AUTO])
+@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL,
+                                      ffn.SCHEDULE_STREAM_K_TAIL, ffn.SCHEDULE_AUTO])
 @pytest.mark.parametrize("variant", [ffn.VARIANT_1SM, ffn.VARIANT_2SM])
 @pytest.mark.parametrize("M,K,N", SCHED_SHAPES)
 def test_parity_schedules(cuda_device, M, K, N, variant, schedule):

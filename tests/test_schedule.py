@@ -23,6 +23,8 @@ def plan(T, KB, max_clusters, schedule=0):
     if schedule != 1 and KB > 1:
         if schedule == 2:
             sk_tiles = T
+        elif rem != 0 and schedule == 3:
+            sk_tiles = T if waves == 0 else rem
         elif rem != 0:
             sk_tiles = T if waves == 0 else rem + max_clusters
         if sk_tiles > 0:
@@ -59,7 +61,7 @@ def segments(cluster, C, KB, T_dp, I):
 
 
 SHAPES = list(itertools.product([1, 2, 5, 8, 16, 22, 86, 88, 96, 148, 176, 512, 688, 700, 3584],
-                                [1, 2, 3, 16, 64, 128], [74, 148], [0, 1, 2]))
+                                [1, 2, 3, 16, 64, 128], [74, 148], [0, 1, 2, 3]))
 
 
 @pytest.mark.parametrize("T,KB,maxc,sched", SHAPES)
@@ -130,7 +132,7 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
             t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
             rem = tiles % units
             sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
-            gm = min(mblk, 16)
+            gm = min(mblk, max(1, min(16, (32 << 20) // (128 * cg * K * esize))))
             region = (-(-sk_tiles // gm) + 1) * tn * K * esize + min(M, gm * 128 * cg) * K * esize
             l2_pen = 1.32 if region > 120e6 else 1.0
             sk_units = min(units, 2 * tiles) if tiles < units else units
