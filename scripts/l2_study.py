@@ -26,6 +26,8 @@ POLS = [2, 0, 2 | (1 << 2), 0 | (1 << 2)]   # x last/W normal, both normal, x la
 
 
 def configs():
+    if os.environ.get("L2_STUDY_SHAPES"):
+        return [(s, 0, 2) for s in os.environ["L2_STUDY_SHAPES"].split(",")]
     return [(s, g, p) for s in SHAPES for g in GROUPS for p in POLS]
 
 
