@@ -227,6 +227,23 @@ class ClockSampler:
                         "(CUASM_OPT_TRACE) measured ~1.44 GHz during the 7B prefill GEMM"}
 
 
+def driver_version():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        v = pynvml.nvmlSystemGetDriverVersion()
+        return v.decode() if isinstance(v, bytes) else v
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def nccl_version():
+    try:
+        return ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def load_peaks():
     path = os.path.join(_ROOT, "MEASURED_PEAKS.json")
     try:
@@ -492,7 +509,8 @@ def run_cuasm(args):
         torch.cuda.synchronize(dev)
         barrier()
     wall = time.perf_counter() - wall0
-    local_ms = sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
+    step_ms = sorted(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
+    local_ms = sum(step_ms)
     t_ms = max_over_ranks(local_ms)
     total_flops = flops_per_step * args.steps
     value = total_flops / (t_ms / 1e3) / 1e12
@@ -642,6 +660,11 @@ def run_cuasm(args):
             "pct_of_nominal_2250": round(value / world / 2250.0, 4),
             "roofline": roofline,
             "back_to_back": back_to_back,
+            "step_stats_ms": {"mean": round(local_ms / args.steps, 5), "median": round(step_ms[len(step_ms) // 2], 5),
+                              "min": round(step_ms[0], 5), "max": round(step_ms[-1], 5),
+                              "note": "rank 0's per-step spans; CUDA events tick in ~2 us steps here"},
+            "versions": {"torch": torch.__version__, "cuda": torch.version.cuda,
+                         "driver": driver_version(), "nccl": nccl_version()},
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
             "gpu_launches": launches_total,

@@ -32,6 +32,8 @@ timeout 600 python scripts/tune_split.py --out $O/tune_split.json > $O/tune_spli
 timeout 300 python scripts/launch_floor.py > $O/launch_floor.log 2>&1; echo "launch_floor=$?"
 timeout 300 python scripts/trace_gemm.py --op gemm --shapes 2048x11008x4096,4096x4096x4096 --scheds 0,1,2 > $O/trace_gemm.log 2>&1; echo "trace_gemm=$?"
 timeout 900 python scripts/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1; echo "sweep=$?"
+timeout 900 python scripts/sweep.py --shard-of 8 --out $O/sweep_shard8.json > $O/sweep_shard8.log 2>&1; echo "sweep8=$?"
+timeout 600 python scripts/plain_vs_fold_stats.py --out $O/plain_vs_fold.json > $O/plain_vs_fold.log 2>&1; echo "pvf=$?"
 timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,16x4096x11008,4096x8192x3584 --json $O/trace.json > $O/trace.log 2>&1; echo "trace=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_prefill.csv \
   python bench.py --steps 5 --warmup 2 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_launch.log 2>&1; echo "ncu_launches=$?"
