@@ -708,8 +708,9 @@ def run_reference(args):
         fl, sec, rows, thr = oracle_sample_time(d, eps, 0, rows_hint=rows_per_step)
         flops += fl
         secs += sec
-    # the sample covers rank 0's column block; scale to the whole job (all ranks' columns)
-    value = flops * (N / N_l) / secs / 1e12
+    # throughput of the FLOPs the oracle actually computed (rank 0's column block on this host's
+    # cores; the CPU throughput per FLOP does not depend on how the columns are split)
+    value = flops / secs / 1e12
     sample = (f"{rows_per_step} of {M} rows x {N_l} columns per step (K={K}), fp64 fold-aware oracle, "
               f"{oracle.num_threads()} OpenMP threads")
     res = {
