@@ -69,6 +69,8 @@ struct FfnGemmParams {
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
+    int tma_store;   // 1: bf16 output tiles leave through TMA stores (tmap_o); 0: 16-byte st.global
+                     // (fp32 handles, and the fused gather's multi-destination / multicast stores)
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
     int rep;         // 1 (SwiGLU, 1-SM, M <= 32): the x rows are loaded into all four 32-row
                      // quarters of the A tile, so every TMEM lane quadrant holds every row and
@@ -221,8 +223,17 @@ struct GemmCfg {
     static constexpr int BAR_BYTES = 1024;
     // as many pipeline stages as fit in 227 KB (4 x 48 KB 1-SM/256, 7 x 32 KB 2-SM/256,
     // 7 x 32 KB 1-SM/128, 9 x 24 KB 2-SM/128)
-    static constexpr int STAGES_FIT = (232448 - BAR_BYTES - 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT < 9 ? STAGES_FIT : 9;
+    // bf16 output goes through TMA stores from a per-warp staging area: two 32 x 32
+    // boxes (2 KB each, 64-byte swizzle) per epilogue warp
+    static constexpr int STG_WARP_BYTES = kKind == 0 ? 4096 : 0;
+    static constexpr int STG_BYTES = 8 * STG_WARP_BYTES;
+    static constexpr int STAGES_FIT = (232448 - BAR_BYTES - 1024 - STG_BYTES) / STAGE_BYTES;
+#ifdef CUASM_STAGE_CAP  // experiments only: cap the pipeline depth
+    static constexpr int STAGES_CAP = CUASM_STAGE_CAP;
+#else
+    static constexpr int STAGES_CAP = 9;
+#endif
+    static constexpr int STAGES = STAGES_FIT < STAGES_CAP ? STAGES_FIT : STAGES_CAP;
     static constexpr int TMEM_COLS = 2 * UMMA_N;                    // 2 accumulators (power of 2)
     // Two epilogue warps per TMEM lane quadrant, each owning half of the
     // accumulator columns (PAIRS pairs of 32-column chunks): two warps per SM
@@ -230,7 +241,7 @@ struct GemmCfg {
     static constexpr int NUM_EPI_WARPS = 8;
     static constexpr int PAIRS = UMMA_N / 128;
     static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 320
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + align slack
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;  // + align slack
     static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
     // Accumulator chunks (32 columns) of epilogue pair `i` of a warp in column half `half`.
     __device__ static constexpr int chunk_a(int half, int i) {
@@ -350,17 +361,44 @@ __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int
     }
 }
 
+// One 32 x 32 bf16 output box (this warp's 32 rows x 32 columns) through a TMA
+// store: lane r writes its row's four 16-byte chunks into the 2 KB staging box in
+// the 64-byte-swizzle layout the tensor map declares (chunk c of row r lands at
+// chunk c ^ ((r >> 1) & 3): conflict-free, 8 lanes of a phase hit 8 distinct
+// bank groups), then lane 0 issues the store.  kPending: bulk groups of this
+// warp allowed to be still reading smem when the box is overwritten (1 = the
+// other box's store may be in flight).
+template <int kPending>
+__device__ __forceinline__ void store_box_tma(const CUtensorMap* tmap, uint8_t* box, const float (&o)[32], int col,
+                                              int row0, uint32_t lane) {
+    if (lane == 0) ptx::tma_store_wait_read<kPending>();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint4 v = make_uint4(ptx::pack_bf16x2(o[8 * c + 0], o[8 * c + 1]), ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
+                                   ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]), ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
+        *reinterpret_cast<uint4*>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        ptx::tma_store_2d(tmap, ptx::smem_u32(box), col, row0);
+        ptx::tma_store_commit();
+    }
+}
+
 template <int kKind, int kCtaGroup, int kEpi, int kN>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                         const FfnGemmParams p) {
+                         const __grid_constant__ CUtensorMap tmap_o, const FfnGemmParams p) {
     using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint8_t* smem_stg = smem + C::STAGES * C::STAGE_BYTES;  // [8 warps][2 boxes][32 x 32] bf16 (1 KB aligned)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::STG_BYTES);
     uint64_t* full_bar = bars;                       // [STAGES]
     uint64_t* empty_bar = bars + C::STAGES;          // [STAGES]
     uint64_t* tfull_bar = bars + 2 * C::STAGES;      // [2]
@@ -558,6 +596,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         const int half = static_cast<int>(ewarp >> 2);  // this warp's half of the accumulator columns
         const uint32_t row_in_cta = quad * 32 + lane;
         int it = 0;
+        int nst = 0;  // TMA-store boxes this warp has issued (staging box = nst & 1)
         Sched sch;
         sch.init(p, cluster_id);
         Seg sg;
@@ -641,11 +680,17 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     ca = static_cast<int>(quad);
                     cb = static_cast<int>(quad) + C::BN / 32;
                 }
+                // TMA-store path: the warp's 32 rows leave as one 32 x 32 box per 32 output
+                // columns, so every lane takes part (rows >= M are clipped by the TMA unit)
+                const bool use_tma = kKind == 0 && p.tma_store && !contributor;
+                const int box_row0 = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
+                                     static_cast<int>(p.rep ? 0u : quad * 32);
+                if (use_tma && box_row0 >= p.M) continue;  // warp-uniform: no row of this warp exists
                 uint32_t v1[32], v3[32];
                 ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
                 ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
                 ptx::tmem_ld_wait();
-                if (!row_ok) continue;
+                if (!row_ok && !use_tma) continue;
                 if (contributor) {
                     float4* d1 = my_slot + (static_cast<int64_t>(ca) * 4 + quad) * 8 * 32 + lane;
                     float4* d3 = my_slot + (static_cast<int64_t>(cb) * 4 + quad) * 8 * 32 + lane;
@@ -682,19 +727,29 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                         v3[4 * q + 3] = __float_as_uint(__uint_as_float(v3[4 * q + 3]) + b[q].w);
                     }
                 }
+                uint8_t* stg = smem_stg + ewarp * C::STG_WARP_BYTES;  // this warp's two 2 KB boxes
                 if constexpr (kEpi == 0) {
                     float o[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = silu_gate(__uint_as_float(v1[j]), __uint_as_float(v3[j]), gr);
-                    store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
+                    if (use_tma) {
+                        // the two boxes alternate store by store: the box written now was last
+                        // used two stores ago, so at most one store (the other box) may be pending
+                        store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0,
+                                         lane);
+                    } else {
+                        store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
+                    }
                 } else {
                     float o[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);
-                    store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
+                    if (use_tma) store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0, lane);
+                    else store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v3[j]), p.act, p.alpha);
-                    store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
+                    if (use_tma) store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + cb * 32, box_row0, lane);
+                    else store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
                 }
             }
             if (warp == 2 && lane == 0) {
@@ -734,6 +789,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         }
     }
 
+    // every TMA store this warp issued has written global memory before the CTA retires
+    if (warp >= 2 && lane == 0 && kKind == 0 && p.tma_store) ptx::tma_store_wait<0>();
     if (warp >= 2 && lane == 0 && p.trace) atomicMax(p.trace + blockIdx.x * kTraceSlots + 5, globaltimer());
     // ----------------------------------------------------------- teardown --
     ptx::tc_fence_before();
