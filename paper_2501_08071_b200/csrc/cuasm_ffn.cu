@@ -327,18 +327,19 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // bf16 output with one destination leaves through TMA stores: a 2-D map over the
     // destination [M rows, ldo stride] x N columns, 32 x 32 boxes, 64-byte swizzle
     // (what the epilogue's staging layout writes); stores past M / N are clipped
-    CUtensorMap tmap_o;
-    p.tma_store = (kKind == 0 && p.num_dst == 1 && !p.dst_mc) ? 1 : 0;
-    if (p.tma_store) {
+    // (one map per destination: the fused gather's P2P fan-out is P TMA stores per box)
+    cuasm::OutMaps omaps{};
+    p.tma_store = (kKind == 0 && !p.dst_mc) ? 1 : 0;
+    for (int q = 0; p.tma_store && q < p.num_dst; ++q) {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldo) * static_cast<cuuint64_t>(h->esize)};
         cuuint32_t box[2] = {32, 32};
         cuuint32_t estr[2] = {1, 1};
-        CUresult r = h->encode(&tmap_o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[0], dims, strides, box, estr,
+        CUresult r = h->encode(&omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[q], dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS)
-            return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (CUresult %d)", (int)r);
+            return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out %d) failed (CUresult %d)", q, (int)r);
     }
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
@@ -431,7 +432,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     cfg.attrs = attrs;
     cfg.numAttrs = na;
     CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, tmap_x, w.tmap,
-                                      p.tma_store ? tmap_o : tmap_x, p),
+                                      omaps, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
     return CUASM_OK;

@@ -69,8 +69,8 @@ struct FfnGemmParams {
     int num_k_blk;   // ceil(K / BK)
     int group_m;     // rasterisation: m-blocks per group (L2 reuse of W13 blocks)
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
-    int tma_store;   // 1: bf16 output tiles leave through TMA stores (tmap_o); 0: 16-byte st.global
-                     // (fp32 handles, and the fused gather's multi-destination / multicast stores)
+    int tma_store;   // 1: bf16 output tiles leave through TMA stores (omaps.m[0..num_dst), one per
+                     // destination); 0: 16-byte st.global (fp32 handles, multicast destinations)
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
     int rep;         // 1 (SwiGLU, 1-SM, M <= 32): the x rows are loaded into all four 32-row
                      // quarters of the A tile, so every TMEM lane quadrant holds every row and
@@ -368,9 +368,15 @@ __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int
 // bank groups), then lane 0 issues the store.  kPending: bulk groups of this
 // warp allowed to be still reading smem when the box is overwritten (1 = the
 // other box's store may be in flight).
+// Output tensor maps: one per destination (the fused gather's P2P fan-out issues
+// one TMA store per destination from the same staged box).
+struct OutMaps {
+    CUtensorMap m[8];
+};
+
 template <int kPending>
-__device__ __forceinline__ void store_box_tma(const CUtensorMap* tmap, uint8_t* box, const float (&o)[32], int col,
-                                              int row0, uint32_t lane) {
+__device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint8_t* box, const float (&o)[32],
+                                              int col, int row0, uint32_t lane) {
     if (lane == 0) ptx::tma_store_wait_read<kPending>();
     __syncwarp();
 #pragma unroll
@@ -382,7 +388,7 @@ __device__ __forceinline__ void store_box_tma(const CUtensorMap* tmap, uint8_t* 
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-        ptx::tma_store_2d(tmap, ptx::smem_u32(box), col, row0);
+        for (int q = 0; q < num; ++q) ptx::tma_store_2d(&maps->m[q], ptx::smem_u32(box), col, row0);
         ptx::tma_store_commit();
     }
 }
@@ -390,7 +396,7 @@ __device__ __forceinline__ void store_box_tma(const CUtensorMap* tmap, uint8_t* 
 template <int kKind, int kCtaGroup, int kEpi, int kN>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                         const __grid_constant__ CUtensorMap tmap_o, const FfnGemmParams p) {
+                         const __grid_constant__ OutMaps omaps, const FfnGemmParams p) {
     using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
@@ -735,7 +741,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if (use_tma) {
                         // the two boxes alternate store by store: the box written now was last
                         // used two stores ago, so at most one store (the other box) may be pending
-                        store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0,
+                        store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0,
                                          lane);
                     } else {
                         store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
@@ -744,11 +750,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     float o[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);
-                    if (use_tma) store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0, lane);
+                    if (use_tma) store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0, lane);
                     else store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v3[j]), p.act, p.alpha);
-                    if (use_tma) store_box_tma<1>(&tmap_o, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + cb * 32, box_row0, lane);
+                    if (use_tma) store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + cb * 32, box_row0, lane);
                     else store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
                 }
             }
