@@ -137,18 +137,18 @@ cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x_dev, const void* r
 /* Tensor-parallel forward with step a4 (the all-gather of the column shards,
  * SURVEY §8(e)/(f) f2) fused into the epilogue: the same computation as
  * cuasm_ffn_forward on this rank's shard (w1_dev/w3_dev = rows [n0, n0+N) of
- * the full W1/W3, N = the shard width), but every 16-byte output store is
- * written to each destination instead of one local buffer, tile by tile while
- * the next tile's mainloop runs -- the gather overlaps the math and no
- * separate collective or interleave pass runs.
+ * the full W1/W3, N = the shard width), but every staged 32 x 32 output box is
+ * written to each destination (one TMA store per destination) instead of one
+ * local buffer, tile by tile while the next tile's mainloop runs -- the gather
+ * overlaps the math and no separate collective or interleave pass runs.
  *   dst[q] (q < num_dst <= 8): device address of THIS shard's column 0 inside
  *     rank q's full row-major [M, ldo] output, i.e. base_q + n0 * elemsize;
  *     base_q mapped into this device's address space (CUDA IPC / symmetric
  *     memory peer pointers; stores travel over NVLink).  num_dst = 1 with a
  *     local pointer is the plain forward with an output stride.
  *   multicast = 1: num_dst must be 1 and dst[0] is an NVLS multicast address
- *     (+ n0 * elemsize) bound to every rank's output buffer; each store is
- *     issued once as multimem.st.relaxed.sys and NVSwitch replicates it.
+ *     (+ n0 * elemsize) bound to every rank's output buffer; each 16-byte store
+ *     is issued once as multimem.st.relaxed.sys and NVSwitch replicates it.
  *   ldo: row stride of every destination, elements, >= N, multiple of 16 bytes.
  * Visibility: a rank's full output is complete once EVERY rank's launch has
  * completed and a cross-rank barrier ordered after those launches has
