@@ -283,7 +283,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // the product depends only on row m of x and rows >= M are never stored.
     // Measured: a 128-row box over an 8-row x streams the weights ~30% slower
     // than over a 16-row x (profiles/r01/trace_small_m.log).
-    const uint32_t a_rows = (kCtaGroup == 1 && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
+    // decode shapes (SwiGLU, M <= 32, either variant): the rows are replicated over
+    // the four TMEM lane quadrants of the (leader) CTA (dual_gemm.cuh `rep`)
+    const bool rep = kEpi == 0 && M <= 32;
+    const uint32_t a_rows =
+        ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
     if (st != CUASM_OK) return st;
     if (w.tmap_rows != C::B_ROWS) {
@@ -343,7 +347,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     }
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
-    p.rep = (kCtaGroup == 1 && kEpi == 0 && M <= 32) ? 1 : 0;
+    p.rep = rep ? 1 : 0;
 
     static bool attr_set = false;  // one per template instance
     if (!attr_set) {

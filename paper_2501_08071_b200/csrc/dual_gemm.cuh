@@ -72,7 +72,7 @@ struct FfnGemmParams {
     int tma_store;   // 1: bf16 output tiles leave through TMA stores (omaps.m[0..num_dst), one per
                      // destination); 0: 16-byte st.global (fp32 handles, multicast destinations)
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
-    int rep;         // 1 (SwiGLU, 1-SM, M <= 32): the x rows are loaded into all four 32-row
+    int rep;         // 1 (SwiGLU, M <= 32; 2-SM: the leader CTA): x rows loaded into all four 32-row
                      // quarters of the A tile, so every TMEM lane quadrant holds every row and
                      // the epilogue spreads the columns over the four SM sub-partitions (warp
                      // w may only read quadrant w%4: without this a decode tile's whole
@@ -479,9 +479,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                             ptx::tma_load_2d(sa + q * 32 * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     } else {
-                        // both CTAs' bytes land on the leader's barrier
-                        if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * (p.a_box_bytes + C::B_BYTES));
-                        ptx::tma_load_2d_2sm(sa, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                        // both CTAs' bytes land on the leader's barrier; rep: the leader's
+                        // A tile gets the <= 32 x rows in all four quarters (the peer's rows
+                        // are all past M)
+                        const int nrep = (p.rep && leader) ? 4 : 1;
+                        if (leader)
+                            ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? 5 : 2) * p.a_box_bytes);
+                        for (int q = 0; q < nrep; ++q)
+                            ptx::tma_load_2d_2sm(sa + q * 32 * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     }
                 }

@@ -45,6 +45,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_
   python bench.py --workload llama7b_decode --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_d.log 2>&1; echo "ncu_gemm_d=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_70b \
   python bench.py --workload llama70b --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_70b.log 2>&1; echo "ncu_gemm_70b=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_70b_shard8 \
+  python bench.py --workload llama70b --shard-of 8 --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_70b8.log 2>&1; echo "ncu_gemm_70b8=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_tiny \
+  python bench.py --workload tiny_fp32 --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_tiny.log 2>&1; echo "ncu_gemm_tiny=$?"
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_memcheck.log 2>&1; echo "memcheck=$?"
 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_synccheck.log 2>&1; echo "synccheck=$?"
 timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_racecheck.log 2>&1; echo "racecheck=$?"
