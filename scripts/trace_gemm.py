@@ -81,7 +81,7 @@ def main():
                 rel = (col - t0) / 1e3
                 rows[name] = {"min": round(rel.min().item(), 2), "med": round(rel.median().item(), 2),
                               "max": round(rel.max().item(), 2)}
-            key = f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all'][sched]}"
+            key = f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all', 'stream-k-tail'][sched]}"
             report[key] = rows
             print(key)
             for name, r in rows.items():
