@@ -590,7 +590,8 @@ def run_cuasm(args):
     if op == "rmsnorm" or gemm_flops / gemm_bytes < peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
         bound, peak, roof_unit = "hbm", peaks["hbm_gbs"], "GB/s"
         achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
-    traffic = load_traffic(args.workload if world == 1 else f"{args.workload}@tp{world}")
+    traffic = load_traffic(f"{args.workload}@tp{world}" if world > 1 else
+                           f"{args.workload}@shard{args.shard_of}" if args.shard_of > 1 else args.workload)
     roofline = {
         "kernel": {"ffn": "ffn_dual_gemm_kernel", "block": "ffn_dual_gemm_kernel x2 (fused FFN + W2 GEMM)",
                    "rmsnorm": "ffn_rmsnorm_kernel",
