@@ -261,6 +261,11 @@ struct EpiSpec {
     int64_t ldo = 0;
 };
 
+// Few-tile decode shapes: at most this many 1-SM tiles take the 1-SM variant with
+// each tile split this many ways (plan_config_raw, launch_gemm).
+constexpr int64_t kFewTiles = 24;
+constexpr int kFewTilesSplit = 3;
+
 // Rasterisation group (m-blocks whose tiles run before the next W13 column
 // block): as many as keep the group's rows of x within ~32 MB of L2, at most
 // 16.  x of a group is re-read once per n-block and must stay L2-resident; a
@@ -379,8 +384,10 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         // than clusters (each finisher then adds a single partial)
         if (sk_tiles > 0) {
             int64_t c = std::min<int64_t>(max_clusters, static_cast<int64_t>(sk_tiles) * p.num_k_blk);
-            if (waves == 0 && (h->schedule == CUASM_SCHEDULE_AUTO || h->sk_split > 0))
-                c = std::min<int64_t>(c, static_cast<int64_t>(h->sk_split > 0 ? h->sk_split : 2) * sk_tiles);
+            if (waves == 0 && (h->schedule == CUASM_SCHEDULE_AUTO || h->sk_split > 0)) {
+                const int split = h->sk_split > 0 ? h->sk_split : (p.num_tiles <= kFewTiles ? kFewTilesSplit : 2);
+                c = std::min<int64_t>(c, static_cast<int64_t>(split) * sk_tiles);
+            }
             clusters = static_cast<int>(c);
         }
     }
@@ -466,6 +473,14 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     const int64_t nblk = (N + out_cols - 1) / out_cols;
     const double w_elems = out_cols == 128 ? 2.0 * N * K : 1.0 * N * K;  // W1+W3, or one weight
     const double hbm_floor = (w_elems + static_cast<double>(M) * K + static_cast<double>(M) * N) * esize / hbm;
+    // Decode-like SwiGLU shapes with few tiles (M <= 256, <= kFewTiles 1-SM tiles: the
+    // tensor-parallel decode shards): weight streaming and the partial fixup decide,
+    // not the tensor pipe, and the 1-SM variant split kFewTilesSplit ways measured
+    // best (16 x 4096 x 1376: 22.6 us vs 24.6 us for the 2-SM split in two;
+    // scripts/tune_split.py, profiles/r01/tune_split.json)
+    if (out_cols == 128 && M <= 256 && KB >= 2 * kFewTilesSplit &&
+        ((M + 127) / 128) * nblk <= kFewTiles)
+        return Plan{CUASM_VARIANT_1SM, true, 256};
     Plan best{CUASM_VARIANT_2SM, false, 256};
     double best_t = 1e30;
     // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM

@@ -368,8 +368,17 @@ def test_gemm_act_fp32_tf32_exact_inputs(cuda_device):
 
 @pytest.mark.parametrize("M,K,N", [(16, 512, 1024), (300, 256, 648), (2048, 1024, 2816)])
 def test_ffn_block_parity(cuda_device, M, K, N):
-    """out = (SiLU(xn W1^T) * (xn W3^T)) W2^T against the oracle with the hidden
-    rounded to bf16 (reading R13) and g folded into bf16 weights (R4)."""
+    """out = (SiLU(xn W1^T) * (xn W3^T)) W2^T, the hidden rounded to bf16 between
+    the two GEMMs (reading R13), g folded into bf16 weights (R4).
+
+    A hidden element whose exact value lies within the fp32 accumulation error of
+    a bf16 rounding boundary may round either way, and which way depends on the
+    summation grouping (the tile schedule), so the block output is checked in the
+    steps the arithmetic fixes: (a) the hidden against the oracle FFN, at the
+    [BJ] tolerance; (b) the output against the exact product of the hidden the
+    GPU produced with W2; (c) the output against the oracle's rounded-hidden
+    block, allowing exactly the contribution of the hidden elements the two
+    rounded differently (|sum_n dh_n W2[k,n]|, dh = gpu hidden - oracle hidden)."""
     d = make_inputs(M, K, N, family="C", seed=5200 + M, dtype="bf16")
     w2 = make_inputs(1, N, K, family="C", seed=5300 + M, dtype="bf16")["w1"]   # [K, N]
     t = {k: v.to(cuda_device) for k, v in d.items()}
@@ -378,14 +387,27 @@ def test_ffn_block_parity(cuda_device, M, K, N):
     torch.cuda.synchronize()
     assert y.shape == (M, K)
     rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 24)))))
-    ref = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, 1e-6, mode="fold_bf16", round_hidden=True,
-                           rows=rows)
-    check(y[rows], ref, f"ffn block {M}x{K}x{N}")
     # the hidden it used is exactly the fused FFN's output
     hid = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
     y2 = h.gemm_act(hid, w2.to(cuda_device), "identity")
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+    hid_rows = hid[rows].double().cpu()
+    # (a) the hidden = the fused FFN, at the [BJ] tolerance against the oracle
+    ref_h = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(hid[rows], ref_h, f"ffn block hidden {M}x{K}x{N}")
+    # (b) the down projection of that hidden, against its exact product
+    w2d = w2.double()
+    check(y[rows], (hid_rows @ w2d.T).numpy(), f"ffn block down projection {M}x{K}x{N}")
+    # (c) the block against the oracle, up to the hidden elements rounded the other way
+    ref = oracle.ffn_block(d["x"], d["g"], d["w1"], d["w3"], w2, 1e-6, mode="fold_bf16", round_hidden=True,
+                           rows=rows)
+    ref_hr = torch.from_numpy(ref_h).to(torch.bfloat16).double()
+    flip = ((hid_rows - ref_hr) @ w2d.T).abs().numpy()
+    err = np.abs(y[rows].double().cpu().numpy() - ref)
+    assert (err <= RTOL * np.abs(ref) + ATOL + flip * (1 + 1e-6)).all(), f"ffn block {M}x{K}x{N} vs oracle"
+    nflip = int((hid_rows != ref_hr).sum())
+    assert nflip <= max(8, hid_rows.numel() // 200), f"{nflip} hidden elements rounded differently"
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
