@@ -263,7 +263,7 @@ struct EpiSpec {
 
 // Few-tile decode shapes: at most this many 1-SM tiles take the 1-SM variant with
 // each tile split this many ways (plan_config_raw, launch_gemm).
-constexpr int64_t kFewTiles = 24;
+constexpr int64_t kFewTiles = 32;
 constexpr int kFewTilesSplit = 3;
 
 // Rasterisation group (m-blocks whose tiles run before the next W13 column
@@ -478,8 +478,11 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // not the tensor pipe, and the 1-SM variant split kFewTilesSplit ways measured
     // best (16 x 4096 x 1376: 22.6 us vs 24.6 us for the 2-SM split in two;
     // scripts/tune_split.py, profiles/r01/tune_split.json)
-    if (out_cols == 128 && M <= 256 && KB >= 2 * kFewTilesSplit &&
-        ((M + 127) / 128) * nblk <= kFewTiles)
+    // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
+    // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
+    const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
+    if (out_cols == 128 && KB >= 2 * kFewTilesSplit &&
+        ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
         return Plan{CUASM_VARIANT_1SM, true, 256};
     Plan best{CUASM_VARIANT_2SM, false, 256};
     double best_t = 1e30;

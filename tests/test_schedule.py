@@ -30,7 +30,7 @@ def plan(T, KB, max_clusters, schedule=0):
         if sk_tiles > 0:
             clusters = min(max_clusters, sk_tiles * KB)
             if schedule == 0 and waves == 0:
-                clusters = min(clusters, (3 if T <= 24 else 2) * sk_tiles)   # kFewTiles / kFewTilesSplit
+                clusters = min(clusters, (3 if T <= 32 else 2) * sk_tiles)   # kFewTiles / kFewTilesSplit
     return clusters, T - sk_tiles, sk_tiles * KB
 
 
@@ -119,7 +119,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     BK = 128 // esize
     KB = -(-K // BK)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
-    if out_cols == 128 and M <= 256 and KB >= 6 and -(-M // 128) * -(-N // 128) <= 24:
+    t1 = -(-M // 128) * -(-N // 128)
+    if out_cols == 128 and KB >= 6 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
         return ("1sm", True, 256)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
     best, best_t = ("2sm", False, 256), 1e30
     for tn in ((256,) if out_cols == 128 else (256, 128)):
