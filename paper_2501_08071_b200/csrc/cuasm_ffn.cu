@@ -290,7 +290,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // than over a 16-row x (profiles/r01/trace_small_m.log).
     // decode shapes (SwiGLU, M <= 32, either variant): the rows are replicated over
     // the four TMEM lane quadrants of the (leader) CTA (dual_gemm.cuh `rep`)
-    const bool rep = kEpi == 0 && M <= 32;
+    const int rep = kEpi != 0 ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
     const uint32_t a_rows =
         ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
@@ -352,7 +352,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     }
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
-    p.rep = rep ? 1 : 0;
+    p.rep = rep;
 
     static bool attr_set = false;  // one per template instance
     if (!attr_set) {

@@ -72,11 +72,11 @@ struct FfnGemmParams {
     int tma_store;   // 1: bf16 output tiles leave through TMA stores (omaps.m[0..num_dst), one per
                      // destination); 0: 16-byte st.global (fp32 handles, multicast destinations)
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
-    int rep;         // 1 (SwiGLU, M <= 32; 2-SM: the leader CTA): x rows loaded into all four 32-row
-                     // quarters of the A tile, so every TMEM lane quadrant holds every row and
-                     // the epilogue spreads the columns over the four SM sub-partitions (warp
-                     // w may only read quadrant w%4: without this a decode tile's whole
-                     // epilogue runs on sub-partition 0)
+    int rep;         // 4 (SwiGLU, M <= 32) / 2 (M <= 64) / 0; 2-SM: the leader CTA.  The x rows are
+                     // loaded rep times into the A tile (at smem rows q*128/rep), so every TMEM
+                     // lane quadrant holds rows and the epilogue spreads the column pairs over
+                     // the four SM sub-partitions (warp w may only read quadrant w%4: without
+                     // this a decode tile's whole epilogue runs on sub-partition 0 or 0-1)
     int num_tiles;
     // --- persistent schedule: data-parallel tiles, then a stream-K region ---
     int num_clusters;   // persistent clusters (CTA pairs for the 2-SM variant)
@@ -473,20 +473,20 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
                 if (ptx::elect_one()) {
                     if constexpr (kCtaGroup == 1) {
-                        const int nrep = p.rep ? 4 : 1;
+                        const int nrep = p.rep ? p.rep : 1;
                         ptx::mbar_arrive_expect_tx(fb, nrep * p.a_box_bytes + C::B_BYTES);
-                        for (int q = 0; q < nrep; ++q)  // quarter q of the A tile: smem rows 32q.. (4 KB aligned)
-                            ptx::tma_load_2d(sa + q * 32 * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                        for (int q = 0; q < nrep; ++q)  // copy q of the rows: smem rows q*128/nrep.. (4 KB aligned)
+                            ptx::tma_load_2d(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     } else {
                         // both CTAs' bytes land on the leader's barrier; rep: the leader's
                         // A tile gets the <= 32 x rows in all four quarters (the peer's rows
                         // are all past M)
-                        const int nrep = (p.rep && leader) ? 4 : 1;
+                        const int nrep = (p.rep && leader) ? p.rep : 1;
                         if (leader)
-                            ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? 5 : 2) * p.a_box_bytes);
+                            ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? p.rep + 1 : 2) * p.a_box_bytes);
                         for (int q = 0; q < nrep; ++q)
-                            ptx::tma_load_2d_2sm(sa + q * 32 * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                            ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
                         ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
                     }
                 }
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // rep: quadrant `quad` holds rows 0..31 of the tile (lane = row), and only its
             // own column pair is drained by it (below)
             const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
-                            static_cast<int>(p.rep ? lane : row_in_cta);
+                            static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 + lane : row_in_cta);
             const bool row_ok = row < p.M;
             const bool contributor = sg.kb0 > 0;                       // stream-K: partial, not the tile's start
             const bool finisher = sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
@@ -685,17 +685,20 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             for (int i = 0; i < C::PAIRS; ++i) {
                 int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
                 if (kEpi == 0 && p.rep) {
-                    // quadrant q drains column pair q (h1 chunk q, h3 chunk q + BN/32); the
-                    // second warp of each quadrant idles
-                    if (half != 0 || i != 0) continue;
-                    ca = static_cast<int>(quad);
-                    cb = static_cast<int>(quad) + C::BN / 32;
+                    // rep 4 (M <= 32): quadrant q holds rows 0..31 and drains column pair q
+                    // (h1 chunk q, h3 chunk q + BN/32), the second warp of each quadrant idles;
+                    // rep 2 (M <= 64): quadrants q, q+2 hold rows 32(q%2).., and each of their
+                    // four warps drains one pair (2 * (q / 2) + half)
+                    if (i != 0 || (p.rep == 4 && half != 0)) continue;
+                    const int pair = p.rep == 4 ? static_cast<int>(quad) : static_cast<int>(quad / 2) * 2 + half;
+                    ca = pair;
+                    cb = pair + C::BN / 32;
                 }
                 // TMA-store path: the warp's 32 rows leave as one 32 x 32 box per 32 output
                 // columns, so every lane takes part (rows >= M are clipped by the TMA unit)
                 const bool use_tma = kKind == 0 && p.tma_store && !contributor;
                 const int box_row0 = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
-                                     static_cast<int>(p.rep ? 0u : quad * 32);
+                                     static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 : quad * 32);
                 if (use_tma && box_row0 >= p.M) continue;  // warp-uniform: no row of this warp exists
                 uint32_t v1[32], v3[32];
                 ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
