@@ -99,6 +99,8 @@ SMALL_SHAPES = [
     (129, 200, 136),
     (257, 1024, 1000),
     (640, 320, 1408),
+    (33, 512, 1032),     # rows replicated twice over the TMEM quadrants (33 <= M <= 64)
+    (64, 256, 264),
 ]
 
 
@@ -114,6 +116,7 @@ def test_parity_small_bf16(cuda_device, M, K, N, family, variant):
 
 SCHED_SHAPES = [
     (16, 4096, 512),     # 4-8 tiles over 74-148 clusters: many contributors per tile
+    (48, 4096, 1376),    # twice-replicated rows, few tiles split by stream-K
     (300, 1024, 1000),   # ragged M and N, a few tiles
     (1000, 512, 2056),   # several waves + tail
     (2048, 4096, 1376),  # 7B prefill, 8-way shard width (88 / 176 tiles)
