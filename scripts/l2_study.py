@@ -27,7 +27,8 @@ POLS = [2, 0, 2 | (1 << 2), 0 | (1 << 2)]   # x last/W normal, both normal, x la
 
 def configs():
     if os.environ.get("L2_STUDY_SHAPES"):
-        return [(s, 0, 2) for s in os.environ["L2_STUDY_SHAPES"].split(",")]
+        pols = [int(x) for x in os.environ.get("L2_STUDY_POLS", "2").split(",")]
+        return [(s, 0, pol) for s in os.environ["L2_STUDY_SHAPES"].split(",") for pol in pols]
     return [(s, g, p) for s in SHAPES for g in GROUPS for p in POLS]
 
 
