@@ -391,6 +391,12 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
             clusters = static_cast<int>(c);
         }
     }
+    // the kernel's stream-K arithmetic is 32-bit (dual_gemm.cuh sk_begin): keep
+    // sk_iters * clusters below 2^32, else whole tiles only
+    if (static_cast<uint64_t>(sk_tiles) * p.num_k_blk * static_cast<uint64_t>(clusters) >= (uint64_t(1) << 32)) {
+        sk_tiles = 0;
+        clusters = std::min(p.num_tiles, max_clusters);
+    }
     p.num_clusters = clusters;
     p.num_dp_tiles = p.num_tiles - sk_tiles;
     p.sk_iters = static_cast<int64_t>(sk_tiles) * p.num_k_blk;

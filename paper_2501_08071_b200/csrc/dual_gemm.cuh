@@ -96,13 +96,19 @@ struct Seg {
     int tile, kb0, kb1;
 };
 
+// Stream-K arithmetic in 32 bits: the host guarantees sk_iters * num_clusters < 2^32
+// (launch_gemm), and 64-bit divisions compile to a subroutine call whose first,
+// instruction-cache-cold execution put ~1 us between griddepcontrol.wait and the
+// first TMA of every launch (per-CTA trace).
 __device__ __forceinline__ int64_t sk_begin(const FfnGemmParams& p, int c) {
-    return (p.sk_iters * c) / p.num_clusters;
+    return static_cast<int64_t>(static_cast<uint32_t>(p.sk_iters) * static_cast<uint32_t>(c) /
+                                static_cast<uint32_t>(p.num_clusters));
 }
 
 // The cluster whose stream-K range holds iteration i.
 __device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
-    int c = static_cast<int>((i * p.num_clusters) / (p.sk_iters > 0 ? p.sk_iters : 1));
+    int c = static_cast<int>(static_cast<uint32_t>(i) * static_cast<uint32_t>(p.num_clusters) /
+                             static_cast<uint32_t>(p.sk_iters > 0 ? p.sk_iters : 1));
     while (c + 1 < p.num_clusters && sk_begin(p, c + 1) <= i) ++c;
     while (c > 0 && sk_begin(p, c) > i) --c;
     return c;
@@ -135,7 +141,7 @@ struct Sched {
             return true;
         }
         if (cur < end) {
-            const int64_t t = cur / KB;
+            const int64_t t = static_cast<uint32_t>(cur) / static_cast<uint32_t>(KB);
             const int kb0 = static_cast<int>(cur - t * KB);
             const int64_t take = (KB - kb0) < (end - cur) ? (KB - kb0) : (end - cur);
             s.tile = T_dp + static_cast<int>(t);
