@@ -546,3 +546,23 @@ def test_gate_extremes(cuda_device, schedule):
     torch.cuda.synchronize()
     assert bool(torch.isnan(outn[3]).all())
     assert not torch.isnan(outn[torch.arange(M, device=cuda_device) != 3]).any()
+
+
+def test_option_values_are_validated(cuda_device):
+    """cuasm_ffn_set_option rejects out-of-range values and leaves the handle usable."""
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    lib = h.lib
+    bad = [(ffn.OPT_SCHEDULE, 4), (ffn.OPT_SCHEDULE, -1), (ffn.OPT_SK_SPLIT, 1), (ffn.OPT_SK_SPLIT, 17),
+           (ffn.OPT_L2_POLICY, 3), (ffn.OPT_L2_POLICY, 12), (ffn.OPT_L2_POLICY, 16), (ffn.OPT_TILE_N, 64),
+           (ffn.OPT_FUSED_NORM, 2), (99, 0)]
+    for opt, val in bad:
+        assert lib.cuasm_ffn_set_option(h._h, opt, val) == ffn.ERR_INVALID_ARG, (opt, val)
+    good = [(ffn.OPT_SCHEDULE, ffn.SCHEDULE_STREAM_K_TAIL), (ffn.OPT_SK_SPLIT, 3), (ffn.OPT_L2_POLICY, 0),
+            (ffn.OPT_L2_POLICY, 2 | (1 << 2))]
+    for opt, val in good:
+        assert lib.cuasm_ffn_set_option(h._h, opt, val) == ffn.OK, (opt, val)
+    # every option combination above still computes the FFN correctly
+    M, K, N = 200, 512, 384
+    d = make_inputs(M, K, N, family="C", seed=3500, dtype="bf16")
+    out, _ = run_gpu(d, 1e-6, "bf16", handle=h, schedule=ffn.SCHEDULE_STREAM_K_TAIL)
+    check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), "options")
