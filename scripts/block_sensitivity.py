@@ -1,6 +1,8 @@
+"""Block (f1) sensitivity to the hidden's bf16 rounding (reading R13): hidden flips vs the oracle and the
+block output error per schedule."""
 import sys, os
 sys.path.insert(0, os.getcwd())
-import numpy as np, torch
+import torch
 import oracle, paper_2501_08071_b200 as ffn
 from ffn_inputs import make_inputs
 dev = torch.device("cuda:0")
