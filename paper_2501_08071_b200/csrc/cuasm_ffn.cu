@@ -490,6 +490,15 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     if (out_cols == 128 && KB >= 2 * kFewTilesSplit &&
         ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
         return Plan{CUASM_VARIANT_1SM, true, 256};
+    // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
+    // 512 x 2048 x 512): latency-bound, and the 1-SM variant skips the cluster launch,
+    // cluster barriers and 2-SM TMEM allocation -- 16.4 vs 18.3 us (GEMM mode, 128-wide
+    // tiles; scripts/tune_split_gemm.py)
+    if (KB <= 32) {
+        // 128 outputs per tile: the SwiGLU tile, or the GEMM mode's 128-wide tile
+        if (((M + 127) / 128) * ((N + 127) / 128) <= sm_count)
+            return Plan{CUASM_VARIANT_1SM, false, out_cols == 128 ? 256 : 128};
+    }
     Plan best{CUASM_VARIANT_2SM, false, 256};
     double best_t = 1e30;
     // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM
