@@ -487,18 +487,20 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
     // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
-    if (out_cols == 128 && KB >= 2 * kFewTilesSplit &&
+    // (k-loops of >= 48 k-blocks: a split must save more MMA time than its partial fixup costs;
+    // the paper's fused_ff shape 512 x 2048 x 512 split three ways finished its tail 5 us late)
+    if (out_cols == 128 && KB >= 48 &&
         ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
         return Plan{CUASM_VARIANT_1SM, true, 256};
     // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
     // 512 x 2048 x 512): latency-bound, and the 1-SM variant skips the cluster launch,
     // cluster barriers and 2-SM TMEM allocation -- 16.4 vs 18.3 us (GEMM mode, 128-wide
     // tiles; scripts/tune_split_gemm.py)
-    if (KB <= 32) {
-        // 128 outputs per tile: the SwiGLU tile, or the GEMM mode's 128-wide tile
-        if (((M + 127) / 128) * ((N + 127) / 128) <= sm_count)
-            return Plan{CUASM_VARIANT_1SM, false, out_cols == 128 ? 256 : 128};
-    }
+    // (GEMM mode only: its 128-wide 1-SM tile does the same MMA work per SM as the 2-SM
+    // tile, whereas a SwiGLU 1-SM tile pays the 16% smem penalty -- 2048 x 2048 x 512 FFN:
+    // 1-SM 23.8 vs 2-SM 23.0 us)
+    if (KB <= 32 && out_cols != 128 && ((M + 127) / 128) * ((N + 127) / 128) <= sm_count)
+        return Plan{CUASM_VARIANT_1SM, false, 128};
     Plan best{CUASM_VARIANT_2SM, false, 256};
     double best_t = 1e30;
     // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM

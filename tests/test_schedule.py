@@ -120,10 +120,10 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     KB = -(-K // BK)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
-    if out_cols == 128 and KB >= 6 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
+    if out_cols == 128 and KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
         return ("1sm", True, 256)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
-    if KB <= 32 and t1 <= sm_count:   # short k-loops in one 1-SM wave: latency-bound
-        return ("1sm", False, 256 if out_cols == 128 else 128)
+    if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
+        return ("1sm", False, 128)
     best, best_t = ("2sm", False, 256), 1e30
     for tn in ((256,) if out_cols == 128 else (256, 128)):
         oc = 128 if out_cols == 128 else tn
