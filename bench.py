@@ -66,6 +66,8 @@ WORKLOADS = {
 EXTRA = {
     "llama7b_block": ("block", 2048, 4096, 11008),
     "mmleakyrelu_paper": ("gemm_lrelu", 512, 2048, 512),
+    # the paper's own fused_ff shape (B,M,N,K = 1,512,512,2048; reading R10)
+    "fused_ff_paper": ("ffn", 512, 2048, 512),
     "mmleakyrelu_large": ("gemm_lrelu", 4096, 4096, 4096),
     # the paper's stand-alone rmsnorm: 4096 rows x 2048 features; N unused
     "rmsnorm_paper": ("rmsnorm", 4096, 2048, 8),

@@ -13,7 +13,7 @@ timeout 600 python bench.py > $O/bench_llama7b_prefill.json 2> $O/bench.err; ech
 timeout 600 python bench.py --workload llama7b_decode > $O/bench_llama7b_decode.json 2>> $O/bench.err; echo "bench_decode=$?"
 timeout 600 python bench.py --workload llama70b --skip-cpu-baseline > $O/bench_llama70b.json 2>> $O/bench.err; echo "bench_70b=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference.json 2>> $O/bench.err; echo "bench_ref=$?"
-for w in llama7b_block mmleakyrelu_paper mmleakyrelu_large rmsnorm_paper; do
+for w in llama7b_block mmleakyrelu_paper mmleakyrelu_large rmsnorm_paper fused_ff_paper; do
   timeout 600 python bench.py --workload $w --skip-cpu-baseline --skip-e2e > $O/bench_$w.json 2>> $O/bench.err; echo "bench_$w=$?"
 done
 timeout 600 python bench.py --workload tiny_fp32 --skip-cpu-baseline --skip-e2e > $O/bench_tiny_fp32.json 2>> $O/bench.err; echo "bench_tiny=$?"
