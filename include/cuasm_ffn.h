@@ -93,9 +93,14 @@ typedef enum {
                                this many stream-K ranges per tile, 2..16 (0 = 2, the
                                default; each extra range is one more partial for the
                                tile's finisher to add)                                 */
-    CUASM_OPT_L2_POLICY = 9   /* L2 eviction policy of the TMA loads, 2 bits each: bits 0-1
+    CUASM_OPT_L2_POLICY = 9,  /* L2 eviction policy of the TMA loads, 2 bits each: bits 0-1
                                x, bits 2-3 packed W13; 0 evict_normal, 1 evict_first,
                                2 evict_last.  Default 2 (x evict_last, W13 normal)    */
+    CUASM_OPT_CSPLIT = 10     /* 1-SM variant, fewer tiles than SMs: split every tile's
+                               k-range over a cluster of S CTAs and reduce the partials
+                               through distributed shared memory.  0 = the
+                               configuration model decides, 1 = off, 2..8 = S (used
+                               only when tiles * S <= SMs and S <= k-blocks)           */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -263,7 +268,8 @@ const char* cuasm_ffn_last_error(cuasm_ffn_t h);
  * type `dtype`, problem M x K x N and op (0: fused FFN, 128 outputs per tile;
  * 1: GEMM + activation, 256- or 128-output tiles) it returns the chosen
  * cuasm_variant_t and in *stream_k bit 0 = stream-K tail used, bit 1 = the
- * 128-wide tile.  Pure host code. */
+ * 128-wide tile, bits 4..7 = the cluster split-K width (CTAs per tile, 0 =
+ * none; see CUASM_OPT_CSPLIT).  Pure host code. */
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k);
 

@@ -63,6 +63,8 @@ struct cuasm_ffn_s {
     int trace = 0;     // CUASM_OPT_TRACE
     int tile_n = 0;    // CUASM_OPT_TILE_N (GEMM + activation): 0 auto, 128, 256
     int l2pol = 2;     // CUASM_OPT_L2_POLICY (x evict_last, W13 evict_normal)
+    int csplit_opt = 0;  // CUASM_OPT_CSPLIT: 0 auto (plan), 1 off, 2..8 force a cluster split-K of that many CTAs
+    int plan_csplit = 0; // plan_config's cluster split for the current launch
     int sk_split = 0;  // CUASM_OPT_SK_SPLIT: max stream-K ranges per tile when tiles < clusters (0: 2)
     int last_tile_n = 256;
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
@@ -265,6 +267,7 @@ struct EpiSpec {
 // each tile split this many ways (plan_config_raw, launch_gemm).
 constexpr int64_t kFewTiles = 32;
 constexpr int kFewTilesSplit = 3;
+constexpr int kDecodeCsplit = 4;  // cluster split-K width the planner uses for decode shards
 
 // Rasterisation group (m-blocks whose tiles run before the next W13 column
 // block): as many as keep the group's rows of x within ~32 MB of L2, at most
@@ -290,7 +293,16 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // than over a 16-row x (profiles/r01/trace_small_m.log).
     // decode shapes (SwiGLU, M <= 32, either variant): the rows are replicated over
     // the four TMEM lane quadrants of the (leader) CTA (dual_gemm.cuh `rep`)
-    const int rep = kEpi != 0 ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
+    // cluster split-K (1-SM; dual_gemm.cuh split_k_reduce): S CTAs per tile, one tile per cluster
+    int csplit = 0;
+    if (kCtaGroup == 1) {
+        const int want = h->csplit_opt >= 2 ? h->csplit_opt : (h->csplit_opt == 0 ? h->plan_csplit : 0);
+        const int64_t tiles = ((M + C::TILE_M - 1) / C::TILE_M) * ((N + C::OUT_COLS - 1) / C::OUT_COLS);
+        const int64_t kbs = (K + C::BK - 1) / C::BK;
+        if (want >= 2 && want <= 8 && tiles * want <= h->sm_count && kbs >= want) csplit = want;
+    }
+    const int rep_plain = kEpi != 0 ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
+    const int rep = csplit ? 0 : rep_plain;
     const uint32_t a_rows =
         ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
@@ -353,6 +365,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
     p.rep = rep;
+    p.csplit = csplit;
 
     static bool attr_set = false;  // one per template instance
     if (!attr_set) {
@@ -361,6 +374,30 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
                     "cudaFuncSetAttribute(smem)");
         attr_set = true;
+    }
+    if (csplit) {
+        // the whole grid must be co-resident (fused RMS grid barrier); clusters are placed
+        // inside one GPC, so S-CTA clusters may not all fit (S = 8 over 16 tiles did not)
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(static_cast<unsigned>(p.num_tiles * csplit), 1, 1);
+        qc.blockDim = dim3(C::NUM_THREADS, 1, 1);
+        qc.dynamicSmemBytes = C::SMEM_BYTES;
+        cudaLaunchAttribute qa;
+        qa.id = cudaLaunchAttributeClusterDimension;
+        qa.val.clusterDim.x = static_cast<unsigned>(csplit);
+        qa.val.clusterDim.y = 1;
+        qa.val.clusterDim.z = 1;
+        qc.attrs = &qa;
+        qc.numAttrs = 1;
+        int max_active = 0;
+        if (cudaOccupancyMaxActiveClusters(&max_active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, &qc) !=
+                cudaSuccess ||
+            max_active < p.num_tiles) {
+            (void)cudaGetLastError();
+            csplit = 0;
+            p.csplit = 0;
+            p.rep = rep_plain;
+        }
     }
     const int max_clusters = h->sm_count / kCtaGroup;
     // Persistent schedule (DESIGN.md §6 "Stream-K"): whole tiles round-robin
@@ -373,8 +410,9 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // Stream-K only where plan_config's cost model says the balanced tail is
     // worth the partial fixup (e.g. 7B prefill: 9.3 waves; not decode, where
     // whole tiles already saturate HBM).
-    const bool sk_ok = h->schedule == CUASM_SCHEDULE_STREAM_K_ALL || h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL ||
-                       (h->schedule == CUASM_SCHEDULE_AUTO && h->plan_sk);
+    const bool sk_ok = !csplit && (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
+                                   h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL ||
+                                   (h->schedule == CUASM_SCHEDULE_AUTO && h->plan_sk));
     if (sk_ok && p.num_k_blk > 1) {
         if (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL) sk_tiles = p.num_tiles;
         else if (rem != 0 && h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL) sk_tiles = waves == 0 ? p.num_tiles : rem;
@@ -424,19 +462,19 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.trace = nullptr;
     if (h->trace) {
         p.trace = h->trace_buf;
-        h->trace_ctas = clusters * kCtaGroup;
+        h->trace_ctas = clusters * (csplit ? csplit : kCtaGroup);
     }
 
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(clusters * kCtaGroup), 1, 1);
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * (csplit ? csplit : kCtaGroup)), 1, 1);
     cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
     int na = 0;
-    if (kCtaGroup == 2) {
+    if (kCtaGroup == 2 || csplit) {
         attrs[na].id = cudaLaunchAttributeClusterDimension;
-        attrs[na].val.clusterDim.x = 2;
+        attrs[na].val.clusterDim.x = csplit ? csplit : 2;
         attrs[na].val.clusterDim.y = 1;
         attrs[na].val.clusterDim.z = 1;
         ++na;
@@ -469,6 +507,7 @@ struct Plan {
     int variant;
     bool stream_k;
     int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
+    int csplit;  // cluster split-K: CTAs per tile (1-SM variant), 0 = none
 };
 
 Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,
@@ -487,11 +526,19 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
     // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
+    // Decode shards (M <= 32, <= kFewTiles tiles): split each tile's k-loop over a cluster
+    // of kDecodeCsplit CTAs and reduce the partials through distributed shared memory
+    // (dual_gemm.cuh split_k_reduce) -- no global partials, no flags, no second wave:
+    // 16 x 4096 x 1376: 20.5 vs 22.5 us (stream-K split 3 ways), 16 x 4096 x 2752: 23.1 vs
+    // 25.4, 16 x 8192 x 3584: 34.5 vs 36.9 (scripts/tune_csplit.py, profiles/r01/tune_csplit.log);
+    // at M >= 64 the reduction's smem traffic costs more than it saves
+    if (out_cols == 128 && KB >= 48 && M <= 32 && tiles_1sm <= kFewTiles && tiles_1sm * kDecodeCsplit <= sm_count)
+        return Plan{CUASM_VARIANT_1SM, false, 256, kDecodeCsplit};
     // (k-loops of >= 48 k-blocks: a split must save more MMA time than its partial fixup costs;
     // the paper's fused_ff shape 512 x 2048 x 512 split three ways finished its tail 5 us late)
     if (out_cols == 128 && KB >= 48 &&
         ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
-        return Plan{CUASM_VARIANT_1SM, true, 256};
+        return Plan{CUASM_VARIANT_1SM, true, 256, 0};
     // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
     // 512 x 2048 x 512): latency-bound, and the 1-SM variant skips the cluster launch,
     // cluster barriers and 2-SM TMEM allocation -- 16.4 vs 18.3 us (GEMM mode, 128-wide
@@ -500,8 +547,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // tile, whereas a SwiGLU 1-SM tile pays the 16% smem penalty -- 2048 x 2048 x 512 FFN:
     // 1-SM 23.8 vs 2-SM 23.0 us)
     if (KB <= 32 && out_cols != 128 && ((M + 127) / 128) * ((N + 127) / 128) <= sm_count)
-        return Plan{CUASM_VARIANT_1SM, false, 128};
-    Plan best{CUASM_VARIANT_2SM, false, 256};
+        return Plan{CUASM_VARIANT_1SM, false, 128, 0};
+    Plan best{CUASM_VARIANT_2SM, false, 256, 0};
     double best_t = 1e30;
     // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM
     // mode may also use 128 (128 outputs, half the k-block time per tile)
@@ -542,8 +589,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             const int v = cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM;
             // ties go to the earlier candidate: N=256 before 128, 2-SM before 1-SM,
             // whole tiles before stream-K
-            if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{v, false, tn}; }
-            if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn}; }
+            if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{v, false, tn, 0}; }
+            if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn, 0}; }
         }
     }
     return best;
@@ -613,6 +660,7 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     const Plan plan = plan_config(h, M, K, N, kepi == 0 ? 128 : 256);
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
+    h->plan_csplit = v == plan.variant ? plan.csplit : 0;
     if (kepi == 0) st = dispatch_gemm<0, 256>(h, e, v, x, out, M, K, N, eps, s);
     else if (plan.tile_n == 128) st = dispatch_gemm<1, 128>(h, e, v, x, out, M, K, N, eps, s);
     else st = dispatch_gemm<1, 256>(h, e, v, x, out, M, K, N, eps, s);
@@ -688,7 +736,7 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
         return CUASM_ERR_INVALID_ARG;
     const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
     *variant = pl.variant;
-    *stream_k = pl.stream_k ? (pl.tile_n == 128 ? 3 : 1) : (pl.tile_n == 128 ? 2 : 0);
+    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.csplit << 4);
     return CUASM_OK;
 }
 
@@ -990,6 +1038,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         if (value < 0 || value > 15 || (value & 3) == 3 || ((value >> 2) & 3) == 3)
             return fail(h, CUASM_ERR_INVALID_ARG, "L2_POLICY: 2-bit codes 0..2 for x (bits 0-1) and W13 (bits 2-3)");
         h->l2pol = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_CSPLIT:
+        if (value < 0 || value > 8) return fail(h, CUASM_ERR_INVALID_ARG, "CSPLIT is 0 (auto), 1 (off) or 2..8");
+        h->csplit_opt = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_SK_SPLIT:
         if (value != 0 && (value < 2 || value > 16)) return fail(h, CUASM_ERR_INVALID_ARG, "SK_SPLIT is 0 or 2..16");

@@ -71,6 +71,9 @@ struct FfnGemmParams {
     int a_box_bytes; // bytes of one x TMA box (rows actually loaded x 128 B; < BM rows when M < BM)
     int tma_store;   // 1: bf16 output tiles leave through TMA stores (omaps.m[0..num_dst), one per
                      // destination); 0: 16-byte st.global (fp32 handles, multicast destinations)
+    int csplit;      // 1-SM only: S > 0 = cluster split-K: a cluster of S CTAs owns one
+                     // tile, CTA rank j computes k-blocks [j*KB/S, (j+1)*KB/S) and the S partial
+                     // accumulators are reduced through distributed shared memory; 0 = off
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
     int rep;         // 4 (SwiGLU, M <= 32) / 2 (M <= 64) / 0; 2-SM: the leader CTA.  The x rows are
                      // loaded rep times into the A tile (at smem rows q*128/rep), so every TMEM
@@ -122,21 +125,24 @@ __device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
 // the last can end mid-tile while starting at k-block 0 (the "finisher": it
 // adds the later clusters' partials and runs the epilogue).
 struct Sched {
-    int next_dp, C, KB, T_dp;
+    int next_dp, C, KB, T_dp, kb_lo, kb_hi;
     int64_t cur, end;
-    __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster) {
+    __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster, int part = 0) {
         next_dp = cluster;
         C = p.num_clusters;
         KB = p.num_k_blk;
         T_dp = p.num_dp_tiles;
         cur = sk_begin(p, cluster);
         end = sk_begin(p, cluster + 1);
+        // cluster split-K: this CTA's share of every tile's k-blocks
+        kb_lo = p.csplit ? part * KB / p.csplit : 0;
+        kb_hi = p.csplit ? (part + 1) * KB / p.csplit : KB;
     }
     __device__ __forceinline__ bool next(Seg& s) {
         if (next_dp < T_dp) {
             s.tile = next_dp;
-            s.kb0 = 0;
-            s.kb1 = KB;
+            s.kb0 = kb_lo;
+            s.kb1 = kb_hi;
             next_dp += C;
             return true;
         }
@@ -399,6 +405,117 @@ __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint
     }
 }
 
+// Cluster split-K (csplit, 1-SM): the S CTAs of a cluster hold partial accumulators
+// of one tile over disjoint k-ranges.  (a) Every CTA copies its TMEM accumulator
+// into its own (by now idle) pipeline shared memory, [chunk][row][32 fp32] with the
+// 16-byte column groups of row r XOR-swizzled by r & 7 (conflict-free); (b) every
+// epilogue warp arrives, release.cluster, on the partial-ready barrier of every CTA
+// of the cluster; (c) after acquiring its own, (d) CTA `part` sums the S partials --
+// in rank order, so the result does not depend on arrival order -- for the output
+// column pairs p with p % S == part, reading the other CTAs' shared memory directly
+// (ld.shared::cluster), applies the epilogue and stores.  The 256 epilogue threads
+// take (row, column group): 4 threads x 8 columns per row for tiles with <= 64 valid
+// rows, else 2 x 16; only TMEM quadrants holding valid rows are copied out.
+template <class C, int kKind, int kEpi>
+__device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t tmem_base, int acc, uint8_t* smem,
+                                               uint64_t* xbar, uint32_t part, int mb, int nb, uint32_t quad, int half,
+                                               uint32_t ewarp, uint32_t lane, int it) {
+    const uint32_t buf = ptx::smem_u32(smem);
+    const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
+    const uint32_t r_own = quad * 32 + lane;
+    const int row0 = mb * C::TILE_M;
+    const int rows = min(C::BM, p.M - row0);  // valid rows of the tile
+    // only TMEM lane quadrants holding valid rows are copied out
+#pragma unroll 1
+    for (int i = 0; i < C::PAIRS && static_cast<int>(quad * 32) < rows; ++i) {
+        const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+        uint32_t v1[32], v3[32];
+        ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
+        ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t off = ((q ^ (r_own & 7)) << 4);
+            *reinterpret_cast<uint4*>(smem + (static_cast<uint32_t>(ca) * C::BM + r_own) * 128 + off) =
+                make_uint4(v1[4 * q], v1[4 * q + 1], v1[4 * q + 2], v1[4 * q + 3]);
+            *reinterpret_cast<uint4*>(smem + (static_cast<uint32_t>(cb) * C::BM + r_own) * 128 + off) =
+                make_uint4(v3[4 * q], v3[4 * q + 1], v3[4 * q + 2], v3[4 * q + 3]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int j = 0; j < p.csplit; ++j) ptx::mbar_arrive_cluster(ptx::smem_u32(xbar), static_cast<uint32_t>(j));
+    ptx::mbar_wait_acq_cluster(ptx::smem_u32(xbar), static_cast<uint32_t>(it & 1));
+
+    // threads -> (row, column group): with <= 64 valid rows four threads share a row
+    // (8 columns each), else two (16 columns each), so small-M tiles still use all warps
+    const int tid = static_cast<int>(ewarp * 32 + lane);
+    const int rows_pad = rows <= 64 ? 64 : 128;
+    const int cpt = rows <= 64 ? 8 : 16;  // columns per thread per pair
+    const int row = tid % rows_pad, sub = tid / rows_pad;
+    const int grow = row0 + row;
+    if (row >= rows) return;
+    const float rr = p.use_r ? __ldcg(p.r + grow) : 1.f;
+    const GateRow gr = gate_row(rr);
+    constexpr int NPAIR = C::UMMA_N / 64;  // SwiGLU: (h1 chunk q, h3 chunk q + BN/32); GEMM: chunks (2q, 2q + 1)
+    constexpr int kEs = kKind == 0 ? 2 : 4;
+    const int64_t rbase = static_cast<int64_t>(grow) * p.ldo;
+#pragma unroll 1
+    for (int pr = static_cast<int>(part); pr < NPAIR; pr += p.csplit) {
+        const int ca = kEpi == 0 ? pr : 2 * pr, cb = kEpi == 0 ? pr + C::BN / 32 : 2 * pr + 1;
+        float a[16], b[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a[k] = b[k] = 0.f;
+        const int nq = cpt / 4;  // float4 groups per thread (2 or 4)
+#pragma unroll 1
+        for (int j = 0; j < p.csplit; ++j) {  // rank order
+            const uint32_t rb = ptx::mapa(buf, static_cast<uint32_t>(j));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (q >= nq) break;
+                const uint32_t off = (((sub * nq + q) ^ (row & 7)) << 4);
+                const float4 x = ptx::ld_dsmem_v4(rb + (static_cast<uint32_t>(ca) * C::BM + row) * 128 + off);
+                const float4 y = ptx::ld_dsmem_v4(rb + (static_cast<uint32_t>(cb) * C::BM + row) * 128 + off);
+                a[4 * q] += x.x; a[4 * q + 1] += x.y; a[4 * q + 2] += x.z; a[4 * q + 3] += x.w;
+                b[4 * q] += y.x; b[4 * q + 1] += y.y; b[4 * q + 2] += y.z; b[4 * q + 3] += y.w;
+            }
+        }
+        // store cpt (8 or 16) outputs at column c0 of this row: 16-byte groups, columns >= N dropped
+        auto put16 = [&](int c0, const float (&o)[16]) {
+            if constexpr (kKind == 0) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+                    if (8 * g < cpt && c0 + 8 * g < p.N)
+                        store16<kKind>(p, (rbase + c0 + 8 * g) * kEs,
+                                       make_uint4(ptx::pack_bf16x2(o[8 * g], o[8 * g + 1]),
+                                                  ptx::pack_bf16x2(o[8 * g + 2], o[8 * g + 3]),
+                                                  ptx::pack_bf16x2(o[8 * g + 4], o[8 * g + 5]),
+                                                  ptx::pack_bf16x2(o[8 * g + 6], o[8 * g + 7])));
+            } else {
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    if (4 * g < cpt && c0 + 4 * g < p.N)
+                        store16<kKind>(p, (rbase + c0 + 4 * g) * kEs,
+                                       make_uint4(__float_as_uint(o[4 * g]), __float_as_uint(o[4 * g + 1]),
+                                                  __float_as_uint(o[4 * g + 2]), __float_as_uint(o[4 * g + 3])));
+            }
+        };
+        float o[16];
+        if constexpr (kEpi == 0) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = silu_gate(a[k], b[k], gr);
+            put16(nb * C::OUT_COLS + ca * 32 + sub * cpt, o);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = apply_act(rr * a[k], p.act, p.alpha);
+            put16(nb * C::OUT_COLS + ca * 32 + sub * cpt, o);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = apply_act(rr * b[k], p.act, p.alpha);
+            put16(nb * C::OUT_COLS + cb * 32 + sub * cpt, o);
+        }
+    }
+}
+
 template <int kKind, int kCtaGroup, int kEpi, int kN>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
@@ -416,11 +533,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     uint64_t* tfull_bar = bars + 2 * C::STAGES;      // [2]
     uint64_t* tempty_bar = bars + 2 * C::STAGES + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+    uint64_t* xbar = bars + 2 * C::STAGES + 6;        // cluster split-K: partials of all S CTAs in smem
 
     const uint32_t warp = ptx::warp_id_uniform();
     const uint32_t lane = ptx::lane_id();
     const uint32_t cta_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;
     const bool leader = cta_rank == 0;
+    const bool csplit = kCtaGroup == 1 && p.csplit > 0;
+    const uint32_t part = csplit ? ptx::cluster_ctarank() : 0;  // split-K share of the cluster's tile
 
     if (warp == 0 && lane == 0) {
         trace_stamp(p, 0);
@@ -437,16 +557,20 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // every epilogue warp of BOTH CTAs releases the leader's accumulator
             ptx::mbar_init(ptx::smem_u32(&tempty_bar[a]), C::NUM_EPI_WARPS * kCtaGroup);
         }
+        // every epilogue warp of every CTA of a split-K cluster arrives once per tile
+        if (csplit) ptx::mbar_init(ptx::smem_u32(xbar), C::NUM_EPI_WARPS * p.csplit);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS, kCtaGroup>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
-    if constexpr (kCtaGroup == 2) ptx::cluster_sync(); else __syncthreads();
+    // (split-K clusters: remote arrivals on xbar need every CTA's barriers initialised)
+    if (kCtaGroup == 2 || csplit) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // Cluster-level work: both CTAs of a pair walk the same segment sequence.
-    const int cluster_id = blockIdx.x / kCtaGroup;
+    // Cluster-level work: both CTAs of a pair (every CTA of a split-K cluster) walk
+    // the same tile sequence.
+    const int cluster_id = csplit ? static_cast<int>(blockIdx.x) / p.csplit : static_cast<int>(blockIdx.x) / kCtaGroup;
 
     if (warp == 0) {
         // ========================= TMA producer =========================
@@ -464,7 +588,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         uint32_t phase = 0;
         bool first_load = true;
         Sched sch;
-        sch.init(p, cluster_id);
+        sch.init(p, cluster_id, static_cast<int>(part));
         Seg sg;
         while (sch.next(sg)) {
             int mb, nb;
@@ -525,7 +649,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const uint64_t adesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a));
             const uint64_t bdesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b));
             Sched sch;
-            sch.init(p, cluster_id);
+            sch.init(p, cluster_id, static_cast<int>(part));
             Seg sg;
             for (; sch.next(sg); ++it) {
                 const int acc = it & 1;
@@ -615,7 +739,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         int it = 0;
         int nst = 0;  // TMA-store boxes this warp has issued (staging box = nst & 1)
         Sched sch;
-        sch.init(p, cluster_id);
+        sch.init(p, cluster_id, static_cast<int>(part));
         Seg sg;
         for (; sch.next(sg); ++it) {
             int mb, nb;
@@ -627,8 +751,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
                             static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 + lane : row_in_cta);
             const bool row_ok = row < p.M;
-            const bool contributor = sg.kb0 > 0;                       // stream-K: partial, not the tile's start
-            const bool finisher = sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
+            const bool contributor = !csplit && sg.kb0 > 0;                       // stream-K: partial, not the tile's start
+            const bool finisher = !csplit && sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
             // this CTA's 128 x 2BN fp32 partial slot, lane-contiguous so every warp
             // access is 512 contiguous bytes: float4 index ((chunk*4 + quad)*8 + q)*32 + lane
             // holds columns chunk*32 + 4q..+3 of row quad*32 + lane (chunk < BN/32: h1, else h3)
@@ -679,6 +803,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             if (warp == 2 && lane == 0) {
                 trace_stamp(p, 7);  // (last write wins: the final tile)
                 if (it == 0) trace_stamp(p, 8);
+            }
+            if (csplit) {
+                // cluster split-K: partials through distributed shared memory, this CTA
+                // reduces and stores its share of the tile's output columns
+                split_k_reduce<C, kKind, kEpi>(p, tmem_base, acc, smem, xbar, part, mb, nb, quad, half, ewarp, lane,
+                                               it);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
+                continue;
             }
             for (int cc = c_first; cc <= c_last; ++cc) {
                 if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;  // empty range: not a contributor
@@ -814,7 +948,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     if (warp >= 2 && lane == 0 && p.trace) atomicMax(p.trace + blockIdx.x * kTraceSlots + 5, globaltimer());
     // ----------------------------------------------------------- teardown --
     ptx::tc_fence_before();
-    if constexpr (kCtaGroup == 2) ptx::cluster_sync(); else __syncthreads();
+    // (split-K clusters: no CTA may retire while another still reads its shared memory)
+    if (kCtaGroup == 2 || csplit) ptx::cluster_sync(); else __syncthreads();
     if (p.fused_norm && threadIdx.x == 0) {
         // the last CTA out resets the grid counters for the next launch (graph-safe)
         if (atomicAdd(p.sync + 1, 1u) == gridDim.x - 1) {

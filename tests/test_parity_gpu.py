@@ -566,3 +566,42 @@ def test_option_values_are_validated(cuda_device):
     d = make_inputs(M, K, N, family="C", seed=3500, dtype="bf16")
     out, _ = run_gpu(d, 1e-6, "bf16", handle=h, schedule=ffn.SCHEDULE_STREAM_K_TAIL)
     check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), "options")
+
+
+# ------------------------------------------ cluster split-K (CUASM_OPT_CSPLIT) ---
+@pytest.mark.parametrize("M,K,N,S", [(16, 4096, 1376, 4), (512, 2048, 512, 4), (512, 2048, 512, 8),
+                                     (128, 2048, 2048, 2), (300, 512, 520, 3), (48, 1024, 264, 5)])
+def test_cluster_split_k_ffn(cuda_device, M, K, N, S):
+    """1-SM tiles split over S-CTA clusters, partials reduced through distributed
+    shared memory in rank order: oracle tolerance and bitwise run-to-run."""
+    d = make_inputs(M, K, N, family="C", seed=8100 + M + S, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_option(ffn.OPT_CSPLIT, S)
+    out, _ = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_1SM, handle=h, schedule=ffn.SCHEDULE_DATA_PARALLEL)
+    again, _ = run_gpu(d, 1e-6, "bf16", ffn.VARIANT_1SM, handle=h, schedule=ffn.SCHEDULE_DATA_PARALLEL)
+    assert torch.equal(out, again)
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 32)))))
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(out[rows], ref, f"csplit {S} {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("M,K,N,S", [(512, 2048, 512, 4), (200, 1024, 392, 2)])
+def test_cluster_split_k_gemm(cuda_device, M, K, N, S):
+    d = make_inputs(M, K, N, family="C", seed=8200 + M, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_variant(ffn.VARIANT_1SM)
+    h.set_option(ffn.OPT_CSPLIT, S)
+    for tn in (128, 256):
+        h.set_option(ffn.OPT_TILE_N, tn)
+        out = h.gemm_act(t["x"], t["w1"], "leaky_relu", 0.01)
+        torch.cuda.synchronize()
+        check(out, oracle.gemm_act(d["x"], d["w1"], "leaky_relu", 0.01), f"csplit gemm {S} n{tn} {M}x{K}x{N}")
+
+
+def test_cluster_split_k_fp32(cuda_device):
+    d = make_inputs(16, 64, 128, family="T", seed=8300, dtype="fp32")
+    h = ffn.FusedFFN(cuda_device, torch.float32)
+    h.set_option(ffn.OPT_CSPLIT, 2)
+    out, _ = run_gpu(d, 1e-6, "fp32", ffn.VARIANT_1SM, handle=h, schedule=ffn.SCHEDULE_DATA_PARALLEL)
+    check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6), "csplit fp32")

@@ -120,11 +120,13 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     KB = -(-K // BK)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
+    if out_cols == 128 and KB >= 48 and M <= 32 and t1 <= 32 and 4 * t1 <= sm_count:
+        return ("1sm", False, 256, 4)   # decode shards: cluster split-K 4 ways (csrc kDecodeCsplit)
     if out_cols == 128 and KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
-        return ("1sm", True, 256)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
+        return ("1sm", True, 256, 0)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
     if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
-        return ("1sm", False, 128)
-    best, best_t = ("2sm", False, 256), 1e30
+        return ("1sm", False, 128, 0)
+    best, best_t = ("2sm", False, 256, 0), 1e30
     for tn in ((256,) if out_cols == 128 else (256, 128)):
         oc = 128 if out_cols == 128 else tn
         nblk = -(-N // oc)
@@ -144,9 +146,9 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
             t_sk = max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup)
             name = "2sm" if cg == 2 else "1sm"
             if t_dp < best_t * 0.999:
-                best_t, best = t_dp, (name, False, tn)
+                best_t, best = t_dp, (name, False, tn, 0)
             if K // BK > 1 and t_sk < best_t * 0.98:
-                best_t, best = t_sk, (name, True, tn)
+                best_t, best = t_sk, (name, True, tn, 0)
     return best
 
 
@@ -181,7 +183,7 @@ def test_plan_70b_shard_uses_stream_k():
 def test_plan_w2_down_projection_avoids_l2_thrashing_stream_k():
     # hidden [2048, 11008] x W2 [4096, 11008]: whole tiles 128 us vs stream-K 158 us measured
     # (256-wide stream-K would thrash L2: 128 us whole tiles vs 158 us measured)
-    assert plan_config(2048, 11008, 4096, out_cols=256) != ("2sm", True, 256)
+    assert plan_config(2048, 11008, 4096, out_cols=256)[:3] != ("2sm", True, 256)
 
 
 # ---- the library's own implementation agrees with the model above -------------------
@@ -199,7 +201,7 @@ def test_library_plan_matches_measured_best(lib_plan, M):
 
 
 @pytest.mark.parametrize("M,K,N,op", [(m, k, n, op) for m in (1, 16, 200, 512, 1000, 2048, 4096, 16384)
-                                      for k, n in ((4096, 11008), (8192, 3584), (11008, 4096), (2048, 512))
+                                      for k, n in ((4096, 11008), (8192, 3584), (11008, 4096), (2048, 512), (4096, 1376))
                                       for op in ("ffn", "gemm")])
 def test_library_plan_equals_python_mirror(lib_plan, M, K, N, op):
     assert lib_plan(M, K, N, op) == plan_config(M, K, N, out_cols=128 if op == "ffn" else 256)
@@ -227,9 +229,18 @@ GEMM_MEASURED = {
 @pytest.mark.parametrize("shape", sorted(GEMM_MEASURED))
 def test_library_gemm_plan_matches_measured_best(lib_plan, shape):
     M, K, N = shape
-    assert lib_plan(M, K, N, "gemm") in GEMM_MEASURED[shape]
+    assert lib_plan(M, K, N, "gemm")[:3] in GEMM_MEASURED[shape]
 
 
 def test_library_plan_w2_and_70b(lib_plan):
-    assert lib_plan(2048, 11008, 4096, "gemm") != ("2sm", True, 256)
+    assert lib_plan(2048, 11008, 4096, "gemm")[:3] != ("2sm", True, 256)
     assert lib_plan(4096, 8192, 3584)[:2] == ("2sm", True)
+
+
+# measured (profiles/r01/tune_csplit.log): cluster split-K 4 ways wins at M = 16 on
+# few-tile shards and loses at M >= 64 (the DSMEM reduction outweighs the shorter k-loop)
+@pytest.mark.parametrize("M,K,N,cs", [(16, 4096, 1376, 4), (16, 4096, 2752, 4), (16, 8192, 3584, 4),
+                                      (64, 4096, 1376, 0), (128, 4096, 1376, 0), (16, 4096, 11008, 0)])
+def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs):
+    assert plan_config(M, K, N)[3] == cs
+    assert lib_plan(M, K, N)[3] == cs
