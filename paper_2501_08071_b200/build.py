@@ -43,7 +43,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "cuasm_ffn.cu")]
+    # CUASM_NVCC_EXTRA: experiment-only defines (e.g. -DCUASM_DIAG=1); never set for a product build
+    extra = os.environ.get("CUASM_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", tmp, os.path.join(CSRC, "cuasm_ffn.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

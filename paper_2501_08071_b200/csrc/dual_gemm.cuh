@@ -416,10 +416,12 @@ __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint
 // (ld.shared::cluster), applies the epilogue and stores.  The 256 epilogue threads
 // take (row, column group): 4 threads x 8 columns per row for tiles with <= 64 valid
 // rows, else 2 x 16; only TMEM quadrants holding valid rows are copied out.
+constexpr int kMaxCsplit = 8;  // CTAs per split-K cluster (portable cluster size)
+
 template <class C, int kKind, int kEpi>
 __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t tmem_base, int acc, uint8_t* smem,
                                                uint64_t* xbar, uint32_t part, int mb, int nb, uint32_t quad, int half,
-                                               uint32_t ewarp, uint32_t lane, int it) {
+                                               uint32_t ewarp, uint32_t lane, int it, bool& cl_pending) {
     const uint32_t buf = ptx::smem_u32(smem);
     const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
     const uint32_t r_own = quad * 32 + lane;
@@ -443,9 +445,15 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
         }
     }
     __syncwarp();
+    if (cl_pending) {  // the prologue's cluster barrier: every CTA's xbar is initialised
+        ptx::cluster_wait_acquire();
+        cl_pending = false;
+    }
     if (lane == 0)
         for (int j = 0; j < p.csplit; ++j) ptx::mbar_arrive_cluster(ptx::smem_u32(xbar), static_cast<uint32_t>(j));
+    if (ewarp == 0 && lane == 0) trace_stamp(p, 9);   // own partial published
     ptx::mbar_wait_acq_cluster(ptx::smem_u32(xbar), static_cast<uint32_t>(it & 1));
+    if (ewarp == 0 && lane == 0) trace_stamp(p, 10);  // all partials visible
 
     // threads -> (row, column group): with <= 64 valid rows four threads share a row
     // (8 columns each), else two (16 columns each), so small-M tiles still use all warps
@@ -467,17 +475,28 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
 #pragma unroll
         for (int k = 0; k < 16; ++k) a[k] = b[k] = 0.f;
         const int nq = cpt / 4;  // float4 groups per thread (2 or 4)
-#pragma unroll 1
-        for (int j = 0; j < p.csplit; ++j) {  // rank order
-            const uint32_t rb = ptx::mapa(buf, static_cast<uint32_t>(j));
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (q >= nq) break;
-                const uint32_t off = (((sub * nq + q) ^ (row & 7)) << 4);
-                const float4 x = ptx::ld_dsmem_v4(rb + (static_cast<uint32_t>(ca) * C::BM + row) * 128 + off);
-                const float4 y = ptx::ld_dsmem_v4(rb + (static_cast<uint32_t>(cb) * C::BM + row) * 128 + off);
-                a[4 * q] += x.x; a[4 * q + 1] += x.y; a[4 * q + 2] += x.z; a[4 * q + 3] += x.w;
-                b[4 * q] += y.x; b[4 * q + 1] += y.y; b[4 * q + 2] += y.z; b[4 * q + 3] += y.w;
+        for (int q = 0; q < 4; ++q) {
+            if (q >= nq) break;
+            const uint32_t off = (((sub * nq + q) ^ (row & 7)) << 4);
+            const uint32_t oa = buf + (static_cast<uint32_t>(ca) * C::BM + row) * 128 + off;
+            const uint32_t ob = buf + (static_cast<uint32_t>(cb) * C::BM + row) * 128 + off;
+            // four ranks' loads in flight before the first add; the adds stay in rank order
+#pragma unroll 1
+            for (int j0 = 0; j0 < p.csplit; j0 += 4) {
+                float4 xs[4], ys[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j0 + j < p.csplit) {
+                        xs[j] = ptx::ld_dsmem_v4(ptx::mapa(oa, static_cast<uint32_t>(j0 + j)));
+                        ys[j] = ptx::ld_dsmem_v4(ptx::mapa(ob, static_cast<uint32_t>(j0 + j)));
+                    }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j0 + j < p.csplit) {
+                        a[4 * q] += xs[j].x; a[4 * q + 1] += xs[j].y; a[4 * q + 2] += xs[j].z; a[4 * q + 3] += xs[j].w;
+                        b[4 * q] += ys[j].x; b[4 * q + 1] += ys[j].y; b[4 * q + 2] += ys[j].z; b[4 * q + 3] += ys[j].w;
+                    }
             }
         }
         // store cpt (8 or 16) outputs at column c0 of this row: 16-byte groups, columns >= N dropped
@@ -514,6 +533,165 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
             put16(nb * C::OUT_COLS + cb * 32 + sub * cpt, o);
         }
     }
+    if (ewarp == 0 && lane == 0) trace_stamp(p, 11);  // this CTA's share stored
+}
+
+// Cluster split-K, push form (bf16 output, tiles with <= 32 valid rows, whose
+// partials fit the TMA-store staging area this mode leaves unused).  Column pair
+// p (32 columns of chunk a + 32 of chunk b) belongs to CTA p % S.  (a) The warp of
+// TMEM quadrant 0 holding pair p reads it (lane = row) and writes it into slot
+// [p / S][its rank] of the owner's staging area: plain shared-memory stores for its
+// own pairs, st.async with a transaction-count credit on the owner's barrier for
+// the others -- no copy, flag or remote read on the way; (b) the owner waits for
+// the bytes (it armed the barrier with their count), sums the S slots in rank
+// order (result independent of arrival order), applies the epilogue and stores.
+// Slot rows are 256 bytes, 16-byte groups XOR-swizzled by row & 7.
+template <class C, int kKind>
+__device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
+    if (kKind != 0 || rows > 32) return false;
+    constexpr int NPAIR = C::UMMA_N / 64;
+    return ((NPAIR + S - 1) / S) * S * (rows <= 16 ? 16 : 32) * 256 <= C::STG_BYTES;
+}
+
+#if CUASM_DIAG
+__device__ __forceinline__ bool i_own_first_pair(int half, uint32_t part, int S) {
+    return half == static_cast<int>(part % S) / 2;  // (NPAIR 4, PAIRS 2: the warp holding pair `part`)
+}
+#endif
+
+// The owner's reduction of one column pair for this lane's row (split_k_push (b)):
+// sum the S slots in rank order, apply the epilogue, store columns < n_lim.  A
+// loop over 8-column groups, not unrolled over the 32 columns: this code runs once
+// per launch, fetched cold (the measurement's L2 flush evicts code too), so its
+// size, not its instruction count, sets its time (~10 SM cycles per instruction).
+template <class C, int kKind, int kEpi>
+__device__ __forceinline__ void push_reduce_pair(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
+                                              uint32_t swz, const GateRow& gr, float rr, int64_t rbase, int col_a,
+                                              int col_b, int n_lim) {
+    constexpr int kEs = kKind == 0 ? 2 : 4;
+    // the store's kernel parameters, read in the dry pass too (constant-cache lines warm)
+    char* const dst0 = static_cast<char*>(p.dst[0]);
+    const bool plain = p.num_dst == 1 && !p.dst_mc;
+#pragma unroll 1
+    for (int g8 = 0; g8 < 4; ++g8) {
+        float a[8], b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = b[k] = 0.f;
+#pragma unroll 1
+        for (int j = 0; j < S; ++j) {  // rank order
+            const uint8_t* src = slot0 + static_cast<uint32_t>(j * rc) * 256;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 x = *reinterpret_cast<const float4*>(src + (((2 * g8 + h) ^ swz) << 4));
+                const float4 y = *reinterpret_cast<const float4*>(src + (((8 + 2 * g8 + h) ^ swz) << 4));
+                a[4 * h] += x.x; a[4 * h + 1] += x.y; a[4 * h + 2] += x.z; a[4 * h + 3] += x.w;
+                b[4 * h] += y.x; b[4 * h + 1] += y.y; b[4 * h + 2] += y.z; b[4 * h + 3] += y.w;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < (kEpi == 0 ? 1 : 2); ++h) {
+            const int c0 = (h == 0 ? col_a : col_b) + 8 * g8;
+            float o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                o[k] = kEpi == 0 ? silu_gate(a[k], b[k], gr) : apply_act(rr * (h == 0 ? a[k] : b[k]), p.act, p.alpha);
+            const uint4 v = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
+                                       ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
+            if (c0 < n_lim) {
+                if (plain) *reinterpret_cast<uint4*>(dst0 + (rbase + c0) * kEs) = v;
+                else store16<kKind>(p, (rbase + c0) * kEs, v);
+            }
+        }
+    }
+}
+
+template <class C, int kKind, int kEpi>
+__device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tmem_base, int acc, uint8_t* stg,
+                                             uint64_t* rbar, uint32_t part, int mb, int nb, uint32_t quad, int half,
+                                             uint32_t ewarp, uint32_t lane, bool& cl_pending, bool dry) {
+    constexpr int NPAIR = C::UMMA_N / 64;
+    const int S = p.csplit;
+    const int row0 = mb * C::TILE_M;
+    const int rows = min(C::BM, p.M - row0);
+    const int rc = rows <= 16 ? 16 : 32;  // slot rows
+    const uint32_t stg_u = ptx::smem_u32(stg), rbar_u = ptx::smem_u32(rbar);
+    if (!dry && ewarp == 0 && lane == 0 && static_cast<int>(part) < NPAIR) {
+        const int owned = (NPAIR - 1 - static_cast<int>(part)) / S + 1;
+        ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 256));
+    }
+    if (quad != 0) return;  // every valid row lives in TMEM lane quadrant 0
+    const bool row_ok = static_cast<int>(lane) < rows;
+    const int grow = row0 + static_cast<int>(lane);
+    const float rr = row_ok && p.use_r ? __ldcg(p.r + grow) : 1.f;
+#if CUASM_DIAG  // experiments only: SM-cycle stamps of the phases into trace slots 12..15
+    const long long dclk0 = clock64();
+    const bool dbg = p.trace && lane == 0 && i_own_first_pair(half, part, S);
+#define CUASM_DIAG_STAMP(slot) \
+    if (dbg) p.trace[blockIdx.x * kTraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - dclk0)
+#else
+#define CUASM_DIAG_STAMP(slot)
+#endif
+    if (!dry && cl_pending) {  // the prologue's cluster barrier: every CTA's barriers are initialised
+        ptx::cluster_wait_acquire();
+        cl_pending = false;
+    }
+    const uint32_t t_row = tmem_base + acc * C::UMMA_N;
+    const uint32_t swz = lane & 7;
+    // (a) scatter this warp's pairs to their owners
+#pragma unroll 1
+    for (int i = 0; i < C::PAIRS; ++i) {
+        const int pr = half * C::PAIRS + i;
+        const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+        uint32_t v1[32], v3[32];
+        if (!dry) {
+            ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
+            ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
+            ptx::tmem_ld_wait();
+        }
+        if (!row_ok || dry) continue;
+        const uint32_t owner = static_cast<uint32_t>(pr % S);
+        const uint32_t dst = stg_u + static_cast<uint32_t>(((pr / S) * S + static_cast<int>(part)) * rc + lane) * 256;
+        if (owner == part) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                *reinterpret_cast<uint4*>(stg + (dst - stg_u) + ((g ^ swz) << 4)) =
+                    make_uint4(v1[4 * g], v1[4 * g + 1], v1[4 * g + 2], v1[4 * g + 3]);
+                *reinterpret_cast<uint4*>(stg + (dst - stg_u) + (((g + 8) ^ swz) << 4)) =
+                    make_uint4(v3[4 * g], v3[4 * g + 1], v3[4 * g + 2], v3[4 * g + 3]);
+            }
+        } else {
+            const uint32_t rdst = ptx::mapa(dst, owner), rb = ptx::mapa(rbar_u, owner);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                ptx::st_async_v4(rdst + ((g ^ swz) << 4), make_uint4(v1[4 * g], v1[4 * g + 1], v1[4 * g + 2], v1[4 * g + 3]),
+                                 rb);
+                ptx::st_async_v4(rdst + (((g + 8) ^ swz) << 4),
+                                 make_uint4(v3[4 * g], v3[4 * g + 1], v3[4 * g + 2], v3[4 * g + 3]), rb);
+            }
+        }
+    }
+    CUASM_DIAG_STAMP(12);
+    // (b) reduce the pairs this CTA owns
+    const GateRow gr = gate_row(rr);
+    const int64_t rbase = static_cast<int64_t>(grow) * p.ldo;
+    bool waited = false;
+#pragma unroll 1
+    for (int i = 0; i < C::PAIRS; ++i) {
+        const int pr = half * C::PAIRS + i;
+        if (pr % S != static_cast<int>(part)) continue;
+        if (!waited && !dry) {
+            ptx::mbar_wait_acq_cluster(rbar_u, 0u);  // one tile per cluster: phase 0
+            waited = true;
+            CUASM_DIAG_STAMP(13);
+        }
+        if (!row_ok) continue;
+        const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+        const uint8_t* slot0 = stg + static_cast<uint32_t>((pr / S) * S * rc + static_cast<int>(lane)) * 256;
+        CUASM_DIAG_STAMP(14);
+        push_reduce_pair<C, kKind, kEpi>(p, slot0, S, rc, swz, gr, rr, rbase, nb * C::OUT_COLS + ca * 32,
+                                         nb * C::OUT_COLS + cb * 32, dry ? 0 : p.N);
+        CUASM_DIAG_STAMP(15);
+    }
 }
 
 template <int kKind, int kCtaGroup, int kEpi, int kN>
@@ -534,6 +712,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     uint64_t* tempty_bar = bars + 2 * C::STAGES + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
     uint64_t* xbar = bars + 2 * C::STAGES + 6;        // cluster split-K: partials of all S CTAs in smem
+    uint64_t* rbar = bars + 2 * C::STAGES + 7;        // cluster split-K, push form: partials received
 
     const uint32_t warp = ptx::warp_id_uniform();
     const uint32_t lane = ptx::lane_id();
@@ -558,13 +737,25 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             ptx::mbar_init(ptx::smem_u32(&tempty_bar[a]), C::NUM_EPI_WARPS * kCtaGroup);
         }
         // every epilogue warp of every CTA of a split-K cluster arrives once per tile
-        if (csplit) ptx::mbar_init(ptx::smem_u32(xbar), C::NUM_EPI_WARPS * p.csplit);
+        if (csplit) {
+            ptx::mbar_init(ptx::smem_u32(xbar), C::NUM_EPI_WARPS * p.csplit);
+            ptx::mbar_init(ptx::smem_u32(rbar), 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS, kCtaGroup>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
-    // (split-K clusters: remote arrivals on xbar need every CTA's barriers initialised)
-    if (kCtaGroup == 2 || csplit) ptx::cluster_sync(); else __syncthreads();
+    // (split-K clusters: remote arrivals on xbar need every CTA's barriers initialised;
+    // the wait half is deferred to the first remote arrival, after the mainloop)
+    bool cl_pending = csplit;
+    if (kCtaGroup == 2) {
+        ptx::cluster_sync();
+    } else {
+        // (the barriers' initialisation is already released to the cluster by
+        // fence.mbarrier_init: a relaxed arrive, no GPU-scope membar)
+        if (csplit) ptx::cluster_arrive_relaxed();
+        __syncthreads();
+    }
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -796,6 +987,29 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
                 r_ready = true;
             }
+            if (csplit && split_k_push_fits<C, kKind>(min(C::BM, p.M - mb * C::TILE_M), p.csplit)) {
+                // cluster split-K, push form.  Pass 0 runs the same code dry (no TMEM
+                // reads, remote writes, waits or stores) while the mainloop runs, so
+                // that pass 1, on the critical path, finds it in the instruction cache
+                // (it runs once per launch and would be fetched cold otherwise)
+#pragma unroll 1
+                for (int pass = 0; pass < 2; ++pass) {
+                    if (pass == 1) {
+                        ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
+                        ptx::tc_fence_after();
+                        if (warp == 2 && lane == 0) {
+                            trace_stamp(p, 7);
+                            if (it == 0) trace_stamp(p, 8);
+                        }
+                    }
+                    split_k_push<C, kKind, kEpi>(p, tmem_base, acc, smem_stg, rbar, part, mb, nb, quad, half, ewarp,
+                                                 lane, cl_pending, pass == 0);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
+                continue;
+            }
             const float rr = !row_ok ? 0.f : (p.use_r ? __ldcg(p.r + row) : 1.f);
             const GateRow gr = gate_row(rr);
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
@@ -808,7 +1022,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 // cluster split-K: partials through distributed shared memory, this CTA
                 // reduces and stores its share of the tile's output columns
                 split_k_reduce<C, kKind, kEpi>(p, tmem_base, acc, smem, xbar, part, mb, nb, quad, half, ewarp, lane,
-                                               it);
+                                               it, cl_pending);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
@@ -949,7 +1163,18 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     // ----------------------------------------------------------- teardown --
     ptx::tc_fence_before();
     // (split-K clusters: no CTA may retire while another still reads its shared memory)
-    if (kCtaGroup == 2 || csplit) ptx::cluster_sync(); else __syncthreads();
+    if (cl_pending) ptx::cluster_wait_acquire();  // threads that never reached a remote arrival
+    if (csplit) {
+        // lifetime only: every remote read of this CTA's shared memory has been consumed
+        // and every push into it waited for, so the arrive need not order memory (a
+        // release arrive costs a GPU-scope membar behind this CTA's output stores)
+        ptx::cluster_arrive_relaxed();
+        ptx::cluster_wait_acquire();
+    } else if (kCtaGroup == 2) {
+        ptx::cluster_sync();
+    } else {
+        __syncthreads();
+    }
     if (p.fused_norm && threadIdx.x == 0) {
         // the last CTA out resets the grid counters for the next launch (graph-safe)
         if (atomicAdd(p.sync + 1, 1u) == gridDim.x - 1) {

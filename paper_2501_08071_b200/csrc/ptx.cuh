@@ -312,6 +312,20 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// The two halves of cluster_sync, for a barrier whose wait can be deferred to the
+// first cross-CTA access (not .aligned: callers may be divergent warps).
+__device__ __forceinline__ void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+}
+// Arrive without ordering this thread's memory accesses (no GPU-scope membar): for
+// barriers that only mark CTA lifetimes, or after fence.mbarrier_init.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+}
+
 // Address of the same shared-memory location in CTA `cta` of the cluster.
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t cta) {
     uint32_t r;
@@ -326,6 +340,13 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
                  : "r"(addr)
                  : "memory");
     return v;
+}
+// Store 16 bytes into another CTA's shared memory (addresses from mapa) and credit
+// them to that CTA's mbarrier transaction count (the receiver waits on the phase).
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint4 v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(remote_addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(remote_bar)
+                 : "memory");
 }
 // Wait for a phase of this CTA's mbarrier whose arrivals come from other CTAs of the
 // cluster (acquire at cluster scope: their prior shared-memory writes are visible).

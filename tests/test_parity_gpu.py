@@ -570,10 +570,15 @@ def test_option_values_are_validated(cuda_device):
 
 # ------------------------------------------ cluster split-K (CUASM_OPT_CSPLIT) ---
 @pytest.mark.parametrize("M,K,N,S", [(16, 4096, 1376, 4), (512, 2048, 512, 4), (512, 2048, 512, 8),
-                                     (128, 2048, 2048, 2), (300, 512, 520, 3), (48, 1024, 264, 5)])
+                                     (128, 2048, 2048, 2), (300, 512, 520, 3), (48, 1024, 264, 5),
+                                     (1, 4096, 1376, 4), (24, 1024, 1000, 2), (9, 2048, 264, 8),
+                                     (16, 1024, 520, 6), (32, 2048, 600, 3), (32, 1024, 392, 4)])
 def test_cluster_split_k_ffn(cuda_device, M, K, N, S):
     """1-SM tiles split over S-CTA clusters, partials reduced through distributed
-    shared memory in rank order: oracle tolerance and bitwise run-to-run."""
+    shared memory in rank order: oracle tolerance and bitwise run-to-run.  Tiles
+    with <= 32 rows whose partials fit the staging area take the push form
+    (dual_gemm.cuh split_k_push: (1|9|16|24|32, S) here, except 32 rows x S=3),
+    the others the pull form (split_k_reduce)."""
     d = make_inputs(M, K, N, family="C", seed=8100 + M + S, dtype="bf16")
     h = ffn.FusedFFN(cuda_device, torch.bfloat16)
     h.set_option(ffn.OPT_CSPLIT, S)
@@ -585,7 +590,8 @@ def test_cluster_split_k_ffn(cuda_device, M, K, N, S):
     check(out[rows], ref, f"csplit {S} {M}x{K}x{N}")
 
 
-@pytest.mark.parametrize("M,K,N,S", [(512, 2048, 512, 4), (200, 1024, 392, 2)])
+@pytest.mark.parametrize("M,K,N,S", [(512, 2048, 512, 4), (200, 1024, 392, 2), (16, 1024, 392, 4),
+                                     (30, 2048, 1000, 2)])
 def test_cluster_split_k_gemm(cuda_device, M, K, N, S):
     d = make_inputs(M, K, N, family="C", seed=8200 + M, dtype="bf16")
     t = {k: v.to(cuda_device) for k, v in d.items()}
