@@ -267,7 +267,6 @@ struct EpiSpec {
 // each tile split this many ways (plan_config_raw, launch_gemm).
 constexpr int64_t kFewTiles = 32;
 constexpr int kFewTilesSplit = 3;
-constexpr int kDecodeCsplit = 4;  // cluster split-K width the planner uses for decode shards
 
 // Rasterisation group (m-blocks whose tiles run before the next W13 column
 // block): as many as keep the group's rows of x within ~32 MB of L2, at most
@@ -526,14 +525,20 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
     // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
-    // Decode shards (M <= 32, <= kFewTiles tiles): split each tile's k-loop over a cluster
-    // of kDecodeCsplit CTAs and reduce the partials through distributed shared memory
-    // (dual_gemm.cuh split_k_reduce) -- no global partials, no flags, no second wave:
-    // 16 x 4096 x 1376: 20.5 vs 22.5 us (stream-K split 3 ways), 16 x 4096 x 2752: 23.1 vs
-    // 25.4, 16 x 8192 x 3584: 34.5 vs 36.9 (scripts/tune_csplit.py, profiles/r01/tune_csplit.log);
-    // at M >= 64 the reduction's smem traffic costs more than it saves
-    if (out_cols == 128 && KB >= 48 && M <= 32 && tiles_1sm <= kFewTiles && tiles_1sm * kDecodeCsplit <= sm_count)
-        return Plan{CUASM_VARIANT_1SM, false, 256, kDecodeCsplit};
+    // Decode shards (M <= 32, up to 2 * kFewTiles tiles): split each tile's k-loop over a
+    // cluster of S CTAs, partials pushed into the owner CTA's shared memory (dual_gemm.cuh
+    // split_k_push) -- no global partials, no flags, no second wave.  S = 4 up to 37 tiles,
+    // 3 up to 49 (M <= 16: the 3-way slots fit the staging area), else 2 up to 64.  Kernel
+    // times under ncu (profiles/r01/csplit/): 16 x 4096 x 1376: 15.3 vs 17.5 us (stream-K
+    // split 3 ways), 16 x 4096 x 5504 (S = 3): 23.0 vs 27.1, 16 x 4096 x 6880 (S = 2): 26.5 vs
+    // 29.5, 32 x 4096 x 5504 (S = 2): 24.9 vs 27.2; at M >= 64 (pull form) it loses
+    if (out_cols == 128 && KB >= 48 && M <= 32) {
+        const int S = tiles_1sm * 4 <= sm_count && tiles_1sm <= 37   ? 4
+                      : M <= 16 && tiles_1sm * 3 <= sm_count && tiles_1sm <= 49 ? 3
+                      : tiles_1sm * 2 <= sm_count && tiles_1sm <= 2 * kFewTiles ? 2
+                                                                                : 0;
+        if (S) return Plan{CUASM_VARIANT_1SM, false, 256, S};
+    }
     // (k-loops of >= 48 k-blocks: a split must save more MMA time than its partial fixup costs;
     // the paper's fused_ff shape 512 x 2048 x 512 split three ways finished its tail 5 us late)
     if (out_cols == 128 && KB >= 48 &&

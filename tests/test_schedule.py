@@ -120,8 +120,12 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     KB = -(-K // BK)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
-    if out_cols == 128 and KB >= 48 and M <= 32 and t1 <= 32 and 4 * t1 <= sm_count:
-        return ("1sm", False, 256, 4)   # decode shards: cluster split-K 4 ways (csrc kDecodeCsplit)
+    if out_cols == 128 and KB >= 48 and M <= 32:   # decode shards: cluster split-K
+        S = (4 if 4 * t1 <= sm_count and t1 <= 37 else
+             3 if M <= 16 and 3 * t1 <= sm_count and t1 <= 49 else
+             2 if 2 * t1 <= sm_count and t1 <= 64 else 0)
+        if S:
+            return ("1sm", False, 256, S)
     if out_cols == 128 and KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
         return ("1sm", True, 256, 0)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
     if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
@@ -237,9 +241,11 @@ def test_library_plan_w2_and_70b(lib_plan):
     assert lib_plan(4096, 8192, 3584)[:2] == ("2sm", True)
 
 
-# measured (profiles/r01/tune_csplit.log): cluster split-K 4 ways wins at M = 16 on
-# few-tile shards and loses at M >= 64 (the DSMEM reduction outweighs the shorter k-loop)
+# measured (profiles/r01/csplit/ncu_ab_*.txt): the cluster split-K wins on few-tile
+# shards with M <= 32 and loses at M >= 64 (pull-form reduction); 65 tiles: no gain
 @pytest.mark.parametrize("M,K,N,cs", [(16, 4096, 1376, 4), (16, 4096, 2752, 4), (16, 8192, 3584, 4),
+                                      (32, 4096, 1376, 4), (16, 4096, 5504, 3), (32, 4096, 5504, 2),
+                                      (16, 4096, 6880, 2), (16, 8192, 7168, 2), (16, 4096, 8256, 0),
                                       (64, 4096, 1376, 0), (128, 4096, 1376, 0), (16, 4096, 11008, 0)])
 def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs):
     assert plan_config(M, K, N)[3] == cs
