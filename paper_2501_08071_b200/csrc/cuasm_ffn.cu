@@ -527,13 +527,15 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
     // Decode shards (M <= 32, up to 2 * kFewTiles tiles): split each tile's k-loop over a
     // cluster of S CTAs, partials pushed into the owner CTA's shared memory (dual_gemm.cuh
-    // split_k_push) -- no global partials, no flags, no second wave.  S = 4 up to 37 tiles,
-    // 3 up to 49 (M <= 16: the 3-way slots fit the staging area), else 2 up to 64.  Kernel
-    // times under ncu (profiles/r01/csplit/): 16 x 4096 x 1376: 15.3 vs 17.5 us (stream-K
-    // split 3 ways), 16 x 4096 x 5504 (S = 3): 23.0 vs 27.1, 16 x 4096 x 6880 (S = 2): 26.5 vs
-    // 29.5, 32 x 4096 x 5504 (S = 2): 24.9 vs 27.2; at M >= 64 (pull form) it loses
+    // split_k_push) -- no global partials, no flags, no second wave.  S = 6 up to 16 tiles
+    // at M <= 16, 4 up to 37 tiles, 3 up to 49 (M <= 16: the 3-way slots fit the staging
+    // area), else 2 up to 64.  Kernel times under ncu (profiles/r01/csplit/): 16 x 4096 x
+    // 1376: 14.5 us (S = 6), 15.0 (S = 4) vs 17.5 us (stream-K split 3 ways), 16 x 4096 x 5504
+    // (S = 3): 23.0 vs 27.1, 16 x 4096 x 6880 (S = 2): 26.5 vs 29.5, 32 x 4096 x 5504 (S = 2):
+    // 24.9 vs 27.2; at M >= 64 (pull form) it loses
     if (out_cols == 128 && KB >= 48 && M <= 32) {
-        const int S = tiles_1sm * 4 <= sm_count && tiles_1sm <= 37   ? 4
+        const int S = M <= 16 && tiles_1sm * 6 <= sm_count && tiles_1sm <= 16 ? 6
+                      : tiles_1sm * 4 <= sm_count && tiles_1sm <= 37   ? 4
                       : M <= 16 && tiles_1sm * 3 <= sm_count && tiles_1sm <= 49 ? 3
                       : tiles_1sm * 2 <= sm_count && tiles_1sm <= 2 * kFewTiles ? 2
                                                                                 : 0;

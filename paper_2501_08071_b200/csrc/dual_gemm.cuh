@@ -537,53 +537,53 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
 }
 
 // Cluster split-K, push form (bf16 output, tiles with <= 32 valid rows, whose
-// partials fit the TMA-store staging area this mode leaves unused).  Column pair
-// p (32 columns of chunk a + 32 of chunk b) belongs to CTA p % S.  (a) The warp of
-// TMEM quadrant 0 holding pair p reads it (lane = row) and writes it into slot
-// [p / S][its rank] of the owner's staging area: plain shared-memory stores for its
-// own pairs, st.async with a transaction-count credit on the owner's barrier for
-// the others -- no copy, flag or remote read on the way; (b) the owner waits for
-// the bytes (it armed the barrier with their count), sums the S slots in rank
-// order (result independent of arrival order), applies the epilogue and stores.
-// Slot rows are 256 bytes, 16-byte groups XOR-swizzled by row & 7.
+// partials fit the TMA-store staging area this mode leaves unused).  The accumulator
+// is cut into units of 16 columns of chunk a + the same 16 of chunk b (8 units per
+// 256-column tile); unit u belongs to CTA u % S, so with S <= 8 every CTA owns one.
+// (a) The warp of TMEM quadrant 0 holding unit u reads it (lane = row) and writes it
+// into slot [u / S][its rank] of the owner's staging area: plain shared-memory stores
+// for its own units, st.async with a transaction-count credit on the owner's barrier
+// for the others -- no copy, flag or remote read on the way; (b) the owner waits for
+// the bytes (it armed the barrier with their count), sums the S slots in rank order
+// (result independent of arrival order), applies the epilogue and stores.  Slot rows
+// are 128 bytes, 16-byte groups XOR-swizzled by row & 7.
+template <class C>
+struct PushUnits {
+    static constexpr int NUNIT = C::UMMA_N / 32;  // 16-column units (a and b halves)
+};
+
 template <class C, int kKind>
 __device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
     if (kKind != 0 || rows > 32) return false;
-    constexpr int NPAIR = C::UMMA_N / 64;
-    return ((NPAIR + S - 1) / S) * S * (rows <= 16 ? 16 : 32) * 256 <= C::STG_BYTES;
+    constexpr int NU = PushUnits<C>::NUNIT;
+    return ((NU + S - 1) / S) * S * (rows <= 16 ? 16 : 32) * 128 <= C::STG_BYTES;
 }
 
-#if CUASM_DIAG
-__device__ __forceinline__ bool i_own_first_pair(int half, uint32_t part, int S) {
-    return half == static_cast<int>(part % S) / 2;  // (NPAIR 4, PAIRS 2: the warp holding pair `part`)
-}
-#endif
-
-// The owner's reduction of one column pair for this lane's row (split_k_push (b)):
-// sum the S slots in rank order, apply the epilogue, store columns < n_lim.  A
-// loop over 8-column groups, not unrolled over the 32 columns: this code runs once
-// per launch, fetched cold (the measurement's L2 flush evicts code too), so its
-// size, not its instruction count, sets its time (~10 SM cycles per instruction).
+// The owner's reduction of one unit for this lane's row (split_k_push (b)): sum the
+// S slots in rank order, apply the epilogue, store columns < n_lim.  Two passes of
+// 8 columns, not unrolled: this code runs once per launch, fetched cold (the
+// measurement's L2 flush evicts code too), so its size, not its instruction count,
+// sets its time (~10 SM cycles per straight-line instruction).
 template <class C, int kKind, int kEpi>
-__device__ __forceinline__ void push_reduce_pair(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
-                                              uint32_t swz, const GateRow& gr, float rr, int64_t rbase, int col_a,
-                                              int col_b, int n_lim) {
+__device__ __forceinline__ void push_reduce_unit(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
+                                                 uint32_t swz, const GateRow& gr, float rr, int64_t rbase, int col_a,
+                                                 int col_b, int n_lim) {
     constexpr int kEs = kKind == 0 ? 2 : 4;
     // the store's kernel parameters, read in the dry pass too (constant-cache lines warm)
     char* const dst0 = static_cast<char*>(p.dst[0]);
     const bool plain = p.num_dst == 1 && !p.dst_mc;
 #pragma unroll 1
-    for (int g8 = 0; g8 < 4; ++g8) {
+    for (int g8 = 0; g8 < 2; ++g8) {
         float a[8], b[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = b[k] = 0.f;
 #pragma unroll 1
         for (int j = 0; j < S; ++j) {  // rank order
-            const uint8_t* src = slot0 + static_cast<uint32_t>(j * rc) * 256;
+            const uint8_t* src = slot0 + static_cast<uint32_t>(j * rc) * 128;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float4 x = *reinterpret_cast<const float4*>(src + (((2 * g8 + h) ^ swz) << 4));
-                const float4 y = *reinterpret_cast<const float4*>(src + (((8 + 2 * g8 + h) ^ swz) << 4));
+                const float4 y = *reinterpret_cast<const float4*>(src + (((4 + 2 * g8 + h) ^ swz) << 4));
                 a[4 * h] += x.x; a[4 * h + 1] += x.y; a[4 * h + 2] += x.z; a[4 * h + 3] += x.w;
                 b[4 * h] += y.x; b[4 * h + 1] += y.y; b[4 * h + 2] += y.z; b[4 * h + 3] += y.w;
             }
@@ -609,15 +609,15 @@ template <class C, int kKind, int kEpi>
 __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tmem_base, int acc, uint8_t* stg,
                                              uint64_t* rbar, uint32_t part, int mb, int nb, uint32_t quad, int half,
                                              uint32_t ewarp, uint32_t lane, bool& cl_pending, bool dry) {
-    constexpr int NPAIR = C::UMMA_N / 64;
+    constexpr int NU = PushUnits<C>::NUNIT;
     const int S = p.csplit;
     const int row0 = mb * C::TILE_M;
     const int rows = min(C::BM, p.M - row0);
     const int rc = rows <= 16 ? 16 : 32;  // slot rows
     const uint32_t stg_u = ptx::smem_u32(stg), rbar_u = ptx::smem_u32(rbar);
-    if (!dry && ewarp == 0 && lane == 0 && static_cast<int>(part) < NPAIR) {
-        const int owned = (NPAIR - 1 - static_cast<int>(part)) / S + 1;
-        ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 256));
+    if (!dry && ewarp == 0 && lane == 0 && static_cast<int>(part) < NU) {
+        const int owned = (NU - 1 - static_cast<int>(part)) / S + 1;
+        ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 128));
     }
     if (quad != 0) return;  // every valid row lives in TMEM lane quadrant 0
     const bool row_ok = static_cast<int>(lane) < rows;
@@ -625,7 +625,7 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     const float rr = row_ok && p.use_r ? __ldcg(p.r + grow) : 1.f;
 #if CUASM_DIAG  // experiments only: SM-cycle stamps of the phases into trace slots 12..15
     const long long dclk0 = clock64();
-    const bool dbg = p.trace && lane == 0 && i_own_first_pair(half, part, S);
+    const bool dbg = p.trace && lane == 0 && half == 0;
 #define CUASM_DIAG_STAMP(slot) \
     if (dbg) p.trace[blockIdx.x * kTraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - dclk0)
 #else
@@ -637,10 +637,9 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     }
     const uint32_t t_row = tmem_base + acc * C::UMMA_N;
     const uint32_t swz = lane & 7;
-    // (a) scatter this warp's pairs to their owners
+    // (a) scatter this warp's units to their owners
 #pragma unroll 1
     for (int i = 0; i < C::PAIRS; ++i) {
-        const int pr = half * C::PAIRS + i;
         const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
         uint32_t v1[32], v3[32];
         if (!dry) {
@@ -649,36 +648,47 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
             ptx::tmem_ld_wait();
         }
         if (!row_ok || dry) continue;
-        const uint32_t owner = static_cast<uint32_t>(pr % S);
-        const uint32_t dst = stg_u + static_cast<uint32_t>(((pr / S) * S + static_cast<int>(part)) * rc + lane) * 256;
-        if (owner == part) {
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                *reinterpret_cast<uint4*>(stg + (dst - stg_u) + ((g ^ swz) << 4)) =
-                    make_uint4(v1[4 * g], v1[4 * g + 1], v1[4 * g + 2], v1[4 * g + 3]);
-                *reinterpret_cast<uint4*>(stg + (dst - stg_u) + (((g + 8) ^ swz) << 4)) =
-                    make_uint4(v3[4 * g], v3[4 * g + 1], v3[4 * g + 2], v3[4 * g + 3]);
-            }
-        } else {
-            const uint32_t rdst = ptx::mapa(dst, owner), rb = ptx::mapa(rbar_u, owner);
+        for (int h = 0; h < 2; ++h) {
+            const int u = 2 * (half * C::PAIRS + i) + h;
+            const uint32_t owner = static_cast<uint32_t>(u % S);
+            const uint32_t off = static_cast<uint32_t>(((u / S) * S + static_cast<int>(part)) * rc + lane) * 128;
+            if (owner == part) {
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                ptx::st_async_v4(rdst + ((g ^ swz) << 4), make_uint4(v1[4 * g], v1[4 * g + 1], v1[4 * g + 2], v1[4 * g + 3]),
-                                 rb);
-                ptx::st_async_v4(rdst + (((g + 8) ^ swz) << 4),
-                                 make_uint4(v3[4 * g], v3[4 * g + 1], v3[4 * g + 2], v3[4 * g + 3]), rb);
+                for (int g = 0; g < 4; ++g) {
+                    *reinterpret_cast<uint4*>(stg + off + ((g ^ swz) << 4)) =
+                        make_uint4(v1[16 * h + 4 * g], v1[16 * h + 4 * g + 1], v1[16 * h + 4 * g + 2],
+                                   v1[16 * h + 4 * g + 3]);
+                    *reinterpret_cast<uint4*>(stg + off + (((g + 4) ^ swz) << 4)) =
+                        make_uint4(v3[16 * h + 4 * g], v3[16 * h + 4 * g + 1], v3[16 * h + 4 * g + 2],
+                                   v3[16 * h + 4 * g + 3]);
+                }
+            } else {
+                const uint32_t rdst = ptx::mapa(stg_u + off, owner), rb = ptx::mapa(rbar_u, owner);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    ptx::st_async_v4(rdst + ((g ^ swz) << 4),
+                                     make_uint4(v1[16 * h + 4 * g], v1[16 * h + 4 * g + 1], v1[16 * h + 4 * g + 2],
+                                                v1[16 * h + 4 * g + 3]),
+                                     rb);
+                    ptx::st_async_v4(rdst + (((g + 4) ^ swz) << 4),
+                                     make_uint4(v3[16 * h + 4 * g], v3[16 * h + 4 * g + 1], v3[16 * h + 4 * g + 2],
+                                                v3[16 * h + 4 * g + 3]),
+                                     rb);
+                }
             }
         }
     }
     CUASM_DIAG_STAMP(12);
-    // (b) reduce the pairs this CTA owns
+    // (b) reduce the units this CTA owns
     const GateRow gr = gate_row(rr);
     const int64_t rbase = static_cast<int64_t>(grow) * p.ldo;
     bool waited = false;
 #pragma unroll 1
-    for (int i = 0; i < C::PAIRS; ++i) {
-        const int pr = half * C::PAIRS + i;
-        if (pr % S != static_cast<int>(part)) continue;
+    for (int v = 0; v < 2 * C::PAIRS; ++v) {
+        const int i = v >> 1, h = v & 1;
+        const int u = 2 * (half * C::PAIRS + i) + h;
+        if (u % S != static_cast<int>(part)) continue;
         if (!waited && !dry) {
             ptx::mbar_wait_acq_cluster(rbar_u, 0u);  // one tile per cluster: phase 0
             waited = true;
@@ -686,10 +696,10 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         }
         if (!row_ok) continue;
         const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
-        const uint8_t* slot0 = stg + static_cast<uint32_t>((pr / S) * S * rc + static_cast<int>(lane)) * 256;
+        const uint8_t* slot0 = stg + static_cast<uint32_t>((u / S) * S * rc + static_cast<int>(lane)) * 128;
         CUASM_DIAG_STAMP(14);
-        push_reduce_pair<C, kKind, kEpi>(p, slot0, S, rc, swz, gr, rr, rbase, nb * C::OUT_COLS + ca * 32,
-                                         nb * C::OUT_COLS + cb * 32, dry ? 0 : p.N);
+        push_reduce_unit<C, kKind, kEpi>(p, slot0, S, rc, swz, gr, rr, rbase, nb * C::OUT_COLS + ca * 32 + 16 * h,
+                                         nb * C::OUT_COLS + cb * 32 + 16 * h, dry ? 0 : p.N);
         CUASM_DIAG_STAMP(15);
     }
 }

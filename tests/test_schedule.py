@@ -121,7 +121,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
     if out_cols == 128 and KB >= 48 and M <= 32:   # decode shards: cluster split-K
-        S = (4 if 4 * t1 <= sm_count and t1 <= 37 else
+        S = (6 if M <= 16 and 6 * t1 <= sm_count and t1 <= 16 else
+             4 if 4 * t1 <= sm_count and t1 <= 37 else
              3 if M <= 16 and 3 * t1 <= sm_count and t1 <= 49 else
              2 if 2 * t1 <= sm_count and t1 <= 64 else 0)
         if S:
@@ -243,7 +244,7 @@ def test_library_plan_w2_and_70b(lib_plan):
 
 # measured (profiles/r01/csplit/ncu_ab_*.txt): the cluster split-K wins on few-tile
 # shards with M <= 32 and loses at M >= 64 (pull-form reduction); 65 tiles: no gain
-@pytest.mark.parametrize("M,K,N,cs", [(16, 4096, 1376, 4), (16, 4096, 2752, 4), (16, 8192, 3584, 4),
+@pytest.mark.parametrize("M,K,N,cs", [(16, 4096, 1376, 6), (16, 4096, 2752, 4), (16, 8192, 3584, 4),
                                       (32, 4096, 1376, 4), (16, 4096, 5504, 3), (32, 4096, 5504, 2),
                                       (16, 4096, 6880, 2), (16, 8192, 7168, 2), (16, 4096, 8256, 0),
                                       (64, 4096, 1376, 0), (128, 4096, 1376, 0), (16, 4096, 11008, 0)])
