@@ -49,6 +49,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_
   python bench.py --workload llama70b --shard-of 8 --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_70b8.log 2>&1; echo "ncu_gemm_70b8=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_tiny \
   python bench.py --workload tiny_fp32 --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_tiny.log 2>&1; echo "ncu_gemm_tiny=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_decode_shard8 \
+  python bench.py --workload llama7b_decode --shard-of 8 --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-b2b --no-graph > $O/ncu_gemm_d8.log 2>&1; echo "ncu_gemm_d8=$?"
+# cluster split-K: kernel times per width (ncu, cold L2) and the per-CTA timeline of the decode shards
+SHAPES=16x4096x1376,16x4096x2752,16x4096x5504,16x8192x3584 CS=0,1,2,4,6,8 REPS=10 timeout 600 ncu --metrics gpu__time_duration.sum \
+  --clock-control none --csv --log-file $O/csplit_ab.csv python scripts/ncu_ab_decode.py > $O/csplit_ab_marks.log 2>&1; echo "csplit_ab=$?"
+timeout 300 python scripts/trace_decode.py > $O/trace_decode.log 2>&1; echo "trace_decode=$?"
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_memcheck.log 2>&1; echo "memcheck=$?"
 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_synccheck.log 2>&1; echo "synccheck=$?"
 timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_racecheck.log 2>&1; echo "racecheck=$?"
