@@ -98,9 +98,13 @@ typedef enum {
                                2 evict_last.  Default 2 (x evict_last, W13 normal)    */
     CUASM_OPT_CSPLIT = 10     /* 1-SM variant, fewer tiles than SMs: split every tile's
                                k-range over a cluster of S CTAs and reduce the partials
-                               through distributed shared memory.  0 = the
-                               configuration model decides, 1 = off, 2..8 = S (used
-                               only when tiles * S <= SMs and S <= k-blocks)           */
+                               through distributed shared memory (bf16 tiles of <= 32
+                               rows: pushed into the owner CTA with st.async; else
+                               pulled with ld.shared::cluster); summed in rank order,
+                               so results are bitwise reproducible.  0 = the
+                               configuration model decides (decode shards, M <= 32),
+                               1 = off, 2..8 = S (used only when tiles * S <= SMs,
+                               S <= k-blocks and S clusters fit co-resident)           */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
