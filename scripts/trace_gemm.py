@@ -49,8 +49,9 @@ def main():
             for _ in range(3):
                 run()
             h.set_option(ffn.OPT_TRACE, 1)
-            wbuf.zero_()
-            rbuf.sum()
+            if not os.environ.get("NOFLUSH"):  # NOFLUSH=1: code and operands stay in L2 (cold-code A/B)
+                wbuf.zero_()
+                rbuf.sum()
             torch.cuda.synchronize()
             torch.cuda._sleep(int(1e8))
             run()
