@@ -30,7 +30,9 @@ def _inputs(M, K, N, seed, dev):
 
 
 @pytest.mark.parametrize("M,K,N,P", [(300, 512, 2048, 4), (16, 1024, 1376 * 2, 2), (2048, 1024, 2752, 8),
-                                     (129, 256, 8 * 24, 3)])
+                                     (129, 256, 8 * 24, 3),
+                                     # decode shards through the cluster split-K push form (S = 6 / 4)
+                                     (16, 4096, 1376 * 2, 2), (24, 4096, 688 * 4, 4)])
 def test_simulated_peers_hold_the_full_output(cuda_device, M, K, N, P):
     d, t = _inputs(M, K, N, 7100 + M, cuda_device)
     bufs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda_device) for _ in range(P)]
