@@ -251,3 +251,17 @@ def test_library_plan_w2_and_70b(lib_plan):
 def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs):
     assert plan_config(M, K, N)[3] == cs
     assert lib_plan(M, K, N)[3] == cs
+
+
+# every cluster split the planner picks must take the push form (dual_gemm.cuh split_k_push_fits:
+# bf16, <= 32 rows, ceil(8 / S) * S * rc * 128 bytes of slots within the 32 KB staging area, rc =
+# 16 or 32 slot rows); the pull form is only reachable by forcing CUASM_OPT_CSPLIT
+@pytest.mark.parametrize("K", [4096, 8192])
+def test_planner_cluster_splits_take_the_push_form(K):
+    for M in range(1, 33):
+        for n_blocks in range(1, 80):
+            S = plan_config(M, K, 128 * n_blocks)[3]
+            if S:
+                rc = 16 if M <= 16 else 32
+                assert -(-8 // S) * S * rc * 128 <= 32768, (M, n_blocks, S)
+                assert n_blocks * S <= 148
