@@ -42,6 +42,7 @@ struct PackedWeights {
     const void* key_w3 = nullptr;
     int64_t key_K = 0, key_N = 0;
     bool packed = false;
+    bool fresh = false;   // packed by a kernel the next GEMM launch directly follows (no early weight loads)
     CUtensorMap tmap;     // box {BK, tmap_rows}; tmap_rows = B_ROWS of the launched variant
     int tmap_rows = 0;
 };
@@ -209,6 +210,7 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     w.key_K = K;
     w.key_N = N;
     w.packed = true;
+    w.fresh = true;
     return CUASM_OK;
 }
 
@@ -344,6 +346,10 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.num_tiles = p.num_m_blk * p.num_n_blk;
     p.a_box_bytes = static_cast<int>(a_rows) * 128;
     p.l2pol = h->l2pol;
+    // weights packed before an earlier GEMM launch on this stream (which waited for the
+    // pack) are safe to load before griddepcontrol.wait; the first GEMM after a pack is not
+    p.w_early = w.fresh ? 0 : 1;
+    w.fresh = false;
     // bf16 output with one destination leaves through TMA stores: a 2-D map over the
     // destination [M rows, ldo stride] x N columns, 32 x 32 boxes, 64-byte swizzle
     // (what the epilogue's staging layout writes); stores past M / N are clipped

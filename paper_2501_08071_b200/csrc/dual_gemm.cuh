@@ -75,6 +75,8 @@ struct FfnGemmParams {
                      // tile, CTA rank j computes k-blocks [j*KB/S, (j+1)*KB/S) and the S partial
                      // accumulators are reduced through distributed shared memory; 0 = off
     int l2pol;       // TMA L2 policies: bits 0-1 x, bits 2-3 W13 (0 evict_normal, 1 evict_first, 2 evict_last)
+    int w_early;     // 1: the packed weights predate the preceding kernel, so the producer may
+                     // load the first pipeline stages' weights before griddepcontrol.wait
     int rep;         // 4 (SwiGLU, M <= 32) / 2 (M <= 64) / 0; 2-SM: the leader CTA.  The x rows are
                      // loaded rep times into the A tile (at smem rows q*128/rep), so every TMEM
                      // lane quadrant holds rows and the epilogue spreads the column pairs over
@@ -777,7 +779,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         // ========================= TMA producer =========================
         // Whole warp walks the loop, one elected lane issues (uniform operands,
         // no per-instruction uniformity loops around UTMALDG).
-        ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
         // default: x evict_last (re-read by every n-block), W13 evict_normal (shared by the
         // group's tiles); CUASM_OPT_L2_POLICY overrides (2 bits each: 0 normal, 1 first, 2 last)
         auto pol = [](int c) {
@@ -785,11 +786,57 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         };
         const uint64_t pol_x = pol(p.l2pol & 3);
         const uint64_t pol_w = pol((p.l2pol >> 2) & 3);
+        // arm stage s for k-block kb (its full transaction count: x and weights) and load the weights
+        auto arm_and_load_w = [&](int s, int kb, int row_b0) {
+            const uint32_t fb = ptx::smem_u32(&full_bar[s]);
+            const uint32_t sb = ptx::smem_u32(smem_b + s * C::B_BYTES);
+            if constexpr (kCtaGroup == 1) {
+                ptx::mbar_arrive_expect_tx(fb, (p.rep ? p.rep : 1) * p.a_box_bytes + C::B_BYTES);
+                ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
+            } else {
+                // both CTAs' bytes land on the leader's barrier
+                if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? p.rep + 1 : 2) * p.a_box_bytes);
+                ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
+            }
+        };
+        // the x rows of stage s (rep: <= 32 rows copied into every 32-row quarter; 2-SM: the
+        // leader's A tile only -- the peer's rows are all past M)
+        auto load_x = [&](int s, int kb, int row_a) {
+            const uint32_t fb = ptx::smem_u32(&full_bar[s]);
+            const uint32_t sa = ptx::smem_u32(smem_a + s * C::A_BYTES);
+            if constexpr (kCtaGroup == 1) {
+                const int nrep = p.rep ? p.rep : 1;
+                for (int q = 0; q < nrep; ++q)  // copy q of the rows: smem rows q*128/nrep.. (4 KB aligned)
+                    ptx::tma_load_2d(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+            } else {
+                const int nrep = (p.rep && leader) ? p.rep : 1;
+                for (int q = 0; q < nrep; ++q)
+                    ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+            }
+        };
+        Sched sch;
+        sch.init(p, cluster_id, static_cast<int>(part));
+        // Weights do not depend on the preceding kernel (they were packed before it): the
+        // first segment's first STAGES weight boxes go out before griddepcontrol.wait, so
+        // under PDL they stream while the preceding kernel drains (its x loads follow the wait)
+        int pre = 0;
+        if (p.w_early) {
+            Sched s0 = sch;
+            Seg g0;
+            if (s0.next(g0)) {
+                int mb0, nb0;
+                tile_coords(g0.tile, p, mb0, nb0);
+                const int row_b0 = C::b_row0(nb0, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
+                pre = min(C::STAGES, g0.kb1 - g0.kb0);
+                if (ptx::elect_one())
+                    for (int i = 0; i < pre; ++i) arm_and_load_w(i, g0.kb0 + i, row_b0);
+                __syncwarp();
+            }
+        }
+        ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
         int stage = 0;
         uint32_t phase = 0;
         bool first_load = true;
-        Sched sch;
-        sch.init(p, cluster_id, static_cast<int>(part));
         Seg sg;
         while (sch.next(sg)) {
             int mb, nb;
@@ -798,27 +845,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // k-block-tiled weights (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*UMMA_N
             const int row_b0 = C::b_row0(nb, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
             for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
-                ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
-                const uint32_t fb = ptx::smem_u32(&full_bar[stage]);
-                const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
-                const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
-                if (ptx::elect_one()) {
-                    if constexpr (kCtaGroup == 1) {
-                        const int nrep = p.rep ? p.rep : 1;
-                        ptx::mbar_arrive_expect_tx(fb, nrep * p.a_box_bytes + C::B_BYTES);
-                        for (int q = 0; q < nrep; ++q)  // copy q of the rows: smem rows q*128/nrep.. (4 KB aligned)
-                            ptx::tma_load_2d(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
-                    } else {
-                        // both CTAs' bytes land on the leader's barrier; rep: the leader's
-                        // A tile gets the <= 32 x rows in all four quarters (the peer's rows
-                        // are all past M)
-                        const int nrep = (p.rep && leader) ? p.rep : 1;
-                        if (leader)
-                            ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? p.rep + 1 : 2) * p.a_box_bytes);
-                        for (int q = 0; q < nrep; ++q)
-                            ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
-                        ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
+                if (pre > 0) {
+                    // stage armed and its weights requested before the wait (first use of the
+                    // stage: no empty-barrier wait needed)
+                    if (ptx::elect_one()) load_x(stage, kb, row_a);
+                    --pre;
+                } else {
+                    ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
+                    if (ptx::elect_one()) {
+                        arm_and_load_w(stage, kb, row_b0);
+                        load_x(stage, kb, row_a);
                     }
                 }
                 __syncwarp();
