@@ -611,3 +611,27 @@ def test_cluster_split_k_fp32(cuda_device):
     h.set_option(ffn.OPT_CSPLIT, 2)
     out, _ = run_gpu(d, 1e-6, "fp32", ffn.VARIANT_1SM, handle=h, schedule=ffn.SCHEDULE_DATA_PARALLEL)
     check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6), "csplit fp32")
+
+
+# ------------------------------------------ weight loads ahead of griddepcontrol.wait ---
+@pytest.mark.parametrize("M,K,N", [(16, 4096, 1376), (300, 1024, 1000), (512, 2048, 2048)])
+def test_weights_changed_between_forwards(cuda_device, M, K, N):
+    """The producer loads weights before griddepcontrol.wait only when the packed
+    weights predate the preceding kernel (PackedWeights::fresh): a forward right after
+    a re-pack (weights changed in place -> invalidation) must see the new weights, and
+    the next forward (early weight loads) must agree with it bitwise."""
+    d = make_inputs(M, K, N, family="C", seed=8400 + M, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    a0 = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    a1 = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(a0, a1)
+    t["w1"].neg_()  # in place: the binding invalidates the cache, the next forward re-packs
+    b0 = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    b1 = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(b0, b1)
+    w1n = -d["w1"]
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 16)))))
+    check(b1[rows], oracle.ffn(d["x"], d["g"], w1n, d["w3"], 1e-6, mode="fold_bf16", rows=rows), "after re-pack")
