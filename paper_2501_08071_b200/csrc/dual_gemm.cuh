@@ -1060,6 +1060,13 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const GateRow gr = gate_row(rr);
             ptx::mbar_wait(ptx::smem_u32(&tfull_bar[acc]), acc_phase);
             ptx::tc_fence_after();
+#if CUASM_DIAG  // experiments only: SM cycles of the final tile's epilogue phases (slots 12..15)
+            const long long eclk0 = clock64();
+#define CUASM_EPI_STAMP(slot) \
+    if (p.trace && warp == 2 && lane == 0) p.trace[blockIdx.x * kTraceSlots + (slot)] = clock64() - eclk0
+#else
+#define CUASM_EPI_STAMP(slot)
+#endif
             if (warp == 2 && lane == 0) {
                 trace_stamp(p, 7);  // (last write wins: the final tile)
                 if (it == 0) trace_stamp(p, 8);
@@ -1080,6 +1087,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 wait_flag(p.flags + ((static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * C::NUM_EPI_WARPS + ewarp));
             }
             if (warp == 2 && lane == 0) trace_stamp(p, 10);
+            CUASM_EPI_STAMP(12);
             const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
 #pragma unroll 1
             for (int i = 0; i < C::PAIRS; ++i) {
@@ -1165,6 +1173,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if (use_tma) store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + cb * 32, box_row0, lane);
                     else store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
                 }
+                CUASM_EPI_STAMP(13 + (i > 0 ? 1 : 0));
             }
             if (warp == 2 && lane == 0) {
                 trace_stamp(p, 11);

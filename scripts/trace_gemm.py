@@ -59,6 +59,12 @@ def main():
             h.close()
             t0 = tr[:, 0][tr[:, 0] > 0].min()
             rows = {}
+            if os.environ.get("EPI_DIAG"):  # library built with -DCUASM_DIAG=1: final-tile epilogue phases
+                e = tr[:, 12:15]
+                e = e[e[:, 0] > 0]
+                print(f"   epilogue cycles after tfull (flags, pair 0 done, pair 1 done): med "
+                      f"{e.median(0).values.tolist()} max {e.max(0).values.tolist()}")
+                tr[:, 12:16] = 0
             cyc, kbs = tr[:, 12], tr[:, 13]
             sel = kbs > 1
             if sel.any():
