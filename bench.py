@@ -658,6 +658,10 @@ def run_cuasm(args):
                 "l2": "flushed before every step outside the per-step CUDA-event pair: 256 MiB memset, then a "
                       "256 MiB read so the flush's dirty lines are written back before the step",
                 "op": op, "flops_per_step": flops_per_step, "prep_ms": round(prep_ms, 4),
+                # the configuration model's plan for this rank's problem: (variant, stream-K tail,
+                # MMA N, cluster split-K width); the launch follows it unless options override
+                "plan": list(ffn.plan_config(M, K, N_l, "gemm" if op == "gemm_lrelu" else "ffn", wdtype))
+                if op in ("ffn", "gemm_lrelu") else None,
             },
             "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),
             "pct_of_nominal_2250": round(value / world / 2250.0, 4),
