@@ -22,11 +22,15 @@
 //               the accumulator to the epilogue
 //   warps 2..9  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32*(w%4)..+31
 //               = tile rows, and half of the accumulator columns), r-scale,
-//               activation / SiLU gate, bf16 pack, 16-byte global stores; at
-//               kernel entry they also compute r for a 1/grid slice of the rows
+//               activation / SiLU gate, bf16 pack, staged TMA stores (fp32:
+//               16-byte global stores); at kernel entry they also compute r for
+//               a 1/grid slice of the rows
 // TMEM holds two UMMA_N-column accumulators so the epilogue of tile i overlaps
 // the mainloop of tile i+1.  The schedule (Sched) is whole tiles, optionally
-// followed by a stream-K tail whose partials go through a global workspace.
+// followed by a stream-K tail whose partials go through a global workspace, or
+// (1-SM, few tiles) a cluster split-K: the S CTAs of a cluster share one tile's
+// k-range and reduce through distributed shared memory (split_k_push /
+// split_k_reduce).
 //
 // kCtaGroup == 2 (2-SM variant): a cluster of two CTAs on one TPC computes a
 // 256 x UMMA_N tile with tcgen05.mma.cta_group::2.  Each CTA TMA-loads its own
