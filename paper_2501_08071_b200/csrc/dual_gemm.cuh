@@ -973,6 +973,30 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             if (lane == 0) atomicAdd(p.sync, 1u);
         }
         bool r_ready = !p.fused_norm;
+        // Wait until every epilogue warp of the grid has published its rows of r, then count
+        // this warp as past the wait; the last warp past it resets both grid counters for the
+        // next launch (graph-safe: nobody reads them again in this launch).  The returning
+        // atomic sits here, under the first tile's mainloop, not on the kernel's exit path.
+        auto acquire_r = [&]() {
+            const uint32_t target = gridDim.x * C::NUM_EPI_WARPS;
+            if (ld_acquire_u32(p.sync) < target) {
+#if CUASM_WATCHDOG
+                const long long t0 = clock64();
+#endif
+                while (ld_acquire_u32(p.sync) < target) {
+                    __nanosleep(100);
+#if CUASM_WATCHDOG
+                    if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
+#endif
+                }
+            }
+            if (lane == 0 && atomicAdd(p.sync + 1, 1u) == target - 1) {
+                p.sync[0] = 0u;
+                p.sync[1] = 0u;
+                __threadfence();
+            }
+            __syncwarp();
+        };
         const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t ewarp = warp - 2;  // 0..7: flag slot
         const int half = static_cast<int>(ewarp >> 2);  // this warp's half of the accumulator columns
@@ -1023,18 +1047,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
             if (!r_ready) {
-                const uint32_t target = gridDim.x * C::NUM_EPI_WARPS;
-                if (ld_acquire_u32(p.sync) < target) {
-#if CUASM_WATCHDOG
-                    const long long t0 = clock64();
-#endif
-                    while (ld_acquire_u32(p.sync) < target) {
-                        __nanosleep(100);
-#if CUASM_WATCHDOG
-                        if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
-#endif
-                    }
-                }
+                acquire_r();
                 r_ready = true;
             }
             if (csplit && split_k_push_fits<C, kKind>(min(C::BM, p.M - mb * C::TILE_M), p.csplit)) {
@@ -1214,6 +1227,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
+        // a warp with no tile still has to be counted past the r wait (counter reset)
+        if (!r_ready) acquire_r();
     }
 
     // every TMA store this warp issued has written global memory before the CTA retires
@@ -1233,14 +1248,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         ptx::cluster_sync();
     } else {
         __syncthreads();
-    }
-    if (p.fused_norm && threadIdx.x == 0) {
-        // the last CTA out resets the grid counters for the next launch (graph-safe)
-        if (atomicAdd(p.sync + 1, 1u) == gridDim.x - 1) {
-            p.sync[0] = 0u;
-            p.sync[1] = 0u;
-            __threadfence();
-        }
     }
     if (warp == 1) {
         ptx::tc_fence_after();
