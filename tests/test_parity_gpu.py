@@ -635,3 +635,34 @@ def test_weights_changed_between_forwards(cuda_device, M, K, N):
     w1n = -d["w1"]
     rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 16)))))
     check(b1[rows], oracle.ffn(d["x"], d["g"], w1n, d["w3"], 1e-6, mode="fold_bf16", rows=rows), "after re-pack")
+
+
+# ------------------------------------------ one handle, mixed launches back to back ---
+def test_mixed_shapes_one_handle_back_to_back(cuda_device):
+    """Launches of different grids on one handle and stream (cluster split-K, 2-SM stream-K,
+    whole tiles, GEMM mode) share its fused-a1 grid counters, which the last warp past the
+    r wait resets mid-kernel; PDL lets each launch start before the previous one ends.
+    Every output must equal the same problem run alone on a fresh handle."""
+    shapes = [(16, 4096, 1376), (1000, 1024, 2752), (16, 4096, 11008), (300, 512, 520), (32, 4096, 2752)]
+    data = []
+    for i, (M, K, N) in enumerate(shapes):
+        d = make_inputs(M, K, N, family="C", seed=8500 + i, dtype="bf16")
+        data.append({k: v.to(cuda_device) for k, v in d.items()})
+    alone = []
+    for t in data:
+        h1 = ffn.FusedFFN(cuda_device, torch.bfloat16)
+        alone.append(h1.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6))
+    torch.cuda.synchronize()
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    outs = []
+    for rep in range(3):
+        for t in data:
+            outs.append(h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6))
+            if rep == 2:
+                outs.append(h.gemm_act(t["x"], t["w1"], "leaky_relu", 0.01))
+    torch.cuda.synchronize()
+    k = 0
+    for rep in range(3):
+        for i in range(len(data)):
+            assert torch.equal(outs[k], alone[i]), f"rep {rep} shape {shapes[i]}"
+            k += 1 + (rep == 2)
