@@ -565,46 +565,48 @@ __device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
     return ((NU + S - 1) / S) * S * (rows <= 16 ? 16 : 32) * 128 <= C::STG_BYTES;
 }
 
-// The owner's reduction of one item -- 8 columns of one owned unit for one row --
-// (split_k_push (b)): sum the S slots in rank order, apply the epilogue, store if
-// `live`.  Every epilogue thread takes at most one item (<= 4 units x 32 rows x 2),
-// so the reduction is spread over the whole epilogue instead of the two warps that
-// can read TMEM quadrant 0.  Straight-line and small: this code runs once per launch,
-// fetched cold (the measurement's L2 flush evicts code too), so its size sets its time.
+// The owner's reduction of one unit for this lane's row (split_k_push (b)): sum the
+// S slots in rank order, apply the epilogue, store columns < n_lim.  Two passes of
+// 8 columns, not unrolled: this code runs once per launch, fetched cold (the
+// measurement's L2 flush evicts code too), so its size, not its instruction count,
+// sets its time (~10 SM cycles per straight-line instruction).
 template <class C, int kKind, int kEpi>
-__device__ __forceinline__ void push_reduce_item(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
-                                                 uint32_t swz, int hh, const GateRow& gr, float rr, int64_t rbase,
-                                                 int col_a, int col_b, bool live) {
+__device__ __forceinline__ void push_reduce_unit(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
+                                                 uint32_t swz, const GateRow& gr, float rr, int64_t rbase, int col_a,
+                                                 int col_b, int n_lim) {
     constexpr int kEs = kKind == 0 ? 2 : 4;
     // the store's kernel parameters, read in the dry pass too (constant-cache lines warm)
     char* const dst0 = static_cast<char*>(p.dst[0]);
     const bool plain = p.num_dst == 1 && !p.dst_mc;
-    float a[8], b[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = b[k] = 0.f;
 #pragma unroll 1
-    for (int j = 0; j < S; ++j) {  // rank order
-        const uint8_t* src = slot0 + static_cast<uint32_t>(j * rc) * 128;
+    for (int g8 = 0; g8 < 2; ++g8) {
+        float a[8], b[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float4 x = *reinterpret_cast<const float4*>(src + (((2 * hh + h) ^ swz) << 4));
-            const float4 y = *reinterpret_cast<const float4*>(src + (((4 + 2 * hh + h) ^ swz) << 4));
-            a[4 * h] += x.x; a[4 * h + 1] += x.y; a[4 * h + 2] += x.z; a[4 * h + 3] += x.w;
-            b[4 * h] += y.x; b[4 * h + 1] += y.y; b[4 * h + 2] += y.z; b[4 * h + 3] += y.w;
+        for (int k = 0; k < 8; ++k) a[k] = b[k] = 0.f;
+#pragma unroll 1
+        for (int j = 0; j < S; ++j) {  // rank order
+            const uint8_t* src = slot0 + static_cast<uint32_t>(j * rc) * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 x = *reinterpret_cast<const float4*>(src + (((2 * g8 + h) ^ swz) << 4));
+                const float4 y = *reinterpret_cast<const float4*>(src + (((4 + 2 * g8 + h) ^ swz) << 4));
+                a[4 * h] += x.x; a[4 * h + 1] += x.y; a[4 * h + 2] += x.z; a[4 * h + 3] += x.w;
+                b[4 * h] += y.x; b[4 * h + 1] += y.y; b[4 * h + 2] += y.z; b[4 * h + 3] += y.w;
+            }
         }
-    }
 #pragma unroll
-    for (int h = 0; h < (kEpi == 0 ? 1 : 2); ++h) {
-        const int c0 = h == 0 ? col_a : col_b;
-        float o[8];
+        for (int h = 0; h < (kEpi == 0 ? 1 : 2); ++h) {
+            const int c0 = (h == 0 ? col_a : col_b) + 8 * g8;
+            float o[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            o[k] = kEpi == 0 ? silu_gate(a[k], b[k], gr) : apply_act(rr * (h == 0 ? a[k] : b[k]), p.act, p.alpha);
-        const uint4 v = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
-                                   ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
-        if (live && c0 < p.N) {
-            if (plain) *reinterpret_cast<uint4*>(dst0 + (rbase + c0) * kEs) = v;
-            else store16<kKind>(p, (rbase + c0) * kEs, v);
+            for (int k = 0; k < 8; ++k)
+                o[k] = kEpi == 0 ? silu_gate(a[k], b[k], gr) : apply_act(rr * (h == 0 ? a[k] : b[k]), p.act, p.alpha);
+            const uint4 v = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
+                                       ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
+            if (c0 < n_lim) {
+                if (plain) *reinterpret_cast<uint4*>(dst0 + (rbase + c0) * kEs) = v;
+                else store16<kKind>(p, (rbase + c0) * kEs, v);
+            }
         }
     }
 }
@@ -619,15 +621,14 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     const int rows = min(C::BM, p.M - row0);
     const int rc = rows <= 16 ? 16 : 32;  // slot rows
     const uint32_t stg_u = ptx::smem_u32(stg), rbar_u = ptx::smem_u32(rbar);
-    const int owned = static_cast<int>(part) < NU ? (NU - 1 - static_cast<int>(part)) / S + 1 : 0;  // units
-    if (!dry && ewarp == 0 && lane == 0 && owned > 0)
+    if (!dry && ewarp == 0 && lane == 0 && static_cast<int>(part) < NU) {
+        const int owned = (NU - 1 - static_cast<int>(part)) / S + 1;
         ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 128));
-    // this thread's reduction item (b): owned unit iu (the item / (2 rows)-th), row irow, 8-column half ihh
-    const int item = static_cast<int>(ewarp * 32 + lane);
-    const bool has_item = item < owned * rows * 2;
-    const int irow = (item % (rows * 2)) >> 1, ihh = item & 1, iu = static_cast<int>(part) + (item / (rows * 2)) * S;
-    const float rr = has_item && p.use_r ? __ldcg(p.r + row0 + irow) : 1.f;  // early: hidden by (a)
+    }
+    if (quad != 0) return;  // every valid row lives in TMEM lane quadrant 0
     const bool row_ok = static_cast<int>(lane) < rows;
+    const int grow = row0 + static_cast<int>(lane);
+    const float rr = row_ok && p.use_r ? __ldcg(p.r + grow) : 1.f;
 #if CUASM_DIAG  // experiments only: SM-cycle stamps of the phases into trace slots 12..15
     const long long dclk0 = clock64();
     const bool dbg = p.trace && lane == 0 && half == 0;
@@ -636,15 +637,15 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
 #else
 #define CUASM_DIAG_STAMP(slot)
 #endif
-    const uint32_t t_row = tmem_base + acc * C::UMMA_N;
-    const uint32_t swz = lane & 7;
-    if (quad == 0 && !dry && cl_pending) {  // the prologue's cluster barrier: every CTA's barriers are initialised
+    if (!dry && cl_pending) {  // the prologue's cluster barrier: every CTA's barriers are initialised
         ptx::cluster_wait_acquire();
         cl_pending = false;
     }
-    // (a) scatter this warp's units to their owners (every valid row lives in TMEM lane quadrant 0)
+    const uint32_t t_row = tmem_base + acc * C::UMMA_N;
+    const uint32_t swz = lane & 7;
+    // (a) scatter this warp's units to their owners
 #pragma unroll 1
-    for (int i = 0; i < (quad == 0 ? C::PAIRS : 0); ++i) {
+    for (int i = 0; i < C::PAIRS; ++i) {
         const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
         uint32_t v1[32], v3[32];
         if (!dry) {
@@ -685,21 +686,28 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         }
     }
     CUASM_DIAG_STAMP(12);
-    // (b) reduce the units this CTA owns, one 8-column item per epilogue thread
-    if (!has_item) return;
-    if (!dry) {
-        ptx::mbar_wait_acq_cluster(rbar_u, 0u);  // one tile per cluster: phase 0
-        CUASM_DIAG_STAMP(13);
+    // (b) reduce the units this CTA owns
+    const GateRow gr = gate_row(rr);
+    const int64_t rbase = static_cast<int64_t>(grow) * p.ldo;
+    bool waited = false;
+#pragma unroll 1
+    for (int v = 0; v < 2 * C::PAIRS; ++v) {
+        const int i = v >> 1, h = v & 1;
+        const int u = 2 * (half * C::PAIRS + i) + h;
+        if (u % S != static_cast<int>(part)) continue;
+        if (!waited && !dry) {
+            ptx::mbar_wait_acq_cluster(rbar_u, 0u);  // one tile per cluster: phase 0
+            waited = true;
+            CUASM_DIAG_STAMP(13);
+        }
+        if (!row_ok) continue;
+        const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
+        const uint8_t* slot0 = stg + static_cast<uint32_t>((u / S) * S * rc + static_cast<int>(lane)) * 128;
+        CUASM_DIAG_STAMP(14);
+        push_reduce_unit<C, kKind, kEpi>(p, slot0, S, rc, swz, gr, rr, rbase, nb * C::OUT_COLS + ca * 32 + 16 * h,
+                                         nb * C::OUT_COLS + cb * 32 + 16 * h, dry ? 0 : p.N);
+        CUASM_DIAG_STAMP(15);
     }
-    const int pr = iu >> 1, hu = iu & 1;  // unit iu = 16 columns hu of column pair pr
-    const int ca = C::chunk_a(pr / C::PAIRS, pr % C::PAIRS), cb = C::chunk_b(pr / C::PAIRS, pr % C::PAIRS);
-    const uint8_t* slot0 = stg + static_cast<uint32_t>((iu / S) * S * rc + irow) * 128;
-    CUASM_DIAG_STAMP(14);
-    push_reduce_item<C, kKind, kEpi>(p, slot0, S, rc, static_cast<uint32_t>(irow & 7), ihh, gate_row(rr), rr,
-                                     static_cast<int64_t>(row0 + irow) * p.ldo,
-                                     nb * C::OUT_COLS + ca * 32 + 16 * hu + 8 * ihh,
-                                     nb * C::OUT_COLS + cb * 32 + 16 * hu + 8 * ihh, !dry);
-    CUASM_DIAG_STAMP(15);
 }
 
 template <int kKind, int kCtaGroup, int kEpi, int kN>
