@@ -573,13 +573,13 @@ __device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
 template <class C, int kKind, int kEpi>
 __device__ __forceinline__ void push_reduce_unit(const FfnGemmParams& p, const uint8_t* slot0, int S, int rc,
                                                  uint32_t swz, const GateRow& gr, float rr, int64_t rbase, int col_a,
-                                                 int col_b, int n_lim) {
+                                                 int col_b, int n_lim, int g8_lo, int g8_hi) {
     constexpr int kEs = kKind == 0 ? 2 : 4;
     // the store's kernel parameters, read in the dry pass too (constant-cache lines warm)
     char* const dst0 = static_cast<char*>(p.dst[0]);
     const bool plain = p.num_dst == 1 && !p.dst_mc;
 #pragma unroll 1
-    for (int g8 = 0; g8 < 2; ++g8) {
+    for (int g8 = g8_lo; g8 < g8_hi; ++g8) {
         float a[8], b[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = b[k] = 0.f;
@@ -627,8 +627,11 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     }
     if (quad != 0) return;  // every valid row lives in TMEM lane quadrant 0
     const bool row_ok = static_cast<int>(lane) < rows;
-    const int grow = row0 + static_cast<int>(lane);
-    const float rr = row_ok && p.use_r ? __ldcg(p.r + grow) : 1.f;
+    // reduction (b): with <= 16 rows two lanes share a row, 8 of its 16 unit columns each
+    const bool pair_lanes = rows <= 16;
+    const int rrow = pair_lanes ? static_cast<int>(lane >> 1) : static_cast<int>(lane);
+    const bool red_ok = rrow < rows;
+    const float rr = red_ok && p.use_r ? __ldcg(p.r + row0 + rrow) : 1.f;  // early: hidden by (a)
 #if CUASM_DIAG  // experiments only: SM-cycle stamps of the phases into trace slots 12..15
     const long long dclk0 = clock64();
     const bool dbg = p.trace && lane == 0 && half == 0;
@@ -685,10 +688,11 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
             }
         }
     }
+    __syncwarp();  // this warp's own-slot stores (lane = row) before other lanes of it read them
     CUASM_DIAG_STAMP(12);
     // (b) reduce the units this CTA owns
     const GateRow gr = gate_row(rr);
-    const int64_t rbase = static_cast<int64_t>(grow) * p.ldo;
+    const int64_t rbase = static_cast<int64_t>(row0 + rrow) * p.ldo;
     bool waited = false;
 #pragma unroll 1
     for (int v = 0; v < 2 * C::PAIRS; ++v) {
@@ -700,12 +704,14 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
             waited = true;
             CUASM_DIAG_STAMP(13);
         }
-        if (!row_ok) continue;
+        if (!red_ok) continue;
         const int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
-        const uint8_t* slot0 = stg + static_cast<uint32_t>((u / S) * S * rc + static_cast<int>(lane)) * 128;
+        const uint8_t* slot0 = stg + static_cast<uint32_t>((u / S) * S * rc + rrow) * 128;
+        const int g8_lo = pair_lanes ? static_cast<int>(lane & 1) : 0;
         CUASM_DIAG_STAMP(14);
-        push_reduce_unit<C, kKind, kEpi>(p, slot0, S, rc, swz, gr, rr, rbase, nb * C::OUT_COLS + ca * 32 + 16 * h,
-                                         nb * C::OUT_COLS + cb * 32 + 16 * h, dry ? 0 : p.N);
+        push_reduce_unit<C, kKind, kEpi>(p, slot0, S, rc, static_cast<uint32_t>(rrow & 7), gr, rr, rbase,
+                                         nb * C::OUT_COLS + ca * 32 + 16 * h, nb * C::OUT_COLS + cb * 32 + 16 * h,
+                                         dry ? 0 : p.N, g8_lo, pair_lanes ? g8_lo + 1 : 2);
         CUASM_DIAG_STAMP(15);
     }
 }
