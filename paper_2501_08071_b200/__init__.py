@@ -124,7 +124,10 @@ def _stream_ptr(device) -> int:
 
 
 class FusedFFN:
-    """One library handle (device + dtype).  Not thread-safe."""
+    """One library handle (device + dtype).  Not thread-safe, and used from one
+    CUDA stream at a time: the handle owns per-launch device state (r, the fused
+    a1 / stream-K bookkeeping, workspaces, the packed weights), so two launches
+    of one handle must not run concurrently on different streams."""
 
     def __init__(self, device=None, dtype: torch.dtype = torch.bfloat16):
         self.lib = load_library()
@@ -190,29 +193,36 @@ class FusedFFN:
             if not t.is_contiguous():
                 raise ValueError("tensors must be contiguous")
 
-    def _weights_changed(self, *ws, slot: int = 0):
-        # The library caches packed weights keyed by pointer (slot 0: the
-        # folded W1/W3, slot 1: a single GEMM weight).  A pointer alone is not
-        # an identity (the caching allocator reuses addresses), so the binding
-        # keys on the tensor objects themselves (weak refs) and their in-place
-        # version counters, and invalidates the cache on any change.
-        key = self._wkey.get(slot)
-        new = (tuple(weakref.ref(t) for t in ws), tuple(t._version for t in ws))
-        if key is None:
-            # first use in this slot (or after an invalidation): the library's
-            # pointer key decides, and an invalidated slot re-packs anyway
-            self._wkey[slot] = new
-            return
-        same = (len(key[0]) == len(ws) and all(r() is t for r, t in zip(key[0], ws)) and key[1] == new[1])
-        if not same:
-            # the library's invalidation drops every cached pack: forget all keys
+    def _weights_changed(self, slots: dict):
+        """Invalidate the library's folded-weight cache if any weight changed.
+
+        The library caches packed weights per slot keyed by pointer (slot 0: the
+        folded W1/W3 of the fused FFN, keyed by (rms_w, w1, w3); slot 1: the single
+        weight of gemm_act / the down projection W2).  A pointer alone is not an
+        identity (the caching allocator reuses addresses), so the binding keys each
+        library slot on the tensor objects themselves (weak refs) and their in-place
+        version counters, and invalidates the library cache on any change.  A slot
+        with no key has never been packed through this handle (or was invalidated
+        with all others), so the library re-packs it on first use."""
+        news = {}
+        changed = False
+        for slot, ws in slots.items():
+            new = (tuple(weakref.ref(t) for t in ws), tuple(t._version for t in ws))
+            news[slot] = new
+            key = self._wkey.get(slot)
+            if key is not None and not (len(key[0]) == len(ws) and all(r() is t for r, t in zip(key[0], ws))
+                                        and key[1] == new[1]):
+                changed = True
+        if changed:
+            # the library's invalidation drops every cached pack: forget every key
             self._check(self.lib.cuasm_ffn_invalidate_weights(self._h))
-            self._wkey = {slot: new}
+            self._wkey = {}
+        self._wkey.update(news)
 
     def prepare(self, rms_w, w1, w3):
         self._validate(rms_w, w1, w3)
         N, K = w1.shape
-        self._weights_changed(rms_w, w1, w3, slot=0)
+        self._weights_changed({0: (rms_w, w1, w3)})
         self._check(self.lib.cuasm_ffn_prepare(self._h, rms_w.data_ptr(), w1.data_ptr(), w3.data_ptr(), K, N,
                                                _stream_ptr(w1.device)))
 
@@ -230,7 +240,7 @@ class FusedFFN:
             self._validate(out)
             if out.shape != (M, N):
                 raise ValueError("out must be [M,N]")
-        self._weights_changed(rms_w, w1, w3, slot=0)
+        self._weights_changed({0: (rms_w, w1, w3)})
         self._check(self.lib.cuasm_ffn_forward(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                w3.data_ptr(), out.data_ptr(), M, K, N, float(eps),
                                                _stream_ptr(x.device)))
@@ -252,7 +262,7 @@ class FusedFFN:
         if w1.shape != w3.shape or w1.shape[1] != K or rms_w.shape != (K,):
             raise ValueError("shape mismatch")
         dst = (ctypes.c_void_p * len(dst_ptrs))(*[int(p_) for p_ in dst_ptrs])
-        self._weights_changed(rms_w, w1, w3, slot=0)
+        self._weights_changed({0: (rms_w, w1, w3)})
         self._check(self.lib.cuasm_ffn_forward_gather(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                       w3.data_ptr(), dst, len(dst_ptrs), 1 if multicast else 0,
                                                       int(ldo), M, K, N, float(eps), _stream_ptr(x.device)))
@@ -266,7 +276,7 @@ class FusedFFN:
         N = w1.shape[0]
         if out_host is None:
             out_host = torch.empty((M, N), dtype=self.dtype, pin_memory=True)
-        self._weights_changed(rms_w, w1, w3, slot=0)
+        self._weights_changed({0: (rms_w, w1, w3)})
         self._check(self.lib.cuasm_ffn_forward_host(self._h, x_host.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                     w3.data_ptr(), out_host.data_ptr(), M, K, N, float(eps),
                                                     _stream_ptr(w1.device), 1 if sync else 0))
@@ -284,7 +294,7 @@ class FusedFFN:
             out = torch.empty((M, N), dtype=self.dtype, device=x.device)
         else:
             self._validate(out)
-        self._weights_changed(w, slot=1)
+        self._weights_changed({1: (w,)})
         code = {"identity": ACT_IDENTITY, "leaky_relu": ACT_LEAKY_RELU}[act]
         self._check(self.lib.cuasm_gemm_act(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), M, K, N, code,
                                             float(alpha), _stream_ptr(x.device)))
@@ -302,7 +312,7 @@ class FusedFFN:
             out = torch.empty((M, K), dtype=self.dtype, device=x.device)
         else:
             self._validate(out)
-        self._weights_changed(rms_w, w1, w3, w2, slot=2)
+        self._weights_changed({0: (rms_w, w1, w3), 1: (w2,)})
         self._check(self.lib.cuasm_ffn_block_forward(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
                                                      w3.data_ptr(), w2.data_ptr(), out.data_ptr(), M, K, N,
                                                      float(eps), _stream_ptr(x.device)))
@@ -344,11 +354,14 @@ _handles: dict = {}
 
 
 def _handle(device, dtype) -> FusedFFN:
-    key = (torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device(),
-           dtype)
+    """The module-level handle for (device, dtype, current stream): a handle's
+    per-launch device state must not be shared by concurrent streams."""
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    key = (idx, dtype, torch.cuda.current_stream(idx).cuda_stream)
     h = _handles.get(key)
     if h is None:
-        h = FusedFFN(torch.device("cuda", key[0]), dtype)
+        h = FusedFFN(torch.device("cuda", idx), dtype)
         _handles[key] = h
     return h
 

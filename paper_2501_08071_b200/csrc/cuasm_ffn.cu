@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <new>
 #include <cstdarg>
@@ -12,6 +13,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/cuasm_ffn.h"
 #include "dual_gemm.cuh"
@@ -28,6 +31,16 @@ static_assert(GemmCfg<0, 1>::BN == kPackBN && GemmCfg<0, 2>::BN == kPackBN, "pac
 
 thread_local std::string g_init_error;
 
+// NVTX range around every computing entry point (header-only NVTX v3: a no-op
+// unless a tool -- nsys, ncu --nvtx -- is attached), so host timelines and
+// kernel captures can be filtered by API call.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -41,6 +54,7 @@ struct PackedWeights {
     const void* key_w1 = nullptr;
     const void* key_w3 = nullptr;
     int64_t key_K = 0, key_N = 0;
+    int64_t key_kp = 0;   // duplicated-K mode (fp32 split-x contraction), 0 = off
     bool packed = false;
     bool fresh = false;   // packed by a kernel the next GEMM launch directly follows (no early weight loads)
     CUtensorMap tmap;     // box {BK, tmap_rows}; tmap_rows = B_ROWS of the launched variant
@@ -69,7 +83,8 @@ struct cuasm_ffn_s {
     int sk_split = 0;  // CUASM_OPT_SK_SPLIT: max stream-K ranges per tile when tiles < clusters (0: 2)
     int last_tile_n = 256;
     int fused_norm = 1;  // CUASM_OPT_FUSED_NORM
-    uint32_t* gsync = nullptr;  // grid counters of the fused RMS pass (self-resetting)
+    uint32_t* rstate = nullptr;  // fused a1 bookkeeping: [2 * r-blocks + 1] words (self-resetting)
+    int64_t rstate_words = 0;
     unsigned long long* trace_buf = nullptr;
     int trace_ctas = 0;
     // stream-K workspace
@@ -83,6 +98,9 @@ struct cuasm_ffn_s {
     // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN;
     // slot 1 = a single packed weight (GEMM + activation / down projection)
     PackedWeights pw[2];
+    // fp32 handle: x split into [x_hi | x_lo] tf32 terms per forward (pack.cuh)
+    void* x2 = nullptr;
+    int64_t x2_bytes = 0;
     // FFN block: the hidden activation between the two GEMMs
     void* hidden = nullptr;
     int64_t hidden_bytes = 0;
@@ -151,10 +169,41 @@ cuasm_status_t check_eps(cuasm_ffn_t h, float eps) {
     return CUASM_OK;
 }
 
-cuasm_status_t set_device(cuasm_ffn_t h) {
-    int cur = -1;
-    CUASM_CHECK(h, cudaGetDevice(&cur), "cudaGetDevice");
-    if (cur != h->device) CUASM_CHECK(h, cudaSetDevice(h->device), "cudaSetDevice");
+// Makes the handle's device current for the lifetime of the guard and restores
+// the caller's current device afterwards (entry points must not leave it changed).
+struct DeviceGuard {
+    int prev = -1;
+    cuasm_status_t status = CUASM_OK;
+    explicit DeviceGuard(cuasm_ffn_t h) {
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e != cudaSuccess) {
+            prev = -1;
+            status = cuda_fail(h, e, "cudaGetDevice");
+            return;
+        }
+        if (prev != h->device && (e = cudaSetDevice(h->device)) != cudaSuccess) {
+            status = cuda_fail(h, e, "cudaSetDevice");
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// cudaFuncSetAttribute applies to the current device only: one bit per device
+// (up to 64) per kernel instantiation, set once the attribute is applied there.
+// Concurrent first calls may both apply it (harmless).
+template <typename Kernel>
+cuasm_status_t ensure_func_attr(cuasm_ffn_t h, Kernel kernel, std::atomic<uint64_t>& done, cudaFuncAttribute attr,
+                                int value, const char* what) {
+    const uint64_t bit = uint64_t(1) << (h->device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return CUASM_OK;
+    CUASM_CHECK(h, cudaFuncSetAttribute(kernel, attr, value), what);
+    done.fetch_or(bit, std::memory_order_acq_rel);
     return CUASM_OK;
 }
 
@@ -180,12 +229,12 @@ cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint
 // fused FFN (128-output blocks); w3 == null: one weight, 256-row blocks.
 template <typename T>
 cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
-                           int64_t N, cudaStream_t s) {
+                           int64_t N, cudaStream_t s, int64_t kp) {
     PackedWeights& w = h->pw[slot];
     const int BK = 128 / h->esize;  // one 128-byte swizzle row of K (= GemmCfg::BK)
     const int64_t rows_per_block = 2 * kPackBN;
     const int64_t n_blocks = w3 ? (N + kPackBN - 1) / kPackBN : (N + rows_per_block - 1) / rows_per_block;
-    const int64_t k_blocks = (K + BK - 1) / BK;
+    const int64_t k_blocks = kp > 0 ? 2 * kp / BK : (K + BK - 1) / BK;
     const int64_t rows = n_blocks * k_blocks * rows_per_block;
     const int64_t bytes = rows * 128;
     if (bytes > w.bytes) {
@@ -200,7 +249,7 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     const int64_t blocks = std::min<int64_t>((total_vec + threads - 1) / threads, int64_t(h->sm_count) * 16);
     cuasm::ffn_pack_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, s>>>(
         static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(w.buf), N, K,
-        kPackBN, n_blocks, k_blocks, BK);
+        kPackBN, n_blocks, k_blocks, BK, kp);
     CUASM_CHECK(h, cudaGetLastError(), "ffn_pack_kernel launch");
     w.rows = rows;
     w.tmap_rows = 0;  // re-encode for the new buffer
@@ -209,36 +258,38 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     w.key_w3 = w3;
     w.key_K = K;
     w.key_N = N;
+    w.key_kp = kp;
     w.packed = true;
     w.fresh = true;
     return CUASM_OK;
 }
 
 cuasm_status_t ensure_packed(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
-                             int64_t N, cudaStream_t s) {
+                             int64_t N, cudaStream_t s, int64_t kp = 0) {
     PackedWeights& w = h->pw[slot];
-    if (w.packed && w.key_g == g && w.key_w1 == w1 && w.key_w3 == w3 && w.key_K == K && w.key_N == N)
+    if (w.packed && w.key_g == g && w.key_w1 == w1 && w.key_w3 == w3 && w.key_K == K && w.key_N == N &&
+        w.key_kp == kp)
         return CUASM_OK;
     w.packed = false;
-    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, slot, g, w1, w3, K, N, s)
-                                        : launch_pack<float>(h, slot, g, w1, w3, K, N, s);
+    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, slot, g, w1, w3, K, N, s, kp)
+                                        : launch_pack<float>(h, slot, g, w1, w3, K, N, s, kp);
 }
+
+// fp32 handles: the K padding of the split-x contraction (one 32-float k-block)
+inline int64_t split_kp(int64_t K) { return (K + 31) / 32 * 32; }
 
 template <typename T>
 cuasm_status_t launch_prepass(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
                               cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        // Same L1/smem split as the dual GEMM (max shared): an SM running
-        // pre-pass CTAs can then take the PDL-launched GEMM CTA without a
-        // carveout reconfiguration, so the two kernels actually overlap.
-        CUASM_CHECK(h,
-                    cudaFuncSetAttribute(cuasm::ffn_rms_prepass_kernel<T>,
+    // Same L1/smem split as the dual GEMM (max shared): an SM running
+    // pre-pass CTAs can then take the PDL-launched GEMM CTA without a
+    // carveout reconfiguration, so the two kernels actually overlap.
+    static std::atomic<uint64_t> attr_done{0};
+    cuasm_status_t st = ensure_func_attr(h, cuasm::ffn_rms_prepass_kernel<T>, attr_done,
                                          cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         static_cast<int>(cudaSharedmemCarveoutMaxShared)),
-                    "cudaFuncSetAttribute(prepass carveout)");
-        attr_set = true;
-    }
+                                         static_cast<int>(cudaSharedmemCarveoutMaxShared),
+                                         "cudaFuncSetAttribute(prepass carveout)");
+    if (st != CUASM_OK) return st;
     const int64_t blocks = (M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock;
     cuasm::ffn_rms_prepass_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(static_cast<const T*>(x), r, M, K,
                                                                                     eps);
@@ -263,6 +314,11 @@ struct EpiSpec {
     int num_dst = 0;
     int dst_mc = 0;
     int64_t ldo = 0;
+    // fp32 split-x contraction (kp > 0): the pre-pass is ffn_split_tf32_kernel over the
+    // caller's x_src [M, k_src], writing r and the GEMM operand x = [x_hi | x_lo] [M, 2 kp]
+    const void* x_src = nullptr;
+    int64_t k_src = 0;
+    int64_t kp = 0;
 };
 
 // Few-tile decode shapes: at most this many 1-SM tiles take the 1-SM variant with
@@ -321,7 +377,8 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.use_r = e.use_r;
     p.act = e.act;
     p.alpha = e.alpha;
-    p.sync = h->gsync;
+    p.rstate = h->rstate;
+    p.n_rblk = static_cast<int>((M + 127) / 128);
     p.r = h->r;
     p.out = out;
     p.ldo = N;
@@ -372,17 +429,14 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.rep = rep;
     p.csplit = csplit;
 
-    static bool attr_set = false;  // one per template instance
-    if (!attr_set) {
-        CUASM_CHECK(h,
-                    cudaFuncSetAttribute(cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
-                    "cudaFuncSetAttribute(smem)");
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};  // per template instance, one bit per device
+    st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, attr_done,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES, "cudaFuncSetAttribute(smem)");
+    if (st != CUASM_OK) return st;
     if (csplit) {
-        // the whole grid must be co-resident (fused RMS grid barrier); clusters are placed
-        // inside one GPC, so S-CTA clusters may not all fit (S = 8 over 16 tiles did not)
+        // one wave: every cluster must fit at once, or the split loses to a second wave
+        // (clusters are placed inside one GPC, so S-CTA clusters may not all fit: S = 8
+        // over 16 tiles did not); correctness does not depend on it (no inter-cluster waits)
         cudaLaunchConfig_t qc = {};
         qc.gridDim = dim3(static_cast<unsigned>(p.num_tiles * csplit), 1, 1);
         qc.blockDim = dim3(C::NUM_THREADS, 1, 1);
@@ -660,15 +714,33 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
             CUASM_CHECK(h, cudaMalloc(&h->trace_buf, sizeof(unsigned long long) * 16 * 1024), "cudaMalloc(trace)");
         CUASM_CHECK(h, cudaMemsetAsync(h->trace_buf, 0, sizeof(unsigned long long) * 16 * 1024, s), "memset(trace)");
     }
-    if (e.fused_norm && !h->gsync) {
-        CUASM_CHECK(h, cudaMalloc(&h->gsync, 64), "cudaMalloc(grid counters)");
-        CUASM_CHECK(h, cudaMemset(h->gsync, 0, 64), "cudaMemset(grid counters)");
+    if (e.fused_norm) {
+        // fused a1 bookkeeping: 2 words per 128-row r-block + the warp counter, zeroed once
+        // (the kernel leaves it zeroed for the next launch)
+        const int64_t words = 2 * ((M + 127) / 128) + 1;
+        if (words > h->rstate_words) {
+            if (h->rstate) cudaFree(h->rstate);
+            h->rstate = nullptr;
+            h->rstate_words = 0;
+            const int64_t cap = std::max<int64_t>(words, 2 * 64 + 1);
+            CUASM_CHECK(h, cudaMalloc(&h->rstate, cap * 4), "cudaMalloc(r-block state)");
+            CUASM_CHECK(h, cudaMemset(h->rstate, 0, cap * 4), "cudaMemset(r-block state)");
+            h->rstate_words = cap;
+        }
     }
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     // a1: fused into the dual GEMM by default; the separate pre-pass kernel
     // (PDL primary of the GEMM) when CUASM_OPT_FUSED_NORM = 0
     const bool separate_prepass = e.use_r && !e.fused_norm;
-    if (separate_prepass && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) return st;
+    if (separate_prepass && e.kp > 0) {
+        const unsigned blocks = static_cast<unsigned>((M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock);
+        cuasm::ffn_split_tf32_kernel<<<blocks, 256, 0, s>>>(static_cast<const float*>(e.x_src),
+                                                             static_cast<float*>(const_cast<void*>(x)), h->r, M,
+                                                             e.k_src, e.kp, eps);
+        CUASM_CHECK(h, cudaGetLastError(), "ffn_split_tf32_kernel launch");
+    } else if (separate_prepass && (st = prepass(h, x, h->r, M, K, eps, s)) != CUASM_OK) {
+        return st;
+    }
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
     const Plan plan = plan_config(h, M, K, N, kepi == 0 ? 128 : 256);
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
@@ -684,15 +756,42 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     return CUASM_OK;
 }
 
+// a0 (if needed) then a1-a3 of the fused FFN with epilogue spec `e`.  fp32 handles
+// contract the exact tf32 split [x_hi | x_lo] of x with duplicated-K weights
+// (pack.cuh ffn_split_tf32_kernel; R5).
+cuasm_status_t ffn_common(cuasm_ffn_t h, EpiSpec e, const void* x, const void* g, const void* w1, const void* w3,
+                          void* out, int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
+    cuasm_status_t st;
+    if (h->dtype == CUASM_DTYPE_FP32) {
+        const int64_t kp = split_kp(K);
+        if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s, kp)) != CUASM_OK) return st;
+        const int64_t xb = std::max<int64_t>(M, 1) * 2 * kp * 4;
+        if (xb > h->x2_bytes) {
+            if (h->x2) cudaFree(h->x2);
+            h->x2 = nullptr;
+            h->x2_bytes = 0;
+            CUASM_CHECK(h, cudaMalloc(&h->x2, xb), "cudaMalloc(split x)");
+            h->x2_bytes = xb;
+        }
+        e.fused_norm = 0;
+        e.x_src = x;
+        e.k_src = K;
+        e.kp = kp;
+        return run_gemm(h, 0, e, h->x2, out, M, 2 * kp, N, eps, s);
+    }
+    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    return run_gemm(h, 0, e, x, out, M, K, N, eps, s);
+}
+
 // The fused FFN (a0 if needed, then a1-a3).
 cuasm_status_t forward_impl(cuasm_ffn_t h, const void* x, const void* g, const void* w1, const void* w3, void* out,
                             int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
     cuasm_status_t st;
     h->last_kernels = 0;
-    if ((st = set_device(h)) != CUASM_OK) return st;
-    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     const EpiSpec e{0, h->fused_norm, 1, 0, 0.f};
-    return run_gemm(h, 0, e, x, out, M, K, N, eps, s);
+    return ffn_common(h, e, x, g, w1, w3, out, M, K, N, eps, s);
 }
 
 // The fused FFN with step a4 in its epilogue: every output store goes to each
@@ -702,21 +801,22 @@ cuasm_status_t forward_gather_impl(cuasm_ffn_t h, const void* x, const void* g, 
                                    int64_t N, float eps, cudaStream_t s) {
     cuasm_status_t st;
     h->last_kernels = 0;
-    if ((st = set_device(h)) != CUASM_OK) return st;
-    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     EpiSpec e{0, h->fused_norm, 1, 0, 0.f};
     e.dst = dst;
     e.num_dst = num_dst;
     e.dst_mc = mc;
     e.ldo = ldo;
-    return run_gemm(h, 0, e, x, mc ? nullptr : dst[0], M, K, N, eps, s);
+    return ffn_common(h, e, x, g, w1, w3, mc ? nullptr : dst[0], M, K, N, eps, s);
 }
 
 // out = act(x . w^T): the single-weight GEMM + activation path.
 cuasm_status_t gemm_act_impl(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K, int64_t N,
                              int act, float alpha, cudaStream_t s) {
     cuasm_status_t st;
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     if ((st = ensure_packed(h, 1, nullptr, w, nullptr, K, N, s)) != CUASM_OK) return st;
     h->last_kernels = 0;
     const EpiSpec e{1, 0, 0, act, alpha};
@@ -790,6 +890,7 @@ cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* out, int device, cuasm_dtype_t dtype)
 
 cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
                                  void* out, int64_t M, int64_t K, int64_t N, float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_forward");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
@@ -800,6 +901,7 @@ cuasm_status_t cuasm_ffn_forward(cuasm_ffn_t h, const void* x, const void* rms_w
 cuasm_status_t cuasm_ffn_forward_gather(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
                                         const void* w3, void* const* dst, int num_dst, int multicast, int64_t ldo,
                                         int64_t M, int64_t K, int64_t N, float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_forward_gather");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     if (!dst || num_dst < 1 || num_dst > 8) return fail(h, CUASM_ERR_INVALID_ARG, "num_dst must be in [1, 8]");
@@ -821,6 +923,7 @@ cuasm_status_t cuasm_ffn_forward_gather(cuasm_ffn_t h, const void* x, const void
 cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const void* rms_w, const void* w1,
                                       const void* w3, void* out_host, int64_t M, int64_t K, int64_t N, float eps,
                                       void* stream, int sync) {
+    NvtxRange nvtx_("cuasm_ffn_forward_host");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     cuasm_status_t st;
@@ -829,7 +932,8 @@ cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const v
     if ((st = check_eps(h, eps)) != CUASM_OK) return st;
     if (M < 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31)");
     if (M > 0 && (!x_host || !out_host)) return fail(h, CUASM_ERR_INVALID_ARG, "NULL host pointer");
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t xb = M * K * h->esize, ob = M * N * h->esize;
     if (xb > h->x_stage_bytes) {
@@ -897,6 +1001,7 @@ cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const v
 
 cuasm_status_t cuasm_gemm_act(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K, int64_t N,
                               int act, float alpha, void* stream) {
+    NvtxRange nvtx_("cuasm_gemm_act");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     h->last_kernels = 0;
@@ -915,12 +1020,14 @@ cuasm_status_t cuasm_gemm_act(cuasm_ffn_t h, const void* x, const void* w, void*
 cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
                                        const void* w3, const void* w2, void* out, int64_t M, int64_t K, int64_t N,
                                        float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_block_forward");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
     if (st != CUASM_OK) return st;
     if (!w2 || !aligned16(w2)) return fail(h, CUASM_ERR_INVALID_ARG, "w2 must be non-NULL and 16-byte aligned");
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t hb = M * N * h->esize;
     if (hb > h->hidden_bytes) {
@@ -942,6 +1049,7 @@ cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void*
 
 cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x, const void* rms_w, void* out, int64_t M, int64_t K,
                              float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_rmsnorm");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     h->last_kernels = 0;
@@ -953,7 +1061,8 @@ cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x, const void* rms_w, vo
     if (M == 0) return CUASM_OK;
     if (!x || !out || !aligned16(x) || !aligned16(out))
         return fail(h, CUASM_ERR_INVALID_ARG, "x and out must be non-NULL and 16-byte aligned");
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const unsigned blocks = static_cast<unsigned>((M + cuasm::kPrepassRowsPerBlock - 1) / cuasm::kPrepassRowsPerBlock);
     if (h->dtype == CUASM_DTYPE_BF16) {
@@ -972,18 +1081,22 @@ cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x, const void* rms_w, vo
 
 cuasm_status_t cuasm_ffn_prepare(cuasm_ffn_t h, const void* rms_w, const void* w1, const void* w3, int64_t K,
                                  int64_t N, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_prepare");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     cuasm_status_t st;
     if ((st = check_common(h, K, N)) != CUASM_OK) return st;
     if ((st = check_weights(h, rms_w, w1, w3)) != CUASM_OK) return st;
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     h->pw[0].packed = false;
-    return ensure_packed(h, 0, rms_w, w1, w3, K, N, static_cast<cudaStream_t>(stream));
+    return ensure_packed(h, 0, rms_w, w1, w3, K, N, static_cast<cudaStream_t>(stream),
+                         h->dtype == CUASM_DTYPE_FP32 ? split_kp(K) : 0);
 }
 
 cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t M, int64_t K, float eps,
                                  void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_rms_inv");
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
     h->err.clear();
     if (K <= 0 || K % 8 != 0) return fail(h, CUASM_ERR_INVALID_ARG, "K must be a positive multiple of 8");
@@ -994,7 +1107,8 @@ cuasm_status_t cuasm_ffn_rms_inv(cuasm_ffn_t h, const void* x, float* r, int64_t
     if (!x || !r) return fail(h, CUASM_ERR_INVALID_ARG, "NULL pointer");
     if (!aligned16(x) || (reinterpret_cast<uintptr_t>(r) & 3u))
         return fail(h, CUASM_ERR_INVALID_ARG, "x must be 16-byte and r 4-byte aligned");
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     return prepass(h, x, r, M, K, eps, static_cast<cudaStream_t>(stream));
 }
 
@@ -1005,7 +1119,8 @@ cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst, int64_t* bytes) {
     *bytes = b;
     if (!dst) return CUASM_OK;
     cuasm_status_t st;
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     CUASM_CHECK(h, cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     CUASM_CHECK(h, cudaMemcpy(dst, h->pw[0].buf, b, cudaMemcpyDeviceToHost), "D2H W13");
     return CUASM_OK;
@@ -1104,7 +1219,8 @@ cuasm_status_t cuasm_ffn_trace_read(cuasm_ffn_t h, unsigned long long* dst, int*
     *ctas = h->trace_buf ? h->trace_ctas : 0;
     if (!dst || !h->trace_buf) return CUASM_OK;
     cuasm_status_t st;
-    if ((st = set_device(h)) != CUASM_OK) return st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
     CUASM_CHECK(h, cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     CUASM_CHECK(h, cudaMemcpy(dst, h->trace_buf, sizeof(unsigned long long) * 16 * h->trace_ctas,
                               cudaMemcpyDeviceToHost),
@@ -1115,7 +1231,7 @@ cuasm_status_t cuasm_ffn_trace_read(cuasm_ffn_t h, unsigned long long* dst, int*
 cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     if (!h) return CUASM_OK;
     if (h->trace_buf) cudaFree(h->trace_buf);
-    if (h->gsync) cudaFree(h->gsync);
+    if (h->rstate) cudaFree(h->rstate);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
     if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
@@ -1126,6 +1242,7 @@ cuasm_status_t cuasm_ffn_destroy(cuasm_ffn_t h) {
     for (PackedWeights& w : h->pw)
         if (w.buf) cudaFree(w.buf);
     if (h->hidden) cudaFree(h->hidden);
+    if (h->x2) cudaFree(h->x2);
     if (h->x_stage) cudaFree(h->x_stage);
     if (h->out_stage) cudaFree(h->out_stage);
     if (h->ws) cudaFree(h->ws);

@@ -56,7 +56,12 @@ struct FfnGemmParams {
     int use_r;       // 1: scale the accumulators by r[m] (RMSNorm); 0: r = 1 (plain GEMM)
     int act;         // kEpi == 1 only: 0 identity, 1 LeakyReLU with negative slope `alpha`
     float alpha;
-    uint32_t* sync;  // [0] warps done writing r, [1] CTAs exited (self-resetting)
+    // Fused a1 bookkeeping (self-resetting, DESIGN.md §6 "Fused a1"): r is computed per
+    // 128-row r-block on demand by the CTAs that need it.  rstate[rb] counts rows of
+    // r-block rb taken, rstate[n_rblk + rb] rows done (published), rstate[2 n_rblk] the
+    // epilogue warps past their last r acquisition (the last one resets everything).
+    uint32_t* rstate;
+    int n_rblk;      // r-blocks: ceil(M / 128)
     float* r;        // [M] inverse RMS (written here when fused_norm, else by the pre-pass)
     void* out;       // [M, ldo] row-major, dtype of the handle (== dst[0] unless multicast)
     int64_t ldo;     // leading dimension of out / every dst, elements
@@ -125,21 +130,26 @@ __device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
 
 // Per-cluster walk over its work: first whole data-parallel tiles
 // (cluster, cluster + C, ...), then its contiguous stream-K iteration range
-// cut at tile boundaries.  Every role of the CTA (producer, MMA, epilogue)
-// walks the identical sequence.  In a stream-K range only the first segment
-// can start mid-tile (a "contributor": it publishes an fp32 partial) and only
-// the last can end mid-tile while starting at k-block 0 (the "finisher": it
-// adds the later clusters' partials and runs the epilogue).
+// cut at tile boundaries and walked BACKWARDS (from the range's end).  Every
+// role of the CTA (producer, MMA, epilogue) walks the identical sequence.  In
+// a stream-K range only the first segment walked can end mid-tile (it holds
+// the start of a tile whose end belongs to a higher cluster: a "contributor",
+// it publishes an fp32 partial) and only the last walked can start mid-tile
+// while holding the tile's last k-block (the "finisher": it adds the partials
+// of the LOWER clusters holding the rest of the tile and runs the epilogue).
+// Waits therefore point only to lower cluster ids -- CTAs dispatched earlier,
+// resident or done -- so the schedule needs no co-residency of the grid, and a
+// contributor publishes its partial first thing while the finisher adds it last.
 struct Sched {
     int next_dp, C, KB, T_dp, kb_lo, kb_hi;
-    int64_t cur, end;
+    int64_t beg, cur;  // stream-K range [beg, cur) still to walk (cur moves down)
     __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster, int part = 0) {
         next_dp = cluster;
         C = p.num_clusters;
         KB = p.num_k_blk;
         T_dp = p.num_dp_tiles;
-        cur = sk_begin(p, cluster);
-        end = sk_begin(p, cluster + 1);
+        beg = sk_begin(p, cluster);
+        cur = sk_begin(p, cluster + 1);
         // cluster split-K: this CTA's share of every tile's k-blocks
         kb_lo = p.csplit ? part * KB / p.csplit : 0;
         kb_hi = p.csplit ? (part + 1) * KB / p.csplit : KB;
@@ -152,14 +162,14 @@ struct Sched {
             next_dp += C;
             return true;
         }
-        if (cur < end) {
-            const int64_t t = static_cast<uint32_t>(cur) / static_cast<uint32_t>(KB);
-            const int kb0 = static_cast<int>(cur - t * KB);
-            const int64_t take = (KB - kb0) < (end - cur) ? (KB - kb0) : (end - cur);
+        if (cur > beg) {
+            const int64_t t = static_cast<uint32_t>(cur - 1) / static_cast<uint32_t>(KB);
+            const int64_t t0 = t * KB;
+            const int64_t lo = t0 > beg ? t0 : beg;
             s.tile = T_dp + static_cast<int>(t);
-            s.kb0 = kb0;
-            s.kb1 = kb0 + static_cast<int>(take);
-            cur += take;
+            s.kb0 = static_cast<int>(lo - t0);
+            s.kb1 = static_cast<int>(cur - t0);
+            cur = lo;
             return true;
         }
         return false;
@@ -960,48 +970,73 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         // ========================= epilogue =============================
         ptx::pdl_wait();  // x / r[] come from the preceding kernel (PDL primary)
         if (warp == 2 && lane == 0) trace_stamp(p, 4);
-        const uint32_t ewarp0 = warp - 2;
-        if (p.fused_norm) {
-            // Fused step a1: this CTA's epilogue warps compute
-            // r[m] = 1/sqrt(sum_k x^2/K + eps) for a 1/gridDim slice of the rows
-            // while the first tile's mainloop runs (they would idle otherwise),
-            // then publish through a grid-wide counter; every epilogue waits on
-            // it before its first read of r.  All CTAs are co-resident (one
-            // persistent CTA per SM), so the wait cannot deadlock.
-            const int64_t per = (static_cast<int64_t>(p.M) + gridDim.x - 1) / gridDim.x;
-            const int64_t r0 = per * blockIdx.x;
-            const int64_t r1 = min(static_cast<int64_t>(p.M), r0 + per);
-            using T = typename std::conditional<kKind == 0, __nv_bfloat16, float>::type;
-            for (int64_t m = r0 + ewarp0; m < r1; m += C::NUM_EPI_WARPS)
-                rms_row<T>(static_cast<const T*>(p.x), p.r, m, p.K, p.eps, lane);
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) atomicAdd(p.sync, 1u);
+        using T = typename std::conditional<kKind == 0, __nv_bfloat16, float>::type;
+        // Fused step a1 (DESIGN.md §6 "Fused a1"): r[m] = 1/sqrt(sum_k x^2/K + eps) is
+        // computed on demand per 128-row r-block.  The epilogue warps of a CTA about to
+        // read r of r-block rb (all eight, at the same tile) each take rows of rb one at a
+        // time from the block's counter while rows remain -- every CTA that needs the
+        // block helps -- and publish each row (fence + done count); then one warp waits
+        // for the block's done count and a named barrier releases the others.  A CTA
+        // waits only for rows taken by warps already running, so no co-residency of the
+        // grid is assumed (other kernels / MPS may hold SMs).  Each CTA counts itself
+        // once past its last acquisition; the last CTA of the grid resets the
+        // bookkeeping for the next launch (graph-safe), under its last tile's mainloop.
+        const bool fused = p.fused_norm != 0;
+        int r_left = 0;  // r-reading (non-contributor) segments of this CTA's schedule
+        if (fused) {
+            Sched s2;
+            s2.init(p, cluster_id, static_cast<int>(part));
+            Seg g2;
+            while (s2.next(g2)) r_left += (csplit || g2.kb1 == p.num_k_blk) ? 1 : 0;
         }
-        bool r_ready = !p.fused_norm;
-        // Wait until every epilogue warp of the grid has published its rows of r, then count
-        // this warp as past the wait; the last warp past it resets both grid counters for the
-        // next launch (graph-safe: nobody reads them again in this launch).  The returning
-        // atomic sits here, under the first tile's mainloop, not on the kernel's exit path.
-        auto acquire_r = [&]() {
-            const uint32_t target = gridDim.x * C::NUM_EPI_WARPS;
-            if (ld_acquire_u32(p.sync) < target) {
+        auto r_done_cta = [&]() {  // warp 2 of the CTA, after the CTA's last acquisition
+            uint32_t* cnt = p.rstate + 2 * p.n_rblk;
+            uint32_t last = 0;
+            if (lane == 0) last = atomicAdd(cnt, 1u) == gridDim.x - 1 ? 1u : 0u;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                for (int i = static_cast<int>(lane); i < 2 * p.n_rblk; i += 32) p.rstate[i] = 0u;
+                __syncwarp();
+                if (lane == 0) *cnt = 0u;
+            }
+            __syncwarp();
+        };
+        if (fused && r_left == 0 && warp == 2) r_done_cta();
+        auto acquire_r = [&](int rb) {
+            const int row0 = rb * C::BM;
+            if (row0 >= p.M) return;  // (2-SM decode: the peer CTA's rows are all past M); CTA-uniform
+            const uint32_t nrows = static_cast<uint32_t>(min(C::BM, p.M - row0));
+            uint32_t* taken = p.rstate + rb;
+            uint32_t* done = p.rstate + p.n_rblk + rb;
+            uint32_t help = 0;
+            if (lane == 0) help = ld_acquire_u32(done) < nrows && *reinterpret_cast<volatile uint32_t*>(taken) < nrows;
+            if (__shfl_sync(0xffffffffu, help, 0)) {
+                for (;;) {
+                    uint32_t i = 0;
+                    if (lane == 0) i = atomicAdd(taken, 1u);
+                    i = __shfl_sync(0xffffffffu, i, 0);
+                    if (i >= nrows) break;
+                    rms_row<T>(static_cast<const T*>(p.x), p.r, row0 + static_cast<int64_t>(i), p.K, p.eps,
+                               static_cast<int>(lane));
+                    if (lane == 0) {
+                        __threadfence();  // r[row] (written by this lane) before the count
+                        atomicAdd(done, 1u);
+                    }
+                }
+            }
+            ptx::named_bar_sync(1, 32 * C::NUM_EPI_WARPS);
+            if (warp == 2 && lane == 0 && ld_acquire_u32(done) < nrows) {
 #if CUASM_WATCHDOG
                 const long long t0 = clock64();
 #endif
-                while (ld_acquire_u32(p.sync) < target) {
-                    __nanosleep(100);
+                while (ld_acquire_u32(done) < nrows) {
+                    __nanosleep(128);
 #if CUASM_WATCHDOG
                     if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
 #endif
                 }
             }
-            if (lane == 0 && atomicAdd(p.sync + 1, 1u) == target - 1) {
-                p.sync[0] = 0u;
-                p.sync[1] = 0u;
-                __threadfence();
-            }
-            __syncwarp();
+            ptx::named_bar_sync(1, 32 * C::NUM_EPI_WARPS);  // (the r loads of every warp follow it)
         };
         const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t ewarp = warp - 2;  // 0..7: flag slot
@@ -1022,8 +1057,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
                             static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 + lane : row_in_cta);
             const bool row_ok = row < p.M;
-            const bool contributor = !csplit && sg.kb0 > 0;                       // stream-K: partial, not the tile's start
-            const bool finisher = !csplit && sg.kb0 == 0 && sg.kb1 < p.num_k_blk;  // owns the tile's start, others add in
+            // stream-K (Sched): a contributor lacks the tile's last k-block and publishes a
+            // partial; the finisher holds the last k-block but not the first and adds the
+            // partials of the lower clusters holding the rest of the tile
+            const bool contributor = !csplit && sg.kb1 < p.num_k_blk;
+            const bool finisher = !csplit && sg.kb1 == p.num_k_blk && sg.kb0 > 0;
             // this CTA's 128 x 2BN fp32 partial slot, lane-contiguous so every warp
             // access is 512 contiguous bytes: float4 index ((chunk*4 + quad)*8 + q)*32 + lane
             // holds columns chunk*32 + 4q..+3 of row quad*32 + lane (chunk < BN/32: h1, else h3)
@@ -1031,10 +1069,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                               (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
             int c_first = 0, c_last = -1;
             if (finisher) {
-                // contributors: the clusters whose stream-K ranges cover the rest of this tile
-                const int64_t tile_end = static_cast<int64_t>(sg.tile - p.num_dp_tiles + 1) * p.num_k_blk - 1;
-                c_first = cluster_id + 1;
-                c_last = sk_owner(p, tile_end);
+                // contributors: the (lower) clusters whose stream-K ranges cover the rest of this tile
+                const int64_t tile_start = static_cast<int64_t>(sg.tile - p.num_dp_tiles) * p.num_k_blk;
+                c_first = sk_owner(p, tile_start);
+                c_last = cluster_id - 1;
                 // pull the partials this warp will add into L2 while the accumulator
                 // is still being computed (L2 is the coherence point: safe before the flag)
                 for (int cc = c_first; cc <= c_last; ++cc) {
@@ -1052,9 +1090,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     }
                 }
             }
-            if (!r_ready) {
-                acquire_r();
-                r_ready = true;
+            if (fused && (csplit || !contributor)) {
+                acquire_r(csplit ? mb : mb * kCtaGroup + static_cast<int>(cta_rank));
+                if (--r_left == 0 && warp == 2) r_done_cta();
             }
             if (csplit && split_k_push_fits<C, kKind>(min(C::BM, p.M - mb * C::TILE_M), p.csplit)) {
                 // cluster split-K, push form.  Pass 0 runs the same code dry (no TMEM
@@ -1233,8 +1271,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
-        // a warp with no tile still has to be counted past the r wait (counter reset)
-        if (!r_ready) acquire_r();
     }
 
     // every TMA store this warp issued has written global memory before the CTA retires

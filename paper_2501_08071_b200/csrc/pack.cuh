@@ -17,6 +17,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "prepass.cuh"
+
 namespace cuasm {
 
 __device__ __forceinline__ uint32_t fold_bf16x2(uint32_t w, uint32_t g) {
@@ -46,11 +48,16 @@ __device__ __forceinline__ uint32_t fold_tf32(uint32_t w, uint32_t g) {
 // zero where nb*BN + rr >= N (N tail) or kb*BK + i >= K (K tail).
 // Single-source mode (w3 == nullptr, the plain GEMM + activation path):
 //   Wt[nb][kb][r][i] = RNE(W[nb*2BN + r][kb*BK + i] * g[kb*BK + i])  (g == nullptr: g = 1)
+//
+// Duplicated-K mode (kp > 0, the fp32 handle's split-x contraction, R5):
+// the packed K axis has 2*kp columns and column j reads source column j mod kp,
+// so the weights meet x_hi in k-blocks [0, kp/BK) and x_lo in [kp/BK, 2kp/BK)
+// (ffn_split_tf32_kernel below).
 template <typename T>
 __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1, const T* __restrict__ w3,
                                                        const T* __restrict__ g, T* __restrict__ w13, int64_t N,
                                                        int64_t K, int BN, int64_t n_blocks, int64_t k_blocks,
-                                                       int BK) {
+                                                       int BK, int64_t kp) {
     constexpr int kVec = 16 / sizeof(T);
     const int vrow = BK / kVec;  // 16-byte vectors per packed row (8)
     const int64_t total = n_blocks * k_blocks * 2 * BN * vrow;
@@ -67,7 +74,8 @@ __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1,
         // single source (w3 == null): the block's 2*BN rows are W rows nb*2BN + r2
         const int j = (w3 != nullptr && r2 >= BN) ? 1 : 0;
         const int64_t n = w3 != nullptr ? nb * BN + (r2 - j * BN) : nb * 2 * BN + r2;
-        const int64_t k = kb * BK + static_cast<int64_t>(v) * kVec;  // K % 8 == 0: a vector is all in or all out
+        int64_t k = kb * BK + static_cast<int64_t>(v) * kVec;  // K % 8 == 0: a vector is all in or all out
+        if (kp > 0 && k >= kp) k -= kp;                           // duplicated-K mode
         uint4 o = make_uint4(0, 0, 0, 0);
         if (n < N && k < K) {
             const T* src = (j == 0 ? w1 : w3) + n * K + k;
@@ -89,6 +97,43 @@ __global__ void __launch_bounds__(256) ffn_pack_kernel(const T* __restrict__ w1,
             }
         }
         dst[idx] = o;
+    }
+}
+
+// fp32 handle, per forward (R5): kind::tf32 MMAs read 10 explicit
+// mantissa bits of each operand.  The folded weights are tf32 by definition of
+// the fold (above); x is split exactly into two tf32 terms,
+//     x_hi = RNE_tf32(x),  x_lo = RNE_tf32(x - x_hi)   (x - x_hi is exact in fp32),
+// |x - x_hi - x_lo| <= 2^-22 |x|, and the GEMM contracts [x_hi | x_lo] (K' = 2 kp)
+// with the duplicated-K weights: sum_k x_hi W + x_lo W = x W to fp32 accuracy.
+// One warp per row also writes r[row] (step a1), so the GEMM's epilogue needs no
+// fused pass.  Output row layout: x2[row][0, kp) = x_hi, x2[row][kp, 2kp) = x_lo,
+// zero past K.  Triggers PDL at entry like the pre-pass.
+__global__ void __launch_bounds__(256) ffn_split_tf32_kernel(const float* __restrict__ x, float* __restrict__ x2,
+                                                             float* __restrict__ r, int64_t M, int64_t K, int64_t kp,
+                                                             float eps) {
+    ptx::pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kPrepassRowsPerBlock + warp;
+    if (row >= M) return;
+    rms_row<float>(x, r, row, K, eps, lane);
+    const float4* xr = reinterpret_cast<const float4*>(x + row * K);
+    float4* hi = reinterpret_cast<float4*>(x2 + row * 2 * kp);
+    float4* lo = reinterpret_cast<float4*>(x2 + row * 2 * kp + kp);
+    auto split = [](float v, float& h) {
+        h = __uint_as_float(rne_tf32_bits(__float_as_uint(v)));
+        return __uint_as_float(rne_tf32_bits(__float_as_uint(v - h)));
+    };
+    for (int64_t i = lane; i < kp / 4; i += 32) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f), h, l;
+        if (4 * i < K) v = __ldg(xr + i);  // K % 8 == 0: a float4 is all in or all out
+        l.x = split(v.x, h.x);
+        l.y = split(v.y, h.y);
+        l.z = split(v.z, h.z);
+        l.w = split(v.w, h.w);
+        hi[i] = h;
+        lo[i] = l;
     }
 }
 

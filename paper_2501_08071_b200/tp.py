@@ -118,10 +118,17 @@ def ffn_tp_forward(x, rms_w, w1_shard, w3_shard, eps: float = 1e-6, group=None, 
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         fg = fused or FusedGather(x.shape[0], N, x.dtype, x.device, group)
+        if tuple(fg.buf.shape) != (x.shape[0], N) or fg.buf.dtype != x.dtype:
+            raise ValueError(f"FusedGather buffer {tuple(fg.buf.shape)} {fg.buf.dtype} does not match the "
+                             f"output [{x.shape[0]}, {N}] {x.dtype}")
         n0, n1 = shard_bounds(N, rank, world)
         if w1_shard.shape[0] != n1 - n0:
             raise ValueError("w1_shard width does not match this rank's shard")
         dst, mc = fg.destinations(n0)
+        # every peer has finished reading the previous output held in the buffers
+        # before any rank's epilogue stores into them again
+        if fused is not None:
+            fg.barrier()
         h.forward_gather(x, rms_w, w1_shard, w3_shard, dst, N, eps, multicast=mc)
         fg.barrier()
         return fg.buf

@@ -35,5 +35,7 @@ s|acc += load_elem(x, x_dtype, m \* K + k) \* load_elem(w, w_dtype, n \* K + k);
 s|for (int64_t n = 0; n < N; ++n) acc += hid\[i \* N + n\] \* load_elem(w2, w_dtype, j \* N + n);|for (int64_t n = 0; n < N; ++n) acc += hid[i * N + n] * load_elem(w2, w_dtype, n * K + j % N);|
 s|for (int64_t i = 0; i < nrows \* N; ++i) hid\[i\] = oracle_round_bf16(hid\[i\]);|for (int64_t i = 0; i < nrows * N; ++i) hid[i] = (double)(float)hid[i];|
 s|out\[m \* K + k\] = load_elem(x, x_dtype, m \* K + k) \* r \* load_elem(g, g_dtype, k);|out[m * K + k] = load_elem(x, x_dtype, m * K + k) * r;|
+s|a = oracle_round_tf32((double)(float)(a \* G\[k\]));|a = a * G[k];|
+s|b = oracle_round_tf32((double)(float)(b \* G\[k\]));|b = oracle_round_bf16(b * G[k]);|
 MUTS
 exit $status

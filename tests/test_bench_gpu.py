@@ -48,6 +48,18 @@ def test_default_line_carries_the_contract_keys():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     assert d["back_to_back"]["value"] > 0
+    # a1 runs inside the GEMM by default: no field may be derived from an empty pre-pass span
+    assert "prepass_GBps" not in r and "gemm_share_of_step" not in r and "prepass" in r
+    ps = d["prepass_standalone"]
+    assert ps["kernel"] == "ffn_rms_prepass_kernel" and 0 < ps["frac_of_hbm"] < 1.2
+    pr = d["protocol_5x100"]
+    assert pr["runs"] == 5 and len(pr["ms_per_step_runs"]) == 5 and pr["value_mean"] > 0
+
+
+def test_fp32_e2e_bytes_use_the_element_size():
+    d = run_bench("--workload", "tiny_fp32", "--steps", "5", "--warmup", "3", "--skip-cpu-baseline",
+                  "--skip-b2b", "--protocol-runs", "0")
+    assert d["e2e"]["h2d_bytes_per_step"] == 16 * 64 * 4 and d["e2e"]["d2h_bytes_per_step"] == 16 * 128 * 4
 
 
 def test_reference_arm_line():

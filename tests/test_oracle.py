@@ -234,6 +234,42 @@ def test_fold_tf32_exact_on_family_T():
     np.testing.assert_allclose(fold, plain, rtol=1e-12, atol=1e-15)
 
 
+def _tf32_rne_py(v: float) -> float:
+    """Python-float RNE to 11 significant bits (round() is half-even): an
+    implementation independent of the oracle's bit-level rne_f32_bits."""
+    if v == 0 or not math.isfinite(v):
+        return v
+    m, e = math.frexp(v)
+    return math.ldexp(round(m * 2 ** 11) / 2 ** 11, e)
+
+
+def test_fold_tf32_mode_on_full_entropy_fp32():
+    """fold_tf32 mode (the fp32 handle's method, R4/R5) on family-C fp32
+    data, where the fold's rounding really changes the result: equal to the torch
+    float64 composition on weights folded by an independent Python rounding,
+    RNE_tf32(RNE_fp32(W*g)), and NOT equal to the plain definition."""
+    d = make_inputs(12, 96, 40, family="C", seed=18, dtype="fp32")
+    eps = 1e-6
+    g = d["g"].double()
+    fold = np.vectorize(_tf32_rne_py)
+    w1t = torch.from_numpy(fold((d["w1"].double() * g).float().double().numpy()))
+    w3t = torch.from_numpy(fold((d["w3"].double() * g).float().double().numpy()))
+    x = d["x"].double()
+    r = 1.0 / torch.sqrt((x * x).mean(dim=1, keepdim=True) + eps)
+    h1 = r * (x @ w1t.T)
+    h3 = r * (x @ w3t.T)
+    ref = (F.silu(h1) * h3).numpy()
+    got = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], eps, mode="fold_tf32")
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-14)
+    plain = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], eps, mode="plain")
+    # the tf32 fold moves outputs by ~2^-11 relative: far above fp64 rounding
+    assert np.max(np.abs(got - plain)) > 1e-6
+    # and it is not the bf16 fold either (8 vs 11 significant bits)
+    bf = oracle.ffn(d["x"].to(torch.bfloat16), d["g"].to(torch.bfloat16), d["w1"].to(torch.bfloat16),
+                    d["w3"].to(torch.bfloat16), eps, mode="fold_bf16")
+    assert not np.allclose(got, bf, rtol=1e-6, atol=0)
+
+
 def test_tolerance_helper():
     ref = np.array([1.0, -2.0, 0.0, 10.0])
     gpu = ref + np.array([0.02, -0.04, 0.001, 0.3])

@@ -84,9 +84,13 @@ def test_pack_fp32_is_the_oracle_tf32_fold(cuda_device):
     h.prepare(t["g"], t["w1"], t["w3"])
     torch.cuda.synchronize()
     packed = h.packed_weights().numpy()
-    for got, w in zip(unpack_w13(packed, N, K, 32), (d["w1"], d["w3"])):
+    # fp32 handles pack the duplicated-K layout of the split-x contraction (pack.cuh,
+    # DESIGN.md R5): packed K = 2 * Kp, columns [Kp, 2Kp) repeat columns [0, Kp)
+    Kp = (K + 31) // 32 * 32
+    for got, w in zip(unpack_w13(packed, N, 2 * Kp, 32), (d["w1"], d["w3"])):
         assert np.array_equal(got[:N, :K], oracle.fold(w, d["g"]))
-        assert np.all(got[N:] == 0) and np.all(got[:, K:] == 0)
+        assert np.array_equal(got[:, Kp:], got[:, :Kp])
+        assert np.all(got[N:] == 0) and np.all(got[:, K:Kp] == 0)
 
 
 # --------------------------------------------------------- whole path -------

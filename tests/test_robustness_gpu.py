@@ -1,0 +1,130 @@
+"""Robustness of the library under conditions a production caller creates
+(VERDICT r1 "What's weak" #8/#9):
+
+* a forward launched while another kernel holds most SMs completes without
+  waiting for that kernel: the fused a1 pass and the stream-K fixup wait only
+  for work already running (r-blocks taken by running warps, lower cluster
+  ids), never for the whole grid to be co-resident;
+* the binding's folded-weight cache follows in-place weight updates across
+  entry points that share a library cache slot;
+* entry points leave the caller's current device unchanged.
+"""
+import ctypes
+import os
+import subprocess
+import tempfile
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2501_08071_b200 as ffn
+from ffn_inputs import make_inputs
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RTOL, ATOL = 2e-2, 1e-3
+
+
+def check(gpu, ref, what):
+    worst, nbad, maxerr = oracle.tolerance_ratio(gpu.double().cpu().numpy(), ref, RTOL, ATOL)
+    assert nbad == 0, f"{what}: {nbad} elements out of tolerance (worst ratio {worst:.3f})"
+
+
+@pytest.fixture(scope="module")
+def holder():
+    out = os.path.join(tempfile.mkdtemp(prefix="smhold"), "libsm_holder.so")
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared",
+                           "-o", out, os.path.join(HERE, "helpers", "sm_holder.cu")])
+    lib = ctypes.CDLL(out)
+    lib.hold_sms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                             ctypes.c_void_p]
+    lib.hold_sms.restype = ctypes.c_int
+    return lib
+
+
+# (M, K, N, variant, schedule, csplit): the 2-SM stream-K tail (7B prefill P=8 shard width),
+# 1-SM stream-K few tiles, the cluster split-K decode shard, whole tiles
+CASES = [
+    (2048, 4096, 1376, ffn.VARIANT_AUTO, ffn.SCHEDULE_AUTO, 0),
+    (1000, 512, 2056, ffn.VARIANT_2SM, ffn.SCHEDULE_STREAM_K_ALL, 0),
+    (256, 4096, 1376, ffn.VARIANT_1SM, ffn.SCHEDULE_STREAM_K_ALL, 0),
+    (16, 4096, 1376, ffn.VARIANT_AUTO, ffn.SCHEDULE_AUTO, 0),
+    (640, 1024, 1408, ffn.VARIANT_1SM, ffn.SCHEDULE_DATA_PARALLEL, 0),
+]
+
+
+@pytest.mark.parametrize("held", [100, 140])
+@pytest.mark.parametrize("M,K,N,variant,schedule,csplit", CASES)
+def test_forward_completes_while_other_kernel_holds_sms(cuda_device, holder, M, K, N, variant, schedule, csplit,
+                                                        held):
+    """`held` SMs are occupied by spinning CTAs that only exit once the forward
+    has finished (a flag set on the forward's stream after it).  A kernel whose
+    CTAs waited for the whole grid to be resident would never finish before the
+    holder's 20 s timeout; the holder must see the flag instead."""
+    plan = ffn.plan_config(M, K, N)
+    if held > 100 and (csplit or (variant == ffn.VARIANT_AUTO and plan[3])):
+        # an S-CTA cluster needs S free SMs inside one GPC: with 8 SMs left anywhere,
+        # a 4- or 6-CTA split-K cluster may have no place until the holder exits (a
+        # hardware placement constraint of cluster launches, not a wait in the kernel)
+        pytest.skip("cluster split-K plan: needs S free SMs in one GPC")
+    d = make_inputs(M, K, N, family="C", seed=7700 + M, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_variant(variant)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
+    if csplit:
+        h.set_option(ffn.OPT_CSPLIT, csplit)
+    ref_out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)  # packs the weights; reference launch
+    torch.cuda.synchronize()
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda_device)
+    timed_out = torch.zeros(1, dtype=torch.int32, device=cuda_device)
+    side = torch.cuda.Stream(cuda_device)
+    st = holder.hold_sms(held, 120 * 1024, flag.data_ptr(), timed_out.data_ptr(), int(20e9), side.cuda_stream)
+    assert st == 0, f"hold_sms launch failed ({st})"
+    time.sleep(0.2)  # the holder's CTAs are resident before the forward is launched
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    flag.fill_(1)    # on the forward's stream: after the forward completes
+    torch.cuda.synchronize()
+    assert int(timed_out.item()) == 0, "the forward did not finish while other work held SMs"
+    assert torch.equal(out, ref_out)
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 8)))))
+    check(out[rows], oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows),
+          f"held {held}: {M}x{K}x{N}")
+
+
+def test_weight_cache_follows_inplace_updates_across_entry_points(cuda_device):
+    """forward() packs (g, w1, w3) into library slot 0; an in-place
+    update of w1 followed by block_forward() (which uses slot 0 too) must re-pack."""
+    M, K, N = 64, 256, 384
+    d = make_inputs(M, K, N, family="C", seed=7800, dtype="bf16")
+    w2 = make_inputs(1, N, K, family="C", seed=7801, dtype="bf16")["w1"].to(cuda_device)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    t["w1"].neg_()
+    y = h.block_forward(t["x"], t["g"], t["w1"], t["w3"], w2, 1e-6)
+    fresh = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    y_ref = fresh.block_forward(t["x"], t["g"], t["w1"], t["w3"], w2, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    # and gemm_act (slot 1) followed by an in-place update of that weight, then block_forward
+    z = h.gemm_act(t["x"], t["w1"])
+    w2.mul_(2.0)
+    y2 = h.block_forward(t["x"], t["g"], t["w1"], t["w3"], w2, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(y2.float(), y_ref.float() * 2.0)
+    assert z.shape == (M, N)
+
+
+def test_entry_points_restore_current_device(cuda_device):
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    d = {k: v.to(cuda_device) for k, v in make_inputs(8, 64, 128, family="C", seed=7900, dtype="bf16").items()}
+    before = torch.cuda.current_device()
+    h.forward(d["x"], d["g"], d["w1"], d["w3"])
+    h.rmsnorm(d["x"], d["g"])
+    torch.cuda.synchronize()
+    assert torch.cuda.current_device() == before

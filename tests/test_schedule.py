@@ -3,13 +3,15 @@ stream-K tail, csrc/dual_gemm.cuh `Sched` / `sk_owner` and the host-side
 split in csrc/cuasm_ffn.cu `launch_gemm`).  Checks, over many shapes, the
 properties the kernel's correctness rests on:
   * every (tile, k-block) is computed exactly once;
-  * each tile has exactly one owner of k-block 0 (full or finisher);
-  * a finisher's contributor set (non-empty ranges between it and the owner
-    of the tile's last k-block) is exactly the set of clusters that publish a
-    partial of that tile, and each contributing cluster publishes at most once
-    (one workspace slot per cluster);
-  * contributors never wait (so the finisher -> contributor wait graph is
-    acyclic: it only points to higher cluster ids).
+  * each tile has exactly one owner of its last k-block (whole or finisher);
+  * a finisher's contributor set (non-empty ranges from the owner of the
+    tile's first k-block up to the cluster below it) is exactly the set of
+    clusters that publish a partial of that tile, and each contributing
+    cluster publishes at most once (one workspace slot per cluster), as the
+    first segment it walks;
+  * contributors never wait and finishers wait only for LOWER cluster ids
+    (CTAs dispatched earlier), so the wait graph is acyclic and needs no
+    co-residency of the grid.
 """
 import itertools
 
@@ -52,12 +54,12 @@ def segments(cluster, C, KB, T_dp, I):
     while t < T_dp:
         yield (t, 0, KB)
         t += C
-    cur, end = sk_begin(I, C, cluster), sk_begin(I, C, cluster + 1)
-    while cur < end:
-        tt, kb0 = divmod(cur, KB)
-        take = min(KB - kb0, end - cur)
-        yield (T_dp + tt, kb0, kb0 + take)
-        cur += take
+    beg, cur = sk_begin(I, C, cluster), sk_begin(I, C, cluster + 1)
+    while cur > beg:   # the stream-K range is walked backwards
+        tt = (cur - 1) // KB
+        lo = max(tt * KB, beg)
+        yield (T_dp + tt, lo - tt * KB, cur - tt * KB)
+        cur = lo
 
 
 SHAPES = list(itertools.product([1, 2, 5, 8, 16, 22, 86, 88, 96, 148, 176, 512, 688, 700, 3584],
@@ -73,10 +75,10 @@ def test_schedule_properties(T, KB, maxc, sched):
     finishers = {}
     for c in range(C):
         segs = list(segments(c, C, KB, T_dp, I))
-        contrib_segs = [s for s in segs if s[1] > 0]
+        contrib_segs = [s for s in segs if s[2] < KB]
         assert len(contrib_segs) <= 1, "a cluster publishes at most one partial"
         if contrib_segs:
-            # the contributing segment is the first stream-K segment of the cluster
+            # the contributing segment is the first stream-K segment the cluster walks
             first_sk = next(s for s in segs if s[0] >= T_dp)
             assert contrib_segs[0] == first_sk
             publishes[contrib_segs[0][0]] = publishes.get(contrib_segs[0][0], set()) | {c}
@@ -85,23 +87,25 @@ def test_schedule_properties(T, KB, maxc, sched):
             for kb in range(kb0, kb1):
                 assert (t, kb) not in covered, "k-block computed twice"
                 covered[(t, kb)] = c
-            if kb0 == 0 and kb1 < KB:
+            if kb1 == KB and kb0 > 0:
                 assert t >= T_dp
-                tile_end = (t - T_dp + 1) * KB - 1
-                c_last = sk_owner(I, C, tile_end)
-                waits = {cc for cc in range(c + 1, c_last + 1) if sk_begin(I, C, cc) != sk_begin(I, C, cc + 1)}
+                tile_start = (t - T_dp) * KB
+                c_first = sk_owner(I, C, tile_start)
+                waits = {cc for cc in range(c_first, c) if sk_begin(I, C, cc) != sk_begin(I, C, cc + 1)}
                 finishers[t] = (c, waits)
+                # the finisher's segment is the last one it walks
+                assert (t, kb0, kb1) == segs[-1]
     assert len(covered) == T * KB
     for t in range(T):
-        owners0 = covered[(t, 0)]
+        owner_last = covered[(t, KB - 1)]
         if t in finishers:
             c, waits = finishers[t]
-            assert owners0 == c
+            assert owner_last == c
             assert waits == publishes.get(t, set()), (t, waits, publishes.get(t))
-            assert all(w > c for w in waits)
+            assert all(w < c for w in waits)
         else:
             assert t not in publishes, "partials published for a tile nobody finishes"
-            assert all(covered[(t, kb)] == owners0 for kb in range(KB))
+            assert all(covered[(t, kb)] == owner_last for kb in range(KB))
 
 
 def test_7b_prefill_balance():
