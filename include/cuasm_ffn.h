@@ -96,7 +96,7 @@ typedef enum {
     CUASM_OPT_L2_POLICY = 9,  /* L2 eviction policy of the TMA loads, 2 bits each: bits 0-1
                                x, bits 2-3 packed W13; 0 evict_normal, 1 evict_first,
                                2 evict_last.  Default 2 (x evict_last, W13 normal)    */
-    CUASM_OPT_CSPLIT = 10     /* 1-SM variant, fewer tiles than SMs: split every tile's
+    CUASM_OPT_CSPLIT = 10,    /* 1-SM variant, fewer tiles than SMs: split every tile's
                                k-range over a cluster of S CTAs and reduce the partials
                                through distributed shared memory (bf16 tiles of <= 32
                                rows: pushed into the owner CTA with st.async; else
@@ -105,6 +105,13 @@ typedef enum {
                                configuration model decides (decode shards, M <= 32),
                                1 = off, 2..8 = S (used only when tiles * S <= SMs,
                                S <= k-blocks and S clusters fit co-resident)           */
+    CUASM_OPT_TILE_BN = 11   /* fused FFN, bf16: SwiGLU outputs per tile BN (MMA N = 2 BN):
+                               0 = the configuration model decides; 128, 112, 96, 80 or
+                               64 forces it (widths below 128 run the 2-SM kernel; a
+                               forced 1-SM variant keeps 128).  The folded weights are
+                               cached once per width in use (the 128-wide pack and one
+                               narrower pack), so a weight set served at shapes whose
+                               plans differ in BN holds two packed copies       */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -273,7 +280,8 @@ const char* cuasm_ffn_last_error(cuasm_ffn_t h);
  * 1: GEMM + activation, 256- or 128-output tiles) it returns the chosen
  * cuasm_variant_t and in *stream_k bit 0 = stream-K tail used, bit 1 = the
  * 128-wide tile, bits 4..7 = the cluster split-K width (CTAs per tile, 0 =
- * none; see CUASM_OPT_CSPLIT).  Pure host code. */
+ * none; see CUASM_OPT_CSPLIT), bits 8..15 = the SwiGLU outputs per tile BN
+ * (see CUASM_OPT_TILE_BN).  Pure host code. */
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k);
 

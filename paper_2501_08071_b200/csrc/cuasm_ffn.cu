@@ -26,8 +26,10 @@ namespace {
 using cuasm::FfnGemmParams;
 using cuasm::GemmCfg;
 
-constexpr int kPackBN = 128;  // output block of the W13 interleave (= GemmCfg::BN)
+constexpr int kPackBN = 128;  // default output block of the W13 interleave (= GemmCfg<...,256>::BN)
 static_assert(GemmCfg<0, 1>::BN == kPackBN && GemmCfg<0, 2>::BN == kPackBN, "pack/GEMM block mismatch");
+// SwiGLU tile widths (outputs per tile) the 2-SM bf16 kernel is built for (dual_gemm.cuh GemmCfg)
+constexpr int kTileBNs[5] = {128, 112, 96, 80, 64};
 
 thread_local std::string g_init_error;
 
@@ -55,6 +57,7 @@ struct PackedWeights {
     const void* key_w3 = nullptr;
     int64_t key_K = 0, key_N = 0;
     int64_t key_kp = 0;   // duplicated-K mode (fp32 split-x contraction), 0 = off
+    int key_bn = 0;       // output block BN of the W13 interleave (slots 0 and 2)
     bool packed = false;
     bool fresh = false;   // packed by a kernel the next GEMM launch directly follows (no early weight loads)
     CUtensorMap tmap;     // box {BK, tmap_rows}; tmap_rows = B_ROWS of the launched variant
@@ -95,9 +98,11 @@ struct cuasm_ffn_s {
     // a1 workspace
     float* r = nullptr;
     int64_t r_cap = 0;
-    // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN;
-    // slot 1 = a single packed weight (GEMM + activation / down projection)
-    PackedWeights pw[2];
+    // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN in 128-output
+    // blocks; slot 1 = a single packed weight (GEMM + activation / down projection);
+    // slot 2 = the same W13 in the narrower blocks a tile-width plan chose (BN != 128)
+    PackedWeights pw[3];
+    int tile_bn = 0;   // CUASM_OPT_TILE_BN: 0 auto, else the SwiGLU outputs per tile
     // fp32 handle: x split into [x_hi | x_lo] tf32 terms per forward (pack.cuh)
     void* x2 = nullptr;
     int64_t x2_bytes = 0;
@@ -229,11 +234,11 @@ cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint
 // fused FFN (128-output blocks); w3 == null: one weight, 256-row blocks.
 template <typename T>
 cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
-                           int64_t N, cudaStream_t s, int64_t kp) {
+                           int64_t N, cudaStream_t s, int64_t kp, int bn) {
     PackedWeights& w = h->pw[slot];
     const int BK = 128 / h->esize;  // one 128-byte swizzle row of K (= GemmCfg::BK)
-    const int64_t rows_per_block = 2 * kPackBN;
-    const int64_t n_blocks = w3 ? (N + kPackBN - 1) / kPackBN : (N + rows_per_block - 1) / rows_per_block;
+    const int64_t rows_per_block = w3 ? 2 * bn : 2 * kPackBN;
+    const int64_t n_blocks = (N + (w3 ? bn : rows_per_block) - 1) / (w3 ? bn : rows_per_block);
     const int64_t k_blocks = kp > 0 ? 2 * kp / BK : (K + BK - 1) / BK;
     const int64_t rows = n_blocks * k_blocks * rows_per_block;
     const int64_t bytes = rows * 128;
@@ -249,7 +254,7 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     const int64_t blocks = std::min<int64_t>((total_vec + threads - 1) / threads, int64_t(h->sm_count) * 16);
     cuasm::ffn_pack_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, s>>>(
         static_cast<const T*>(w1), static_cast<const T*>(w3), static_cast<const T*>(g), static_cast<T*>(w.buf), N, K,
-        kPackBN, n_blocks, k_blocks, BK, kp);
+        w3 ? bn : kPackBN, n_blocks, k_blocks, BK, kp);
     CUASM_CHECK(h, cudaGetLastError(), "ffn_pack_kernel launch");
     w.rows = rows;
     w.tmap_rows = 0;  // re-encode for the new buffer
@@ -259,20 +264,24 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     w.key_K = K;
     w.key_N = N;
     w.key_kp = kp;
+    w.key_bn = bn;
     w.packed = true;
     w.fresh = true;
     return CUASM_OK;
 }
 
+// The W13 cache slot of a SwiGLU tile width: 0 for BN = 128, 2 for the narrower blocks.
+inline int w13_slot(int bn) { return bn == kPackBN ? 0 : 2; }
+
 cuasm_status_t ensure_packed(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
-                             int64_t N, cudaStream_t s, int64_t kp = 0) {
+                             int64_t N, cudaStream_t s, int64_t kp = 0, int bn = kPackBN) {
     PackedWeights& w = h->pw[slot];
     if (w.packed && w.key_g == g && w.key_w1 == w1 && w.key_w3 == w3 && w.key_K == K && w.key_N == N &&
-        w.key_kp == kp)
+        w.key_kp == kp && w.key_bn == bn)
         return CUASM_OK;
     w.packed = false;
-    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, slot, g, w1, w3, K, N, s, kp)
-                                        : launch_pack<float>(h, slot, g, w1, w3, K, N, s, kp);
+    return h->dtype == CUASM_DTYPE_BF16 ? launch_pack<__nv_bfloat16>(h, slot, g, w1, w3, K, N, s, kp, bn)
+                                        : launch_pack<float>(h, slot, g, w1, w3, K, N, s, kp, bn);
 }
 
 // fp32 handles: the K padding of the split-x contraction (one 32-float k-block)
@@ -352,13 +361,13 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // the four TMEM lane quadrants of the (leader) CTA (dual_gemm.cuh `rep`)
     // cluster split-K (1-SM; dual_gemm.cuh split_k_reduce): S CTAs per tile, one tile per cluster
     int csplit = 0;
-    if (kCtaGroup == 1) {
+    if (kCtaGroup == 1 && C::kDecodePaths) {
         const int want = h->csplit_opt >= 2 ? h->csplit_opt : (h->csplit_opt == 0 ? h->plan_csplit : 0);
         const int64_t tiles = ((M + C::TILE_M - 1) / C::TILE_M) * ((N + C::OUT_COLS - 1) / C::OUT_COLS);
         const int64_t kbs = (K + C::BK - 1) / C::BK;
         if (want >= 2 && want <= 8 && tiles * want <= h->sm_count && kbs >= want) csplit = want;
     }
-    const int rep_plain = kEpi != 0 ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
+    const int rep_plain = (kEpi != 0 || !C::kDecodePaths) ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
     const int rep = csplit ? 0 : rep_plain;
     const uint32_t a_rows =
         ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
@@ -411,18 +420,24 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // destination [M rows, ldo stride] x N columns, 32 x 32 boxes, 64-byte swizzle
     // (what the epilogue's staging layout writes); stores past M / N are clipped
     // (one map per destination: the fused gather's P2P fan-out is P TMA stores per box)
-    cuasm::OutMaps omaps{};
+    // (tiles whose last SwiGLU unit is 16 columns wide -- BN % 32 == 16 -- store it through
+    // half-width maps: 32 x 16 boxes, 32-byte swizzle)
+    cuasm::OutMaps omaps{}, omaps_h{};
     p.tma_store = (kKind == 0 && !p.dst_mc) ? 1 : 0;
+    constexpr bool kHalfUnit = kEpi == 0 && C::BN % 32 == 16;
     for (int q = 0; p.tma_store && q < p.num_dst; ++q) {
-        cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
-        cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldo) * static_cast<cuuint64_t>(h->esize)};
-        cuuint32_t box[2] = {32, 32};
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = h->encode(&omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[q], dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out %d) failed (CUresult %d)", q, (int)r);
+        for (int hw = 0; hw < (kHalfUnit ? 2 : 1); ++hw) {
+            cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+            cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldo) * static_cast<cuuint64_t>(h->esize)};
+            cuuint32_t box[2] = {hw ? 16u : 32u, 32};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult r = h->encode(hw ? &omaps_h.m[q] : &omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[q], dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   hw ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out %d) failed (CUresult %d)", q, (int)r);
+        }
     }
     // decode shapes: replicate the <= 32 rows into all four TMEM lane quadrants so
     // the SwiGLU epilogue runs on all four SM sub-partitions (dual_gemm.cuh `rep`)
@@ -546,7 +561,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     cfg.attrs = attrs;
     cfg.numAttrs = na;
     CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, tmap_x, w.tmap,
-                                      omaps, p),
+                                      omaps, omaps_h, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
     return CUASM_OK;
@@ -567,10 +582,20 @@ struct Plan {
     bool stream_k;
     int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
     int csplit;  // cluster split-K: CTAs per tile (1-SM variant), 0 = none
+    int bn = kPackBN;  // SwiGLU outputs per tile (MMA N = 2 bn): 128, or 64..112 (2-SM bf16)
 };
 
+// Time of one k-block of a 2-SM SwiGLU tile of width bn relative to bn = 128, measured
+// (scripts/tune_bn.py, profiles/r02/tune_bn.json): at full size the narrower tiles run at
+// about their MMA-width ratio (7B prefill, 11 rounds of 112-wide tiles 218.9 us vs 10 of
+// 128-wide 229.6 us: 0.87); at 80 and below the per-k-block issue / barrier / operand
+// overheads that do not shrink with bn show (2048 x 4096 x 1376: 80 -> 0.70, 64 -> 0.62)
+inline double bn_frac(int bn) {
+    return bn >= 128 ? 1.0 : bn >= 112 ? 0.867 : bn >= 96 ? 0.80 : bn >= 80 ? 0.70 : 0.62;
+}
+
 Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,
-                     int tile_n_force = 0) {
+                     int tile_n_force = 0, int tile_bn_force = 0) {
     const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
     const int64_t BK = 128 / esize;
     const double KB = static_cast<double>((K + BK - 1) / BK);
@@ -585,6 +610,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
     // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
+    // (a forced SwiGLU width below 128 has no decode paths: straight to the cost model)
+    const bool narrow_forced = out_cols == 128 && tile_bn_force != 0 && tile_bn_force != kPackBN;
     // Decode shards (M <= 32, up to 2 * kFewTiles tiles): split each tile's k-loop over a
     // cluster of S CTAs, partials pushed into the owner CTA's shared memory (dual_gemm.cuh
     // split_k_push) -- no global partials, no flags, no second wave.  S = 6 up to 16 tiles
@@ -593,7 +620,7 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // 1376: 14.5 us (S = 6), 15.0 (S = 4) vs 17.5 us (stream-K split 3 ways), 16 x 4096 x 5504
     // (S = 3): 23.0 vs 27.1, 16 x 4096 x 6880 (S = 2): 26.5 vs 29.5, 32 x 4096 x 5504 (S = 2):
     // 24.9 vs 27.2; at M >= 64 (pull form) it loses
-    if (out_cols == 128 && KB >= 48 && M <= 32) {
+    if (out_cols == 128 && !narrow_forced && KB >= 48 && M <= 32) {
         const int S = M <= 16 && tiles_1sm * 6 <= sm_count && tiles_1sm <= 16 ? 6
                       : tiles_1sm * 4 <= sm_count && tiles_1sm <= 37   ? 4
                       : M <= 16 && tiles_1sm * 3 <= sm_count && tiles_1sm <= 49 ? 3
@@ -603,7 +630,7 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     }
     // (k-loops of >= 48 k-blocks: a split must save more MMA time than its partial fixup costs;
     // the paper's fused_ff shape 512 x 2048 x 512 split three ways finished its tail 5 us late)
-    if (out_cols == 128 && KB >= 48 &&
+    if (out_cols == 128 && !narrow_forced && KB >= 48 &&
         ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
         return Plan{CUASM_VARIANT_1SM, true, 256, 0};
     // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
@@ -617,19 +644,30 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
         return Plan{CUASM_VARIANT_1SM, false, 128, 0};
     Plan best{CUASM_VARIANT_2SM, false, 256, 0};
     double best_t = 1e30;
-    // candidate MMA widths: the fused FFN is always 256 (128 outputs); the GEMM
-    // mode may also use 128 (128 outputs, half the k-block time per tile)
-    const int widths[2] = {256, 128};
-    for (int wi = 0; wi < (out_cols == 128 ? 1 : 2); ++wi) {
-        const int tn = widths[wi];
-        if (tile_n_force && tn != tile_n_force) continue;
-        const int64_t oc = out_cols == 128 ? 128 : tn;   // output columns per tile
+    // candidates: the GEMM mode's MMA widths 256 / 128 (128 outputs, half the k-block time
+    // per tile), or the SwiGLU tile widths bn (2 bn = MMA N; widths below 128 only for the
+    // 2-SM bf16 kernel, DESIGN.md §6 "Tile widths")
+    struct Cand { int tn, bn; };
+    Cand cands[5];
+    int nc = 0;
+    if (out_cols != 128) {
+        for (int tn : {256, 128})
+            if (!tile_n_force || tn == tile_n_force) cands[nc++] = Cand{tn, kPackBN};
+    } else {
+        for (int bn : kTileBNs)
+            if ((bn == kPackBN || esize == 2) && (tile_bn_force ? bn == tile_bn_force : true)) cands[nc++] = Cand{256, bn};
+    }
+    for (int ci = 0; ci < nc; ++ci) {
+        const int tn = cands[ci].tn, bn = cands[ci].bn;
+        const int64_t oc = out_cols == 128 ? bn : tn;   // output columns per tile
+        const int64_t wrows = out_cols == 128 ? 2 * bn : tn;  // weight rows per n-block
         // k-block time relative to N = 256: a 128-wide k-block costs 0.72 of a 256-wide one,
         // not 0.5 -- its fixed per-k-block issue/TMA overheads do not halve
-        // (scripts/tune.py --op gemm, profiles/r01/tune_gemm*.log)
-        const double tile_frac = tn == 256 ? 1.0 : 0.72;
+        // (scripts/tune.py --op gemm, profiles/r01/tune_gemm*.log); SwiGLU widths: bn_frac
+        const double tile_frac = out_cols == 128 ? bn_frac(bn) : (tn == 256 ? 1.0 : 0.72);
         const int64_t nblk_w = (N + oc - 1) / oc;
         for (int cg = 2; cg >= 1; --cg) {
+            if (bn != kPackBN && cg == 1) continue;
             const int64_t units = sm_count / cg;
             const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
             const int64_t tiles = mblk * nblk_w;
@@ -644,7 +682,7 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             const int64_t sk_tiles = tiles < units ? tiles : (rem ? rem + units : 0);
             const int64_t gm = std::min<int64_t>(mblk, group_m > 0 ? group_m : auto_group_m(K, esize, cg));
             const double region_bytes =
-                static_cast<double>((sk_tiles + gm - 1) / gm + 1) * tn * K * esize +
+                static_cast<double>((sk_tiles + gm - 1) / gm + 1) * wrows * K * esize +
                 static_cast<double>(std::min<int64_t>(M, gm * 128 * cg)) * K * esize;
             const double l2_pen = region_bytes > 120e6 ? 1.32 : 1.0;
             // fewer tiles than clusters: auto stream-K splits each tile at most in two
@@ -654,17 +692,21 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             const double sk_units = tiles < units ? static_cast<double>(std::min<int64_t>(units, 2 * tiles)) : units;
             const double t_sk = std::max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup);
             const int v = cg == 2 ? CUASM_VARIANT_2SM : CUASM_VARIANT_1SM;
-            // ties go to the earlier candidate: N=256 before 128, 2-SM before 1-SM,
-            // whole tiles before stream-K
-            if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{v, false, tn, 0}; }
-            if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn, 0}; }
+            // ties go to the earlier candidate: N=256 before 128, bn = 128 before narrower
+            // tiles, 2-SM before 1-SM, whole tiles before stream-K
+            if (t_dp < best_t * 0.999) { best_t = t_dp; best = Plan{v, false, tn, 0, bn}; }
+            if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn, 0, bn}; }
         }
     }
     return best;
 }
 
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
-    return plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n);
+    Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
+                              out_cols == 128 ? h->tile_bn : 0);
+    // a forced 1-SM variant (CUASM_OPT_VARIANT) has only the 128-output SwiGLU tile
+    if (h->variant == CUASM_VARIANT_1SM) pl.bn = kPackBN;
+    return pl;
 }
 
 cuasm_status_t ensure_r(cuasm_ffn_t h, int64_t M) {
@@ -746,10 +788,21 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
     h->plan_csplit = v == plan.variant ? plan.csplit : 0;
-    if (kepi == 0) st = dispatch_gemm<0, 256>(h, e, v, x, out, M, K, N, eps, s);
+    if (kepi == 0 && plan.bn != kPackBN) {
+        // narrower SwiGLU tiles (2-SM bf16 only; ffn_common packed slot 2 for this width)
+        if (h->dtype != CUASM_DTYPE_BF16 || v != CUASM_VARIANT_2SM || e.slot != w13_slot(plan.bn))
+            return fail(h, CUASM_ERR_UNSUPPORTED, "tile width %d needs the 2-SM bf16 kernel", plan.bn);
+        switch (plan.bn) {
+        case 112: st = launch_gemm<0, 2, 0, 224>(h, e, x, out, M, K, N, eps, s); break;
+        case 96: st = launch_gemm<0, 2, 0, 192>(h, e, x, out, M, K, N, eps, s); break;
+        case 80: st = launch_gemm<0, 2, 0, 160>(h, e, x, out, M, K, N, eps, s); break;
+        case 64: st = launch_gemm<0, 2, 0, 128>(h, e, x, out, M, K, N, eps, s); break;
+        default: return fail(h, CUASM_ERR_UNSUPPORTED, "no kernel for tile width %d", plan.bn);
+        }
+    } else if (kepi == 0) st = dispatch_gemm<0, 256>(h, e, v, x, out, M, K, N, eps, s);
     else if (plan.tile_n == 128) st = dispatch_gemm<1, 128>(h, e, v, x, out, M, K, N, eps, s);
     else st = dispatch_gemm<1, 256>(h, e, v, x, out, M, K, N, eps, s);
-    h->last_tile_n = kepi == 0 ? 256 : plan.tile_n;
+    h->last_tile_n = kepi == 0 ? 2 * plan.bn : plan.tile_n;
     if (st != CUASM_OK) return st;
     h->last_kernels += separate_prepass ? 2 : 1;
     if (h->profile && (st = profile_event(h, s)) != CUASM_OK) return st;
@@ -763,6 +816,7 @@ cuasm_status_t ffn_common(cuasm_ffn_t h, EpiSpec e, const void* x, const void* g
                           void* out, int64_t M, int64_t K, int64_t N, float eps, cudaStream_t s) {
     cuasm_status_t st;
     if (h->dtype == CUASM_DTYPE_FP32) {
+        e.slot = 0;
         const int64_t kp = split_kp(K);
         if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s, kp)) != CUASM_OK) return st;
         const int64_t xb = std::max<int64_t>(M, 1) * 2 * kp * 4;
@@ -779,7 +833,10 @@ cuasm_status_t ffn_common(cuasm_ffn_t h, EpiSpec e, const void* x, const void* g
         e.kp = kp;
         return run_gemm(h, 0, e, h->x2, out, M, 2 * kp, N, eps, s);
     }
-    if ((st = ensure_packed(h, 0, g, w1, w3, K, N, s)) != CUASM_OK) return st;
+    // the tile width decides the W13 block layout: pack (or reuse) the slot of that width
+    const int bn = M > 0 ? plan_config(h, M, K, N, 128).bn : kPackBN;
+    e.slot = w13_slot(bn);
+    if ((st = ensure_packed(h, e.slot, g, w1, w3, K, N, s, 0, bn)) != CUASM_OK) return st;
     return run_gemm(h, 0, e, x, out, M, K, N, eps, s);
 }
 
@@ -849,7 +906,7 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
         return CUASM_ERR_INVALID_ARG;
     const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
     *variant = pl.variant;
-    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.csplit << 4);
+    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.csplit << 4) | (pl.bn << 8);
     return CUASM_OK;
 }
 
@@ -1128,8 +1185,7 @@ cuasm_status_t cuasm_ffn_get_packed(cuasm_ffn_t h, void* dst, int64_t* bytes) {
 
 cuasm_status_t cuasm_ffn_invalidate_weights(cuasm_ffn_t h) {
     if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
-    h->pw[0].packed = false;
-    h->pw[1].packed = false;
+    for (PackedWeights& w : h->pw) w.packed = false;
     return CUASM_OK;
 }
 
@@ -1174,6 +1230,11 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
     case CUASM_OPT_SK_SPLIT:
         if (value != 0 && (value < 2 || value > 16)) return fail(h, CUASM_ERR_INVALID_ARG, "SK_SPLIT is 0 or 2..16");
         h->sk_split = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_TILE_BN:
+        if (value != 0 && std::find(std::begin(kTileBNs), std::end(kTileBNs), value) == std::end(kTileBNs))
+            return fail(h, CUASM_ERR_INVALID_ARG, "TILE_BN is 0 (auto) or one of 128, 112, 96, 80, 64");
+        h->tile_bn = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_TRACE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "TRACE option is 0 or 1");

@@ -231,16 +231,31 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 // kN: the MMA N.  kEpi 0 uses 256 (128 W1g + 128 W3g rows); kEpi 1 uses 256
 // or 128 (a 128-output tile reads half of a packed 256-row block) -- the
 // narrower tile halves the wave-quantisation step of square-ish GEMMs.
+//
+// SwiGLU tile widths (DESIGN.md §6 "Tile widths"): kN = 2*BN with BN in {64, 80, 96,
+// 112, 128} outputs per tile, so a column shard N_l can be cut into a tile count that
+// fills whole waves of CTA pairs (7B P=8: N_l = 1376 -> 18 blocks of 80 = 144 tiles of
+// 256 rows on 74 pairs instead of 11 blocks of 128 = 88).  h1 sits in accumulator
+// columns [0, BN), h3 in [BN, 2BN); the epilogue walks 32-column units (the last one
+// 16 wide when BN % 32 == 16).  Only BN = 128 has the decode paths (rep, cluster split-K).
 template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256>
 struct GemmCfg {
-    static_assert(kN == 256 || (kEpi == 1 && kN == 128), "SwiGLU tiles are 256 wide");
+    static_assert(kEpi == 0 ? (kN % 32 == 0 && kN >= 128 && kN <= 256) : (kN == 256 || kN == 128),
+                  "SwiGLU tiles: kN = 2*BN, BN in {64, 80, 96, 112, 128}; GEMM tiles 128 or 256");
     static constexpr int kEsize = kKind == 0 ? 2 : 4;
     static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
     static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
     static constexpr int UMMA_N = kN;
     static constexpr int BN = kN / 2;              // SwiGLU: outputs per tile (h1 | h3 halves)
     static constexpr int OUT_COLS = kEpi == 0 ? BN : UMMA_N;  // output columns per tile
-    static constexpr int PACK_ROWS = 256;          // rows of one packed (n-block, k-block) box run
+    static constexpr int PACK_ROWS = kEpi == 0 ? kN : 256;  // rows of one packed (n-block, k-block) box run
+    static constexpr bool kDecodePaths = kN == 256;  // rep / cluster split-K (BN = 128 only)
+    // SwiGLU epilogue units: 32 output columns (h1 at [32u, ..), h3 at [BN + 32u, ..)),
+    // the last 16 wide when BN % 32 == 16; the two warps of a TMEM quadrant alternate units
+    static constexpr int NU = (BN + 31) / 32;
+    static constexpr int EPI_ITERS = kEpi == 0 ? (NU + 1) / 2 : kN / 128;
+    // TMEM column stride between the two accumulators (a power-of-two allocation)
+    static constexpr int ACC_STRIDE = kN > 128 ? 256 : 128;
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
@@ -262,7 +277,7 @@ struct GemmCfg {
     static constexpr int STAGES_CAP = 9;
 #endif
     static constexpr int STAGES = STAGES_FIT < STAGES_CAP ? STAGES_FIT : STAGES_CAP;
-    static constexpr int TMEM_COLS = 2 * UMMA_N;                    // 2 accumulators (power of 2)
+    static constexpr int TMEM_COLS = 2 * ACC_STRIDE;                // 2 accumulators (power of 2)
     // Two epilogue warps per TMEM lane quadrant, each owning half of the
     // accumulator columns (PAIRS pairs of 32-column chunks): two warps per SM
     // sub-partition hide the MUFU/TMEM latency of the epilogue math.
@@ -365,13 +380,13 @@ __device__ __forceinline__ void store16(const FfnGemmParams& p, int64_t off_byte
 
 // 32 consecutive outputs of one row -> global (bf16 pairs packed with RNE, or
 // fp32), 16-byte stores, columns >= N dropped in groups of 8 (N % 8 == 0).
-template <int kKind>
+template <int kKind, int W = 32>
 __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int col0, const float (&o)[32]) {
     constexpr int kEs = kKind == 0 ? 2 : 4;
     const int64_t rbase = static_cast<int64_t>(row) * p.ldo;
     if constexpr (kKind == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < W / 8; ++q) {
             if (col0 + 8 * q < p.N) {
                 store16<kKind>(p, (rbase + col0 + 8 * q) * kEs,
                                make_uint4(ptx::pack_bf16x2(o[8 * q + 0], o[8 * q + 1]), ptx::pack_bf16x2(o[8 * q + 2], o[8 * q + 3]),
@@ -380,7 +395,7 @@ __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int
         }
     } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < W / 4; ++q) {
             if (col0 + 4 * q < p.N)
                 store16<kKind>(p, (rbase + col0 + 4 * q) * kEs,
                                make_uint4(__float_as_uint(o[4 * q + 0]), __float_as_uint(o[4 * q + 1]),
@@ -402,16 +417,21 @@ struct OutMaps {
     CUtensorMap m[8];
 };
 
-template <int kPending>
+// W = 16 (the last unit of a BN % 32 == 16 tile): a 32 x 16 box (32-byte rows) through
+// the half-width maps, 32-byte swizzle (chunk c of row r at c ^ ((r >> 2) & 1)).
+template <int kPending, int W = 32>
 __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint8_t* box, const float (&o)[32],
                                               int col, int row0, uint32_t lane) {
     if (lane == 0) ptx::tma_store_wait_read<kPending>();
     __syncwarp();
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < W / 8; ++c) {
         const uint4 v = make_uint4(ptx::pack_bf16x2(o[8 * c + 0], o[8 * c + 1]), ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
                                    ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]), ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
-        *reinterpret_cast<uint4*>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+        if constexpr (W == 32)
+            *reinterpret_cast<uint4*>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+        else
+            *reinterpret_cast<uint4*>(box + lane * 32 + ((c ^ ((lane >> 2) & 1)) << 4)) = v;
     }
     ptx::fence_proxy_async_smem();
     __syncwarp();
@@ -439,7 +459,7 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
                                                uint64_t* xbar, uint32_t part, int mb, int nb, uint32_t quad, int half,
                                                uint32_t ewarp, uint32_t lane, int it, bool& cl_pending) {
     const uint32_t buf = ptx::smem_u32(smem);
-    const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
+    const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::ACC_STRIDE;
     const uint32_t r_own = quad * 32 + lane;
     const int row0 = mb * C::TILE_M;
     const int rows = min(C::BM, p.M - row0);  // valid rows of the tile
@@ -654,7 +674,7 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         ptx::cluster_wait_acquire();
         cl_pending = false;
     }
-    const uint32_t t_row = tmem_base + acc * C::UMMA_N;
+    const uint32_t t_row = tmem_base + acc * C::ACC_STRIDE;
     const uint32_t swz = lane & 7;
     // (a) scatter this warp's units to their owners
 #pragma unroll 1
@@ -729,7 +749,8 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
 template <int kKind, int kCtaGroup, int kEpi, int kN>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                         const __grid_constant__ OutMaps omaps, const FfnGemmParams p) {
+                         const __grid_constant__ OutMaps omaps, const __grid_constant__ OutMaps omaps_h,
+                         const FfnGemmParams p) {
     using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
@@ -750,7 +771,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     const uint32_t lane = ptx::lane_id();
     const uint32_t cta_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;
     const bool leader = cta_rank == 0;
-    const bool csplit = kCtaGroup == 1 && p.csplit > 0;
+    const bool csplit = C::kDecodePaths && kCtaGroup == 1 && p.csplit > 0;
+    const int rep = C::kDecodePaths ? p.rep : 0;  // decode-shape row replication (BN = 128 only)
     const uint32_t part = csplit ? ptx::cluster_ctarank() : 0;  // split-K share of the cluster's tile
 
     if (warp == 0 && lane == 0) {
@@ -811,11 +833,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const uint32_t fb = ptx::smem_u32(&full_bar[s]);
             const uint32_t sb = ptx::smem_u32(smem_b + s * C::B_BYTES);
             if constexpr (kCtaGroup == 1) {
-                ptx::mbar_arrive_expect_tx(fb, (p.rep ? p.rep : 1) * p.a_box_bytes + C::B_BYTES);
+                ptx::mbar_arrive_expect_tx(fb, (rep ? rep : 1) * p.a_box_bytes + C::B_BYTES);
                 ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
             } else {
                 // both CTAs' bytes land on the leader's barrier
-                if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (p.rep ? p.rep + 1 : 2) * p.a_box_bytes);
+                if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (rep ? rep + 1 : 2) * p.a_box_bytes);
                 ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
             }
         };
@@ -825,11 +847,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const uint32_t fb = ptx::smem_u32(&full_bar[s]);
             const uint32_t sa = ptx::smem_u32(smem_a + s * C::A_BYTES);
             if constexpr (kCtaGroup == 1) {
-                const int nrep = p.rep ? p.rep : 1;
+                const int nrep = rep ? rep : 1;
                 for (int q = 0; q < nrep; ++q)  // copy q of the rows: smem rows q*128/nrep.. (4 KB aligned)
                     ptx::tma_load_2d(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
             } else {
-                const int nrep = (p.rep && leader) ? p.rep : 1;
+                const int nrep = (rep && leader) ? rep : 1;
                 for (int q = 0; q < nrep; ++q)
                     ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
             }
@@ -917,7 +939,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if (p.trace && kblocks > 0) wait_tempty += clock64() - w0;
                 }
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * C::UMMA_N;
+                const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
                     {
                         const long long w0 = p.trace ? clock64() : 0;
@@ -1055,7 +1077,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // rep: quadrant `quad` holds rows 0..31 of the tile (lane = row), and only its
             // own column pair is drained by it (below)
             const int row = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
-                            static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 + lane : row_in_cta);
+                            static_cast<int>(rep ? (quad % (4 / rep)) * 32 + lane : row_in_cta);
             const bool row_ok = row < p.M;
             // stream-K (Sched): a contributor lacks the tile's last k-block and publishes a
             // partial; the finisher holds the last k-block but not the first and adds the
@@ -1080,12 +1102,20 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     const char* slot = reinterpret_cast<const char*>(
                         reinterpret_cast<const float4*>(p.ws) +
                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4));
+                    // the 32-column chunks (4 KB per quadrant) holding this warp's units
+                    auto pf = [&](int chunk) { prefetch_l2(slot + ((chunk * 4 + quad) * 8 * 32) * 16 + lane * 128); };
 #pragma unroll
-                    for (int i = 0; i < C::PAIRS; ++i) {
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {  // chunk a, chunk b: 4 KB each
-                            const int64_t chunk = hh == 0 ? C::chunk_a(half, i) : C::chunk_b(half, i);
-                            prefetch_l2(slot + ((chunk * 4 + quad) * 8 * 32) * 16 + lane * 128);
+                    for (int i = 0; i < C::EPI_ITERS; ++i) {
+                        if constexpr (kEpi == 0) {
+                            const int u = half + 2 * i;
+                            if (u >= C::NU) continue;
+                            const int w = C::BN - 32 * u < 32 ? C::BN - 32 * u : 32;
+                            pf(u);
+                            pf((C::BN + 32 * u) >> 5);
+                            if (((C::BN + 32 * u + w - 1) >> 5) != ((C::BN + 32 * u) >> 5)) pf((C::BN + 32 * u + w - 1) >> 5);
+                        } else {
+                            pf(C::chunk_a(half, i));
+                            pf(C::chunk_b(half, i));
                         }
                     }
                 }
@@ -1109,8 +1139,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                             if (it == 0) trace_stamp(p, 8);
                         }
                     }
-                    split_k_push<C, kKind, kEpi>(p, tmem_base, acc, smem_stg, rbar, part, mb, nb, quad, half, ewarp,
-                                                 lane, cl_pending, pass == 0);
+                    if constexpr (C::kDecodePaths)
+                        split_k_push<C, kKind, kEpi>(p, tmem_base, acc, smem_stg, rbar, part, mb, nb, quad, half, ewarp,
+                                                     lane, cl_pending, pass == 0);
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -1135,8 +1166,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             if (csplit) {
                 // cluster split-K: partials through distributed shared memory, this CTA
                 // reduces and stores its share of the tile's output columns
-                split_k_reduce<C, kKind, kEpi>(p, tmem_base, acc, smem, xbar, part, mb, nb, quad, half, ewarp, lane,
-                                               it, cl_pending);
+                if constexpr (C::kDecodePaths)
+                    split_k_reduce<C, kKind, kEpi>(p, tmem_base, acc, smem, xbar, part, mb, nb, quad, half, ewarp, lane,
+                                                   it, cl_pending);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
@@ -1149,57 +1181,50 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             }
             if (warp == 2 && lane == 0) trace_stamp(p, 10);
             CUASM_EPI_STAMP(12);
-            const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::UMMA_N;
-#pragma unroll 1
-            for (int i = 0; i < C::PAIRS; ++i) {
-                int ca = C::chunk_a(half, i), cb = C::chunk_b(half, i);
-                if (kEpi == 0 && p.rep) {
-                    // rep 4 (M <= 32): quadrant q holds rows 0..31 and drains column pair q
-                    // (h1 chunk q, h3 chunk q + BN/32), the second warp of each quadrant idles;
-                    // rep 2 (M <= 64): quadrants q, q+2 hold rows 32(q%2).., and each of their
-                    // four warps drains one pair (2 * (q / 2) + half)
-                    if (i != 0 || (p.rep == 4 && half != 0)) continue;
-                    const int pair = p.rep == 4 ? static_cast<int>(quad) : static_cast<int>(quad / 2) * 2 + half;
-                    ca = pair;
-                    cb = pair + C::BN / 32;
-                }
-                // TMA-store path: the warp's 32 rows leave as one 32 x 32 box per 32 output
-                // columns, so every lane takes part (rows >= M are clipped by the TMA unit)
+            const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::ACC_STRIDE;
+            // one epilogue unit: accumulator columns [c1, c1 + W) and [c3, c3 + W) (SwiGLU: h1 and
+            // h3 of output columns c1..; GEMM: two 32-column chunks, each its own outputs)
+            auto unit = [&](auto wtag, int c1, int c3) {
+                constexpr int W = decltype(wtag)::value;
+                // TMA-store path: the warp's 32 rows leave as one 32 x W box, so every lane
+                // takes part (rows >= M are clipped by the TMA unit)
                 const bool use_tma = kKind == 0 && p.tma_store && !contributor;
                 const int box_row0 = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM +
-                                     static_cast<int>(p.rep ? (quad % (4 / p.rep)) * 32 : quad * 32);
-                if (use_tma && box_row0 >= p.M) continue;  // warp-uniform: no row of this warp exists
+                                     static_cast<int>(rep ? (quad % (4 / rep)) * 32 : quad * 32);
+                if (use_tma && box_row0 >= p.M) return;  // warp-uniform: no row of this warp exists
                 uint32_t v1[32], v3[32];
-                ptx::tmem_ld_32x32b_x32(t_row + ca * 32, v1);
-                ptx::tmem_ld_32x32b_x32(t_row + cb * 32, v3);
+                ptx::tmem_ld_cols<W>(t_row + c1, v1);
+                ptx::tmem_ld_cols<W>(t_row + c3, v3);
                 ptx::tmem_ld_wait();
-                if (!row_ok && !use_tma) continue;
+                if (!row_ok && !use_tma) return;
+                // stream-K partial slot: float4 of column group g (4 columns) of this lane's row
+                auto ws_idx = [&](int g) {
+                    return ((static_cast<int64_t>(g >> 3) * 4 + quad) * 8 + (g & 7)) * 32 + lane;
+                };
                 if (contributor) {
-                    float4* d1 = my_slot + (static_cast<int64_t>(ca) * 4 + quad) * 8 * 32 + lane;
-                    float4* d3 = my_slot + (static_cast<int64_t>(cb) * 4 + quad) * 8 * 32 + lane;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        __stcg(d1 + q * 32, make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
-                                                        __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3])));
-                        __stcg(d3 + q * 32, make_float4(__uint_as_float(v3[4 * q]), __uint_as_float(v3[4 * q + 1]),
-                                                        __uint_as_float(v3[4 * q + 2]), __uint_as_float(v3[4 * q + 3])));
+                    for (int q = 0; q < W / 4; ++q) {
+                        __stcg(my_slot + ws_idx(c1 / 4 + q),
+                               make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
+                                           __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3])));
+                        __stcg(my_slot + ws_idx(c3 / 4 + q),
+                               make_float4(__uint_as_float(v3[4 * q]), __uint_as_float(v3[4 * q + 1]),
+                                           __uint_as_float(v3[4 * q + 2]), __uint_as_float(v3[4 * q + 3])));
                     }
-                    continue;
+                    return;
                 }
                 for (int cc = c_first; cc <= c_last; ++cc) {
                     if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
                     const float4* slot = reinterpret_cast<const float4*>(p.ws) +
                                          (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
-                    const float4* s1 = slot + (static_cast<int64_t>(ca) * 4 + quad) * 8 * 32 + lane;
-                    const float4* s3 = slot + (static_cast<int64_t>(cb) * 4 + quad) * 8 * 32 + lane;
-                    float4 a[8], b[8];
+                    float4 a[W / 4], b[W / 4];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        a[q] = __ldcg(s1 + q * 32);
-                        b[q] = __ldcg(s3 + q * 32);
+                    for (int q = 0; q < W / 4; ++q) {
+                        a[q] = __ldcg(slot + ws_idx(c1 / 4 + q));
+                        b[q] = __ldcg(slot + ws_idx(c3 / 4 + q));
                     }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < W / 4; ++q) {
                         v1[4 * q + 0] = __float_as_uint(__uint_as_float(v1[4 * q + 0]) + a[q].x);
                         v1[4 * q + 1] = __float_as_uint(__uint_as_float(v1[4 * q + 1]) + a[q].y);
                         v1[4 * q + 2] = __float_as_uint(__uint_as_float(v1[4 * q + 2]) + a[q].z);
@@ -1211,28 +1236,45 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     }
                 }
                 uint8_t* stg = smem_stg + ewarp * C::STG_WARP_BYTES;  // this warp's two 2 KB boxes
+                // the two boxes alternate store by store: the box written now was last used two
+                // stores ago, so at most one store (the other box) may be pending
+                const OutMaps* maps = W == 32 ? &omaps : &omaps_h;
+                float o[32];
                 if constexpr (kEpi == 0) {
-                    float o[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = silu_gate(__uint_as_float(v1[j]), __uint_as_float(v3[j]), gr);
-                    if (use_tma) {
-                        // the two boxes alternate store by store: the box written now was last
-                        // used two stores ago, so at most one store (the other box) may be pending
-                        store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0,
-                                         lane);
-                    } else {
-                        store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
-                    }
+                    for (int j = 0; j < W; ++j) o[j] = silu_gate(__uint_as_float(v1[j]), __uint_as_float(v3[j]), gr);
+                    if (use_tma) store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + c1, box_row0, lane);
+                    else store_row32<kKind, W>(p, row, nb * C::OUT_COLS + c1, o);
                 } else {
-                    float o[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);
-                    if (use_tma) store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + ca * 32, box_row0, lane);
-                    else store_row32<kKind>(p, row, nb * C::OUT_COLS + ca * 32, o);
+                    for (int j = 0; j < W; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);
+                    if (use_tma) store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + c1, box_row0, lane);
+                    else store_row32<kKind, W>(p, row, nb * C::OUT_COLS + c1, o);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = apply_act(rr * __uint_as_float(v3[j]), p.act, p.alpha);
-                    if (use_tma) store_box_tma<1>(&omaps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + cb * 32, box_row0, lane);
-                    else store_row32<kKind>(p, row, nb * C::OUT_COLS + cb * 32, o);
+                    for (int j = 0; j < W; ++j) o[j] = apply_act(rr * __uint_as_float(v3[j]), p.act, p.alpha);
+                    if (use_tma) store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + c3, box_row0, lane);
+                    else store_row32<kKind, W>(p, row, nb * C::OUT_COLS + c3, o);
+                }
+            };
+#pragma unroll 1
+            for (int i = 0; i < C::EPI_ITERS; ++i) {
+                if constexpr (kEpi == 0) {
+                    // SwiGLU: the two warps of a quadrant alternate 32-column units
+                    int u = half + 2 * i;
+                    if (rep) {
+                        // rep 4 (M <= 32): quadrant q holds rows 0..31 and drains unit q, the
+                        // second warp of each quadrant idles; rep 2 (M <= 64): quadrants q, q+2
+                        // hold rows 32(q%2).., and each of their four warps drains one unit
+                        if (i != 0 || (rep == 4 && half != 0)) continue;
+                        u = rep == 4 ? static_cast<int>(quad) : static_cast<int>(quad / 2) * 2 + half;
+                    }
+                    if (u >= C::NU) continue;
+                    if (C::BN % 32 == 0 || u + 1 < C::NU)
+                        unit(std::integral_constant<int, 32>{}, 32 * u, C::BN + 32 * u);
+                    else
+                        unit(std::integral_constant<int, 16>{}, 32 * u, C::BN + 32 * u);
+                } else {
+                    unit(std::integral_constant<int, 32>{}, 32 * C::chunk_a(half, i), 32 * C::chunk_b(half, i));
                 }
                 CUASM_EPI_STAMP(13 + (i > 0 ? 1 : 0));
             }

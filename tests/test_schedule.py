@@ -118,6 +118,10 @@ def test_7b_prefill_balance():
 
 # ---- shape-keyed configuration model (csrc/cuasm_ffn.cu plan_config) ---------
 
+def bn_frac(bn):
+    return 1.0 if bn >= 128 else 0.867 if bn >= 112 else 0.80 if bn >= 96 else 0.70 if bn >= 80 else 0.62
+
+
 def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     t_kb, fixup, hbm, pen_1sm = 0.37e-6, 10e-6, 6.5e12, 1.16
     BK = 128 // esize
@@ -130,34 +134,42 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
              3 if M <= 16 and 3 * t1 <= sm_count and t1 <= 49 else
              2 if 2 * t1 <= sm_count and t1 <= 64 else 0)
         if S:
-            return ("1sm", False, 256, S)
+            return ("1sm", False, 256, S, 128)
     if out_cols == 128 and KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
-        return ("1sm", True, 256, 0)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
+        return ("1sm", True, 256, 0, 128)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
     if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
-        return ("1sm", False, 128, 0)
-    best, best_t = ("2sm", False, 256, 0), 1e30
-    for tn in ((256,) if out_cols == 128 else (256, 128)):
-        oc = 128 if out_cols == 128 else tn
+        return ("1sm", False, 128, 0, 128)
+    best, best_t = ("2sm", False, 256, 0, 128), 1e30
+    if out_cols == 128:   # SwiGLU tile widths (narrower than 128: 2-SM bf16 only)
+        cands = [(256, bn) for bn in (128, 112, 96, 80, 64) if bn == 128 or esize == 2]
+    else:
+        cands = [(256, 128), (128, 128)]
+    for tn, bn in cands:
+        oc = bn if out_cols == 128 else tn
+        wrows = 2 * bn if out_cols == 128 else tn
+        frac = bn_frac(bn) if out_cols == 128 else (1.0 if tn == 256 else 0.72)
         nblk = -(-N // oc)
         for cg in (2, 1):
+            if bn != 128 and cg == 1:
+                continue
             units = sm_count // cg
             mblk = -(-M // (128 * cg))
             tiles = mblk * nblk
             rounds = -(-tiles // units)
-            pen = (pen_1sm if cg == 1 else 1.0) * (1.0 if tn == 256 else 0.72)
+            pen = (pen_1sm if cg == 1 else 1.0) * frac
             t_dp = max(hbm_floor, rounds * KB * t_kb * pen)
             rem = tiles % units
             sk_tiles = tiles if tiles < units else (rem + units if rem else 0)
             gm = min(mblk, max(1, min(16, (32 << 20) // (128 * cg * K * esize))))
-            region = (-(-sk_tiles // gm) + 1) * tn * K * esize + min(M, gm * 128 * cg) * K * esize
+            region = (-(-sk_tiles // gm) + 1) * wrows * K * esize + min(M, gm * 128 * cg) * K * esize
             l2_pen = 1.32 if region > 120e6 else 1.0
             sk_units = min(units, 2 * tiles) if tiles < units else units
             t_sk = max(hbm_floor, tiles * KB * t_kb * pen * l2_pen / sk_units + fixup)
             name = "2sm" if cg == 2 else "1sm"
             if t_dp < best_t * 0.999:
-                best_t, best = t_dp, (name, False, tn, 0)
+                best_t, best = t_dp, (name, False, tn, 0, bn)
             if K // BK > 1 and t_sk < best_t * 0.98:
-                best_t, best = t_sk, (name, True, tn, 0)
+                best_t, best = t_sk, (name, True, tn, 0, bn)
     return best
 
 
@@ -181,12 +193,16 @@ MEASURED_BEST = {
 
 @pytest.mark.parametrize("M", sorted(MEASURED_BEST))
 def test_plan_matches_measured_best(M):
-    assert plan_config(M, 4096, 11008)[:2] in MEASURED_BEST[M]
+    # (a table of 128-wide configurations: shapes whose plan takes a narrower tile are
+    # checked against profiles/r02/tune_bn.json below)
+    pl = plan_config(M, 4096, 11008)
+    assert pl[4] != 128 or pl[:2] in MEASURED_BEST[M]
 
 
-def test_plan_70b_shard_uses_stream_k():
-    # 8-way shard of the 70B FFN: 448 tiles = 6.05 waves of 74 CTA pairs
-    assert plan_config(4096, 8192, 3584)[:2] == ("2sm", True)
+def test_plan_70b_shard_uses_narrow_whole_tiles():
+    # 8-way shard of the 70B FFN: 448 128-wide tiles = 6.05 waves of 74 CTA pairs (stream-K
+    # 292.5 us) vs 512 112-wide tiles = 6.92 waves (whole tiles 282.4 us, profiles/r02/tune_bn.json)
+    assert plan_config(4096, 8192, 3584) == ("2sm", False, 256, 0, 112)
 
 
 def test_plan_w2_down_projection_avoids_l2_thrashing_stream_k():
@@ -206,7 +222,8 @@ def lib_plan():
 
 @pytest.mark.parametrize("M", sorted(MEASURED_BEST))
 def test_library_plan_matches_measured_best(lib_plan, M):
-    assert lib_plan(M, 4096, 11008)[:2] in MEASURED_BEST[M]
+    pl = lib_plan(M, 4096, 11008)
+    assert pl[4] != 128 or pl[:2] in MEASURED_BEST[M]
 
 
 @pytest.mark.parametrize("M,K,N,op", [(m, k, n, op) for m in (1, 16, 200, 512, 1000, 2048, 4096, 16384)
@@ -243,7 +260,29 @@ def test_library_gemm_plan_matches_measured_best(lib_plan, shape):
 
 def test_library_plan_w2_and_70b(lib_plan):
     assert lib_plan(2048, 11008, 4096, "gemm")[:3] != ("2sm", True, 256)
-    assert lib_plan(4096, 8192, 3584)[:2] == ("2sm", True)
+    assert lib_plan(4096, 8192, 3584) == ("2sm", False, 256, 0, 112)
+
+
+# best measured SwiGLU tile width (profiles/r02/tune_bn.json; near-ties <= 1.5% accept either)
+BN_MEASURED = {
+    (2048, 4096, 1376): {80},
+    (2048, 4096, 2752): {112, 80},
+    (2048, 4096, 5504): {128},
+    (2048, 4096, 11008): {112, 80},
+    (1024, 4096, 1376): {80, 96},
+    (1024, 4096, 2752): {80},
+    (512, 4096, 11008): {112, 80},
+    (256, 4096, 11008): {80},
+    (4096, 8192, 3584): {112},
+    (4096, 8192, 7168): {112, 128},
+    (16384, 4096, 1376): {128},
+}
+
+
+@pytest.mark.parametrize("shape", sorted(BN_MEASURED))
+def test_plan_tile_width_matches_measured_best(lib_plan, shape):
+    assert plan_config(*shape)[4] in BN_MEASURED[shape]
+    assert lib_plan(*shape)[4] in BN_MEASURED[shape]
 
 
 # measured (profiles/r01/csplit/ncu_ab_*.txt): the cluster split-K wins on few-tile

@@ -1,0 +1,152 @@
+"""GPU parity of the SwiGLU tile widths (DESIGN.md §6 "Tile widths"; VERDICT r1 next #3,
+SURVEY §7 step 9 / Appendix A.5): BN = 64, 80, 96, 112 outputs per 2-SM tile (MMA N =
+2 BN), the last epilogue unit 16 columns wide when BN % 32 == 16.
+
+Every width is run forced (CUASM_OPT_TILE_BN) on ragged shapes -- M and N tails, a
+partial last unit, one and several k-blocks -- under whole tiles and stream-K, and
+compared element by element with the fp64 oracle's fold-aware mode at the [BJ]
+tolerance |gpu - ref| <= 2e-2|ref| + 1e-3 (PAPER.md P:560 inputs B, M, N, K).  The
+planner's own choices at the tensor-parallel shard shapes, the two W13 cache slots
+(128-wide and narrow packs of one weight set) and the fused gather's half-width
+stores are checked too.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2501_08071_b200 as ffn
+from ffn_inputs import make_inputs
+from paper_2501_08071_b200.tp import gather_destinations, shard_bounds, shard_weights
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-2, 1e-3
+WIDTHS = (64, 80, 96, 112)
+
+
+def check(gpu, ref, what):
+    worst, nbad, maxerr = oracle.tolerance_ratio(gpu.double().cpu().numpy(), ref, RTOL, ATOL)
+    assert nbad == 0, f"{what}: {nbad} elements out of tolerance (worst ratio {worst:.3f}, max|err| {maxerr:.3g})"
+    return worst
+
+
+def _run(dev, d, bn, schedule=ffn.SCHEDULE_AUTO, handle=None):
+    h = handle or ffn.FusedFFN(dev, torch.bfloat16)
+    h.set_option(ffn.OPT_TILE_BN, bn)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
+    t = {k: v.to(dev) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    return out, h
+
+
+@pytest.mark.parametrize("bn", WIDTHS)
+@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL])
+@pytest.mark.parametrize("M,K,N", [(300, 512, 0), (1, 64, 8), (16, 256, 1), (513, 1024, 2)])
+def test_forced_width_matches_oracle(cuda_device, bn, schedule, M, K, N):
+    # N given as an offset past a whole number of tiles: 3 tiles + {24 | 8 | bn+8 | 2bn-8}
+    n = {0: 3 * bn + 24, 8: 8, 1: bn + 8, 2: 5 * bn - 8}[N]
+    d = make_inputs(M, K, n, family="C", seed=8100 + bn + M + K, dtype="bf16")
+    out, h = _run(cuda_device, d, bn, schedule)
+    v, _ = h.last_launch()
+    assert v == ffn.VARIANT_2SM
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16")
+    check(out, ref, f"bn={bn} sched={schedule} {M}x{K}x{n}")
+
+
+@pytest.mark.parametrize("bn", WIDTHS)
+def test_forced_width_exact_family_equals_128(cuda_device, bn):
+    """Exact-fold family A: the narrow tile and the 128-wide tile agree with the plain
+    definition, and whole-tile results of both widths agree with each other."""
+    M, K, N = 384, 768, 4 * bn + 40
+    d = make_inputs(M, K, N, family="A", seed=8200 + bn, dtype="bf16")
+    out, _ = _run(cuda_device, d, bn, ffn.SCHEDULE_DATA_PARALLEL)
+    out128, _ = _run(cuda_device, d, 128, ffn.SCHEDULE_DATA_PARALLEL)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6)
+    check(out, ref, f"bn={bn} family A")
+    check(out128, ref, "bn=128 family A")
+    diff = (out.float() - out128.float()).abs().max().item()
+    assert diff <= 2.0 ** -6 * out128.float().abs().max().item()
+
+
+@pytest.mark.parametrize("M,N_l", [(2048, 1376), (1024, 2752), (2048, 2752), (512, 5504), (4096, 1376)])
+def test_planned_widths_at_shard_shapes(cuda_device, M, N_l):
+    """The configuration model's own choice at 7B prefill shard shapes (P = 8 / 4 / 2),
+    sampled rows against the oracle; run-to-run bitwise."""
+    K = 4096
+    plan = ffn.plan_config(M, K, N_l)
+    d = make_inputs(M, K, N_l, family="C", seed=8300 + M + N_l, dtype="bf16")
+    out, h = _run(cuda_device, d, 0)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    again = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(out, again), "bitwise run-to-run"
+    rng = np.random.default_rng(M)
+    rows = sorted({0, M - 1} | set(rng.choice(M, 10, replace=False).tolist()) | {b * 256 for b in range(M // 256)})
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(out[rows], ref, f"{M}x{K}x{N_l} plan {plan}")
+
+
+def test_both_w13_slots_alive(cuda_device):
+    """One weight set served at a decode shape (128-wide pack, cluster split-K) and a
+    prefill shape whose plan takes a narrow width (second pack): alternating calls
+    re-use both packs and stay correct; an in-place weight change re-packs both."""
+    K, N = 4096, 1376
+    big = make_inputs(2048, K, N, family="C", seed=8400, dtype="bf16")
+    assert ffn.plan_config(2048, K, N)[4] != 128 and ffn.plan_config(16, K, N)[4] == 128
+    small_x = make_inputs(16, K, N, family="C", seed=8401, dtype="bf16")["x"]
+    t = {k: v.to(cuda_device) for k, v in big.items()}
+    xs = small_x.to(cuda_device)
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    rows = [0, 777, 2047]
+    for it in range(2):
+        o_big = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+        o_small = h.forward(xs, t["g"], t["w1"], t["w3"], 1e-6)
+        torch.cuda.synchronize()
+        w1 = big["w1"] if it == 0 else -big["w1"]
+        check(o_big[rows], oracle.ffn(big["x"], big["g"], w1, big["w3"], 1e-6, mode="fold_bf16", rows=rows),
+              f"prefill it {it}")
+        check(o_small, oracle.ffn(small_x, big["g"], w1, big["w3"], 1e-6, mode="fold_bf16"), f"decode it {it}")
+        t["w1"].neg_()  # in place: the binding's version counter invalidates every pack
+
+
+@pytest.mark.parametrize("bn", [80, 112])
+def test_fused_gather_half_width_units(cuda_device, bn):
+    """f2 with a narrow tile: every simulated peer buffer holds the concatenated shard
+    outputs, including the 16-column units stored through the half-width maps."""
+    M, K, N, P = 300, 512, 2 * (3 * bn + 16), 2
+    d = make_inputs(M, K, N, family="C", seed=8500 + bn, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    bufs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda_device) for _ in range(P)]
+    outs = []
+    for rank in range(P):
+        n0, _ = shard_bounds(N, rank, P)
+        w1s, w3s = shard_weights(t["w1"], t["w3"], rank, P)
+        h = ffn.FusedFFN(cuda_device)
+        h.set_option(ffn.OPT_TILE_BN, bn)
+        dst, _ = gather_destinations([b.data_ptr() for b in bufs], n0, 2)
+        h.forward_gather(t["x"], t["g"], w1s, w3s, dst, N, 1e-6, keepalive=bufs)
+        outs.append(h.forward(t["x"], t["g"], w1s, w3s, 1e-6))
+    torch.cuda.synchronize()
+    full = torch.cat(outs, dim=1)
+    for q in range(P):
+        assert torch.equal(bufs[q], full)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16")
+    check(full, ref, f"gather bn={bn}")
+
+
+def test_tile_bn_option_contract(cuda_device):
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    for bad in (1, 72, 256, -1):
+        with pytest.raises(ffn.CuasmError):
+            h.set_option(ffn.OPT_TILE_BN, bad)
+    # a forced 1-SM variant keeps the 128-wide tile
+    d = make_inputs(200, 256, 200, family="C", seed=8600, dtype="bf16")
+    h.set_option(ffn.OPT_TILE_BN, 80)
+    h.set_variant(ffn.VARIANT_1SM)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert h.last_launch()[0] == ffn.VARIANT_1SM
+    check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), "1sm with TILE_BN=80")
