@@ -85,6 +85,7 @@ def parse_args(argv=None):
     ap.add_argument("--workload", default="llama7b_prefill",
                     help="llama7b_prefill | llama7b_decode | llama70b | sweep:M (K=4096, N=11008)")
     ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 one-SM, 2 two-SM (CTA pair)")
+    ap.add_argument("--tile-bn", type=int, default=0, help="SwiGLU outputs per tile: 0 auto, 128/112/96/80/64")
     ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step (NCCL)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="a4 fused into the epilogue (cuasm_ffn_forward_gather): every rank's full [M,N] "
@@ -406,6 +407,8 @@ def run_cuasm(args):
     for _ in range(n_layers):
         hh = ffn.FusedFFN(dev, wdtype)
         hh.set_variant(args.variant)
+        if args.tile_bn:
+            hh.set_option(ffn.OPT_TILE_BN, args.tile_bn)
         if args.no_pdl:
             hh.set_option(ffn.OPT_PDL, 0)
         handles.append(hh)
@@ -726,9 +729,11 @@ def run_cuasm(args):
                       "256 MiB read so the flush's dirty lines are written back before the step",
                 "op": op, "flops_per_step": flops_per_step, "prep_ms": round(prep_ms, 4),
                 # the configuration model's plan for this rank's problem: (variant, stream-K tail,
-                # MMA N, cluster split-K width); the launch follows it unless options override
+                # MMA N, cluster split-K width, SwiGLU outputs per tile); the launch follows it
+                # unless options override (--variant, --tile-bn)
                 "plan": list(ffn.plan_config(M, K, N_l, "gemm" if op == "gemm_lrelu" else "ffn", wdtype))
                 if op in ("ffn", "gemm_lrelu") else None,
+                "tile_bn_forced": args.tile_bn or None,
             },
             "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),
             "pct_of_nominal_2250": round(value / world / 2250.0, 4),
