@@ -91,6 +91,9 @@ def parse_args(argv=None):
                     help="a4 fused into the epilogue (cuasm_ffn_forward_gather): every rank's full [M,N] "
                          "symmetric-memory buffer written by every kernel; with --shard-of P on one GPU, P "
                          "simulated peer buffers on this device (store fan-out cost only, no NVLink)")
+    ap.add_argument("--fused-reduce", action="store_true",
+                    help="block workload: the row-parallel W2 reduction fused into the down projection's epilogue "
+                         "(f1; with --shard-of P: P simulated staging / output buffers on this GPU)")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of a CUDA graph")
     ap.add_argument("--shard-of", type=int, default=1,
@@ -398,7 +401,8 @@ def run_cuasm(args):
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     n_layers = 1 + int(-(-2 * l2_bytes // int(step_bytes)))
     fused_gather = args.fused_gather and op == "ffn"
-    b2b_ok = not args.gather and not fused_gather and not args.no_graph and n_layers <= MAX_LAYER_COPIES and not args.skip_b2b
+    fused_reduce = args.fused_reduce and op == "block"
+    b2b_ok = not args.gather and not fused_gather and not fused_reduce and not args.no_graph and n_layers <= MAX_LAYER_COPIES and not args.skip_b2b
     if not b2b_ok:
         n_layers = 1
     layers = [(t, out)] + [({k: v.clone() for k, v in t.items()}, torch.empty_like(out)) for _ in range(n_layers - 1)]
@@ -428,8 +432,31 @@ def run_cuasm(args):
             sim_bufs = [torch.empty((M, N_l * P_sim), dtype=wdtype, device=dev) for _ in range(P_sim)]
             gather_dst, gather_mc = gather_destinations([b.data_ptr() for b in sim_bufs], 0, out.element_size())
 
+    # f1 fused reduction: every rank's symmetric staging / output buffers (world > 1), or
+    # P simulated ones on this GPU (rank 0's scatter + its owner reduction, --shard-of P)
+    fr, sim_stage, sim_y = None, None, None
+    if fused_reduce:
+        if world > 1:
+            from paper_2501_08071_b200.tp import FusedReduce
+            fr = FusedReduce(M, K, dev)
+        else:
+            P_sim = max(1, args.shard_of)
+            sim_stage = [torch.empty((max(ffn.rs_layout(M, K, P_sim, q)[2] // 4, 4),), dtype=torch.float32,
+                                     device=dev) for q in range(P_sim)]
+            sim_y = [torch.empty((M, K), dtype=torch.bfloat16, device=dev) for _ in range(P_sim)]
+
     def fwd(i=0):
         hh, (tt, oo) = handles[i], layers[i]
+        if fused_reduce:
+            if fr is not None:
+                from paper_2501_08071_b200.tp import ffn_block_tp_forward
+                return ffn_block_tp_forward(tt["x"], tt["g"], tt["w1"], tt["w3"], tt["w2"], eps, handle=hh,
+                                            reduce="fused", fused=fr)
+            P_sim = len(sim_stage)
+            hh.block_forward_rs(tt["x"], tt["g"], tt["w1"], tt["w3"], tt["w2"], [b.data_ptr() for b in sim_stage],
+                                P_sim, 0, eps)
+            hh.rs_reduce(sim_stage[0], P_sim, 0, [b.data_ptr() for b in sim_y], K, M, K)
+            return None
         if fused_gather:
             hh.forward_gather(tt["x"], tt["g"], tt["w1"], tt["w3"], gather_dst,
                               N if world > 1 else N_l * max(1, args.shard_of), eps, multicast=gather_mc)
@@ -444,18 +471,18 @@ def run_cuasm(args):
             return hh.rmsnorm(tt["x"], tt["g"], eps, out=oo)
         return hh.gemm_act(tt["x"], tt["w1"], "leaky_relu", 0.01, out=oo)
 
-    # a0: one-time weight fold/pack (reported, not part of a step)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # a0: one-time weight fold/pack (reported, not part of a step): the first forward packs the
+    # weights for the tile width its plan uses; prep = that call minus a second (packed) one
+    e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
     e0.record(stream)
-    if op in ("gemm_lrelu", "rmsnorm"):
-        fwd(0)  # the first call packs the weight (gemm)
-    else:
-        h.prepare(t["g"], t["w1"], t["w3"])
-        if op == "block":
-            fwd(0)
+    fwd(0)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    prep_ms = e0.elapsed_time(e1)
+    e2.record(stream)
+    fwd(0)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    prep_ms = max(0.0, e0.elapsed_time(e1) - e2.elapsed_time(e3))
     for i in range(1, n_layers):
         fwd(i)
     torch.cuda.synchronize(dev)
@@ -720,6 +747,11 @@ def run_cuasm(args):
                 "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else (
                     f"PROJECTION of tp{args.shard_of}: rank 0's shard timed alone on one GPU; value = "
                     f"{args.shard_of} x its FLOPs / its time" if args.shard_of > 1 else "single GPU"),
+                "reduce": (("fused: W2 epilogue scatters fp32 partial tiles to the owners' staging buffers, "
+                            "owner rank-order sum fanned out to every rank's output " + (
+                                "(symmetric memory)" if world > 1 else
+                                f"({max(1, args.shard_of)} simulated ranks on this GPU: rank 0's launches)"))
+                           if fused_reduce else ("none (rank-local partial)" if op == "block" else None)),
                 "gather": ("fused: kernel epilogue stores into " + (
                     f"every rank's symmetric buffer ({'NVLS multicast' if gather_mc else 'P2P peer pointers'})"
                     if world > 1 else f"{max(1, args.shard_of)} simulated peer buffers on this GPU")

@@ -214,6 +214,46 @@ cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x_dev, const v
                                        const void* w3_dev, const void* w2_dev, void* out_dev, int64_t M, int64_t K,
                                        int64_t N, float eps, void* stream);
 
+/* Tensor-parallel FFN block with the row-parallel reduction fused into the down
+ * projection (DESIGN.md §8 "Fused reduction").  Megatron split
+ * over `world` ranks: rank `rank` holds w1/w3 [N,K] = its rows of W1/W3 and w2
+ * [K,N] = the same N columns of W2 (N = this rank's N_l); its partial
+ *   y_rank[m,k] = sum_{n in shard} hidden[m,n] * w2[k,n]
+ * never lands in local memory: the output columns are owned in 256-column blocks
+ * split evenly over the ranks (cuasm_rs_layout), and every fp32 partial tile is
+ * stored by the GEMM epilogue (TMA) straight into the owner q's staging buffer,
+ *   stage[q] + rank * M * Kq * 4 bytes, layout [M][Kq] fp32, Kq = q's column count,
+ * so the transfer overlaps the GEMM tile by tile.  stage[q] is rank q's staging
+ * buffer base ([world][M][Kq] fp32, cuasm_rs_layout's stage_bytes; device memory
+ * of any rank reachable from this GPU: peer / symmetric-memory pointers), 16-byte
+ * aligned; entries of ranks owning no columns may be NULL.  bf16 handles only.
+ * Two launches (fused FFN, W2 GEMM).  The stores are complete when the stream's
+ * work is; the caller orders them with a cross-rank barrier before any owner
+ * runs cuasm_rs_reduce.  Errors as cuasm_ffn_block_forward, plus world in [1, 8],
+ * 0 <= rank < world. */
+cuasm_status_t cuasm_ffn_block_forward_rs(cuasm_ffn_t h, const void* x_dev, const void* rms_w_dev,
+                                          const void* w1_dev, const void* w3_dev, const void* w2_dev,
+                                          void* const* stage, int world, int rank, int64_t M, int64_t K, int64_t N,
+                                          float eps, void* stream);
+
+/* The owner side of f1: y[:, col0:col1] = RNE_bf16( sum_{p = 0..world-1} stage[p][:, :] )
+ * summed in fp32 in rank order (bitwise independent of arrival order), written into
+ * every destination dst[0..num_dst) -- each rank's full [M, ldo] bf16 output
+ * (P2P), so reduce-scatter + this all-gather is the all-reduce -- or, multicast
+ * = 1, once to the NVLS multicast address dst[0] (multimem.st).  stage: this
+ * rank's staging buffer (device, 16-byte aligned); [col0, col1) from
+ * cuasm_rs_layout(M, K, world, rank).  One HBM-bound launch; no launch when the
+ * rank owns no columns or M == 0. */
+cuasm_status_t cuasm_rs_reduce(cuasm_ffn_t h, const void* stage_dev, int world, int rank, void* const* dst,
+                               int num_dst, int multicast, int64_t ldo, int64_t M, int64_t K, void* stream);
+
+/* f1 ownership (pure host code): rank `rank` of `world` reduces output columns
+ * [*col0, *col1) of a [M, K] block output; its staging buffer holds
+ * *stage_bytes = world * M * (col1 - col0) * 4 bytes.  CUASM_ERR_INVALID_ARG on
+ * K <= 0, K % 8 != 0, world outside [1, 8] or rank outside [0, world). */
+cuasm_status_t cuasm_rs_layout(int64_t M, int64_t K, int world, int rank, int64_t* col0, int64_t* col1,
+                               int64_t* stage_bytes);
+
 /* Stand-alone RMSNorm (the paper's memory-bound "rmsnorm"
  * kernel, PAPER.md P:68 / P:523 / P:573):
  *   out[m,k] = x[m,k] * g[k] / sqrt( (sum_k x[m,k]^2)/K + eps )

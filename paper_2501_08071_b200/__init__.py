@@ -20,7 +20,7 @@ import torch
 
 __all__ = [
     "FusedFFN", "ffn_forward", "ffn_forward_host", "rms_inv", "rmsnorm", "gemm_act", "ffn_block_forward", "CuasmError",
-    "lib_path", "load_library",
+    "lib_path", "load_library", "rs_layout",
     "VARIANT_AUTO", "VARIANT_1SM", "VARIANT_2SM", "EXPORTED_SYMBOLS",
 ]
 
@@ -39,7 +39,7 @@ SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL, SCHEDULE_STREAM_K_
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "cuasm_ffn_init", "cuasm_ffn_forward", "cuasm_ffn_forward_gather", "cuasm_ffn_forward_host", "cuasm_gemm_act",
-    "cuasm_ffn_block_forward",
+    "cuasm_ffn_block_forward", "cuasm_ffn_block_forward_rs", "cuasm_rs_reduce", "cuasm_rs_layout",
     "cuasm_rmsnorm",
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
@@ -58,6 +58,17 @@ def plan_config(M: int, K: int, N: int, op: str = "ffn", dtype=torch.bfloat16, s
         raise CuasmError(st, "cuasm_plan_config: invalid arguments")
     return (("1sm" if v.value == VARIANT_1SM else "2sm"), bool(sk.value & 1), (128 if sk.value & 2 else 256),
             (sk.value >> 4) & 15, sk.value >> 8)
+
+
+def rs_layout(M: int, K: int, world: int, rank: int):
+    """f1 ownership (cuasm_rs_layout, host only): (col0, col1, stage_bytes) -- the output
+    columns rank `rank` reduces and the size of its fp32 staging buffer."""
+    lib = load_library()
+    c0, c1, nb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    st = lib.cuasm_rs_layout(M, K, world, rank, ctypes.byref(c0), ctypes.byref(c1), ctypes.byref(nb))
+    if st != OK:
+        raise CuasmError(st, "cuasm_rs_layout: invalid arguments")
+    return c0.value, c1.value, nb.value
 
 
 class CuasmError(RuntimeError):
@@ -88,6 +99,11 @@ def load_library():
                                                  f32, vp]
         lib.cuasm_gemm_act.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, f32, vp]
         lib.cuasm_ffn_block_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, vp]
+        lib.cuasm_ffn_block_forward_rs.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.POINTER(vp), ci, ci, i64, i64, i64,
+                                                    f32, vp]
+        lib.cuasm_rs_reduce.argtypes = [vp, vp, ci, ci, ctypes.POINTER(vp), ci, ci, i64, i64, i64, vp]
+        lib.cuasm_rs_layout.argtypes = [i64, i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                        ctypes.POINTER(i64)]
         lib.cuasm_rmsnorm.argtypes = [vp, vp, vp, vp, i64, i64, f32, vp]
         lib.cuasm_ffn_prepare.argtypes = [vp, vp, vp, vp, i64, i64, vp]
         lib.cuasm_ffn_rms_inv.argtypes = [vp, vp, vp, i64, i64, f32, vp]
@@ -317,6 +333,36 @@ class FusedFFN:
                                                      w3.data_ptr(), w2.data_ptr(), out.data_ptr(), M, K, N,
                                                      float(eps), _stream_ptr(x.device)))
         return out
+
+    def block_forward_rs(self, x, rms_w, w1, w3, w2, stage_ptrs, world: int, rank: int, eps: float = 1e-6,
+                         keepalive=None):
+        """f1: this rank's share of the tensor-parallel FFN block with the row-parallel
+        reduction fused into the down projection (cuasm_ffn_block_forward_rs): every
+        fp32 partial tile goes straight into its owner's staging buffer (`stage_ptrs[q]`
+        = rank q's buffer base, see rs_layout).  w1/w3 [N_l,K], w2 [K,N_l]."""
+        self._validate(x, rms_w, w1, w3, w2)
+        if keepalive is not None:
+            for t in keepalive:
+                if not t.is_cuda:
+                    raise ValueError("staging buffers must be device memory")
+        M, K = x.shape
+        N = w1.shape[0]
+        if w2.shape != (K, N) or w1.shape != (N, K) or w3.shape != (N, K) or len(stage_ptrs) != world:
+            raise ValueError("shape mismatch")
+        stage = (ctypes.c_void_p * world)(*[int(p_) if p_ else None for p_ in stage_ptrs])
+        self._weights_changed({0: (rms_w, w1, w3), 1: (w2,)})
+        self._check(self.lib.cuasm_ffn_block_forward_rs(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(),
+                                                        w3.data_ptr(), w2.data_ptr(), stage, world, rank, M, K, N,
+                                                        float(eps), _stream_ptr(x.device)))
+
+    def rs_reduce(self, stage, world: int, rank: int, dst_ptrs, ldo: int, M: int, K: int, multicast: bool = False):
+        """f1 owner side (cuasm_rs_reduce): sum this rank's staging slots in rank order and
+        write its columns of y into every destination (or the multicast address)."""
+        if stage.dtype != torch.float32 or not stage.is_cuda or stage.device.index != self.device_index:
+            raise ValueError("stage must be an fp32 tensor on the handle's device")
+        dst = (ctypes.c_void_p * len(dst_ptrs))(*[int(p_) for p_ in dst_ptrs])
+        self._check(self.lib.cuasm_rs_reduce(self._h, stage.data_ptr(), world, rank, dst, len(dst_ptrs),
+                                             1 if multicast else 0, int(ldo), M, K, _stream_ptr(stage.device)))
 
     def rmsnorm(self, x, rms_w, eps: float = 1e-6, out=None):
         """RMSNorm(x) = x * g / sqrt(mean(x^2) + eps) (the paper's rmsnorm kernel)."""

@@ -20,6 +20,7 @@
 #include "dual_gemm.cuh"
 #include "pack.cuh"
 #include "prepass.cuh"
+#include "reduce.cuh"
 
 namespace {
 
@@ -328,7 +329,21 @@ struct EpiSpec {
     const void* x_src = nullptr;
     int64_t k_src = 0;
     int64_t kp = 0;
+    // f1 fused reduce-scatter (GEMM mode): stage[q] = rank q's fp32 staging buffer, this
+    // launch's partial tiles go to their owner's slot `rs_rank` (dual_gemm.cuh rs_owner)
+    void* const* rs_stage = nullptr;
+    int rs_world = 0;
+    int rs_rank = 0;
 };
+
+// f1 ownership: rank q reduces the output columns [col0, col1) (256-column blocks split
+// evenly, dual_gemm.cuh rs_owner / rs_col0); its staging buffer is [world][M][col1 - col0] fp32.
+void rs_cols(int64_t K, int world, int q, int64_t& col0, int64_t& col1) {
+    const int nblk = static_cast<int>((K + 255) / 256);
+    col0 = cuasm::rs_col0(q, nblk, world);
+    col1 = std::min<int64_t>(K, cuasm::rs_col0(q + 1, nblk, world));
+    if (col1 < col0) col1 = col0;
+}
 
 // Few-tile decode shapes: at most this many 1-SM tiles take the 1-SM variant with
 // each tile split this many ways (plan_config_raw, launch_gemm).
@@ -365,7 +380,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         const int want = h->csplit_opt >= 2 ? h->csplit_opt : (h->csplit_opt == 0 ? h->plan_csplit : 0);
         const int64_t tiles = ((M + C::TILE_M - 1) / C::TILE_M) * ((N + C::OUT_COLS - 1) / C::OUT_COLS);
         const int64_t kbs = (K + C::BK - 1) / C::BK;
-        if (want >= 2 && want <= 8 && tiles * want <= h->sm_count && kbs >= want) csplit = want;
+        if (want >= 2 && want <= 8 && tiles * want <= h->sm_count && kbs >= want && e.rs_world == 0) csplit = want;
     }
     const int rep_plain = (kEpi != 0 || !C::kDecodePaths) ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
     const int rep = csplit ? 0 : rep_plain;
@@ -425,6 +440,31 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     cuasm::OutMaps omaps{}, omaps_h{};
     p.tma_store = (kKind == 0 && !p.dst_mc) ? 1 : 0;
     constexpr bool kHalfUnit = kEpi == 0 && C::BN % 32 == 16;
+    p.rs_world = 0;
+    p.rs_nblk = static_cast<int>((N + 255) / 256);
+    if (e.rs_world > 0) {
+        // f1: one fp32 map per owner rank q over its staging slot for this rank,
+        // stage[q] + rs_rank * M * Kq floats, [M, Kq], 32 x 16 boxes (64-byte rows, 64-byte swizzle)
+        if (kKind != 0 || kEpi != 1) return fail(h, CUASM_ERR_UNSUPPORTED, "fused reduce-scatter: bf16 GEMM only");
+        p.rs_world = e.rs_world;
+        p.num_dst = 0;
+        for (int q = 0; q < e.rs_world; ++q) {
+            int64_t c0, c1;
+            rs_cols(N, e.rs_world, q, c0, c1);
+            const int64_t kq = c1 - c0;
+            if (kq == 0) continue;  // owns no columns: no tile is ever sent there
+            cuuint64_t dims[2] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(M)};
+            cuuint64_t strides[1] = {static_cast<cuuint64_t>(kq) * 4};
+            cuuint32_t box[2] = {16, 32};
+            cuuint32_t estr[2] = {1, 1};
+            void* base = static_cast<char*>(e.rs_stage[q]) + static_cast<int64_t>(e.rs_rank) * M * kq * 4;
+            CUresult r = h->encode(&omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(stage %d) failed (CUresult %d)", q, (int)r);
+        }
+    }
     for (int q = 0; p.tma_store && q < p.num_dst; ++q) {
         for (int hw = 0; hw < (kHalfUnit ? 2 : 1); ++hw) {
             cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
@@ -1074,18 +1114,15 @@ cuasm_status_t cuasm_gemm_act(cuasm_ffn_t h, const void* x, const void* w, void*
     return gemm_act_impl(h, x, w, out, M, K, N, act, alpha, static_cast<cudaStream_t>(stream));
 }
 
-cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
-                                       const void* w3, const void* w2, void* out, int64_t M, int64_t K, int64_t N,
-                                       float eps, void* stream) {
-    NvtxRange nvtx_("cuasm_ffn_block_forward");
-    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
-    h->err.clear();
-    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
-    if (st != CUASM_OK) return st;
-    if (!w2 || !aligned16(w2)) return fail(h, CUASM_ERR_INVALID_ARG, "w2 must be non-NULL and 16-byte aligned");
+namespace {
+// The FFN block: hidden [M,N] = fused FFN (handle workspace), then out = hidden . W2^T,
+// or -- rs_world > 0 -- its fp32 partial tiles scattered to their owners' staging slots.
+cuasm_status_t block_impl(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
+                          const void* w2, void* out, void* const* stage, int world, int rank, int64_t M, int64_t K,
+                          int64_t N, float eps, cudaStream_t s) {
+    cuasm_status_t st;
     DeviceGuard dg(h);
     if ((st = dg.status) != CUASM_OK) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t hb = M * N * h->esize;
     if (hb > h->hidden_bytes) {
         if (h->hidden) cudaFree(h->hidden);
@@ -1100,8 +1137,94 @@ cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void*
     // out [M,K] = hidden . W2^T  (W2 [K,N], nn.Linear(N -> K) layout)
     if ((st = ensure_packed(h, 1, nullptr, w2, nullptr, N, K, s)) != CUASM_OK) return st;
     h->last_kernels = k1;
-    const EpiSpec e{1, 0, 0, CUASM_ACT_IDENTITY, 0.f};
+    EpiSpec e{1, 0, 0, CUASM_ACT_IDENTITY, 0.f};
+    e.rs_stage = stage;
+    e.rs_world = stage ? world : 0;
+    e.rs_rank = rank;
     return run_gemm(h, 1, e, h->hidden, out, M, N, K, 0.f, s);
+}
+}  // namespace
+
+cuasm_status_t cuasm_ffn_block_forward(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
+                                       const void* w3, const void* w2, void* out, int64_t M, int64_t K, int64_t N,
+                                       float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_block_forward");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    if (!w2 || !aligned16(w2)) return fail(h, CUASM_ERR_INVALID_ARG, "w2 must be non-NULL and 16-byte aligned");
+    return block_impl(h, x, rms_w, w1, w3, w2, out, nullptr, 0, 0, M, K, N, eps, static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_rs_layout(int64_t M, int64_t K, int world, int rank, int64_t* col0, int64_t* col1,
+                               int64_t* stage_bytes) {
+    if (M < 0 || K <= 0 || K % 8 != 0 || world < 1 || world > 8 || rank < 0 || rank >= world || !col0 || !col1)
+        return CUASM_ERR_INVALID_ARG;
+    rs_cols(K, world, rank, *col0, *col1);
+    if (stage_bytes) *stage_bytes = static_cast<int64_t>(world) * M * (*col1 - *col0) * 4;
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_block_forward_rs(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1,
+                                          const void* w3, const void* w2, void* const* stage, int world, int rank,
+                                          int64_t M, int64_t K, int64_t N, float eps, void* stream) {
+    NvtxRange nvtx_("cuasm_ffn_block_forward_rs");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "the fused reduce-scatter is bf16 only");
+    if (world < 1 || world > 8 || rank < 0 || rank >= world)
+        return fail(h, CUASM_ERR_INVALID_ARG, "world must be in [1, 8] and 0 <= rank < world");
+    if (!stage) return fail(h, CUASM_ERR_INVALID_ARG, "NULL stage array");
+    // validate_forward with a stand-in output pointer (the outputs are the staging slots)
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, stage[0] ? stage[0] : x, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    if (!w2 || !aligned16(w2)) return fail(h, CUASM_ERR_INVALID_ARG, "w2 must be non-NULL and 16-byte aligned");
+    for (int q = 0; q < world; ++q) {
+        int64_t c0, c1;
+        rs_cols(K, world, q, c0, c1);
+        if (c1 > c0 && M > 0 && (!stage[q] || !aligned16(stage[q])))
+            return fail(h, CUASM_ERR_INVALID_ARG, "stage[%d] must be non-NULL and 16-byte aligned", q);
+    }
+    return block_impl(h, x, rms_w, w1, w3, w2, nullptr, stage, world, rank, M, K, N, eps,
+                      static_cast<cudaStream_t>(stream));
+}
+
+cuasm_status_t cuasm_rs_reduce(cuasm_ffn_t h, const void* stage, int world, int rank, void* const* dst, int num_dst,
+                               int multicast, int64_t ldo, int64_t M, int64_t K, void* stream) {
+    NvtxRange nvtx_("cuasm_rs_reduce");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    h->last_kernels = 0;
+    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "the fused reduce-scatter is bf16 only");
+    if (world < 1 || world > 8 || rank < 0 || rank >= world)
+        return fail(h, CUASM_ERR_INVALID_ARG, "world must be in [1, 8] and 0 <= rank < world");
+    if (M < 0 || M >= (int64_t(1) << 31) || K <= 0 || K % 8 != 0)
+        return fail(h, CUASM_ERR_INVALID_ARG, "M must be in [0, 2^31) and K a positive multiple of 8");
+    if (!dst || num_dst < 1 || num_dst > 8) return fail(h, CUASM_ERR_INVALID_ARG, "num_dst must be in [1, 8]");
+    if (multicast != 0 && multicast != 1) return fail(h, CUASM_ERR_INVALID_ARG, "multicast is 0 or 1");
+    if (multicast && num_dst != 1) return fail(h, CUASM_ERR_INVALID_ARG, "a multicast destination is one address");
+    if (ldo < K || ldo % 8 != 0) return fail(h, CUASM_ERR_INVALID_ARG, "ldo must be >= K and a multiple of 8");
+    int64_t c0, c1;
+    rs_cols(K, world, rank, c0, c1);
+    if (M == 0 || c1 == c0) return CUASM_OK;  // this rank owns no columns
+    if (!stage || !aligned16(stage)) return fail(h, CUASM_ERR_INVALID_ARG, "stage must be non-NULL, 16-byte aligned");
+    for (int q = 0; q < num_dst; ++q)
+        if (!dst[q] || !aligned16(dst[q])) return fail(h, CUASM_ERR_INVALID_ARG, "destination %d invalid", q);
+    cuasm_status_t st;
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cuasm::RsDst d{};
+    for (int q = 0; q < num_dst; ++q) d.p[q] = dst[q];
+    const int64_t groups = M * ((c1 - c0) / 8);
+    const int64_t blocks = std::min<int64_t>((groups + 255) / 256, int64_t(h->sm_count) * 8);
+    cuasm::ffn_rs_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        static_cast<const float*>(stage), world, M, static_cast<int>(c1 - c0), static_cast<int>(c0), d, num_dst,
+        multicast, ldo);
+    CUASM_CHECK(h, cudaGetLastError(), "ffn_rs_reduce_kernel launch");
+    h->last_kernels = 1;
+    return CUASM_OK;
 }
 
 cuasm_status_t cuasm_rmsnorm(cuasm_ffn_t h, const void* x, const void* rms_w, void* out, int64_t M, int64_t K,

@@ -72,6 +72,12 @@ struct FfnGemmParams {
     void* dst[8];
     int num_dst;     // 1..8 (1 = plain local output)
     int dst_mc;      // 1: dst[0] is a multicast address
+    // f1 fused reduce-scatter (kEpi 1; DESIGN.md §8 "Fused reduction"): rs_world
+    // > 0 makes every output tile an fp32 partial that leaves through omaps.m[q], q = the rank
+    // owning the tile's 256-column block (blocks split evenly over rs_world ranks), into q's
+    // staging slot for this rank at column col - col0(q); 0 = off
+    int rs_world;
+    int rs_nblk;     // 256-column blocks of the output: ceil(N / 256)
     int M, N, K;
     int num_m_blk;   // ceil(M / tile_m)
     int num_n_blk;   // ceil(N / OUT_COLS)
@@ -401,6 +407,35 @@ __device__ __forceinline__ void store_row32(const FfnGemmParams& p, int row, int
                                make_uint4(__float_as_uint(o[4 * q + 0]), __float_as_uint(o[4 * q + 1]),
                                           __float_as_uint(o[4 * q + 2]), __float_as_uint(o[4 * q + 3])));
         }
+    }
+}
+
+// f1 reduce-scatter ownership: the output's 256-column blocks are split evenly over
+// `world` ranks, rank q owning blocks [floor(q nblk / world), floor((q+1) nblk / world)).
+__host__ __device__ __forceinline__ int rs_owner(int blk, int nblk, int world) {
+    return ((blk + 1) * world - 1) / nblk;
+}
+__host__ __device__ __forceinline__ int rs_col0(int q, int nblk, int world) { return (q * nblk / world) * 256; }
+
+// 16 fp32 outputs of this warp's 32 rows (o[16 h .. 16 h + 15]) as one 32 x 16 fp32 box
+// through the TMA map `map` (64-byte rows: the same 64-byte-swizzle staging layout as
+// the bf16 box below).  Used for the f1 reduce-scatter partials.
+template <int kPending>
+__device__ __forceinline__ void store_box_tma_f32(const CUtensorMap* map, uint8_t* box, const float (&o)[32], int h,
+                                                  int col, int row0, uint32_t lane) {
+    if (lane == 0) ptx::tma_store_wait_read<kPending>();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint4 v = make_uint4(__float_as_uint(o[16 * h + 4 * c]), __float_as_uint(o[16 * h + 4 * c + 1]),
+                                   __float_as_uint(o[16 * h + 4 * c + 2]), __float_as_uint(o[16 * h + 4 * c + 3]));
+        *reinterpret_cast<uint4*>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        ptx::tma_store_2d(map, ptx::smem_u32(box), col, row0);
+        ptx::tma_store_commit();
     }
 }
 
@@ -1245,6 +1280,21 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     for (int j = 0; j < W; ++j) o[j] = silu_gate(__uint_as_float(v1[j]), __uint_as_float(v3[j]), gr);
                     if (use_tma) store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + c1, box_row0, lane);
                     else store_row32<kKind, W>(p, row, nb * C::OUT_COLS + c1, o);
+                } else if (kKind == 0 && p.rs_world > 0) {
+                    // f1: the fp32 partial of these 2 x 32 columns goes to the owner rank's
+                    // staging slot (4 boxes of 32 x 16 fp32; one owner per tile)
+                    const int q = rs_owner(nb * C::OUT_COLS / 256, p.rs_nblk, p.rs_world);
+                    const int cq = rs_col0(q, p.rs_nblk, p.rs_world);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                        for (int j = 0; j < W; ++j) o[j] = __uint_as_float(hh == 0 ? v1[j] : v3[j]);
+                        const int col = nb * C::OUT_COLS + (hh == 0 ? c1 : c3) - cq;
+#pragma unroll
+                        for (int h16 = 0; h16 < 2; ++h16)
+                            store_box_tma_f32<1>(&omaps.m[q], stg + (nst++ & 1) * 2048, o, h16, col + 16 * h16, box_row0,
+                                                 lane);
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < W; ++j) o[j] = apply_act(rr * __uint_as_float(v1[j]), p.act, p.alpha);

@@ -147,13 +147,69 @@ def shard_w2(w2: torch.Tensor, rank: int, world: int):
     return w2[:, n0:n1].contiguous()
 
 
+class FusedReduce:
+    """Symmetric-memory buffers of f1's fused all-reduce for one process group and
+    block shape [M, K]: every rank's fp32 staging buffer (cuasm_rs_layout sizes; the
+    largest rank's size on all ranks, as symmetric memory requires) and every rank's
+    full bf16 output y [M, K], with the peer pointers of both (and y's NVLS multicast
+    mapping when torch can create one)."""
+
+    def __init__(self, M: int, K: int, device, group=None, use_multicast: bool = True):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import rs_layout
+        grp = group or dist.group.WORLD
+        world = dist.get_world_size(grp)
+        nbytes = max(rs_layout(M, K, world, q)[2] for q in range(world))
+        self.stage = symm_mem.empty((max(nbytes // 4, 4),), dtype=torch.float32, device=device)
+        self.stage_hdl = symm_mem.rendezvous(self.stage, grp)
+        self.y = symm_mem.empty((M, K), dtype=torch.bfloat16, device=device)
+        self.y_hdl = symm_mem.rendezvous(self.y, grp)
+        self.M, self.K = M, K
+        self.rank, self.world = self.stage_hdl.rank, self.stage_hdl.world_size
+        self.multicast_ptr = int(self.y_hdl.multicast_ptr or 0) if use_multicast else 0
+
+    def stage_ptrs(self):
+        return [int(p_) for p_ in self.stage_hdl.buffer_ptrs]
+
+    def y_destinations(self):
+        if self.multicast_ptr:
+            return [self.multicast_ptr], True
+        return [int(p_) for p_ in self.y_hdl.buffer_ptrs], False
+
+    def barrier(self):
+        """Stream-ordered cross-rank barrier."""
+        self.stage_hdl.barrier(channel=0)
+
+
 def ffn_block_tp_forward(x, rms_w, w1_shard, w3_shard, w2_shard, eps: float = 1e-6, group=None,
-                         handle: FusedFFN | None = None):
+                         handle: FusedFFN | None = None, reduce: str = "nccl", fused: FusedReduce | None = None):
     """Megatron tensor-parallel LLaMA feed-forward block: column-parallel W1/W3
-    (this rank's N-shard of the hidden), row-parallel W2, one all-reduce of
-    the [M,K] partial outputs (NCCL over NVLink on GPUs)."""
+    (this rank's N-shard of the hidden), row-parallel W2, and the all-reduce of the
+    [M,K] partial outputs:
+    reduce="nccl": the block's bf16 partial, then one NCCL all_reduce;
+    reduce="fused": the down projection's epilogue stores every fp32 partial tile into
+    the owner rank's symmetric staging buffer (cuasm_ffn_block_forward_rs, overlapping
+    the GEMM tile by tile), a cross-rank barrier, each owner's rank-order sum stored
+    into every rank's output (cuasm_rs_reduce: P2P stores or one NVLS multicast store),
+    a barrier; returns the full y [M, K] (`fused.y`)."""
     h = handle or _handle(x.device, x.dtype)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if reduce == "fused":
+        M, K = x.shape
+        fr = fused or FusedReduce(M, K, x.device, group)
+        if (fr.M, fr.K) != (M, K):
+            raise ValueError(f"FusedReduce is for [{fr.M}, {fr.K}], the block output is [{M}, {K}]")
+        if fused is not None:
+            fr.barrier()  # every peer has finished reading the previous output and staging
+        h.block_forward_rs(x, rms_w, w1_shard, w3_shard, w2_shard, fr.stage_ptrs(), fr.world, fr.rank, eps)
+        fr.barrier()      # every rank's partial tiles are in their owners' staging buffers
+        dst, mc = fr.y_destinations()
+        h.rs_reduce(fr.stage, fr.world, fr.rank, dst, K, M, K, multicast=mc)
+        fr.barrier()      # every owner's columns are in every rank's y
+        return fr.y
+    if reduce != "nccl":
+        raise ValueError("reduce is 'nccl' or 'fused'")
     y = h.block_forward(x, rms_w, w1_shard, w3_shard, w2_shard, eps)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if world > 1:
         dist.all_reduce(y, group=group)
     return y

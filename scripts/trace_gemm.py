@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--op", default="ffn", choices=["ffn", "gemm"], help="gemm: cuasm_gemm_act (identity)")
     ap.add_argument("--scheds", default="0,1")
+    ap.add_argument("--bns", default="0", help="SwiGLU tile widths (CUASM_OPT_TILE_BN), 0 = auto")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     wbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -36,11 +37,13 @@ def main():
         M, K, N = map(int, shp.split("x"))
         t = make_device_inputs(M, K, N, 1, dev)
         out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        for sched in map(int, a.scheds.split(",")):
+        for sched, bn in [(s_, b_) for s_ in map(int, a.scheds.split(",")) for b_ in map(int, a.bns.split(","))]:
             pdl = 1
             h = ffn.FusedFFN(dev)
             h.set_option(ffn.OPT_PDL, pdl)
             h.set_option(ffn.OPT_SCHEDULE, sched)
+            h.set_option(ffn.OPT_TILE_BN, bn)
+            floor = 4 * (bn or ffn.plan_config(M, K, N)[4]) if a.op == "ffn" else 512
             def run():
                 if a.op == "ffn":
                     h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
@@ -72,7 +75,7 @@ def main():
                 span_ns = (tr[:, 3] - tr[:, 1])[sel]
                 ghz = cyc[sel] / span_ns.clamp(min=1)
                 print(f"   cycles per k-block (MMA issue, leader CTAs): min {cpk.min():.0f} med {cpk.median():.0f} "
-                      f"max {cpk.max():.0f}  (tcgen05 floor: 512); implied SM clock med {ghz.median():.3f} GHz")
+                      f"max {cpk.max():.0f}  (tcgen05 floor: {floor}); implied SM clock med {ghz.median():.3f} GHz")
                 wf = tr[:, 14][sel] / (kbs[sel] - 1)
                 wt = tr[:, 15][sel] / (kbs[sel] - 1)
                 print(f"   MMA-thread wait per k-block: full (data) med {wf.median():.0f} cyc, "
@@ -88,7 +91,8 @@ def main():
                 rel = (col - t0) / 1e3
                 rows[name] = {"min": round(rel.min().item(), 2), "med": round(rel.median().item(), 2),
                               "max": round(rel.max().item(), 2)}
-            key = f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all', 'stream-k-tail'][sched]}"
+            key = (f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all', 'stream-k-tail'][sched]}"
+                   f" bn={bn or 'auto'}")
             report[key] = rows
             print(key)
             for name, r in rows.items():

@@ -167,3 +167,71 @@ def test_gather_destinations_multicast_and_limits():
     assert gather_destinations([100, 200], 8, 2) == ([116, 216], False)
     with pytest.raises(ValueError):
         gather_destinations(list(range(9)), 0, 2)
+
+
+# ---- fused reduction (f1): ownership and staging-slot addressing across processes ----
+@pytest.mark.parametrize("M,K,world", [(5, 4096, 8), (3, 1024, 3), (7, 64, 8), (2, 8192, 3), (4, 520, 2)])
+def test_rs_layout_partitions_columns(M, K, world):
+    from paper_2501_08071_b200 import rs_layout
+    spans = [rs_layout(M, K, world, q) for q in range(world)]
+    cols = []
+    for c0, c1, nb in spans:
+        assert c0 % 256 == 0 and (c1 == K or c1 % 256 == 0) and c1 >= c0
+        assert nb == world * M * (c1 - c0) * 4
+        cols += list(range(c0, c1))
+    assert cols == list(range(K))   # every output column has exactly one owner, in rank order
+
+
+def _fused_reduce_worker(rank, world, port, M, K, N, stages, ys, q):
+    """Each rank scatters its partial y_p's columns into the owner's staging slot
+    [rank] at the offsets cuasm_rs_layout defines (what the GEMM epilogue's TMA stores
+    do), barrier, each owner sums its slots in rank order and writes its columns into
+    every rank's y (what cuasm_rs_reduce does), barrier: every y = hid @ W2^T."""
+    from paper_2501_08071_b200 import rs_layout
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(1)
+        hid = torch.randn(M, N, generator=g, dtype=torch.float64)
+        w2 = torch.randn(K, N, generator=g, dtype=torch.float64)
+        n0, n1 = shard_bounds(N, rank, world)
+        part = hid[:, n0:n1] @ shard_w2(w2, rank, world).T      # [M, K]
+        for owner in range(world):
+            c0, c1, nb = rs_layout(M, K, world, owner)
+            kq = c1 - c0
+            if kq == 0:
+                continue
+            slot = stages[owner][rank * M * kq:(rank + 1) * M * kq].view(M, kq)
+            slot.copy_(part[:, c0:c1])
+        dist.barrier()
+        c0, c1, _ = rs_layout(M, K, world, rank)
+        kq = c1 - c0
+        if kq:
+            acc = torch.zeros(M, kq, dtype=torch.float64)
+            for p in range(world):  # rank order
+                acc += stages[rank][p * M * kq:(p + 1) * M * kq].view(M, kq)
+            for r in range(world):
+                ys[r].view(M, K)[:, c0:c1] = acc
+        dist.barrier()
+        q.put((rank, bool(torch.allclose(ys[rank].view(M, K), hid @ w2.T, rtol=1e-12, atol=1e-12))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M,K,N", [(2, 3, 1024, 48), (3, 4, 1280, 72), (4, 2, 520, 64)])
+def test_fused_reduce_addressing(world, M, K, N):
+    from paper_2501_08071_b200 import rs_layout
+    sizes = [rs_layout(M, K, world, q)[2] // 4 for q in range(world)]
+    stages = [torch.full((max(s, 1),), float("nan"), dtype=torch.float64).share_memory_() for s in sizes]
+    ys = [torch.full((M * K,), float("nan"), dtype=torch.float64).share_memory_() for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_reduce_worker, args=(r, world, port, M, K, N, stages, ys, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}
