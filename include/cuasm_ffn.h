@@ -105,13 +105,23 @@ typedef enum {
                                configuration model decides (decode shards, M <= 32),
                                1 = off, 2..8 = S (used only when tiles * S <= SMs,
                                S <= k-blocks and S clusters fit co-resident)           */
-    CUASM_OPT_TILE_BN = 11   /* fused FFN, bf16: SwiGLU outputs per tile BN (MMA N = 2 BN):
+    CUASM_OPT_TILE_BN = 11,   /* fused FFN, bf16: SwiGLU outputs per tile BN (MMA N = 2 BN):
                                0 = the configuration model decides; 128, 112, 96, 80 or
                                64 forces it (widths below 128 run the 2-SM kernel; a
                                forced 1-SM variant keeps 128).  The folded weights are
                                cached once per width in use (the 128-wide pack and one
                                narrower pack), so a weight set served at shapes whose
                                plans differ in BN holds two packed copies       */
+    CUASM_OPT_DYNAMIC = 12    /* data-parallel tiles of the persistent GEMM claimed from a
+                               global counter (each cluster's first tile static, the rest
+                               claimed one tile ahead by its leader CTA) instead of the
+                               static round-robin: the tiles in flight stay consecutive
+                               in the rasterisation order (L2 reuse) and fast SM pairs
+                               take more tiles.  0 = auto (on when every cluster has >= 24
+                               data-parallel tiles), 1 = off, 2 = on (whenever there is
+                               more than one round).  Results are bitwise independent of
+                               the claim order (each tile is computed whole by one
+                               cluster)                                               */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with

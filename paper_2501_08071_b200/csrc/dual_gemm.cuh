@@ -109,7 +109,26 @@ struct FfnGemmParams {
     uint32_t* flags;    // [cluster][cta rank][8 epilogue warps]: 1 = partial published;
                         // the finisher consumes (resets to 0) it, so launches need no
                         // per-launch state and the kernel can be replayed from a CUDA graph
+    // Dynamic whole-tile claiming (DESIGN.md §6 "Dynamic tiles"): dyn != null makes every
+    // cluster's data-parallel tiles after its first come from a global claim counter, so
+    // the tiles in flight stay consecutive in the rasterisation order (L2 reuse) and fast
+    // SM pairs absorb slow ones.  dyn[0] claim counter, dyn[1] clusters done, dyn[2]
+    // launch epoch (the last cluster resets [0], [1] and advances [2]: graph-safe), then
+    // per cluster a ring of kDynRing (tag, tile) words published by the leader's producer.
+    uint32_t* dyn;
 };
+
+constexpr int kDynRing = 8;           // published-tile ring per cluster (u64 slots)
+constexpr int kDynEnd = 0x7fffffff;   // "no more data-parallel tiles"
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // A unit of work: k-blocks [kb0, kb1) of tile `tile`.
 struct Seg {
@@ -146,10 +165,37 @@ __device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
 // Waits therefore point only to lower cluster ids -- CTAs dispatched earlier,
 // resident or done -- so the schedule needs no co-residency of the grid, and a
 // contributor publishes its partial first thing while the finisher adds it last.
-struct Sched {
+//
+// Dynamic mode (p.dyn): a cluster's first data-parallel tile is its cluster id; the
+// later ones are claimed by the leader CTA's producer from the global counter ahead of
+// use (the atomic for tile i+3 is issued when it starts tile i, its result published in
+// the cluster's ring when it starts tile i+1, so tile i+1 is in the ring a whole tile
+// before anyone needs it), and every role loads the next tile's slot when it starts a
+// tile and uses it when it starts the next one.  Neither the
+// claim's nor the loads' L2 round trips sit on a role's critical path; the published
+// words carry only the tile number, so relaxed accesses suffice (a tag = launch epoch +
+// tile index tells a published slot from a stale one; a role that finds it stale spins,
+// which the two-tile lead makes rare).  The producer runs STAGES k-blocks ahead of the
+// MMA and the MMA at most one tile ahead of the epilogue, so the kDynRing slots of a ring
+// are never overwritten before their readers are done.  The stream-K region after the
+// data-parallel tiles stays static per cluster.
+// kDyn = false compiles the dynamic code out: the producer and MMA roles run a static
+// instance when p.dyn is null, so their loops keep warp-uniform control flow (the MMA
+// issue loop is latency-critical: a lane-0-only branch in the schedule
+// made ptxas add divergence checks and move the stage arithmetic out of uniform
+// registers, 340 -> 434 SM cycles per k-block on the 80-wide tile).
+template <bool kDyn = true>
+struct SchedT {
     int next_dp, C, KB, T_dp, kb_lo, kb_hi;
     int64_t beg, cur;  // stream-K range [beg, cur) still to walk (cur moves down)
-    __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster, int part = 0) {
+    uint32_t* dyn;     // dynamic claiming (null: static round-robin)
+    unsigned long long* ring;
+    uint32_t epoch;
+    int dyn_i;         // index of the next data-parallel tile of this cluster
+    bool fetch, claimer;
+    unsigned long long pre;  // (dynamic) the slot of tile dyn_i, loaded one tile ahead
+    uint32_t claim;          // (claimer) the counter value claimed for tile dyn_i + 1
+    __device__ __forceinline__ void init(const FfnGemmParams& p, int cluster, int part = 0, bool is_claimer = false) {
         next_dp = cluster;
         C = p.num_clusters;
         KB = p.num_k_blk;
@@ -159,15 +205,80 @@ struct Sched {
         // cluster split-K: this CTA's share of every tile's k-blocks
         kb_lo = p.csplit ? part * KB / p.csplit : 0;
         kb_hi = p.csplit ? (part + 1) * KB / p.csplit : KB;
+        dyn = kDyn ? p.dyn : nullptr;
+        ring = dyn ? reinterpret_cast<unsigned long long*>(dyn + 4) + static_cast<int64_t>(cluster) * kDynRing : nullptr;
+        epoch = 0;
+        dyn_i = 0;
+        fetch = false;
+        claimer = is_claimer;
+        pre = 0;
+        claim = 0;
+    }
+    // (dynamic mode) the launch epoch; read after griddepcontrol.wait (the previous launch
+    // advanced it at its very end)
+    __device__ __forceinline__ void load_epoch() {
+        if constexpr (kDyn) {
+            if (dyn) epoch = *reinterpret_cast<volatile uint32_t*>(dyn + 2);
+        }
+    }
+    __device__ __forceinline__ unsigned long long tag(int i) const {
+        return (static_cast<unsigned long long>((epoch << 12) | (static_cast<uint32_t>(i) & 0xFFFu)) << 32);
+    }
+    __device__ __forceinline__ unsigned long long ld_slot(int i) const {
+        return ld_relaxed_u64(ring + (i % kDynRing));
+    }
+    __device__ __forceinline__ void publish(int i, uint32_t counter) const {
+        const int t = C + static_cast<int>(counter);
+        st_relaxed_u64(ring + (i % kDynRing), tag(i) | static_cast<uint32_t>(t < T_dp ? t : kDynEnd));
+    }
+    // the data-parallel tile number dyn_i of this cluster (lane 0's value, shared by the warp)
+    __device__ __forceinline__ void resolve() {
+        int t = 0;
+        if ((threadIdx.x & 31) == 0) {
+            unsigned long long v = pre;
+#if CUASM_WATCHDOG
+            const long long t0 = clock64();
+#endif
+            while ((v & 0xFFFFFFFF00000000ull) != tag(dyn_i)) {
+                __nanosleep(32);
+                v = ld_slot(dyn_i);
+#if CUASM_WATCHDOG
+                if (clock64() - t0 > (1ll << 34)) asm volatile("trap;");
+#endif
+            }
+            t = static_cast<int>(v & 0xFFFFFFFFu);
+        }
+        next_dp = __shfl_sync(0xffffffffu, t, 0);
+        fetch = false;
     }
     __device__ __forceinline__ bool next(Seg& s) {
+        if constexpr (kDyn) {
+            if (fetch) resolve();
+        }
         if (next_dp < T_dp) {
             s.tile = next_dp;
             s.kb0 = kb_lo;
             s.kb1 = kb_hi;
-            next_dp += C;
+            if (kDyn && dyn) {
+                ++dyn_i;  // the tile after this one
+                if ((threadIdx.x & 31) == 0) {
+                    if (claimer) {
+                        // publish tile dyn_i + 1 (claimed a tile ago; at the first tile, tiles 1
+                        // and 2 now), claim dyn_i + 2
+                        if (dyn_i == 1) publish(1, atomicAdd(dyn, 1u));
+                        if (dyn_i == 1) claim = atomicAdd(dyn, 1u);
+                        publish(dyn_i + 1, claim);
+                        claim = atomicAdd(dyn, 1u);  // (result used one tile later)
+                    }
+                    pre = ld_slot(dyn_i);            // (value used one tile later)
+                }
+                fetch = true;
+            } else {
+                next_dp += C;
+            }
             return true;
         }
+        fetch = false;
         if (cur > beg) {
             const int64_t t = static_cast<uint32_t>(cur - 1) / static_cast<uint32_t>(KB);
             const int64_t t0 = t * KB;
@@ -180,7 +291,27 @@ struct Sched {
         }
         return false;
     }
+    // after next() returned a data-parallel tile: does another data-parallel tile follow?
+    // (dynamic mode: reads the next ring slot; the claimer published it with this one)
+    __device__ __forceinline__ bool dp_more() {
+        if constexpr (kDyn) {
+            if (fetch) resolve();
+        }
+        return next_dp < T_dp;
+    }
+    // the r-reading (finishing) segments of this cluster's stream-K range
+    __device__ __forceinline__ int sk_finishing_segments(int num_k_blk) const {
+        SchedT s2 = *this;
+        s2.next_dp = T_dp;
+        s2.fetch = false;
+        s2.dyn = nullptr;
+        Seg g;
+        int n = 0;
+        while (s2.next(g)) n += g.kb1 == num_k_blk ? 1 : 0;
+        return n;
+    }
 };
+using Sched = SchedT<true>;
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -853,6 +984,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     const int cluster_id = csplit ? static_cast<int>(blockIdx.x) / p.csplit : static_cast<int>(blockIdx.x) / kCtaGroup;
 
     if (warp == 0) {
+      auto producer_role = [&](auto dyn_tag) {
+        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= TMA producer =========================
         // Whole warp walks the loop, one elected lane issues (uniform operands,
         // no per-instruction uniformity loops around UTMALDG).
@@ -891,14 +1024,16 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
             }
         };
-        Sched sch;
-        sch.init(p, cluster_id, static_cast<int>(part));
+        SchedT<kDyn> sch;
+        sch.init(p, cluster_id, static_cast<int>(part), leader && part == 0);  // the leader claims tiles
         // Weights do not depend on the preceding kernel (they were packed before it): the
         // first segment's first STAGES weight boxes go out before griddepcontrol.wait, so
         // under PDL they stream while the preceding kernel drains (its x loads follow the wait)
         int pre = 0;
         if (p.w_early) {
-            Sched s0 = sch;
+            auto s0 = sch;
+            s0.dyn = nullptr;  // (the first tile is static: no claim, no ring)
+            s0.claimer = false;
             Seg g0;
             if (s0.next(g0)) {
                 int mb0, nb0;
@@ -911,6 +1046,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             }
         }
         ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
+        sch.load_epoch();
         int stage = 0;
         uint32_t phase = 0;
         bool first_load = true;
@@ -947,7 +1083,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // this grid's completion before reading anything we write)
             ptx::pdl_launch_dependents();
         }
+      };
+      if (p.dyn) producer_role(std::true_type{});
+      else producer_role(std::false_type{});
     } else if (warp == 1) {
+      auto mma_role = [&](auto dyn_tag) {
+        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= MMA issuer ===========================
         // The whole warp walks the loop (barrier waits included) and one
         // elected lane issues: the descriptors then live in uniform registers
@@ -962,8 +1103,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // smem descriptors of stage 0; stage s adds s*bytes >> 4 to the address field
             const uint64_t adesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a));
             const uint64_t bdesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b));
-            Sched sch;
+            SchedT<kDyn> sch;
             sch.init(p, cluster_id, static_cast<int>(part));
+            if (p.dyn) {
+                ptx::pdl_wait();  // (the ring and epoch of the previous launch are final)
+                sch.load_epoch();
+            }
             Seg sg;
             for (; sch.next(sg); ++it) {
                 const int acc = it & 1;
@@ -1023,7 +1168,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
+      };
+      if (p.dyn) mma_role(std::true_type{});
+      else mma_role(std::false_type{});
     } else {
+      auto epilogue_role = [&](auto dyn_tag) {
+        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= epilogue =============================
         ptx::pdl_wait();  // x / r[] come from the preceding kernel (PDL primary)
         if (warp == 2 && lane == 0) trace_stamp(p, 4);
@@ -1039,12 +1189,27 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         // once past its last acquisition; the last CTA of the grid resets the
         // bookkeeping for the next launch (graph-safe), under its last tile's mainloop.
         const bool fused = p.fused_norm != 0;
-        int r_left = 0;  // r-reading (non-contributor) segments of this CTA's schedule
+        SchedT<kDyn> sch;
+        sch.init(p, cluster_id, static_cast<int>(part));
+        sch.load_epoch();
+        // r-reading segments still ahead: the data-parallel tiles (all read r; in dynamic mode
+        // their count is known only one tile ahead, Sched::dp_more) and the stream-K segments
+        // that finish a tile (or, cluster split-K, every segment)
+        int sk_r = 0;
+        bool has_dp = false;
         if (fused) {
-            Sched s2;
-            s2.init(p, cluster_id, static_cast<int>(part));
-            Seg g2;
-            while (s2.next(g2)) r_left += (csplit || g2.kb1 == p.num_k_blk) ? 1 : 0;
+            auto s2 = sch;
+            s2.dyn = nullptr;
+            has_dp = s2.next_dp < s2.T_dp;
+            if (csplit) {
+                Seg g2;
+                int n = 0;
+                while (s2.next(g2)) ++n;
+                sk_r = n;  // (split-K clusters: no data-parallel round-robin past the first tile)
+                has_dp = false;
+            } else {
+                sk_r = s2.sk_finishing_segments(p.num_k_blk);
+            }
         }
         auto r_done_cta = [&]() {  // warp 2 of the CTA, after the CTA's last acquisition
             uint32_t* cnt = p.rstate + 2 * p.n_rblk;
@@ -1058,7 +1223,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             }
             __syncwarp();
         };
-        if (fused && r_left == 0 && warp == 2) r_done_cta();
+        if (fused && !has_dp && sk_r == 0 && warp == 2) r_done_cta();
         auto acquire_r = [&](int rb) {
             const int row0 = rb * C::BM;
             if (row0 >= p.M) return;  // (2-SM decode: the peer CTA's rows are all past M); CTA-uniform
@@ -1101,8 +1266,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         const uint32_t row_in_cta = quad * 32 + lane;
         int it = 0;
         int nst = 0;  // TMA-store boxes this warp has issued (staging box = nst & 1)
-        Sched sch;
-        sch.init(p, cluster_id, static_cast<int>(part));
         Seg sg;
         for (; sch.next(sg); ++it) {
             int mb, nb;
@@ -1157,7 +1320,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             }
             if (fused && (csplit || !contributor)) {
                 acquire_r(csplit ? mb : mb * kCtaGroup + static_cast<int>(cta_rank));
-                if (--r_left == 0 && warp == 2) r_done_cta();
+                // the CTA's last r acquisition: count it past (the last CTA resets the state)
+                const bool dp_seg = !csplit && sg.tile < p.num_dp_tiles;
+                bool last;
+                if (dp_seg) last = !sch.dp_more() && sk_r == 0;
+                else last = --sk_r == 0;
+                if (last && warp == 2) r_done_cta();
             }
             if (csplit && split_k_push_fits<C, kKind>(min(C::BM, p.M - mb * C::TILE_M), p.csplit)) {
                 // cluster split-K, push form.  Pass 0 runs the same code dry (no TMEM
@@ -1363,6 +1531,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
+      };
+      if (p.dyn) epilogue_role(std::true_type{});
+      else epilogue_role(std::false_type{});
     }
 
     // every TMA store this warp issued has written global memory before the CTA retires
@@ -1387,6 +1558,17 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS, kCtaGroup>(tmem_base);
         if (lane == 0) trace_stamp(p, 6);
+        // dynamic claiming: the last cluster out resets the counters and advances the epoch
+        // (every role of every cluster is past its last claim / ring read by now)
+        if (p.dyn && lane == 0 && leader && part == 0) {
+            const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(p.dyn + 2);
+            if (atomicAdd(p.dyn + 1, 1u) == static_cast<uint32_t>(p.num_clusters) - 1) {
+                p.dyn[0] = 0u;
+                p.dyn[1] = 0u;
+                __threadfence();
+                p.dyn[2] = epoch + 1;
+            }
+        }
     }
 }
 

@@ -54,6 +54,9 @@ CASES = [
     (256, 4096, 1376, ffn.VARIANT_1SM, ffn.SCHEDULE_STREAM_K_ALL, 0),
     (16, 4096, 1376, ffn.VARIANT_AUTO, ffn.SCHEDULE_AUTO, 0),
     (640, 1024, 1408, ffn.VARIANT_1SM, ffn.SCHEDULE_DATA_PARALLEL, 0),
+    # dynamic whole-tile claiming (auto-on: many rounds) with a stream-K tail: resident clusters
+    # claim the tiles of clusters not yet launched; nothing waits across clusters
+    (2048, 1024, 11008, ffn.VARIANT_2SM, ffn.SCHEDULE_STREAM_K_TAIL, 0),
 ]
 
 
