@@ -108,10 +108,11 @@ typedef enum {
     CUASM_OPT_TILE_BN = 11,   /* fused FFN, bf16: SwiGLU outputs per tile BN (MMA N = 2 BN):
                                0 = the configuration model decides; 128, 112, 96, 80 or
                                64 forces it (widths below 128 run the 2-SM kernel; a
-                               forced 1-SM variant keeps 128).  The folded weights are
-                               cached once per width in use (the 128-wide pack and one
-                               narrower pack), so a weight set served at shapes whose
-                               plans differ in BN holds two packed copies       */
+                               forced 1-SM variant keeps 128, except 64, which the 1-SM
+                               decode paths have too).  The folded weights are cached
+                               once per width in use, so a weight set served at shapes
+                               whose plans differ in BN (decode shards take 64, prefill
+                               shards 80-112) holds one packed copy per width    */
     CUASM_OPT_DYNAMIC = 12    /* data-parallel tiles of the persistent GEMM claimed from a
                                global counter (each cluster's first tile static, the rest
                                claimed one tile ahead by its leader CTA) instead of the

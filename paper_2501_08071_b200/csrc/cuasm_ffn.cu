@@ -104,8 +104,10 @@ struct cuasm_ffn_s {
     int64_t r_cap = 0;
     // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN in 128-output
     // blocks; slot 1 = a single packed weight (GEMM + activation / down projection);
-    // slot 2 = the same W13 in the narrower blocks a tile-width plan chose (BN != 128)
-    PackedWeights pw[3];
+    // slots 2..5 = the same W13 in the narrower blocks BN = 112, 96, 80, 64 (each packed on
+    // the first forward whose plan takes that width: e.g. a decode shard's 64-wide tiles and
+    // its prefill's 80-wide tiles of one weight set coexist)
+    PackedWeights pw[6];
     int tile_bn = 0;   // CUASM_OPT_TILE_BN: 0 auto, else the SwiGLU outputs per tile
     // fp32 handle: x split into [x_hi | x_lo] tf32 terms per forward (pack.cuh)
     void* x2 = nullptr;
@@ -274,8 +276,8 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     return CUASM_OK;
 }
 
-// The W13 cache slot of a SwiGLU tile width: 0 for BN = 128, 2 for the narrower blocks.
-inline int w13_slot(int bn) { return bn == kPackBN ? 0 : 2; }
+// The W13 cache slot of a SwiGLU tile width: 0 for BN = 128, 2..5 for 112, 96, 80, 64.
+inline int w13_slot(int bn) { return bn == 112 ? 2 : bn == 96 ? 3 : bn == 80 ? 4 : bn == 64 ? 5 : 0; }
 
 cuasm_status_t ensure_packed(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
                              int64_t N, cudaStream_t s, int64_t kp = 0, int bn = kPackBN) {
@@ -491,6 +493,15 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, attr_done,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES, "cudaFuncSetAttribute(smem)");
     if (st != CUASM_OK) return st;
+    // dynamic tile claiming is compiled into the 2-SM bf16 kernels only (the long runs it is for)
+    constexpr bool kDynBuilt = kCtaGroup == 2 && kKind == 0;
+    if constexpr (kDynBuilt) {
+        static std::atomic<uint64_t> attr_done_dyn{0};
+        st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, true>, attr_done_dyn,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES,
+                              "cudaFuncSetAttribute(smem)");
+        if (st != CUASM_OK) return st;
+    }
     if (csplit) {
         // one wave: every cluster must fit at once, or the split loses to a second wave
         // (clusters are placed inside one GPC, so S-CTA clusters may not all fit: S = 8
@@ -584,7 +595,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // 294.9 us); forced on or off by CUASM_OPT_DYNAMIC; never for cluster split-K
     constexpr int kDynRounds = 24;
     p.dyn = nullptr;
-    const bool dyn_on = !csplit && p.num_dp_tiles > clusters &&
+    const bool dyn_on = kDynBuilt && !csplit && p.num_dp_tiles > clusters &&
                         (h->dynamic == 2 || (h->dynamic == 0 && p.num_dp_tiles >= kDynRounds * clusters));
     if (dyn_on) {
         if (!h->dyn) {
@@ -621,6 +632,15 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
+    if constexpr (kDynBuilt) {
+        if (p.dyn) {
+            CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, true>, tmap_x,
+                                              w.tmap, omaps, omaps_h, p),
+                        "ffn_dual_gemm_kernel launch");
+            h->last_variant = CUASM_VARIANT_2SM;
+            return CUASM_OK;
+        }
+    }
     CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, tmap_x, w.tmap,
                                       omaps, omaps_h, p),
                 "ffn_dual_gemm_kernel launch");
@@ -681,6 +701,15 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // 1376: 14.5 us (S = 6), 15.0 (S = 4) vs 17.5 us (stream-K split 3 ways), 16 x 4096 x 5504
     // (S = 3): 23.0 vs 27.1, 16 x 4096 x 6880 (S = 2): 26.5 vs 29.5, 32 x 4096 x 5504 (S = 2):
     // 24.9 vs 27.2; at M >= 64 (pull form) it loses
+    // With 64-output tiles (the 1-SM kernel's decode paths exist for BN = 64 too) a shard has
+    // twice the tiles, so a split of 3 (2) puts up to 147 CTAs on the weight stream while each
+    // owner reduces half the columns: 16 x 4096 x 1376 24.3 -> 22.0 us, 16 x 4096 x 2752
+    // 25.4 -> 23.6, 16 x 8192 x 3584 31.3 -> 30.7 (scripts/tune_decode_bn.py,
+    // profiles/r02/tune_decode_bn.log); wider shards keep the 128-output rule below
+    const int64_t tiles_64 = ((M + 127) / 128) * ((N + 63) / 64);
+    if (out_cols == 128 && esize == 2 && (tile_bn_force == 0 || tile_bn_force == 64) && KB >= 48 && M <= 32 &&
+        tiles_64 * 2 <= sm_count)
+        return Plan{CUASM_VARIANT_1SM, false, 256, tiles_64 * 3 <= sm_count ? 3 : 2, 64};
     if (out_cols == 128 && !narrow_forced && KB >= 48 && M <= 32) {
         const int S = M <= 16 && tiles_1sm * 6 <= sm_count && tiles_1sm <= 16 ? 6
                       : tiles_1sm * 4 <= sm_count && tiles_1sm <= 37   ? 4
@@ -715,8 +744,11 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
         for (int tn : {256, 128})
             if (!tile_n_force || tn == tile_n_force) cands[nc++] = Cand{tn, kPackBN};
     } else {
+        // (narrow 2-SM tiles were measured from M = 256 up; decode-sized M keeps 128 unless forced)
         for (int bn : kTileBNs)
-            if ((bn == kPackBN || esize == 2) && (tile_bn_force ? bn == tile_bn_force : true)) cands[nc++] = Cand{256, bn};
+            if ((bn == kPackBN || (esize == 2 && (M > 128 || tile_bn_force))) &&
+                (tile_bn_force ? bn == tile_bn_force : true))
+                cands[nc++] = Cand{256, bn};
     }
     for (int ci = 0; ci < nc; ++ci) {
         const int tn = cands[ci].tn, bn = cands[ci].bn;
@@ -765,8 +797,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
     Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
                               out_cols == 128 ? h->tile_bn : 0);
-    // a forced 1-SM variant (CUASM_OPT_VARIANT) has only the 128-output SwiGLU tile
-    if (h->variant == CUASM_VARIANT_1SM) pl.bn = kPackBN;
+    // a forced 1-SM variant (CUASM_OPT_VARIANT) has the 128- and 64-output SwiGLU tiles
+    if (h->variant == CUASM_VARIANT_1SM && pl.bn != 64) pl.bn = kPackBN;
     return pl;
 }
 
@@ -849,7 +881,12 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
     h->plan_csplit = v == plan.variant ? plan.csplit : 0;
-    if (kepi == 0 && plan.bn != kPackBN) {
+    if (kepi == 0 && plan.bn == 64 && v == CUASM_VARIANT_1SM) {
+        // the 1-SM 64-output tile: decode shards (more, smaller tiles for the cluster split-K)
+        if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
+            return fail(h, CUASM_ERR_UNSUPPORTED, "tile width 64 needs the bf16 kernel");
+        st = launch_gemm<0, 1, 0, 128>(h, e, x, out, M, K, N, eps, s);
+    } else if (kepi == 0 && plan.bn != kPackBN) {
         // narrower SwiGLU tiles (2-SM bf16 only; ffn_common packed slot 2 for this width)
         if (h->dtype != CUASM_DTYPE_BF16 || v != CUASM_VARIANT_2SM || e.slot != w13_slot(plan.bn))
             return fail(h, CUASM_ERR_UNSUPPORTED, "tile width %d needs the 2-SM bf16 kernel", plan.bn);

@@ -374,7 +374,8 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 // fills whole waves of CTA pairs (7B P=8: N_l = 1376 -> 18 blocks of 80 = 144 tiles of
 // 256 rows on 74 pairs instead of 11 blocks of 128 = 88).  h1 sits in accumulator
 // columns [0, BN), h3 in [BN, 2BN); the epilogue walks 32-column units (the last one
-// 16 wide when BN % 32 == 16).  Only BN = 128 has the decode paths (rep, cluster split-K).
+// 16 wide when BN % 32 == 16).  The decode paths (rep, cluster split-K) exist for BN = 128 and
+// BN = 64 (more, smaller tiles for the decode shards' weight streaming) and every GEMM tile.
 template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256>
 struct GemmCfg {
     static_assert(kEpi == 0 ? (kN % 32 == 0 && kN >= 128 && kN <= 256) : (kN == 256 || kN == 128),
@@ -386,7 +387,7 @@ struct GemmCfg {
     static constexpr int BN = kN / 2;              // SwiGLU: outputs per tile (h1 | h3 halves)
     static constexpr int OUT_COLS = kEpi == 0 ? BN : UMMA_N;  // output columns per tile
     static constexpr int PACK_ROWS = kEpi == 0 ? kN : 256;  // rows of one packed (n-block, k-block) box run
-    static constexpr bool kDecodePaths = kN == 256;  // rep / cluster split-K (BN = 128 only)
+    static constexpr bool kDecodePaths = kEpi == 1 || kN == 256 || kN == 128;  // rep / cluster split-K
     // SwiGLU epilogue units: 32 output columns (h1 at [32u, ..), h3 at [BN + 32u, ..)),
     // the last 16 wide when BN % 32 == 16; the two warps of a TMEM quadrant alternate units
     static constexpr int NU = (BN + 31) / 32;
@@ -425,10 +426,10 @@ struct GemmCfg {
     static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
     // Accumulator chunks (32 columns) of epilogue pair `i` of a warp in column half `half`.
     __device__ static constexpr int chunk_a(int half, int i) {
-        return kEpi == 0 ? half * 2 + i : half * (UMMA_N / 64) + 2 * i;
+        return kEpi == 0 ? half * PAIRS + i : half * (UMMA_N / 64) + 2 * i;
     }
     __device__ static constexpr int chunk_b(int half, int i) {
-        return kEpi == 0 ? half * 2 + i + BN / 32 : half * (UMMA_N / 64) + 2 * i + 1;
+        return kEpi == 0 ? half * PAIRS + i + BN / 32 : half * (UMMA_N / 64) + 2 * i + 1;
     }
     // First packed row of n-block nb's (or its half's) box for k-block 0; k-block kb adds kb * PACK_ROWS.
     __device__ static constexpr int b_row0(int nb, int KB) {
@@ -912,7 +913,10 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     }
 }
 
-template <int kKind, int kCtaGroup, int kEpi, int kN>
+// kDyn: dynamic whole-tile claiming compiled in (p.dyn must be null otherwise); a kernel
+// template parameter rather than a runtime branch so the static kernels' loops are exactly
+// the uniform code they were (DESIGN.md §6 "Dynamic tiles").
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                          const __grid_constant__ OutMaps omaps, const __grid_constant__ OutMaps omaps_h,
@@ -938,7 +942,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     const uint32_t cta_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;
     const bool leader = cta_rank == 0;
     const bool csplit = C::kDecodePaths && kCtaGroup == 1 && p.csplit > 0;
-    const int rep = C::kDecodePaths ? p.rep : 0;  // decode-shape row replication (BN = 128 only)
+    const int rep = C::kDecodePaths ? p.rep : 0;  // decode-shape row replication (BN = 128 / 64)
     const uint32_t part = csplit ? ptx::cluster_ctarank() : 0;  // split-K share of the cluster's tile
 
     if (warp == 0 && lane == 0) {
@@ -984,8 +988,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     const int cluster_id = csplit ? static_cast<int>(blockIdx.x) / p.csplit : static_cast<int>(blockIdx.x) / kCtaGroup;
 
     if (warp == 0) {
-      auto producer_role = [&](auto dyn_tag) {
-        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= TMA producer =========================
         // Whole warp walks the loop, one elected lane issues (uniform operands,
         // no per-instruction uniformity loops around UTMALDG).
@@ -1083,12 +1085,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // this grid's completion before reading anything we write)
             ptx::pdl_launch_dependents();
         }
-      };
-      if (p.dyn) producer_role(std::true_type{});
-      else producer_role(std::false_type{});
     } else if (warp == 1) {
-      auto mma_role = [&](auto dyn_tag) {
-        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= MMA issuer ===========================
         // The whole warp walks the loop (barrier waits included) and one
         // elected lane issues: the descriptors then live in uniform registers
@@ -1105,7 +1102,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             const uint64_t bdesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b));
             SchedT<kDyn> sch;
             sch.init(p, cluster_id, static_cast<int>(part));
-            if (p.dyn) {
+            if (kDyn) {
                 ptx::pdl_wait();  // (the ring and epoch of the previous launch are final)
                 sch.load_epoch();
             }
@@ -1168,12 +1165,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
-      };
-      if (p.dyn) mma_role(std::true_type{});
-      else mma_role(std::false_type{});
     } else {
-      auto epilogue_role = [&](auto dyn_tag) {
-        constexpr bool kDyn = decltype(dyn_tag)::value;
         // ========================= epilogue =============================
         ptx::pdl_wait();  // x / r[] come from the preceding kernel (PDL primary)
         if (warp == 2 && lane == 0) trace_stamp(p, 4);
@@ -1531,9 +1523,6 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 }
             }
         }
-      };
-      if (p.dyn) epilogue_role(std::true_type{});
-      else epilogue_role(std::false_type{});
     }
 
     // every TMA store this warp issued has written global memory before the CTA retires
@@ -1560,7 +1549,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         if (lane == 0) trace_stamp(p, 6);
         // dynamic claiming: the last cluster out resets the counters and advances the epoch
         // (every role of every cluster is past its last claim / ring read by now)
-        if (p.dyn && lane == 0 && leader && part == 0) {
+        if (kDyn && p.dyn && lane == 0 && leader && part == 0) {
             const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(p.dyn + 2);
             if (atomicAdd(p.dyn + 1, 1u) == static_cast<uint32_t>(p.num_clusters) - 1) {
                 p.dyn[0] = 0u;

@@ -128,6 +128,9 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     KB = -(-K // BK)
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
+    t64 = -(-M // 128) * -(-N // 64)
+    if out_cols == 128 and esize == 2 and KB >= 48 and M <= 32 and 2 * t64 <= sm_count:
+        return ("1sm", False, 256, 3 if 3 * t64 <= sm_count else 2, 64)   # decode shards, 64-wide tiles
     if out_cols == 128 and KB >= 48 and M <= 32:   # decode shards: cluster split-K
         S = (6 if M <= 16 and 6 * t1 <= sm_count and t1 <= 16 else
              4 if 4 * t1 <= sm_count and t1 <= 37 else
@@ -141,7 +144,7 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
         return ("1sm", False, 128, 0, 128)
     best, best_t = ("2sm", False, 256, 0, 128), 1e30
     if out_cols == 128:   # SwiGLU tile widths (narrower than 128: 2-SM bf16 only)
-        cands = [(256, bn) for bn in (128, 112, 96, 80, 64) if bn == 128 or esize == 2]
+        cands = [(256, bn) for bn in (128, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > 128)]
     else:
         cands = [(256, 128), (128, 128)]
     for tn, bn in cands:
@@ -285,26 +288,33 @@ def test_plan_tile_width_matches_measured_best(lib_plan, shape):
     assert lib_plan(*shape)[4] in BN_MEASURED[shape]
 
 
-# measured (profiles/r01/csplit/ncu_ab_*.txt): the cluster split-K wins on few-tile
-# shards with M <= 32 and loses at M >= 64 (pull-form reduction); 65 tiles: no gain
-@pytest.mark.parametrize("M,K,N,cs", [(16, 4096, 1376, 6), (16, 4096, 2752, 4), (16, 8192, 3584, 4),
-                                      (32, 4096, 1376, 4), (16, 4096, 5504, 3), (32, 4096, 5504, 2),
-                                      (16, 4096, 6880, 2), (16, 8192, 7168, 2), (16, 4096, 8256, 0),
-                                      (64, 4096, 1376, 0), (128, 4096, 1376, 0), (16, 4096, 11008, 0)])
-def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs):
-    assert plan_config(M, K, N)[3] == cs
-    assert lib_plan(M, K, N)[3] == cs
+# measured (profiles/r01/csplit/ncu_ab_*.txt, profiles/r02/tune_decode_bn.log): the cluster
+# split-K wins on few-tile shards with M <= 32 and loses at M >= 64 (pull-form reduction); with
+# 64-output tiles (up to 74 of them) a split of 3 (2) beats the 128-output tile's; 65 128-wide
+# tiles: no gain
+@pytest.mark.parametrize("M,K,N,cs,bn", [(16, 4096, 1376, 3, 64), (16, 4096, 2752, 3, 64), (16, 8192, 3584, 2, 64),
+                                         (32, 4096, 1376, 3, 64), (1, 4096, 1376, 3, 64), (16, 4096, 5504, 3, 128),
+                                         (32, 4096, 5504, 2, 128), (16, 4096, 6880, 2, 128),
+                                         (16, 8192, 7168, 2, 128), (16, 4096, 8256, 0, 128),
+                                         (64, 4096, 1376, 0, 128), (128, 4096, 1376, 0, 128),
+                                         (16, 4096, 11008, 0, 128)])
+def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
+    assert plan_config(M, K, N)[3:] == (cs, bn)
+    assert lib_plan(M, K, N)[3:] == (cs, bn)
 
 
 # every cluster split the planner picks must take the push form (dual_gemm.cuh split_k_push_fits:
-# bf16, <= 32 rows, ceil(8 / S) * S * rc * 128 bytes of slots within the 32 KB staging area, rc =
-# 16 or 32 slot rows); the pull form is only reachable by forcing CUASM_OPT_CSPLIT
+# bf16, <= 32 rows, ceil(NU / S) * S * rc * 128 bytes of slots within the 32 KB staging area, NU =
+# 2 BN / 16 units, rc = 16 or 32 slot rows); the pull form is only reachable by forcing CUASM_OPT_CSPLIT
 @pytest.mark.parametrize("K", [4096, 8192])
 def test_planner_cluster_splits_take_the_push_form(K):
     for M in range(1, 33):
-        for n_blocks in range(1, 80):
-            S = plan_config(M, K, 128 * n_blocks)[3]
+        for n8 in range(1, 160):
+            N = 64 * n8
+            pl = plan_config(M, K, N)
+            S, bn = pl[3], pl[4]
             if S:
                 rc = 16 if M <= 16 else 32
-                assert -(-8 // S) * S * rc * 128 <= 32768, (M, n_blocks, S)
-                assert n_blocks * S <= 148
+                nu = 2 * bn // 16 // 2
+                assert -(-nu // S) * S * rc * 128 <= 32768, (M, N, S, bn)
+                assert -(-N // bn) * S <= 148

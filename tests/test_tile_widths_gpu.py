@@ -89,12 +89,12 @@ def test_planned_widths_at_shard_shapes(cuda_device, M, N_l):
 
 
 def test_both_w13_slots_alive(cuda_device):
-    """One weight set served at a decode shape (128-wide pack, cluster split-K) and a
-    prefill shape whose plan takes a narrow width (second pack): alternating calls
-    re-use both packs and stay correct; an in-place weight change re-packs both."""
+    """One weight set served at a decode shape (64-wide pack, cluster split-K) and a
+    prefill shape whose plan takes another narrow width (a second pack): alternating
+    calls re-use both packs and stay correct; an in-place weight change re-packs both."""
     K, N = 4096, 1376
     big = make_inputs(2048, K, N, family="C", seed=8400, dtype="bf16")
-    assert ffn.plan_config(2048, K, N)[4] != 128 and ffn.plan_config(16, K, N)[4] == 128
+    assert ffn.plan_config(2048, K, N)[4] not in (64, 128) and ffn.plan_config(16, K, N)[4] == 64
     small_x = make_inputs(16, K, N, family="C", seed=8401, dtype="bf16")["x"]
     t = {k: v.to(cuda_device) for k, v in big.items()}
     xs = small_x.to(cuda_device)
@@ -150,3 +150,24 @@ def test_tile_bn_option_contract(cuda_device):
     torch.cuda.synchronize()
     assert h.last_launch()[0] == ffn.VARIANT_1SM
     check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), "1sm with TILE_BN=80")
+
+
+# ---- the 1-SM 64-output tile with the decode paths (row replication, cluster split-K) ----
+@pytest.mark.parametrize("csplit", [1, 2, 4, 6])
+@pytest.mark.parametrize("M,K,N", [(16, 4096, 1376), (1, 1024, 200), (32, 2048, 64 * 7 + 8), (48, 1024, 520)])
+def test_decode_paths_bn64(cuda_device, M, K, N, csplit):
+    """BN = 64 on the 1-SM kernel: replicated decode rows (csplit 1 = off), and the
+    cluster split-K with S CTAs per tile (push form for <= 32 rows, pull form above)."""
+    d = make_inputs(M, K, N, family="C", seed=8700 + M + K + csplit, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_option(ffn.OPT_TILE_BN, 64)
+    h.set_variant(ffn.VARIANT_1SM)
+    h.set_option(ffn.OPT_CSPLIT, csplit)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    again = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert h.last_launch()[0] == ffn.VARIANT_1SM
+    assert torch.equal(out, again), "bitwise run-to-run"
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16")
+    check(out, ref, f"bn=64 1sm csplit={csplit} {M}x{K}x{N}")
