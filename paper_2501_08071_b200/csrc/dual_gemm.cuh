@@ -170,12 +170,15 @@ __device__ __forceinline__ int sk_owner(const FfnGemmParams& p, int64_t i) {
 // later ones are claimed by the leader CTA's producer from the global counter ahead of
 // use (the atomic for tile i+3 is issued when it starts tile i, its result published in
 // the cluster's ring when it starts tile i+1, so tile i+1 is in the ring a whole tile
-// before anyone needs it), and every role loads the next tile's slot when it starts a
-// tile and uses it when it starts the next one.  Neither the
-// claim's nor the loads' L2 round trips sit on a role's critical path; the published
-// words carry only the tile number, so relaxed accesses suffice (a tag = launch epoch +
-// tile index tells a published slot from a stale one; a role that finds it stale spins,
-// which the two-tile lead makes rare).  The producer runs STAGES k-blocks ahead of the
+// before anyone needs it), and the other producer and the epilogue warps load the next
+// tile's slot when they start a tile and use it when they start the next one; the MMA
+// warp reads only segment lengths, from shared memory (seg_nkb).  Neither the claim's nor
+// the loads' L2 round trips sit on a role's critical path; the published words carry only
+// the tile number, so relaxed accesses suffice (a tag = launch epoch + tile index tells a
+// published slot from a stale one; a role that finds it stale spins, which the two-tile
+// lead makes rare).  (A just-in-time variant -- claims issued a fixed number of k-blocks
+// before each tile's end, so slow pairs claim late -- measured slower everywhere: the
+// claim and prefetch hooks inside the producer's k-loop cost more than the balance gained.)  The producer runs STAGES k-blocks ahead of the
 // MMA and the MMA at most one tile ahead of the epilogue, so the kDynRing slots of a ring
 // are never overwritten before their readers are done.  The stream-K region after the
 // data-parallel tiles stays static per cluster.
@@ -936,6 +939,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
     uint64_t* xbar = bars + 2 * C::STAGES + 6;        // cluster split-K: partials of all S CTAs in smem
     uint64_t* rbar = bars + 2 * C::STAGES + 7;        // cluster split-K, push form: partials received
+    // dynamic claiming: k-blocks of the segment a stage starts (0 = end), byte 512 of the barrier area
+    int* seg_nkb = reinterpret_cast<int*>(bars + 64);
+    static_assert((2 * C::STAGES + 8) * 8 <= 512 && 512 + 4 * C::STAGES <= C::BAR_BYTES, "barrier area layout");
 
     const uint32_t warp = ptx::warp_id_uniform();
     const uint32_t lane = ptx::lane_id();
@@ -1042,8 +1048,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 tile_coords(g0.tile, p, mb0, nb0);
                 const int row_b0 = C::b_row0(nb0, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
                 pre = min(C::STAGES, g0.kb1 - g0.kb0);
-                if (ptx::elect_one())
+                if (ptx::elect_one()) {
+                    if constexpr (kDyn) {
+                        if (leader) seg_nkb[0] = g0.kb1 - g0.kb0;  // (before the arrive that releases it)
+                    }
                     for (int i = 0; i < pre; ++i) arm_and_load_w(i, g0.kb0 + i, row_b0);
+                }
                 __syncwarp();
             }
         }
@@ -1068,6 +1078,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 } else {
                     ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
                     if (ptx::elect_one()) {
+                        if constexpr (kDyn) {
+                            if (leader && kb == sg.kb0) seg_nkb[stage] = sg.kb1 - sg.kb0;
+                        }
                         arm_and_load_w(stage, kb, row_b0);
                         load_x(stage, kb, row_a);
                     }
@@ -1076,6 +1089,18 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 if (first_load && lane == 0) trace_stamp(p, 1);
                 first_load = false;
                 if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+        if constexpr (kDyn) {
+            // end marker for the MMA warp's stage-driven loop: a stage completed by a plain
+            // arrive (no transaction bytes) whose segment length is 0
+            if (leader) {
+                ptx::mbar_wait(ptx::smem_u32(&empty_bar[stage]), phase ^ 1);
+                if (ptx::elect_one()) {
+                    seg_nkb[stage] = 0;
+                    ptx::mbar_arrive(ptx::smem_u32(&full_bar[stage]));
+                }
+                __syncwarp();
             }
         }
         if (lane == 0) {
@@ -1100,14 +1125,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // smem descriptors of stage 0; stage s adds s*bytes >> 4 to the address field
             const uint64_t adesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a));
             const uint64_t bdesc0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b));
-            SchedT<kDyn> sch;
+            SchedT<false> sch;  // (kDyn kernels take the stage-driven loop below)
             sch.init(p, cluster_id, static_cast<int>(part));
-            if (kDyn) {
-                ptx::pdl_wait();  // (the ring and epoch of the previous launch are final)
-                sch.load_epoch();
-            }
             Seg sg;
-            for (; sch.next(sg); ++it) {
+            for (; !kDyn && sch.next(sg); ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 {
@@ -1151,6 +1172,40 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     }
                 }
                 __syncwarp();
+            }
+            if constexpr (kDyn) {
+                // Dynamic claiming: the MMA warp needs no tile numbers, only each segment's
+                // k-block count, which the leader's producer writes into seg_nkb[stage] of the
+                // segment's first stage before arming it (0 = no more segments): the loop reads
+                // it behind the full barrier it waits on anyway (no global loads, no branch on
+                // a lane's value in the issue loop)
+#pragma unroll 1
+                for (;; ++it) {
+                    ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
+                    const int nkb = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile int*>(&seg_nkb[stage]), 0);
+                    if (nkb == 0) break;
+                    const int acc = it & 1;
+                    const uint32_t acc_phase = (it >> 1) & 1;
+                    ptx::mbar_wait(ptx::smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+                    const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
+                    for (int j = 0; j < nkb; ++j) {
+                        if (j > 0) ptx::mbar_wait(ptx::smem_u32(&full_bar[stage]), phase);
+                        ptx::tc_fence_after();
+                        const uint64_t adesc = adesc0 + static_cast<uint64_t>((stage * C::A_BYTES) >> 4);
+                        const uint64_t bdesc = bdesc0 + static_cast<uint64_t>((stage * C::B_BYTES) >> 4);
+                        if (ptx::elect_one()) {
+#pragma unroll
+                            for (int k = 0; k < C::KSTEPS; ++k)
+                                ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
+                                                           (j > 0 || k > 0) ? 1u : 0u);
+                            ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), 0x3);
+                        }
+                        __syncwarp();
+                        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    if (ptx::elect_one()) ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
+                    __syncwarp();
+                }
             }
             if (lane == 0) {
                 trace_stamp(p, 3);
