@@ -39,6 +39,11 @@ for spec in "prefill:llama7b_prefill:1" "decode:llama7b_decode:1" "70b:llama70b:
   IFS=: read name w P <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_$name \
     python bench.py --workload $w --shard-of $P --steps 2 --warmup 1 $NB > $O/ncu_gemm_$name.log 2>&1; echo "ncu_$name=$?"
+  # keep the summary and the raw metric page; only the headline's report travels back whole
+  python scripts/ncu_summary.py $O/prof_gemm_$name.ncu-rep > $O/ncu_summary_$name.json 2>/dev/null
+  ncu -i $O/prof_gemm_$name.ncu-rep --page raw --csv > $O/ncu_raw_$name.csv 2>/dev/null
+  gzip -f $O/ncu_raw_$name.csv
+  [ "$name" = prefill ] || rm -f $O/prof_gemm_$name.ncu-rep
 done
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_memcheck.log 2>&1; echo "memcheck=$?"
 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_synccheck.log 2>&1; echo "synccheck=$?"
