@@ -472,7 +472,12 @@ def run_cuasm(args):
         return hh.gemm_act(tt["x"], tt["w1"], "leaky_relu", 0.01, out=oo)
 
     # a0: one-time weight fold/pack (reported, not part of a step): the first forward packs the
-    # weights for the tile width its plan uses; prep = that call minus a second (packed) one
+    # weights for the tile width its plan uses (and allocates the handle's workspaces); with
+    # the workspaces in place the cache is dropped and prep = a packing forward minus a packed one
+    fwd(0)
+    torch.cuda.synchronize(dev)
+    if op != "rmsnorm":
+        h._check(h.lib.cuasm_ffn_invalidate_weights(h._h))
     e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
     e0.record(stream)
     fwd(0)

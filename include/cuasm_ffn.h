@@ -106,8 +106,8 @@ typedef enum {
                                1 = off, 2..8 = S (used only when tiles * S <= SMs,
                                S <= k-blocks and S clusters fit co-resident)           */
     CUASM_OPT_TILE_BN = 11,   /* fused FFN, bf16: SwiGLU outputs per tile BN (MMA N = 2 BN):
-                               0 = the configuration model decides; 128, 112, 96, 80 or
-                               64 forces it (widths below 128 run the 2-SM kernel; a
+                               0 = the configuration model decides; 128, 120, 112, 96,
+                               80 or 64 forces it (widths below 128 run the 2-SM kernel; a
                                forced 1-SM variant keeps 128, except 64, which the 1-SM
                                decode paths have too).  The folded weights are cached
                                once per width in use, so a weight set served at shapes

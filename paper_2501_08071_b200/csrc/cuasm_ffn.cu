@@ -30,7 +30,8 @@ using cuasm::GemmCfg;
 constexpr int kPackBN = 128;  // default output block of the W13 interleave (= GemmCfg<...,256>::BN)
 static_assert(GemmCfg<0, 1>::BN == kPackBN && GemmCfg<0, 2>::BN == kPackBN, "pack/GEMM block mismatch");
 // SwiGLU tile widths (outputs per tile) the 2-SM bf16 kernel is built for (dual_gemm.cuh GemmCfg)
-constexpr int kTileBNs[5] = {128, 112, 96, 80, 64};
+constexpr int kTileBNs[6] = {128, 120, 112, 96, 80, 64};
+static_assert(sizeof(kTileBNs) / sizeof(kTileBNs[0]) <= 8, "plan_config_raw's candidate array");
 
 thread_local std::string g_init_error;
 
@@ -104,10 +105,10 @@ struct cuasm_ffn_s {
     int64_t r_cap = 0;
     // a0 caches: slot 0 = the folded, interleaved W13 of the fused FFN in 128-output
     // blocks; slot 1 = a single packed weight (GEMM + activation / down projection);
-    // slots 2..5 = the same W13 in the narrower blocks BN = 112, 96, 80, 64 (each packed on
+    // slots 2..6 = the same W13 in the narrower blocks BN = 112, 96, 80, 64, 120 (each packed on
     // the first forward whose plan takes that width: e.g. a decode shard's 64-wide tiles and
     // its prefill's 80-wide tiles of one weight set coexist)
-    PackedWeights pw[6];
+    PackedWeights pw[7];
     int tile_bn = 0;   // CUASM_OPT_TILE_BN: 0 auto, else the SwiGLU outputs per tile
     // fp32 handle: x split into [x_hi | x_lo] tf32 terms per forward (pack.cuh)
     void* x2 = nullptr;
@@ -276,8 +277,10 @@ cuasm_status_t launch_pack(cuasm_ffn_t h, int slot, const void* g, const void* w
     return CUASM_OK;
 }
 
-// The W13 cache slot of a SwiGLU tile width: 0 for BN = 128, 2..5 for 112, 96, 80, 64.
-inline int w13_slot(int bn) { return bn == 112 ? 2 : bn == 96 ? 3 : bn == 80 ? 4 : bn == 64 ? 5 : 0; }
+// The W13 cache slot of a SwiGLU tile width: 0 for BN = 128, 2..6 for 112, 96, 80, 64, 120.
+inline int w13_slot(int bn) {
+    return bn == 112 ? 2 : bn == 96 ? 3 : bn == 80 ? 4 : bn == 64 ? 5 : bn == 120 ? 6 : 0;
+}
 
 cuasm_status_t ensure_packed(cuasm_ffn_t h, int slot, const void* g, const void* w1, const void* w3, int64_t K,
                              int64_t N, cudaStream_t s, int64_t kp = 0, int bn = kPackBN) {
@@ -440,11 +443,12 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // destination [M rows, ldo stride] x N columns, 32 x 32 boxes, 64-byte swizzle
     // (what the epilogue's staging layout writes); stores past M / N are clipped
     // (one map per destination: the fused gather's P2P fan-out is P TMA stores per box)
-    // (tiles whose last SwiGLU unit is 16 columns wide -- BN % 32 == 16 -- store it through
-    // half-width maps: 32 x 16 boxes, 32-byte swizzle)
+    // (tiles whose last SwiGLU unit is narrower -- BN % 32 = 16 or 24 -- store it through a
+    // second set of maps: 32 x 16 boxes with 32-byte swizzle, or 32 x 24 boxes unswizzled)
     cuasm::OutMaps omaps{}, omaps_h{};
     p.tma_store = (kKind == 0 && !p.dst_mc) ? 1 : 0;
-    constexpr bool kHalfUnit = kEpi == 0 && C::BN % 32 == 16;
+    constexpr bool kHalfUnit = kEpi == 0 && C::BN % 32 != 0;
+    constexpr uint32_t kNarrowW = C::BN % 32 == 0 ? 32 : C::BN % 32;
     p.rs_world = 0;
     p.rs_nblk = static_cast<int>((N + 255) / 256);
     if (e.rs_world > 0) {
@@ -474,11 +478,12 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         for (int hw = 0; hw < (kHalfUnit ? 2 : 1); ++hw) {
             cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
             cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldo) * static_cast<cuuint64_t>(h->esize)};
-            cuuint32_t box[2] = {hw ? 16u : 32u, 32};
+            cuuint32_t box[2] = {hw ? kNarrowW : 32u, 32};
             cuuint32_t estr[2] = {1, 1};
             CUresult r = h->encode(hw ? &omaps_h.m[q] : &omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[q], dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   hw ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                   hw ? (kNarrowW == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE)
+                                      : CU_TENSOR_MAP_SWIZZLE_64B,
                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out %d) failed (CUresult %d)", q, (int)r);
@@ -672,7 +677,7 @@ struct Plan {
 // 128-wide 229.6 us: 0.87); at 80 and below the per-k-block issue / barrier / operand
 // overheads that do not shrink with bn show (2048 x 4096 x 1376: 80 -> 0.70, 64 -> 0.62)
 inline double bn_frac(int bn) {
-    return bn >= 128 ? 1.0 : bn >= 112 ? 0.867 : bn >= 96 ? 0.80 : bn >= 80 ? 0.70 : 0.62;
+    return bn >= 128 ? 1.0 : bn >= 120 ? 0.935 : bn >= 112 ? 0.867 : bn >= 96 ? 0.80 : bn >= 80 ? 0.70 : 0.62;
 }
 
 Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,
@@ -738,7 +743,7 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // per tile), or the SwiGLU tile widths bn (2 bn = MMA N; widths below 128 only for the
     // 2-SM bf16 kernel, DESIGN.md §6 "Tile widths")
     struct Cand { int tn, bn; };
-    Cand cands[5];
+    Cand cands[8];  // (>= the SwiGLU widths or the 2 GEMM widths)
     int nc = 0;
     if (out_cols != 128) {
         for (int tn : {256, 128})
@@ -891,6 +896,7 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
         if (h->dtype != CUASM_DTYPE_BF16 || v != CUASM_VARIANT_2SM || e.slot != w13_slot(plan.bn))
             return fail(h, CUASM_ERR_UNSUPPORTED, "tile width %d needs the 2-SM bf16 kernel", plan.bn);
         switch (plan.bn) {
+        case 120: st = launch_gemm<0, 2, 0, 240>(h, e, x, out, M, K, N, eps, s); break;
         case 112: st = launch_gemm<0, 2, 0, 224>(h, e, x, out, M, K, N, eps, s); break;
         case 96: st = launch_gemm<0, 2, 0, 192>(h, e, x, out, M, K, N, eps, s); break;
         case 80: st = launch_gemm<0, 2, 0, 160>(h, e, x, out, M, K, N, eps, s); break;
@@ -1414,7 +1420,7 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         return CUASM_OK;
     case CUASM_OPT_TILE_BN:
         if (value != 0 && std::find(std::begin(kTileBNs), std::end(kTileBNs), value) == std::end(kTileBNs))
-            return fail(h, CUASM_ERR_INVALID_ARG, "TILE_BN is 0 (auto) or one of 128, 112, 96, 80, 64");
+            return fail(h, CUASM_ERR_INVALID_ARG, "TILE_BN is 0 (auto) or one of 128, 120, 112, 96, 80, 64");
         h->tile_bn = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_DYNAMIC:

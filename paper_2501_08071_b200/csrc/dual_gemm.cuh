@@ -373,16 +373,17 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 // narrower tile halves the wave-quantisation step of square-ish GEMMs.
 //
 // SwiGLU tile widths (DESIGN.md §6 "Tile widths"): kN = 2*BN with BN in {64, 80, 96,
-// 112, 128} outputs per tile, so a column shard N_l can be cut into a tile count that
+// 112, 120, 128} outputs per tile, so a column shard N_l can be cut into a tile count that
 // fills whole waves of CTA pairs (7B P=8: N_l = 1376 -> 18 blocks of 80 = 144 tiles of
 // 256 rows on 74 pairs instead of 11 blocks of 128 = 88).  h1 sits in accumulator
 // columns [0, BN), h3 in [BN, 2BN); the epilogue walks 32-column units (the last one
-// 16 wide when BN % 32 == 16).  The decode paths (rep, cluster split-K) exist for BN = 128 and
+// 16 or 24 wide when BN % 32 is 16 or 24).  The decode paths (rep, cluster split-K) exist for BN = 128 and
 // BN = 64 (more, smaller tiles for the decode shards' weight streaming) and every GEMM tile.
 template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256>
 struct GemmCfg {
-    static_assert(kEpi == 0 ? (kN % 32 == 0 && kN >= 128 && kN <= 256) : (kN == 256 || kN == 128),
-                  "SwiGLU tiles: kN = 2*BN, BN in {64, 80, 96, 112, 128}; GEMM tiles 128 or 256");
+    static_assert(kEpi == 0 ? (kN % 16 == 0 && (kN / 2) % 8 == 0 && (kN / 2) % 32 != 8 && kN >= 128 && kN <= 256)
+                            : (kN == 256 || kN == 128),
+                  "SwiGLU tiles: kN = 2*BN, BN in {64, 80, 96, 112, 120, 128}; GEMM tiles 128 or 256");
     static constexpr int kEsize = kKind == 0 ? 2 : 4;
     static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
     static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
@@ -588,7 +589,9 @@ struct OutMaps {
 };
 
 // W = 16 (the last unit of a BN % 32 == 16 tile): a 32 x 16 box (32-byte rows) through
-// the half-width maps, 32-byte swizzle (chunk c of row r at c ^ ((r >> 2) & 1)).
+// the narrow maps, 32-byte swizzle (chunk c of row r at c ^ ((r >> 2) & 1)); W = 24 (BN % 32
+// == 24): a 32 x 24 box, 48-byte rows, no swizzle (rows 48 B apart already put the 8 lanes
+// of a store phase on 8 distinct 16-byte bank groups).
 template <int kPending, int W = 32>
 __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint8_t* box, const float (&o)[32],
                                               int col, int row0, uint32_t lane) {
@@ -600,6 +603,8 @@ __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint
                                    ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]), ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
         if constexpr (W == 32)
             *reinterpret_cast<uint4*>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+        else if constexpr (W == 24)
+            *reinterpret_cast<uint4*>(box + lane * 48 + (c << 4)) = v;
         else
             *reinterpret_cast<uint4*>(box + lane * 32 + ((c ^ ((lane >> 2) & 1)) << 4)) = v;
     }
@@ -1488,7 +1493,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 uint8_t* stg = smem_stg + ewarp * C::STG_WARP_BYTES;  // this warp's two 2 KB boxes
                 // the two boxes alternate store by store: the box written now was last used two
                 // stores ago, so at most one store (the other box) may be pending
-                const OutMaps* maps = W == 32 ? &omaps : &omaps_h;
+                const OutMaps* maps = W == 32 ? &omaps : &omaps_h;  // (the narrow last unit: 16 or 24 wide)
                 float o[32];
                 if constexpr (kEpi == 0) {
 #pragma unroll
@@ -1534,10 +1539,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                         u = rep == 4 ? static_cast<int>(quad) : static_cast<int>(quad / 2) * 2 + half;
                     }
                     if (u >= C::NU) continue;
-                    if (C::BN % 32 == 0 || u + 1 < C::NU)
+                    constexpr int kLastW = C::BN % 32 == 0 ? 32 : C::BN % 32;  // 32, 16 or 24
+                    if (kLastW == 32 || u + 1 < C::NU)
                         unit(std::integral_constant<int, 32>{}, 32 * u, C::BN + 32 * u);
                     else
-                        unit(std::integral_constant<int, 16>{}, 32 * u, C::BN + 32 * u);
+                        unit(std::integral_constant<int, kLastW>{}, 32 * u, C::BN + 32 * u);
                 } else {
                     unit(std::integral_constant<int, 32>{}, 32 * C::chunk_a(half, i), 32 * C::chunk_b(half, i));
                 }

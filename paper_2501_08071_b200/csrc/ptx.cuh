@@ -292,11 +292,27 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)
         : "memory");
 }
 
-// W (32 or 16) consecutive columns per lane.
+// TMEM -> registers: 32 lanes x 8 consecutive 32-bit columns (v[off .. off+7]).
+template <int kOff>
+__device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[kOff]), "=r"(v[kOff + 1]), "=r"(v[kOff + 2]), "=r"(v[kOff + 3]), "=r"(v[kOff + 4]),
+                   "=r"(v[kOff + 5]), "=r"(v[kOff + 6]), "=r"(v[kOff + 7])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// W (32, 24 or 16) consecutive columns per lane.
 template <int W>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[32]) {
-    if constexpr (W == 32) tmem_ld_32x32b_x32(taddr, v);
-    else tmem_ld_32x32b_x16(taddr, v);
+    if constexpr (W == 32) {
+        tmem_ld_32x32b_x32(taddr, v);
+    } else if constexpr (W == 24) {
+        tmem_ld_32x32b_x16(taddr, v);
+        tmem_ld_32x32b_x8<16>(taddr + 16, v);
+    } else {
+        tmem_ld_32x32b_x16(taddr, v);
+    }
 }
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -119,7 +119,8 @@ def test_7b_prefill_balance():
 # ---- shape-keyed configuration model (csrc/cuasm_ffn.cu plan_config) ---------
 
 def bn_frac(bn):
-    return 1.0 if bn >= 128 else 0.867 if bn >= 112 else 0.80 if bn >= 96 else 0.70 if bn >= 80 else 0.62
+    return (1.0 if bn >= 128 else 0.935 if bn >= 120 else 0.867 if bn >= 112 else 0.80 if bn >= 96 else
+            0.70 if bn >= 80 else 0.62)
 
 
 def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
@@ -144,7 +145,7 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
         return ("1sm", False, 128, 0, 128)
     best, best_t = ("2sm", False, 256, 0, 128), 1e30
     if out_cols == 128:   # SwiGLU tile widths (narrower than 128: 2-SM bf16 only)
-        cands = [(256, bn) for bn in (128, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > 128)]
+        cands = [(256, bn) for bn in (128, 120, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > 128)]
     else:
         cands = [(256, 128), (128, 128)]
     for tn, bn in cands:

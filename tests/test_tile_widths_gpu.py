@@ -22,7 +22,7 @@ from paper_2501_08071_b200.tp import gather_destinations, shard_bounds, shard_we
 pytestmark = pytest.mark.gpu
 
 RTOL, ATOL = 2e-2, 1e-3
-WIDTHS = (64, 80, 96, 112)
+WIDTHS = (64, 80, 96, 112, 120)
 
 
 def check(gpu, ref, what):
