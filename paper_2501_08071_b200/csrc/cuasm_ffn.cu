@@ -572,7 +572,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.num_dp_tiles = p.num_tiles - sk_tiles;
     p.sk_iters = static_cast<int64_t>(sk_tiles) * p.num_k_blk;
     if (sk_tiles > 0) {
-        const int64_t ws_need = static_cast<int64_t>(clusters) * kCtaGroup * C::BM * C::UMMA_N * 4;
+        const int64_t ws_need = static_cast<int64_t>(clusters) * kCtaGroup * C::WS_SLOT_F4 * 16;
         const int64_t fl_need = static_cast<int64_t>(clusters) * kCtaGroup * C::NUM_EPI_WARPS * 4;
         if (ws_need > h->ws_bytes) {
             if (h->ws) cudaFree(h->ws);
@@ -675,9 +675,11 @@ struct Plan {
 // (scripts/tune_bn.py, profiles/r02/tune_bn.json): at full size the narrower tiles run at
 // about their MMA-width ratio (7B prefill, 11 rounds of 112-wide tiles 218.9 us vs 10 of
 // 128-wide 229.6 us: 0.87); at 80 and below the per-k-block issue / barrier / operand
-// overheads that do not shrink with bn show (2048 x 4096 x 1376: 80 -> 0.70, 64 -> 0.62)
+// overheads that do not shrink with bn show (2048 x 4096 x 1376: 80 -> 0.70, 64 -> 0.62); 120
+// (MMA N = 240) fills 7B's N = 11008 with 92 blocks: 736 tiles = 9.95 rounds of 74 pairs,
+// 217.4 us vs 223.8 (112) and 224.5 (128, stream-K) on one box -> 0.925
 inline double bn_frac(int bn) {
-    return bn >= 128 ? 1.0 : bn >= 120 ? 0.935 : bn >= 112 ? 0.867 : bn >= 96 ? 0.80 : bn >= 80 ? 0.70 : 0.62;
+    return bn >= 128 ? 1.0 : bn >= 120 ? 0.925 : bn >= 112 ? 0.867 : bn >= 96 ? 0.80 : bn >= 80 ? 0.70 : 0.62;
 }
 
 Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,

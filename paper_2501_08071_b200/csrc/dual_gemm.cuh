@@ -398,6 +398,9 @@ struct GemmCfg {
     static constexpr int EPI_ITERS = kEpi == 0 ? (NU + 1) / 2 : kN / 128;
     // TMEM column stride between the two accumulators (a power-of-two allocation)
     static constexpr int ACC_STRIDE = kN > 128 ? 256 : 128;
+    // stream-K partial slot per CTA, float4s: [32-column chunk][quad][8][32 lanes], whole chunks
+    // (UMMA_N = 240 has a partial last chunk, still addressed at the chunk's full stride)
+    static constexpr int WS_SLOT_F4 = BM * ((kN + 31) / 32 * 32) / 4;
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
@@ -1338,7 +1341,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // access is 512 contiguous bytes: float4 index ((chunk*4 + quad)*8 + q)*32 + lane
             // holds columns chunk*32 + 4q..+3 of row quad*32 + lane (chunk < BN/32: h1, else h3)
             float4* my_slot = reinterpret_cast<float4*>(p.ws) +
-                              (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
+                              (static_cast<int64_t>(cluster_id) * kCtaGroup + cta_rank) * C::WS_SLOT_F4;
             int c_first = 0, c_last = -1;
             if (finisher) {
                 // contributors: the (lower) clusters whose stream-K ranges cover the rest of this tile
@@ -1351,7 +1354,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
                     const char* slot = reinterpret_cast<const char*>(
                         reinterpret_cast<const float4*>(p.ws) +
-                        (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4));
+                        (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * C::WS_SLOT_F4);
                     // the 32-column chunks (4 KB per quadrant) holding this warp's units
                     auto pf = [&](int chunk) { prefetch_l2(slot + ((chunk * 4 + quad) * 8 * 32) * 16 + lane * 128); };
 #pragma unroll
@@ -1471,7 +1474,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 for (int cc = c_first; cc <= c_last; ++cc) {
                     if (sk_begin(p, cc) == sk_begin(p, cc + 1)) continue;
                     const float4* slot = reinterpret_cast<const float4*>(p.ws) +
-                                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * (C::BM * C::UMMA_N / 4);
+                                         (static_cast<int64_t>(cc) * kCtaGroup + cta_rank) * C::WS_SLOT_F4;
                     float4 a[W / 4], b[W / 4];
 #pragma unroll
                     for (int q = 0; q < W / 4; ++q) {

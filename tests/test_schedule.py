@@ -119,7 +119,7 @@ def test_7b_prefill_balance():
 # ---- shape-keyed configuration model (csrc/cuasm_ffn.cu plan_config) ---------
 
 def bn_frac(bn):
-    return (1.0 if bn >= 128 else 0.935 if bn >= 120 else 0.867 if bn >= 112 else 0.80 if bn >= 96 else
+    return (1.0 if bn >= 128 else 0.925 if bn >= 120 else 0.867 if bn >= 112 else 0.80 if bn >= 96 else
             0.70 if bn >= 80 else 0.62)
 
 
@@ -267,18 +267,25 @@ def test_library_plan_w2_and_70b(lib_plan):
     assert lib_plan(4096, 8192, 3584) == ("2sm", False, 256, 0, 112)
 
 
-# best measured SwiGLU tile width (profiles/r02/tune_bn.json; near-ties <= 1.5% accept either)
+# best measured SwiGLU tile width (profiles/r02/tune_bn.json, tune_bn120.json; near-ties <= 1.5%
+# accept either)
 BN_MEASURED = {
     (2048, 4096, 1376): {80},
     (2048, 4096, 2752): {112, 80},
-    (2048, 4096, 5504): {128},
-    (2048, 4096, 11008): {112, 80},
+    (2048, 4096, 5504): {120},
+    (2048, 4096, 11008): {120},
     (1024, 4096, 1376): {80, 96},
     (1024, 4096, 2752): {80},
     (512, 4096, 11008): {112, 80},
+    (1024, 4096, 11008): {120},
+    (4096, 4096, 11008): {120},
+    (16384, 4096, 11008): {120, 112},
     (256, 4096, 11008): {80},
     (4096, 8192, 3584): {112},
-    (4096, 8192, 7168): {112, 128},
+    (4096, 8192, 7168): {112, 120, 128},
+    (4096, 8192, 14336): {112, 120, 128},
+    (4096, 8192, 28672): {120, 112},
+    (768, 4096, 11008): {120},
     (16384, 4096, 1376): {128},
 }
 
