@@ -988,6 +988,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     bool cl_pending = csplit;
     if (kCtaGroup == 2) {
         ptx::cluster_sync();
+#if CUASM_DIAG_PROLOGUE  // experiments only: producer prologue stamps in slots 12..15
+        if (warp == 0 && lane == 0) trace_stamp(p, 12);
+#endif
     } else {
         // (the barriers' initialisation is already released to the cluster by
         // fence.mbarrier_init: a relaxed arrive, no GPU-scope membar)
@@ -1060,12 +1063,23 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if constexpr (kDyn) {
                         if (leader) seg_nkb[0] = g0.kb1 - g0.kb0;  // (before the arrive that releases it)
                     }
-                    for (int i = 0; i < pre; ++i) arm_and_load_w(i, g0.kb0 + i, row_b0);
+                    for (int i = 0; i < pre; ++i) {
+                        arm_and_load_w(i, g0.kb0 + i, row_b0);
+#if CUASM_DIAG_PROLOGUE
+                        if (i == 0) trace_stamp(p, 13);
+#endif
+                    }
                 }
                 __syncwarp();
             }
         }
+#if CUASM_DIAG_PROLOGUE
+        if (lane == 0) trace_stamp(p, 14);
+#endif
         ptx::pdl_wait();  // x may be produced by the preceding kernel (PDL)
+#if CUASM_DIAG_PROLOGUE
+        if (lane == 0) trace_stamp(p, 15);
+#endif
         sch.load_epoch();
         int stage = 0;
         uint32_t phase = 0;
@@ -1221,10 +1235,12 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     // SM cycles from the first to the last MMA issue, k-blocks issued and
                     // cycles spent waiting: (cycles / (k-blocks - 1)) vs the tcgen05 floor
                     // (4 x 128 cycles) tells a starved tensor pipe from a slow clock
+#if !CUASM_DIAG_PROLOGUE
                     p.trace[blockIdx.x * kTraceSlots + 12] = static_cast<unsigned long long>(clock64() - clk0);
                     p.trace[blockIdx.x * kTraceSlots + 13] = static_cast<unsigned long long>(kblocks);
                     p.trace[blockIdx.x * kTraceSlots + 14] = static_cast<unsigned long long>(wait_full);
                     p.trace[blockIdx.x * kTraceSlots + 15] = static_cast<unsigned long long>(wait_tempty);
+#endif
                 }
             }
         }
