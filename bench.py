@@ -94,6 +94,8 @@ def parse_args(argv=None):
     ap.add_argument("--fused-reduce", action="store_true",
                     help="block workload: the row-parallel W2 reduction fused into the down projection's epilogue "
                          "(f1; with --shard-of P: P simulated staging / output buffers on this GPU)")
+    ap.add_argument("--rs-bf16", action="store_true",
+                    help="with --fused-reduce: the partials travel as bf16 (CUASM_OPT_RS_PARTIAL = 1)")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly instead of a CUDA graph")
     ap.add_argument("--shard-of", type=int, default=1,
@@ -413,6 +415,8 @@ def run_cuasm(args):
         hh.set_variant(args.variant)
         if args.tile_bn:
             hh.set_option(ffn.OPT_TILE_BN, args.tile_bn)
+        if args.rs_bf16:
+            hh.set_option(ffn.OPT_RS_PARTIAL, 1)
         if args.no_pdl:
             hh.set_option(ffn.OPT_PDL, 0)
         handles.append(hh)
@@ -752,7 +756,8 @@ def run_cuasm(args):
                 "parallelism": f"tp{world} (W1/W3 column-sharded, x replicated)" if world > 1 else (
                     f"PROJECTION of tp{args.shard_of}: rank 0's shard timed alone on one GPU; value = "
                     f"{args.shard_of} x its FLOPs / its time" if args.shard_of > 1 else "single GPU"),
-                "reduce": (("fused: W2 epilogue scatters fp32 partial tiles to the owners' staging buffers, "
+                "reduce": (("fused: W2 epilogue scatters " + ("bf16" if args.rs_bf16 else "fp32") +
+                            " partial tiles to the owners' staging buffers, "
                             "owner rank-order sum fanned out to every rank's output " + (
                                 "(symmetric memory)" if world > 1 else
                                 f"({max(1, args.shard_of)} simulated ranks on this GPU: rank 0's launches)"))

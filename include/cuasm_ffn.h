@@ -113,7 +113,7 @@ typedef enum {
                                once per width in use, so a weight set served at shapes
                                whose plans differ in BN (decode shards take 64, prefill
                                shards 80-112) holds one packed copy per width    */
-    CUASM_OPT_DYNAMIC = 12    /* data-parallel tiles of the persistent GEMM claimed from a
+    CUASM_OPT_DYNAMIC = 12,   /* data-parallel tiles of the persistent GEMM claimed from a
                                global counter (each cluster's first tile static, the rest
                                claimed one tile ahead by its leader CTA) instead of the
                                static round-robin: the tiles in flight stay consecutive
@@ -123,6 +123,12 @@ typedef enum {
                                more than one round).  Results are bitwise independent of
                                the claim order (each tile is computed whole by one
                                cluster)                                               */
+    CUASM_OPT_RS_PARTIAL = 13 /* fused reduction (cuasm_ffn_block_forward_rs / cuasm_rs_reduce,
+                               which must agree): 0 (default) = the partials travel and are
+                               staged as fp32; 1 = as bf16 (RNE: half the NVLink bytes, one
+                               extra rounding per partial; the owner still sums in fp32 in
+                               rank order).  Staging then needs half of cuasm_rs_layout's
+                               stage_bytes                                            */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with

@@ -33,7 +33,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 ACT_IDENTITY, ACT_LEAKY_RELU = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC = range(13)
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC, OPT_RS_PARTIAL = range(14)
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL, SCHEDULE_STREAM_K_TAIL = 0, 1, 2, 3
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
@@ -358,8 +358,8 @@ class FusedFFN:
     def rs_reduce(self, stage, world: int, rank: int, dst_ptrs, ldo: int, M: int, K: int, multicast: bool = False):
         """f1 owner side (cuasm_rs_reduce): sum this rank's staging slots in rank order and
         write its columns of y into every destination (or the multicast address)."""
-        if stage.dtype != torch.float32 or not stage.is_cuda or stage.device.index != self.device_index:
-            raise ValueError("stage must be an fp32 tensor on the handle's device")
+        if not stage.is_cuda or stage.device.index != self.device_index:
+            raise ValueError("stage must be a tensor on the handle's device")
         dst = (ctypes.c_void_p * len(dst_ptrs))(*[int(p_) for p_ in dst_ptrs])
         self._check(self.lib.cuasm_rs_reduce(self._h, stage.data_ptr(), world, rank, dst, len(dst_ptrs),
                                              1 if multicast else 0, int(ldo), M, K, _stream_ptr(stage.device)))

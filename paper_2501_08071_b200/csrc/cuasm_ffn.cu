@@ -100,6 +100,7 @@ struct cuasm_ffn_s {
     // dynamic whole-tile claiming (dual_gemm.cuh Sched): counters + per-cluster rings, zeroed once
     uint32_t* dyn = nullptr;
     int dynamic = 0;   // CUASM_OPT_DYNAMIC: 0 auto, 1 off, 2 on
+    int rs_bf16 = 0;   // CUASM_OPT_RS_PARTIAL: 0 fp32 partials, 1 bf16
     // a1 workspace
     float* r = nullptr;
     int64_t r_cap = 0;
@@ -450,24 +451,28 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     constexpr bool kHalfUnit = kEpi == 0 && C::BN % 32 != 0;
     constexpr uint32_t kNarrowW = C::BN % 32 == 0 ? 32 : C::BN % 32;
     p.rs_world = 0;
+    p.rs_bf16 = 0;
     p.rs_nblk = static_cast<int>((N + 255) / 256);
     if (e.rs_world > 0) {
         // f1: one fp32 map per owner rank q over its staging slot for this rank,
         // stage[q] + rs_rank * M * Kq floats, [M, Kq], 32 x 16 boxes (64-byte rows, 64-byte swizzle)
         if (kKind != 0 || kEpi != 1) return fail(h, CUASM_ERR_UNSUPPORTED, "fused reduce-scatter: bf16 GEMM only");
         p.rs_world = e.rs_world;
+        p.rs_bf16 = h->rs_bf16;
         p.num_dst = 0;
+        const int pes = h->rs_bf16 ? 2 : 4;  // partial element size
         for (int q = 0; q < e.rs_world; ++q) {
             int64_t c0, c1;
             rs_cols(N, e.rs_world, q, c0, c1);
             const int64_t kq = c1 - c0;
             if (kq == 0) continue;  // owns no columns: no tile is ever sent there
             cuuint64_t dims[2] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(M)};
-            cuuint64_t strides[1] = {static_cast<cuuint64_t>(kq) * 4};
-            cuuint32_t box[2] = {16, 32};
+            cuuint64_t strides[1] = {static_cast<cuuint64_t>(kq) * pes};
+            cuuint32_t box[2] = {h->rs_bf16 ? 32u : 16u, 32};  // 64-byte box rows either way
             cuuint32_t estr[2] = {1, 1};
-            void* base = static_cast<char*>(e.rs_stage[q]) + static_cast<int64_t>(e.rs_rank) * M * kq * 4;
-            CUresult r = h->encode(&omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+            void* base = static_cast<char*>(e.rs_stage[q]) + static_cast<int64_t>(e.rs_rank) * M * kq * pes;
+            CUresult r = h->encode(&omaps.m[q], h->rs_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                   2, base, dims, strides, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
@@ -1285,9 +1290,14 @@ cuasm_status_t cuasm_rs_reduce(cuasm_ffn_t h, const void* stage, int world, int 
     for (int q = 0; q < num_dst; ++q) d.p[q] = dst[q];
     const int64_t groups = M * ((c1 - c0) / 8);
     const int64_t blocks = std::min<int64_t>((groups + 255) / 256, int64_t(h->sm_count) * 8);
-    cuasm::ffn_rs_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-        static_cast<const float*>(stage), world, M, static_cast<int>(c1 - c0), static_cast<int>(c0), d, num_dst,
-        multicast, ldo);
+    if (h->rs_bf16)
+        cuasm::ffn_rs_reduce_kernel<__nv_bfloat16><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(stage), world, M, static_cast<int>(c1 - c0), static_cast<int>(c0), d,
+            num_dst, multicast, ldo);
+    else
+        cuasm::ffn_rs_reduce_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+            static_cast<const float*>(stage), world, M, static_cast<int>(c1 - c0), static_cast<int>(c0), d, num_dst,
+            multicast, ldo);
     CUASM_CHECK(h, cudaGetLastError(), "ffn_rs_reduce_kernel launch");
     h->last_kernels = 1;
     return CUASM_OK;
@@ -1428,6 +1438,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
     case CUASM_OPT_DYNAMIC:
         if (value < 0 || value > 2) return fail(h, CUASM_ERR_INVALID_ARG, "DYNAMIC is 0 (auto), 1 (off) or 2 (on)");
         h->dynamic = static_cast<int>(value);
+        return CUASM_OK;
+    case CUASM_OPT_RS_PARTIAL:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "RS_PARTIAL is 0 (fp32) or 1 (bf16)");
+        h->rs_bf16 = static_cast<int>(value);
         return CUASM_OK;
     case CUASM_OPT_TRACE:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "TRACE option is 0 or 1");

@@ -78,6 +78,7 @@ struct FfnGemmParams {
     // staging slot for this rank at column col - col0(q); 0 = off
     int rs_world;
     int rs_nblk;     // 256-column blocks of the output: ceil(N / 256)
+    int rs_bf16;     // 1: the partials travel as bf16 (RNE; half the bytes), 0: fp32
     int M, N, K;
     int num_m_blk;   // ceil(M / tile_m)
     int num_n_blk;   // ceil(N / OUT_COLS)
@@ -595,9 +596,10 @@ struct OutMaps {
 // the narrow maps, 32-byte swizzle (chunk c of row r at c ^ ((r >> 2) & 1)); W = 24 (BN % 32
 // == 24): a 32 x 24 box, 48-byte rows, no swizzle (rows 48 B apart already put the 8 lanes
 // of a store phase on 8 distinct 16-byte bank groups).
+// (map_idx >= 0: one store through maps->m[map_idx] at column map_col instead of the fan-out)
 template <int kPending, int W = 32>
 __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint8_t* box, const float (&o)[32],
-                                              int col, int row0, uint32_t lane) {
+                                              int col, int row0, uint32_t lane, int map_idx = -1, int map_col = 0) {
     if (lane == 0) ptx::tma_store_wait_read<kPending>();
     __syncwarp();
 #pragma unroll
@@ -614,7 +616,9 @@ __device__ __forceinline__ void store_box_tma(const OutMaps* maps, int num, uint
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-        for (int q = 0; q < num; ++q) ptx::tma_store_2d(&maps->m[q], ptx::smem_u32(box), col, row0);
+        if (map_idx >= 0) ptx::tma_store_2d(&maps->m[map_idx], ptx::smem_u32(box), map_col, row0);
+        else
+            for (int q = 0; q < num; ++q) ptx::tma_store_2d(&maps->m[q], ptx::smem_u32(box), col, row0);
         ptx::tma_store_commit();
     }
 }
@@ -1520,19 +1524,29 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if (use_tma) store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + c1, box_row0, lane);
                     else store_row32<kKind, W>(p, row, nb * C::OUT_COLS + c1, o);
                 } else if (kKind == 0 && p.rs_world > 0) {
-                    // f1: the fp32 partial of these 2 x 32 columns goes to the owner rank's
-                    // staging slot (4 boxes of 32 x 16 fp32; one owner per tile)
+                    // f1: the partial of these 2 x 32 columns goes to the owner rank's staging slot
+                    // (fp32: 4 boxes of 32 x 16; bf16: 2 boxes of 32 x 32; one owner per tile)
                     const int q = rs_owner(nb * C::OUT_COLS / 256, p.rs_nblk, p.rs_world);
                     const int cq = rs_col0(q, p.rs_nblk, p.rs_world);
+                    if (p.rs_bf16) {
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
+                        for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-                        for (int j = 0; j < W; ++j) o[j] = __uint_as_float(hh == 0 ? v1[j] : v3[j]);
-                        const int col = nb * C::OUT_COLS + (hh == 0 ? c1 : c3) - cq;
+                            for (int j = 0; j < W; ++j) o[j] = __uint_as_float(hh == 0 ? v1[j] : v3[j]);
+                            store_box_tma<1, 32>(&omaps, 1, stg + (nst++ & 1) * 2048, o, 0, box_row0, lane,
+                                                 q, nb * C::OUT_COLS + (hh == 0 ? c1 : c3) - cq);
+                        }
+                    } else {
 #pragma unroll
-                        for (int h16 = 0; h16 < 2; ++h16)
-                            store_box_tma_f32<1>(&omaps.m[q], stg + (nst++ & 1) * 2048, o, h16, col + 16 * h16, box_row0,
-                                                 lane);
+                        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                            for (int j = 0; j < W; ++j) o[j] = __uint_as_float(hh == 0 ? v1[j] : v3[j]);
+                            const int col = nb * C::OUT_COLS + (hh == 0 ? c1 : c3) - cq;
+#pragma unroll
+                            for (int h16 = 0; h16 < 2; ++h16)
+                                store_box_tma_f32<1>(&omaps.m[q], stg + (nst++ & 1) * 2048, o, h16, col + 16 * h16,
+                                                     box_row0, lane);
+                        }
                     }
                 } else {
 #pragma unroll

@@ -11,7 +11,8 @@
 // every rank's full y (dst[], P2P peer pointers) or once to the NVLS multicast
 // address (multimem.st): reduce-scatter + all-gather = all-reduce.
 //
-// HBM-bound: reads world * M * Kq * 4 bytes, writes M * Kq * 2 bytes per destination.
+// HBM-bound: reads world * M * Kq * 4 (fp32 partials) or * 2 (bf16) bytes, writes M * Kq * 2 bytes
+// per destination.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -24,7 +25,9 @@ struct RsDst {
     void* p[8];
 };
 
-__global__ void __launch_bounds__(256) ffn_rs_reduce_kernel(const float* __restrict__ stage, int world, int64_t M,
+// TP: float (fp32 partials) or __nv_bfloat16 (bf16 partials: 16 bytes per 8 columns per rank)
+template <typename TP>
+__global__ void __launch_bounds__(256) ffn_rs_reduce_kernel(const TP* __restrict__ stage, int world, int64_t M,
                                                             int Kq, int col0, const RsDst dst, int num_dst, int mc,
                                                             int64_t ldo) {
     const int gpr = Kq / 8;  // 8-column groups per row (Kq % 8 == 0)
@@ -34,7 +37,7 @@ __global__ void __launch_bounds__(256) ffn_rs_reduce_kernel(const float* __restr
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t row = i / gpr;
         const int c = static_cast<int>(i - row * gpr) * 8;
-        const float* src = stage + row * Kq + c;
+        const TP* src = stage + row * Kq + c;
         float a[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = 0.f;
@@ -45,9 +48,17 @@ __global__ void __launch_bounds__(256) ffn_rs_reduce_kernel(const float* __restr
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (p0 + j < world) {
-                    const float4* s = reinterpret_cast<const float4*>(src + (p0 + j) * slot);
-                    lo[j] = __ldcs(s);
-                    hi[j] = __ldcs(s + 1);
+                    if constexpr (sizeof(TP) == 4) {
+                        const float4* s = reinterpret_cast<const float4*>(src + (p0 + j) * slot);
+                        lo[j] = __ldcs(s);
+                        hi[j] = __ldcs(s + 1);
+                    } else {
+                        const uint4 u = __ldcs(reinterpret_cast<const uint4*>(src + (p0 + j) * slot));
+                        lo[j] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                                            __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+                        hi[j] = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u),
+                                            __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xFFFF0000u));
+                    }
                 }
 #pragma unroll
             for (int j = 0; j < 4; ++j)

@@ -117,6 +117,39 @@ def test_partial_scatter_every_schedule(cuda_device, schedule, tile_n):
         assert torch.equal(ys[q], ys[0])
 
 
+@pytest.mark.parametrize("M,K,N,P", [(300, 1024, 3 * 264, 2), (2048, 4096, 2752, 8), (129, 320, 8 * 40, 3)])
+def test_bf16_partials(cuda_device, M, K, N, P):
+    """CUASM_OPT_RS_PARTIAL = 1: the partials travel as bf16 (one RNE each, half the bytes); the
+    owner still sums in fp32 in rank order.  Every rank's y is bitwise equal, and it differs from
+    the default fp32-partial result on the same data (which the oracle checks above pin) by at
+    most the partials' own rounding (bf16 unit roundoff 2^-8 x |partial| each) plus the two
+    results' final bf16 roundings.  (Where partials cancel that rounding alone can exceed the [BJ] tolerance of the
+    small sum: the reason fp32 is the default; reading R16.)"""
+    d = make_inputs(M, K, N, family="C", seed=9500 + M + P, dtype="bf16")
+    w2 = make_inputs(1, N, K, family="C", seed=9600 + M + P, dtype="bf16")["w1"]
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    w2d = w2.to(cuda_device)
+    ys32, hidden, _ = run_simulated(cuda_device, t, w2d, P, M, K)
+    hs = []
+    for _ in range(P):
+        h = ffn.FusedFFN(cuda_device)
+        h.set_option(ffn.OPT_RS_PARTIAL, 1)
+        hs.append(h)
+    ys16, hidden16, _ = run_simulated(cuda_device, t, w2d, P, M, K, hs)
+    for q in range(1, P):
+        assert torch.equal(ys16[q], ys16[0])
+    for p in range(P):
+        assert torch.equal(hidden16[p], hidden[p])  # the same hidden shards
+    parts = []
+    for p in range(P):
+        n0, n1 = shard_bounds(N, p, P)
+        parts.append(hidden[p].double() @ w2d[:, n0:n1].double().T)
+    y32, y16 = ys32[0].double(), ys16[0].double()
+    bound = 2.0 ** -8 * sum(pp.abs() for pp in parts) + 2.0 ** -7 * y32.abs() + 1e-6
+    diff = (y16 - y32).abs()
+    assert (diff <= bound).all(), f"bf16 partials beyond their rounding bound (worst {(diff / bound).max().item():.3f})"
+
+
 def test_fused_reduce_contract_errors(cuda_device):
     h = ffn.FusedFFN(cuda_device)
     lib = h.lib
