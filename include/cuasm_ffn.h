@@ -128,7 +128,11 @@ typedef enum {
                                staged as fp32; 1 = as bf16 (RNE: half the NVLink bytes, one
                                extra rounding per partial; the owner still sums in fp32 in
                                rank order).  Staging then needs half of cuasm_rs_layout's
-                               stage_bytes                                            */
+                               stage_bytes                                            */,
+    CUASM_OPT_L2_PERSIST = 14 /* DEVICE-WIDE (cudaDeviceSetLimit): bytes of L2 set aside for
+                               persisting lines -- the x tiles' TMA loads carry an
+                               evict_last hint (CUASM_OPT_L2_POLICY); 0 = none (default).
+                               Affects every kernel on the device                     */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with

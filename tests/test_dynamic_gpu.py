@@ -94,3 +94,23 @@ def test_dynamic_option_contract(cuda_device):
     for bad in (-1, 3):
         with pytest.raises(ffn.CuasmError):
             h.set_option(ffn.OPT_DYNAMIC, bad)
+
+
+def test_l2_persist_full_group(cuda_device):
+    """CUASM_OPT_L2_PERSIST: with a persisting-L2 set-aside that holds all of x, the rasterisation
+    takes every m-block in one group (W13 read once); results equal the default schedule's
+    bitwise (whole tiles, same k-order per tile).  The device-wide limit is reset afterwards."""
+    M, K, N = 2048, 2048, 8192
+    d = make_inputs(M, K, N, family="C", seed=9800, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    ref = _handle(cuda_device, 1, schedule=ffn.SCHEDULE_DATA_PARALLEL).forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    h = _handle(cuda_device, 0, schedule=ffn.SCHEDULE_DATA_PARALLEL)
+    try:
+        h.set_option(ffn.OPT_L2_PERSIST, 32 << 20)
+        out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+        torch.cuda.synchronize()
+    finally:
+        h.set_option(ffn.OPT_L2_PERSIST, 0)
+    assert torch.equal(out, ref)
+    with pytest.raises(ffn.CuasmError):
+        h.set_option(ffn.OPT_L2_PERSIST, -1)
