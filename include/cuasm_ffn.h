@@ -132,7 +132,12 @@ typedef enum {
     CUASM_OPT_L2_PERSIST = 14 /* DEVICE-WIDE (cudaDeviceSetLimit): bytes of L2 set aside for
                                persisting lines -- the x tiles' TMA loads carry an
                                evict_last hint (CUASM_OPT_L2_POLICY); 0 = none (default).
-                               Affects every kernel on the device                     */
+                               Affects every kernel on the device                     */,
+    CUASM_OPT_MCAST = 15      /* fused FFN, 2-SM bf16: 1 = 4-CTA clusters of two CTA pairs on
+                               two vertically adjacent 256-row tiles of one n-block; the
+                               pair-0 CTAs TMA-load each W13 half once and multicast it into
+                               both pairs' shared memory (.multicast::cluster); whole tiles
+                               only (no stream-K, no dynamic claiming).  0 = off (default) */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with

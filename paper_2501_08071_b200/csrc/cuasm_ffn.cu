@@ -102,6 +102,8 @@ struct cuasm_ffn_s {
     uint32_t* dyn = nullptr;
     int dynamic = 0;   // CUASM_OPT_DYNAMIC: 0 auto, 1 off, 2 on
     int rs_bf16 = 0;   // CUASM_OPT_RS_PARTIAL: 0 fp32 partials, 1 bf16
+    int mcast = 0;     // CUASM_OPT_MCAST: 1 = 4-CTA multicast clusters for 2-SM SwiGLU whole tiles
+    int mcast_clusters = 0;  // co-resident 4-CTA clusters found at the last multicast launch
     int64_t l2_persist = 0;  // CUASM_OPT_L2_PERSIST: the device's persisting-L2 set-aside this handle made
     // a1 workspace
     float* r = nullptr;
@@ -542,6 +544,80 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
             csplit = 0;
             p.csplit = 0;
             p.rep = rep_plain;
+        }
+    }
+    // 4-CTA multicast clusters (CUASM_OPT_MCAST, DESIGN.md §6 "Multicast clusters"): two CTA pairs
+    // per cluster on two vertically adjacent tiles of one n-block, the W13 halves loaded once and
+    // multicast to both; whole tiles only (super-tiles of 512 rows round-robin over the clusters)
+    if constexpr (kDynBuilt && kEpi == 0) {
+        if (h->mcast && !csplit && p.num_m_blk >= 2) {
+            static std::atomic<uint64_t> attr_done_mc{0};
+            st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, true>, attr_done_mc,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES,
+                                  "cudaFuncSetAttribute(smem)");
+            if (st != CUASM_OK) return st;
+            p.num_m_blk = (p.num_m_blk + 1) / 2;  // super-rows of two 256-row tiles
+            p.group_m = std::max(1, std::min((p.group_m + 1) / 2, p.num_m_blk));
+            p.num_tiles = p.num_m_blk * p.num_n_blk;
+            // clusters are placed inside one GPC: fewer 4-CTA clusters than sm_count / 4 may fit at
+            // once, and a persistent grid must not exceed what is co-resident (a late cluster would
+            // run its share after everybody else)
+            int fit4 = h->sm_count / 4;
+            {
+                cudaLaunchConfig_t qc = {};
+                qc.gridDim = dim3(static_cast<unsigned>(4 * fit4), 1, 1);
+                qc.blockDim = dim3(C::NUM_THREADS, 1, 1);
+                qc.dynamicSmemBytes = C::SMEM_BYTES;
+                cudaLaunchAttribute qa;
+                qa.id = cudaLaunchAttributeClusterDimension;
+                qa.val.clusterDim.x = 4;
+                qa.val.clusterDim.y = 1;
+                qa.val.clusterDim.z = 1;
+                qc.attrs = &qa;
+                qc.numAttrs = 1;
+                int active = 0;
+                if (cudaOccupancyMaxActiveClusters(&active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, true>,
+                                                   &qc) == cudaSuccess && active > 0)
+                    fit4 = std::min(fit4, active);
+                (void)cudaGetLastError();
+            }
+            h->mcast_clusters = fit4;
+            const int clusters4 = std::min(p.num_tiles, fit4);
+            p.num_clusters = clusters4;
+            p.num_dp_tiles = p.num_tiles;
+            p.sk_iters = 0;
+            p.ws = h->ws;
+            p.flags = h->flags;
+            p.dyn = nullptr;
+            p.trace = nullptr;
+            if (h->trace) {
+                p.trace = h->trace_buf;
+                h->trace_ctas = clusters4 * 4;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(clusters4 * 4), 1, 1);
+            cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
+            cfg.dynamicSmemBytes = C::SMEM_BYTES;
+            cfg.stream = s;
+            cudaLaunchAttribute attrs[2];
+            int na = 0;
+            attrs[na].id = cudaLaunchAttributeClusterDimension;
+            attrs[na].val.clusterDim.x = 4;
+            attrs[na].val.clusterDim.y = 1;
+            attrs[na].val.clusterDim.z = 1;
+            ++na;
+            if (h->use_pdl && !h->profile) {
+                attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attrs[na].val.programmaticStreamSerializationAllowed = 1;
+                ++na;
+            }
+            cfg.attrs = attrs;
+            cfg.numAttrs = na;
+            CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, true>,
+                                              tmap_x, w.tmap, omaps, omaps_h, p),
+                        "ffn_dual_gemm_kernel launch (multicast clusters)");
+            h->last_variant = CUASM_VARIANT_2SM;
+            return CUASM_OK;
         }
     }
     const int max_clusters = h->sm_count / kCtaGroup;
@@ -1456,6 +1532,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         h->l2_persist = value;
         return CUASM_OK;
     }
+    case CUASM_OPT_MCAST:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "MCAST is 0 or 1");
+        h->mcast = static_cast<int>(value);
+        return CUASM_OK;
     case CUASM_OPT_RS_PARTIAL:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "RS_PARTIAL is 0 (fp32) or 1 (bf16)");
         h->rs_bf16 = static_cast<int>(value);

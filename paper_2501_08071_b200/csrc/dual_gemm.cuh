@@ -931,7 +931,10 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
 // kDyn: dynamic whole-tile claiming compiled in (p.dyn must be null otherwise); a kernel
 // template parameter rather than a runtime branch so the static kernels' loops are exactly
 // the uniform code they were (DESIGN.md §6 "Dynamic tiles").
-template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false>
+// kMcast (2-SM only): 4-CTA clusters of two CTA pairs computing two vertically adjacent
+// 256-row tiles of the same n-block; the pair-0 CTAs TMA-load each W13 half once and multicast
+// it into both pairs' shared memory (DESIGN.md §6 "Multicast clusters").  Whole tiles only.
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false, bool kMcast = false>
 __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                          const __grid_constant__ OutMaps omaps, const __grid_constant__ OutMaps omaps_h,
@@ -957,8 +960,13 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
 
     const uint32_t warp = ptx::warp_id_uniform();
     const uint32_t lane = ptx::lane_id();
-    const uint32_t cta_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;
+    static_assert(!kMcast || (kCtaGroup == 2 && !kDyn), "multicast clusters: 2-SM static kernels");
+    const uint32_t cl_rank = kCtaGroup == 2 ? ptx::cluster_ctarank() : 0;  // rank in the cluster
+    const uint32_t cta_rank = kMcast ? (cl_rank & 1u) : cl_rank;          // rank in the CTA pair
+    const int pair_id = kMcast ? static_cast<int>(cl_rank >> 1) : 0;      // pair in a multicast cluster
     const bool leader = cta_rank == 0;
+    // the tile of this pair inside a multicast cluster's super-tile (m-block pair x n-block)
+    auto pair_mb = [&](int mb) { return kMcast ? mb * 2 + pair_id : mb; };
     const bool csplit = C::kDecodePaths && kCtaGroup == 1 && p.csplit > 0;
     const int rep = C::kDecodePaths ? p.rep : 0;  // decode-shape row replication (BN = 128 / 64)
     const uint32_t part = csplit ? ptx::cluster_ctarank() : 0;  // split-K share of the cluster's tile
@@ -971,7 +979,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             // 2-SM: only the leader's producer arrives (expect_tx of BOTH
             // CTAs' bytes); the peer's TMA bytes are credited to it too.
             ptx::mbar_init(ptx::smem_u32(&full_bar[s]), 1);
-            ptx::mbar_init(ptx::smem_u32(&empty_bar[s]), 1);
+            ptx::mbar_init(ptx::smem_u32(&empty_bar[s]), kMcast ? 2 : 1);  // (multicast: both pairs' MMAs)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(ptx::smem_u32(&tfull_bar[a]), 1);
@@ -1006,7 +1014,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
 
     // Cluster-level work: both CTAs of a pair (every CTA of a split-K cluster) walk
     // the same tile sequence.
-    const int cluster_id = csplit ? static_cast<int>(blockIdx.x) / p.csplit : static_cast<int>(blockIdx.x) / kCtaGroup;
+    const int cluster_id = csplit ? static_cast<int>(blockIdx.x) / p.csplit
+                                  : static_cast<int>(blockIdx.x) / (kMcast ? 4 : kCtaGroup);
 
     if (warp == 0) {
         // ========================= TMA producer =========================
@@ -1029,7 +1038,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             } else {
                 // both CTAs' bytes land on the leader's barrier
                 if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (rep ? rep + 1 : 2) * p.a_box_bytes);
-                ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
+                if constexpr (kMcast) {
+                    // pair 0 loads each W13 half once for both pairs (same n-block)
+                    if (pair_id == 0)
+                        ptx::tma_load_2d_2sm_mc(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS,
+                                                static_cast<uint16_t>((1u << cl_rank) | (1u << (cl_rank + 2))), pol_w);
+                } else {
+                    ptx::tma_load_2d_2sm(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
+                }
             }
         };
         // the x rows of stage s (rep: <= 32 rows copied into every 32-row quarter; 2-SM: the
@@ -1061,6 +1077,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
             if (s0.next(g0)) {
                 int mb0, nb0;
                 tile_coords(g0.tile, p, mb0, nb0);
+                mb0 = pair_mb(mb0);
                 const int row_b0 = C::b_row0(nb0, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
                 pre = min(C::STAGES, g0.kb1 - g0.kb0);
                 if (ptx::elect_one()) {
@@ -1092,6 +1109,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         while (sch.next(sg)) {
             int mb, nb;
             tile_coords(sg.tile, p, mb, nb);
+            mb = pair_mb(mb);
             const int row_a = mb * C::TILE_M + static_cast<int>(cta_rank) * C::BM;
             // k-block-tiled weights (pack.cuh): box (nb, kb) starts at row (nb*KB + kb)*UMMA_N
             const int row_b0 = C::b_row0(nb, p.num_k_blk) + static_cast<int>(cta_rank) * C::B_ROWS;
@@ -1183,7 +1201,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                         if constexpr (kCtaGroup == 1) {
                             ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
                         } else {
-                            ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), 0x3);
+                            // (multicast clusters: every CTA's stage also holds the other pair's W13)
+                            ptx::mma_commit_2sm(ptx::smem_u32(&empty_bar[stage]), kMcast ? 0xF : 0x3);
                         }
                     }
                     __syncwarp();
@@ -1194,7 +1213,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                     if constexpr (kCtaGroup == 1) {
                         ptx::mma_commit(ptx::smem_u32(&tfull_bar[acc]));
                     } else {
-                        ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), 0x3);
+                        ptx::mma_commit_2sm(ptx::smem_u32(&tfull_bar[acc]), static_cast<uint16_t>(0x3u << (2 * pair_id)));
                     }
                 }
                 __syncwarp();
@@ -1345,6 +1364,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
         for (; sch.next(sg); ++it) {
             int mb, nb;
             tile_coords(sg.tile, p, mb, nb);
+            mb = pair_mb(mb);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             // rep: quadrant `quad` holds rows 0..31 of the tile (lane = row), and only its
@@ -1603,7 +1623,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
                 if constexpr (kCtaGroup == 1) {
                     ptx::mbar_arrive(ptx::smem_u32(&tempty_bar[acc]));
                 } else {
-                    ptx::mbar_arrive_cluster(ptx::smem_u32(&tempty_bar[acc]), 0);
+                    ptx::mbar_arrive_cluster(ptx::smem_u32(&tempty_bar[acc]), static_cast<uint32_t>(2 * pair_id));
                 }
             }
             if (contributor) {

@@ -120,6 +120,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const void* tmap, 
         : "memory");
 }
 
+// 2-SM TMA load multicast to the CTAs in `mask` (4-CTA clusters of two CTA pairs): the box
+// lands at the same shared-memory offset in every destination CTA and its bytes are credited
+// to the barrier of each destination's pair leader (peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0,
+                                                   int32_t c1, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
+
 // 2-D TMA store shared -> global (bulk group completion).
 __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int32_t c0, int32_t c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -171,3 +171,31 @@ def test_decode_paths_bn64(cuda_device, M, K, N, csplit):
     assert torch.equal(out, again), "bitwise run-to-run"
     ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16")
     check(out, ref, f"bn=64 1sm csplit={csplit} {M}x{K}x{N}")
+
+
+# ---- 4-CTA multicast clusters (CUASM_OPT_MCAST) ----
+@pytest.mark.parametrize("bn", [128, 120, 80])
+@pytest.mark.parametrize("M,K,N", [(512, 1024, 1000), (300, 512, 520), (1100, 2048, 2064), (2048, 4096, 1376)])
+def test_multicast_clusters(cuda_device, bn, M, K, N):
+    """Two CTA pairs per cluster on vertically adjacent tiles, W13 halves multicast: equal to
+    the default kernel bitwise (whole tiles, same k-order per tile; an odd count of 256-row
+    tiles leaves the second pair of the last super-row on rows past M) and to the oracle."""
+    d = make_inputs(M, K, N, family="C", seed=8800 + M + bn, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    h0 = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h0.set_option(ffn.OPT_TILE_BN, bn)
+    h0.set_variant(ffn.VARIANT_2SM)
+    h0.set_option(ffn.OPT_SCHEDULE, ffn.SCHEDULE_DATA_PARALLEL)
+    ref_gpu = h0.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_option(ffn.OPT_TILE_BN, bn)
+    h.set_variant(ffn.VARIANT_2SM)
+    h.set_option(ffn.OPT_MCAST, 1)
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    again = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref_gpu), "multicast clusters changed the result"
+    assert torch.equal(out, again)
+    rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 12)))))
+    check(out[rows], oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows),
+          f"mcast bn={bn} {M}x{K}x{N}")
