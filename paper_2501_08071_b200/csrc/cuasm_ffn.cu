@@ -855,6 +855,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
         const double tile_frac = out_cols == 128 ? bn_frac(bn) : (tn == 256 ? 1.0 : 0.72);
         const int64_t nblk_w = (N + oc - 1) / oc;
         for (int cg = 2; cg >= 1; --cg) {
+            // (the 1-SM kernel is shared-memory-bandwidth bound: a narrower tile issues no faster
+            // per byte -- M = 288..384, 1-SM 120-wide 61.4-63.5 us vs 128-wide 61.1-61.4)
             if (bn != kPackBN && cg == 1) continue;
             const int64_t units = sm_count / cg;
             const int64_t mblk = (M + 128 * cg - 1) / (128 * cg);
@@ -892,8 +894,8 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
     Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
                               out_cols == 128 ? h->tile_bn : 0);
-    // a forced 1-SM variant (CUASM_OPT_VARIANT) has the 128- and 64-output SwiGLU tiles
-    if (h->variant == CUASM_VARIANT_1SM && pl.bn != 64) pl.bn = kPackBN;
+    // a forced 1-SM variant (CUASM_OPT_VARIANT) has the 128-, 120- and 64-output SwiGLU tiles
+    if (h->variant == CUASM_VARIANT_1SM && pl.bn != 64 && pl.bn != 120) pl.bn = kPackBN;
     return pl;
 }
 
@@ -981,6 +983,11 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
         if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
             return fail(h, CUASM_ERR_UNSUPPORTED, "tile width 64 needs the bf16 kernel");
         st = launch_gemm<0, 1, 0, 128>(h, e, x, out, M, K, N, eps, s);
+    } else if (kepi == 0 && plan.bn == 120 && v == CUASM_VARIANT_1SM) {
+        // the 1-SM 120-output tile (forced only: measured no faster than 128 on the 1-SM kernel)
+        if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
+            return fail(h, CUASM_ERR_UNSUPPORTED, "tile width 120 needs the bf16 kernel");
+        st = launch_gemm<0, 1, 0, 240>(h, e, x, out, M, K, N, eps, s);
     } else if (kepi == 0 && plan.bn != kPackBN) {
         // narrower SwiGLU tiles (2-SM bf16 only; ffn_common packed slot 2 for this width)
         if (h->dtype != CUASM_DTYPE_BF16 || v != CUASM_VARIANT_2SM || e.slot != w13_slot(plan.bn))

@@ -199,3 +199,19 @@ def test_multicast_clusters(cuda_device, bn, M, K, N):
     rows = sorted(set([0, M - 1] + list(range(0, M, max(1, M // 12)))))
     check(out[rows], oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows),
           f"mcast bn={bn} {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("schedule", [ffn.SCHEDULE_DATA_PARALLEL, ffn.SCHEDULE_STREAM_K_ALL])
+@pytest.mark.parametrize("M,K,N", [(384, 1024, 11008 // 4), (300, 512, 3 * 120 + 24), (16, 256, 240)])
+def test_one_sm_bn120(cuda_device, schedule, M, K, N):
+    """The 1-SM kernel with 120-output tiles (24-wide last unit) under whole tiles and stream-K."""
+    d = make_inputs(M, K, N, family="C", seed=8900 + M + schedule, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    h.set_option(ffn.OPT_TILE_BN, 120)
+    h.set_variant(ffn.VARIANT_1SM)
+    h.set_option(ffn.OPT_SCHEDULE, schedule)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert h.last_launch()[0] == ffn.VARIANT_1SM
+    check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), f"1sm bn120 {M}x{K}x{N}")
