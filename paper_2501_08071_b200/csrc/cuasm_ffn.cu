@@ -439,7 +439,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // with a persisting-L2 set-aside that holds all of x (CUASM_OPT_L2_PERSIST; x loads are
     // evict_last), one group of every m-block reads each W13 block from HBM once: 70B FFN
     // 2.54 -> 1.55 GB of DRAM traffic per launch (profiles/r02/l2_persist/)
-    if (h->group_m == 0 && h->l2_persist > 0 && M * K * h->esize * 10 <= h->l2_persist * 9)
+    if (h->group_m == 0 && h->l2_persist > 0 && M * K * h->esize * 20 <= h->l2_persist * 19)
         p.group_m = std::numeric_limits<int>::max();
     p.group_m = std::max(1, std::min(p.group_m, p.num_m_blk));
     p.num_tiles = p.num_m_blk * p.num_n_blk;
