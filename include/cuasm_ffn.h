@@ -137,7 +137,13 @@ typedef enum {
                                two vertically adjacent 256-row tiles of one n-block; the
                                pair-0 CTAs TMA-load each W13 half once and multicast it into
                                both pairs' shared memory (.multicast::cluster); whole tiles
-                               only (no stream-K, no dynamic claiming).  0 = off (default) */
+                               only (no stream-K, no dynamic claiming).  0 = off (default) */,
+    CUASM_OPT_THIN_A = 16     /* decode shards on 64-output tiles with the cluster split-K
+                               (M <= 32): 1 = pipeline stages hold 32 A rows instead of
+                               128 (4 KB instead of 16 KB), so more stages of weights are
+                               in flight per SM; 0 (default) = full A stages (the deeper
+                               pipeline measured no faster: the decode shards are bound
+                               by fixed latencies, not by bytes in flight)            */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with

@@ -33,7 +33,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 ACT_IDENTITY, ACT_LEAKY_RELU = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC, OPT_RS_PARTIAL, OPT_L2_PERSIST, OPT_MCAST = range(16)
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC, OPT_RS_PARTIAL, OPT_L2_PERSIST, OPT_MCAST, OPT_THIN_A = range(17)
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL, SCHEDULE_STREAM_K_TAIL = 0, 1, 2, 3
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).

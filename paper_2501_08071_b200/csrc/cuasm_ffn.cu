@@ -103,6 +103,8 @@ struct cuasm_ffn_s {
     int dynamic = 0;   // CUASM_OPT_DYNAMIC: 0 auto, 1 off, 2 on
     int rs_bf16 = 0;   // CUASM_OPT_RS_PARTIAL: 0 fp32 partials, 1 bf16
     int mcast = 0;     // CUASM_OPT_MCAST: 1 = 4-CTA multicast clusters for 2-SM SwiGLU whole tiles
+    int thin = 0;      // CUASM_OPT_THIN_A: 1 = thin A stages for 64-wide decode split-K tiles (measured
+                       // no faster: 16 x 4096 x 1376 16.57 vs 16.40 us, 16 x 4096 x 2752 18.51 vs 19.55)
     int mcast_clusters = 0;  // co-resident 4-CTA clusters found at the last multicast launch
     int64_t l2_persist = 0;  // CUASM_OPT_L2_PERSIST: the device's persisting-L2 set-aside this handle made
     // a1 workspace
@@ -374,10 +376,10 @@ inline int auto_group_m(int64_t K, int esize, int cta_group) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(32) << 20) / per_mblk)));
 }
 
-template <int kKind, int kCtaGroup, int kEpi, int kN>
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kThin = false>
 cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
                            int64_t N, float eps, cudaStream_t s) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>;
     PackedWeights& w = h->pw[e.slot];
     CUtensorMap tmap_x;
     // A single row block with fewer than BM rows loads only the rows that exist
@@ -395,7 +397,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         const int64_t kbs = (K + C::BK - 1) / C::BK;
         if (want >= 2 && want <= 8 && tiles * want <= h->sm_count && kbs >= want && e.rs_world == 0) csplit = want;
     }
-    const int rep_plain = (kEpi != 0 || !C::kDecodePaths) ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
+    const int rep_plain = (kEpi != 0 || !C::kDecodePaths || kThin) ? 0 : M <= 32 ? 4 : M <= 64 ? 2 : 0;
     const int rep = csplit ? 0 : rep_plain;
     const uint32_t a_rows =
         ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
@@ -509,11 +511,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.csplit = csplit;
 
     static std::atomic<uint64_t> attr_done{0};  // per template instance, one bit per device
-    st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, attr_done,
+    st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>, attr_done,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES, "cudaFuncSetAttribute(smem)");
     if (st != CUASM_OK) return st;
     // dynamic tile claiming is compiled into the 2-SM bf16 kernels only (the long runs it is for)
-    constexpr bool kDynBuilt = kCtaGroup == 2 && kKind == 0;
+    constexpr bool kDynBuilt = kCtaGroup == 2 && kKind == 0 && !kThin;
     if constexpr (kDynBuilt) {
         static std::atomic<uint64_t> attr_done_dyn{0};
         st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, true>, attr_done_dyn,
@@ -537,7 +539,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         qc.attrs = &qa;
         qc.numAttrs = 1;
         int max_active = 0;
-        if (cudaOccupancyMaxActiveClusters(&max_active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, &qc) !=
+        if (cudaOccupancyMaxActiveClusters(&max_active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>, &qc) !=
                 cudaSuccess ||
             max_active < p.num_tiles) {
             (void)cudaGetLastError();
@@ -734,7 +736,8 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
             return CUASM_OK;
         }
     }
-    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN>, tmap_x, w.tmap,
+    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>,
+                                      tmap_x, w.tmap,
                                       omaps, omaps_h, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
@@ -982,7 +985,11 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
         // the 1-SM 64-output tile: decode shards (more, smaller tiles for the cluster split-K)
         if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
             return fail(h, CUASM_ERR_UNSUPPORTED, "tile width 64 needs the bf16 kernel");
-        st = launch_gemm<0, 1, 0, 128>(h, e, x, out, M, K, N, eps, s);
+        // (decode rows with the planner's cluster split-K: thin A stages, more weight bytes in flight)
+        if (M <= 32 && (h->csplit_opt >= 2 || (h->csplit_opt == 0 && plan.csplit >= 2)) && h->thin != 0)
+            st = launch_gemm<0, 1, 0, 128, true>(h, e, x, out, M, K, N, eps, s);
+        else
+            st = launch_gemm<0, 1, 0, 128>(h, e, x, out, M, K, N, eps, s);
     } else if (kepi == 0 && plan.bn == 120 && v == CUASM_VARIANT_1SM) {
         // the 1-SM 120-output tile (forced only: measured no faster than 128 on the 1-SM kernel)
         if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
@@ -1539,6 +1546,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         h->l2_persist = value;
         return CUASM_OK;
     }
+    case CUASM_OPT_THIN_A:
+        if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "THIN_A is 0 or 1");
+        h->thin = static_cast<int>(value);
+        return CUASM_OK;
     case CUASM_OPT_MCAST:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "MCAST is 0 or 1");
         h->mcast = static_cast<int>(value);

@@ -380,7 +380,11 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 // columns [0, BN), h3 in [BN, 2BN); the epilogue walks 32-column units (the last one
 // 16 or 24 wide when BN % 32 is 16 or 24).  The decode paths (rep, cluster split-K) exist for BN = 128 and
 // BN = 64 (more, smaller tiles for the decode shards' weight streaming) and every GEMM tile.
-template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256>
+// kThin (1-SM decode tiles with <= 32 rows, cluster split-K): the A tile of a stage holds only 32
+// rows (4 KB instead of 16 KB), so ~1.5x more weight bytes stay in flight per SM; the MMA still
+// reads 128 A rows, the ones past 32 (the next stages' bytes) feeding accumulator lanes that are
+// never read.
+template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256, bool kThin = false>
 struct GemmCfg {
     static_assert(kEpi == 0 ? (kN % 16 == 0 && (kN / 2) % 8 == 0 && (kN / 2) % 32 != 8 && kN >= 128 && kN <= 256)
                             : (kN == 256 || kN == 128),
@@ -405,7 +409,7 @@ struct GemmCfg {
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
-    static constexpr int A_BYTES = BM * 128;                        // per CTA
+    static constexpr int A_BYTES = (kThin ? 32 : BM) * 128;         // per CTA
     static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // packed-weight rows loaded per CTA
     static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
@@ -420,7 +424,7 @@ struct GemmCfg {
 #ifdef CUASM_STAGE_CAP  // experiments only: cap the pipeline depth
     static constexpr int STAGES_CAP = CUASM_STAGE_CAP;
 #else
-    static constexpr int STAGES_CAP = 9;
+    static constexpr int STAGES_CAP = kThin ? 12 : 9;
 #endif
     static constexpr int STAGES = STAGES_FIT < STAGES_CAP ? STAGES_FIT : STAGES_CAP;
     static constexpr int TMEM_COLS = 2 * ACC_STRIDE;                // 2 accumulators (power of 2)
@@ -934,12 +938,13 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
 // kMcast (2-SM only): 4-CTA clusters of two CTA pairs computing two vertically adjacent
 // 256-row tiles of the same n-block; the pair-0 CTAs TMA-load each W13 half once and multicast
 // it into both pairs' shared memory (DESIGN.md §6 "Multicast clusters").  Whole tiles only.
-template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false, bool kMcast = false>
-__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREADS, 1)
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false, bool kMcast = false, bool kThin = false>
+__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                          const __grid_constant__ OutMaps omaps, const __grid_constant__ OutMaps omaps_h,
                          const FfnGemmParams p) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>;
+    static_assert(!kThin || (kCtaGroup == 1 && !kDyn && !kMcast), "thin A tiles: 1-SM decode kernels");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -968,7 +973,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN>::NUM_THREA
     // the tile of this pair inside a multicast cluster's super-tile (m-block pair x n-block)
     auto pair_mb = [&](int mb) { return kMcast ? mb * 2 + pair_id : mb; };
     const bool csplit = C::kDecodePaths && kCtaGroup == 1 && p.csplit > 0;
-    const int rep = C::kDecodePaths ? p.rep : 0;  // decode-shape row replication (BN = 128 / 64)
+    const int rep = (C::kDecodePaths && !kThin) ? p.rep : 0;  // decode-shape row replication (BN = 128 / 64)
     const uint32_t part = csplit ? ptx::cluster_ctarank() : 0;  // split-K share of the cluster's tile
 
     if (warp == 0 && lane == 0) {

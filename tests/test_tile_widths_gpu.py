@@ -215,3 +215,22 @@ def test_one_sm_bn120(cuda_device, schedule, M, K, N):
     torch.cuda.synchronize()
     assert h.last_launch()[0] == ffn.VARIANT_1SM
     check(out, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), f"1sm bn120 {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("M,K,N,S", [(16, 4096, 1376, 3), (1, 2048, 200, 2), (32, 4096, 2752, 3), (24, 8192, 640, 6)])
+def test_thin_a_stages_equal_full(cuda_device, M, K, N, S):
+    """CUASM_OPT_THIN_A: the decode split-K kernel with 32-row A stages (more weight stages in
+    flight) computes rows 0..M-1 exactly as the full-A kernel does -- bitwise -- and the oracle."""
+    d = make_inputs(M, K, N, family="C", seed=8950 + M + S, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    outs = []
+    for thin in (0, 1):
+        h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+        h.set_option(ffn.OPT_TILE_BN, 64)
+        h.set_variant(ffn.VARIANT_1SM)
+        h.set_option(ffn.OPT_CSPLIT, S)
+        h.set_option(ffn.OPT_THIN_A, thin)
+        outs.append(h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    check(outs[1], oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), f"thin {M}x{K}x{N} S={S}")
