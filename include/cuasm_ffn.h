@@ -143,7 +143,14 @@ typedef enum {
                                128 (4 KB instead of 16 KB), so more stages of weights are
                                in flight per SM; 0 (default) = full A stages (the deeper
                                pipeline measured no faster: the decode shards are bound
-                               by fixed latencies, not by bytes in flight)            */
+                               by fixed latencies, not by bytes in flight)            */,
+    CUASM_OPT_TALL = 17       /* fused FFN, bf16, 256 < M <= 384 (the crossover region):
+                               tall tiles -- one 80-output n-block over all rows, a
+                               256-row tcgen05.mma (M = 256) and a 128-row one (M = 128,
+                               cta_group::2) on the same weight stage, so each W13 block
+                               is streamed once (DESIGN.md §6 "Tall tiles").  0 = the
+                               configuration model decides (default), 1 = off, 2 = on
+                               whenever the shape allows                               */
 } cuasm_option_t;
 
 /* Persistent tile schedule of the dual GEMM (cuasm_ffn_set_option with
@@ -353,7 +360,8 @@ const char* cuasm_ffn_last_error(cuasm_ffn_t h);
  * cuasm_variant_t and in *stream_k bit 0 = stream-K tail used, bit 1 = the
  * 128-wide tile, bits 4..7 = the cluster split-K width (CTAs per tile, 0 =
  * none; see CUASM_OPT_CSPLIT), bits 8..15 = the SwiGLU outputs per tile BN
- * (see CUASM_OPT_TILE_BN).  Pure host code. */
+ * (see CUASM_OPT_TILE_BN), bit 2 = tall tiles (see CUASM_OPT_TALL).  Pure host
+ * code. */
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k);
 

@@ -33,7 +33,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 ACT_IDENTITY, ACT_LEAKY_RELU = 0, 1
 VARIANT_AUTO, VARIANT_1SM, VARIANT_2SM = 0, 1, 2
-OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC, OPT_RS_PARTIAL, OPT_L2_PERSIST, OPT_MCAST, OPT_THIN_A = range(17)
+OPT_VARIANT, OPT_PDL, OPT_GROUP_M, OPT_PROFILE, OPT_SCHEDULE, OPT_TRACE, OPT_FUSED_NORM, OPT_TILE_N, OPT_SK_SPLIT, OPT_L2_POLICY, OPT_CSPLIT, OPT_TILE_BN, OPT_DYNAMIC, OPT_RS_PARTIAL, OPT_L2_PERSIST, OPT_MCAST, OPT_THIN_A, OPT_TALL = range(18)
 SCHEDULE_AUTO, SCHEDULE_DATA_PARALLEL, SCHEDULE_STREAM_K_ALL, SCHEDULE_STREAM_K_TAIL = 0, 1, 2, 3
 
 # Every entry point include/cuasm_ffn.h declares (checked by tests/test_abi.py).
@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = (
 
 
 def plan_config(M: int, K: int, N: int, op: str = "ffn", dtype=torch.bfloat16, sm_count: int = 148):
-    """The library's configuration model: ("1sm" | "2sm", stream_k: bool, tile_n: 256 | 128,
+    """The library's configuration model: ("1sm" | "2sm" | "tall" (2-SM tall tiles), stream_k: bool, tile_n: 256 | 128,
     csplit: CTAs per tile of the cluster split-K, 0 = none, bn: SwiGLU outputs per tile)."""
     lib = load_library()
     v, sk = ctypes.c_int(), ctypes.c_int()
@@ -56,7 +56,8 @@ def plan_config(M: int, K: int, N: int, op: str = "ffn", dtype=torch.bfloat16, s
                                ctypes.byref(sk))
     if st != OK:
         raise CuasmError(st, "cuasm_plan_config: invalid arguments")
-    return (("1sm" if v.value == VARIANT_1SM else "2sm"), bool(sk.value & 1), (128 if sk.value & 2 else 256),
+    return (("1sm" if v.value == VARIANT_1SM else "tall" if sk.value & 4 else "2sm"), bool(sk.value & 1),
+            (128 if sk.value & 2 else 256),
             (sk.value >> 4) & 15, sk.value >> 8)
 
 

@@ -103,6 +103,7 @@ struct cuasm_ffn_s {
     int dynamic = 0;   // CUASM_OPT_DYNAMIC: 0 auto, 1 off, 2 on
     int rs_bf16 = 0;   // CUASM_OPT_RS_PARTIAL: 0 fp32 partials, 1 bf16
     int mcast = 0;     // CUASM_OPT_MCAST: 1 = 4-CTA multicast clusters for 2-SM SwiGLU whole tiles
+    int tall = 0;      // CUASM_OPT_TALL: 0 auto, 1 off, 2 on where the shape allows
     int thin = 0;      // CUASM_OPT_THIN_A: 1 = thin A stages for 64-wide decode split-K tiles (measured
                        // no faster: 16 x 4096 x 1376 16.57 vs 16.40 us, 16 x 4096 x 2752 18.51 vs 19.55)
     int mcast_clusters = 0;  // co-resident 4-CTA clusters found at the last multicast launch
@@ -376,10 +377,14 @@ inline int auto_group_m(int64_t K, int esize, int cta_group) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(32) << 20) / per_mblk)));
 }
 
-template <int kKind, int kCtaGroup, int kEpi, int kN, bool kThin = false>
+// kTall: tall tiles (dual_gemm.cuh GemmCfg; 257..384 rows, 2-SM bf16 SwiGLU, whole tiles)
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kThin = false, bool kTall = false>
 cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void* out, int64_t M, int64_t K,
                            int64_t N, float eps, cudaStream_t s) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>;
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin, kTall>;
+    static_assert(!kTall || kEpi == 0, "tall tiles: fused FFN");
+    if (kTall && (M <= 256 || M > C::TILE_M))
+        return fail(h, CUASM_ERR_UNSUPPORTED, "tall tiles need 256 < M <= %d", C::TILE_M);
     PackedWeights& w = h->pw[e.slot];
     CUtensorMap tmap_x;
     // A single row block with fewer than BM rows loads only the rows that exist
@@ -403,6 +408,13 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         ((kCtaGroup == 1 || rep) && M < C::BM) ? static_cast<uint32_t>((M + 7) / 8 * 8) : C::BM;
     cuasm_status_t st = encode_2d(h, &tmap_x, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, a_rows);
     if (st != CUASM_OK) return st;
+    // tall tiles: x again with 64-row boxes (the 128-row part's rows per CTA); the other kernels
+    // take tmap_x in this slot and never use it
+    CUtensorMap tmap_xh = tmap_x;
+    if constexpr (kTall) {
+        st = encode_2d(h, &tmap_xh, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), C::BK, C::HALF_ROWS);
+        if (st != CUASM_OK) return st;
+    }
     if (w.tmap_rows != C::B_ROWS) {
         st = encode_2d(h, &w.tmap, w.buf, static_cast<uint64_t>(C::BK), static_cast<uint64_t>(w.rows), C::BK,
                        C::B_ROWS);
@@ -511,11 +523,11 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     p.csplit = csplit;
 
     static std::atomic<uint64_t> attr_done{0};  // per template instance, one bit per device
-    st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>, attr_done,
+    st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin, kTall>, attr_done,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES, "cudaFuncSetAttribute(smem)");
     if (st != CUASM_OK) return st;
     // dynamic tile claiming is compiled into the 2-SM bf16 kernels only (the long runs it is for)
-    constexpr bool kDynBuilt = kCtaGroup == 2 && kKind == 0 && !kThin;
+    constexpr bool kDynBuilt = kCtaGroup == 2 && kKind == 0 && !kThin && !kTall;
     if constexpr (kDynBuilt) {
         static std::atomic<uint64_t> attr_done_dyn{0};
         st = ensure_func_attr(h, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, true>, attr_done_dyn,
@@ -539,7 +551,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
         qc.attrs = &qa;
         qc.numAttrs = 1;
         int max_active = 0;
-        if (cudaOccupancyMaxActiveClusters(&max_active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>, &qc) !=
+        if (cudaOccupancyMaxActiveClusters(&max_active, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin, kTall>, &qc) !=
                 cudaSuccess ||
             max_active < p.num_tiles) {
             (void)cudaGetLastError();
@@ -616,7 +628,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
             cfg.attrs = attrs;
             cfg.numAttrs = na;
             CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, true>,
-                                              tmap_x, w.tmap, omaps, omaps_h, p),
+                                              tmap_x, w.tmap, tmap_xh, omaps, omaps_h, p),
                         "ffn_dual_gemm_kernel launch (multicast clusters)");
             h->last_variant = CUASM_VARIANT_2SM;
             return CUASM_OK;
@@ -633,7 +645,7 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     // Stream-K only where plan_config's cost model says the balanced tail is
     // worth the partial fixup (e.g. 7B prefill: 9.3 waves; not decode, where
     // whole tiles already saturate HBM).
-    const bool sk_ok = !csplit && (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
+    const bool sk_ok = !kTall && !csplit && (h->schedule == CUASM_SCHEDULE_STREAM_K_ALL ||
                                    h->schedule == CUASM_SCHEDULE_STREAM_K_TAIL ||
                                    (h->schedule == CUASM_SCHEDULE_AUTO && h->plan_sk));
     if (sk_ok && p.num_k_blk > 1) {
@@ -730,15 +742,14 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
     if constexpr (kDynBuilt) {
         if (p.dyn) {
             CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, true>, tmap_x,
-                                              w.tmap, omaps, omaps_h, p),
+                                              w.tmap, tmap_xh, omaps, omaps_h, p),
                         "ffn_dual_gemm_kernel launch");
             h->last_variant = CUASM_VARIANT_2SM;
             return CUASM_OK;
         }
     }
-    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin>,
-                                      tmap_x, w.tmap,
-                                      omaps, omaps_h, p),
+    CUASM_CHECK(h, cudaLaunchKernelEx(&cfg, cuasm::ffn_dual_gemm_kernel<kKind, kCtaGroup, kEpi, kN, false, false, kThin, kTall>,
+                                      tmap_x, w.tmap, tmap_xh, omaps, omaps_h, p),
                 "ffn_dual_gemm_kernel launch");
     h->last_variant = kCtaGroup == 1 ? CUASM_VARIANT_1SM : CUASM_VARIANT_2SM;
     return CUASM_OK;
@@ -760,7 +771,12 @@ struct Plan {
     int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
     int csplit;  // cluster split-K: CTAs per tile (1-SM variant), 0 = none
     int bn = kPackBN;  // SwiGLU outputs per tile (MMA N = 2 bn): 128, or 64..112 (2-SM bf16)
+    bool tall = false; // tall tiles (2-SM bf16, bn = kTallBN, 256 < M <= 384, whole tiles)
 };
+
+// Tall tiles (dual_gemm.cuh GemmCfg kTall): one kTallBN-output n-block over up to 384 rows.
+constexpr int kTallBN = 80;
+constexpr int64_t kTallMaxM = 384;
 
 // Time of one k-block of a 2-SM SwiGLU tile of width bn relative to bn = 128, measured
 // (scripts/tune_bn.py, profiles/r02/tune_bn.json): at full size the narrower tiles run at
@@ -774,7 +790,7 @@ inline double bn_frac(int bn) {
 }
 
 Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K, int64_t N, int64_t out_cols,
-                     int tile_n_force = 0, int tile_bn_force = 0) {
+                     int tile_n_force = 0, int tile_bn_force = 0, int tall_opt = 0) {
     const double t_kb = 0.37e-6, fixup = 10e-6, hbm = 6.5e12, pen_1sm = 1.16;
     const int64_t BK = 128 / esize;
     const double KB = static_cast<double>((K + BK - 1) / BK);
@@ -789,6 +805,10 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // (up to twice as many tiles, M <= 512: split two ways; 16 x 4096 x 5504: 30.7 vs
     // 32.8 us, 512 x 4096 x 1376: 28.8 vs 30.7 us)
     const int64_t tiles_1sm = ((M + 127) / 128) * nblk;
+    // tall tiles (256 < M <= 384, bf16 SwiGLU): forced on, or a candidate of the cost model below
+    const bool tall_ok = out_cols == 128 && esize == 2 && M > 256 && M <= kTallMaxM && tall_opt != 1 &&
+                         (tile_bn_force == 0 || tile_bn_force == kTallBN);
+    if (tall_ok && tall_opt == 2) return Plan{CUASM_VARIANT_2SM, false, 256, 0, kTallBN, true};
     // (a forced SwiGLU width below 128 has no decode paths: straight to the cost model)
     const bool narrow_forced = out_cols == 128 && tile_bn_force != 0 && tile_bn_force != kPackBN;
     // Decode shards (M <= 32, up to 2 * kFewTiles tiles): split each tile's k-loop over a
@@ -891,12 +911,25 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
             if (K / BK > 1 && t_sk < best_t * 0.98) { best_t = t_sk; best = Plan{v, true, tn, 0, bn}; }
         }
     }
+    // Tall tiles: N / 80 n-blocks of 384 rows in whole rounds of the CTA pairs; a tall k-block (an
+    // 80-wide 256-row MMA + an 80-wide 128-row MMA on one weight stage) costs kTallFrac of a 128-wide
+    // 256-row k-block
+    if (tall_ok) {
+        constexpr double kTallFrac = 1.07;  // measured: 384 x 4096 x 11008 57.5 us vs 1-SM 128-wide 62.9 (scripts/tune_tall.py)
+        const int64_t units = sm_count / 2;
+        const int64_t tiles = (N + kTallBN - 1) / kTallBN;
+        const double rounds = static_cast<double>((tiles + units - 1) / units);
+        const double t_tall = std::max(hbm_floor, rounds * KB * t_kb * kTallFrac);
+        if (t_tall < best_t * 0.98) best = Plan{CUASM_VARIANT_2SM, false, 256, 0, kTallBN, true};
+    }
     return best;
 }
 
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
     Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
-                              out_cols == 128 ? h->tile_bn : 0);
+                              out_cols == 128 ? h->tile_bn : 0, h->tall);
+    // (tall tiles are a 2-SM kernel: a forced 1-SM variant takes the ordinary tiles)
+    if (pl.tall && h->variant == CUASM_VARIANT_1SM) pl = Plan{CUASM_VARIANT_1SM, false, 256, 0, kPackBN};
     // a forced 1-SM variant (CUASM_OPT_VARIANT) has the 128-, 120- and 64-output SwiGLU tiles
     if (h->variant == CUASM_VARIANT_1SM && pl.bn != 64 && pl.bn != 120) pl.bn = kPackBN;
     return pl;
@@ -981,7 +1014,12 @@ cuasm_status_t run_gemm(cuasm_ffn_t h, int kepi, const EpiSpec& e, const void* x
     const int v = h->variant != CUASM_VARIANT_AUTO ? h->variant : plan.variant;
     h->plan_sk = plan.stream_k;
     h->plan_csplit = v == plan.variant ? plan.csplit : 0;
-    if (kepi == 0 && plan.bn == 64 && v == CUASM_VARIANT_1SM) {
+    if (kepi == 0 && plan.tall) {
+        // tall tiles (257..384 rows, 80-wide n-blocks; ffn_common packed the 80-wide slot)
+        if (h->dtype != CUASM_DTYPE_BF16 || v != CUASM_VARIANT_2SM || e.slot != w13_slot(plan.bn))
+            return fail(h, CUASM_ERR_UNSUPPORTED, "tall tiles need the 2-SM bf16 kernel");
+        st = launch_gemm<0, 2, 0, 2 * kTallBN, false, true>(h, e, x, out, M, K, N, eps, s);
+    } else if (kepi == 0 && plan.bn == 64 && v == CUASM_VARIANT_1SM) {
         // the 1-SM 64-output tile: decode shards (more, smaller tiles for the cluster split-K)
         if (h->dtype != CUASM_DTYPE_BF16 || e.slot != w13_slot(plan.bn))
             return fail(h, CUASM_ERR_UNSUPPORTED, "tile width 64 needs the bf16 kernel");
@@ -1114,7 +1152,7 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
         return CUASM_ERR_INVALID_ARG;
     const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
     *variant = pl.variant;
-    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.csplit << 4) | (pl.bn << 8);
+    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.tall ? 4 : 0) | (pl.csplit << 4) | (pl.bn << 8);
     return CUASM_OK;
 }
 
@@ -1546,6 +1584,10 @@ cuasm_status_t cuasm_ffn_set_option(cuasm_ffn_t h, int option, int64_t value) {
         h->l2_persist = value;
         return CUASM_OK;
     }
+    case CUASM_OPT_TALL:
+        if (value < 0 || value > 2) return fail(h, CUASM_ERR_INVALID_ARG, "TALL is 0 (auto), 1 (off) or 2 (on)");
+        h->tall = static_cast<int>(value);
+        return CUASM_OK;
     case CUASM_OPT_THIN_A:
         if (value != 0 && value != 1) return fail(h, CUASM_ERR_INVALID_ARG, "THIN_A is 0 or 1");
         h->thin = static_cast<int>(value);

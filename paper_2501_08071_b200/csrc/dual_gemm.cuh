@@ -384,14 +384,26 @@ __device__ __forceinline__ void wait_flag(const uint32_t* f) {
 // rows (4 KB instead of 16 KB), so ~1.5x more weight bytes stay in flight per SM; the MMA still
 // reads 128 A rows, the ones past 32 (the next stages' bytes) feeding accumulator lanes that are
 // never read.
-template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256, bool kThin = false>
+// kTall (2-SM bf16 SwiGLU, DESIGN.md §6 "Tall tiles"): a tile is one n-block over 384 rows -- a
+// 256-row part (tcgen05.mma M = 256, rows 128 c.. of CTA c) and a 128-row part (M = 128 with
+// cta_group::2: 64 rows per CTA, rows 256 + 64 c..) issued back to back on the SAME weight stage,
+// so a W13 block is streamed once for all 257..384 rows of the crossover region (M = 288..384 at
+// K = 4096, N = 11008) instead of padding them to two 256-row tiles or running 1-SM tiles.  The
+// 128-row part's accumulator sits UMMA_N columns after the 256-row one; its D layout folds the
+// 64 rows x UMMA_N columns into 128 lanes x UMMA_N / 2 columns (MMA columns [BN, 2BN) -- the W3g
+// half -- in lanes 64..127), so its h1 and h3 meet in shared memory (epilogue, "half part").
+template <int kKind, int kCtaGroup, int kEpi = 0, int kN = 256, bool kThin = false, bool kTall = false>
 struct GemmCfg {
     static_assert(kEpi == 0 ? (kN % 16 == 0 && (kN / 2) % 8 == 0 && (kN / 2) % 32 != 8 && kN >= 128 && kN <= 256)
                             : (kN == 256 || kN == 128),
                   "SwiGLU tiles: kN = 2*BN, BN in {64, 80, 96, 112, 120, 128}; GEMM tiles 128 or 256");
+    static_assert(!kTall || (kKind == 0 && kCtaGroup == 2 && kEpi == 0 && !kThin && kN + kN / 2 <= 256),
+                  "tall tiles: 2-SM bf16 SwiGLU, both accumulators within one 256-column TMEM buffer");
     static constexpr int kEsize = kKind == 0 ? 2 : 4;
     static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
-    static constexpr int TILE_M = BM * kCtaGroup;  // rows per MMA tile
+    static constexpr int TILE_M = kTall ? 384 : BM * kCtaGroup;  // rows per tile
+    static constexpr int HALF_ROW0 = 256;          // kTall: first row of the 128-row part
+    static constexpr int HALF_ROWS = 64;           // kTall: rows of the 128-row part per CTA
     static constexpr int UMMA_N = kN;
     static constexpr int BN = kN / 2;              // SwiGLU: outputs per tile (h1 | h3 halves)
     static constexpr int OUT_COLS = kEpi == 0 ? BN : UMMA_N;  // output columns per tile
@@ -402,14 +414,16 @@ struct GemmCfg {
     static constexpr int NU = (BN + 31) / 32;
     static constexpr int EPI_ITERS = kEpi == 0 ? (NU + 1) / 2 : kN / 128;
     // TMEM column stride between the two accumulators (a power-of-two allocation)
-    static constexpr int ACC_STRIDE = kN > 128 ? 256 : 128;
+    static constexpr int ACC_STRIDE = (kN > 128 || kTall) ? 256 : 128;
     // stream-K partial slot per CTA, float4s: [32-column chunk][quad][8][32 lanes], whole chunks
     // (UMMA_N = 240 has a partial last chunk, still addressed at the chunk's full stride)
     static constexpr int WS_SLOT_F4 = BM * ((kN + 31) / 32 * 32) / 4;
     static constexpr int BK = 128 / kEsize;        // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / kEsize;     // K per tcgen05.mma
     static constexpr int KSTEPS = BK / UMMA_K;     // 4
-    static constexpr int A_BYTES = (kThin ? 32 : BM) * 128;         // per CTA
+    static constexpr int A_FULL_BYTES = (kThin ? 32 : BM) * 128;    // per CTA
+    static constexpr int A_HALF_BYTES = kTall ? HALF_ROWS * 128 : 0;  // kTall: the 128-row part's rows
+    static constexpr int A_BYTES = A_FULL_BYTES + A_HALF_BYTES;
     static constexpr int B_ROWS = UMMA_N / kCtaGroup;               // packed-weight rows loaded per CTA
     static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;           // per CTA
@@ -435,7 +449,8 @@ struct GemmCfg {
     static constexpr int PAIRS = UMMA_N / 128;
     static constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;     // 320
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;  // + align slack
-    static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, TILE_M, UMMA_N);
+    static constexpr uint32_t IDESC = ptx::make_idesc(kKind == 0 ? 1u : 2u, BM * kCtaGroup, UMMA_N);
+    static constexpr uint32_t IDESC_HALF = ptx::make_idesc(1u, 128, UMMA_N);  // kTall: M = 128, cta_group::2
     // Accumulator chunks (32 columns) of epilogue pair `i` of a warp in column half `half`.
     __device__ static constexpr int chunk_a(int half, int i) {
         return kEpi == 0 ? half * PAIRS + i : half * (UMMA_N / 64) + 2 * i;
@@ -938,13 +953,17 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
 // kMcast (2-SM only): 4-CTA clusters of two CTA pairs computing two vertically adjacent
 // 256-row tiles of the same n-block; the pair-0 CTAs TMA-load each W13 half once and multicast
 // it into both pairs' shared memory (DESIGN.md §6 "Multicast clusters").  Whole tiles only.
-template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false, bool kMcast = false, bool kThin = false>
-__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NUM_THREADS, 1)
+// kTall: tall tiles (GemmCfg), static whole tiles only; tmap_xh is x with 64-row boxes (the 128-row
+// part's rows per CTA), unused by the other kernels.
+template <int kKind, int kCtaGroup, int kEpi, int kN, bool kDyn = false, bool kMcast = false, bool kThin = false,
+          bool kTall = false>
+__global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin, kTall>::NUM_THREADS, 1)
     ffn_dual_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                         const __grid_constant__ OutMaps omaps, const __grid_constant__ OutMaps omaps_h,
-                         const FfnGemmParams p) {
-    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>;
+                         const __grid_constant__ CUtensorMap tmap_xh, const __grid_constant__ OutMaps omaps,
+                         const __grid_constant__ OutMaps omaps_h, const FfnGemmParams p) {
+    using C = GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin, kTall>;
     static_assert(!kThin || (kCtaGroup == 1 && !kDyn && !kMcast), "thin A tiles: 1-SM decode kernels");
+    static_assert(!kTall || (!kDyn && !kMcast), "tall tiles: static schedule, CTA pairs");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -980,6 +999,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
         trace_stamp(p, 0);
         ptx::prefetch_tmap(&tmap_x);
         ptx::prefetch_tmap(&tmap_w);
+        if constexpr (kTall) ptx::prefetch_tmap(&tmap_xh);
         for (int s = 0; s < C::STAGES; ++s) {
             // 2-SM: only the leader's producer arrives (expect_tx of BOTH
             // CTAs' bytes); the peer's TMA bytes are credited to it too.
@@ -1042,7 +1062,8 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
                 ptx::tma_load_2d(sb, &tmap_w, fb, 0, row_b0 + kb * C::PACK_ROWS, pol_w);
             } else {
                 // both CTAs' bytes land on the leader's barrier
-                if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (rep ? rep + 1 : 2) * p.a_box_bytes);
+                if (leader)
+                    ptx::mbar_arrive_expect_tx(fb, 2 * C::B_BYTES + (rep ? rep + 1 : 2) * p.a_box_bytes + 2 * C::A_HALF_BYTES);
                 if constexpr (kMcast) {
                     // pair 0 loads each W13 half once for both pairs (same n-block)
                     if (pair_id == 0)
@@ -1066,6 +1087,10 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
                 const int nrep = (rep && leader) ? rep : 1;
                 for (int q = 0; q < nrep; ++q)
                     ptx::tma_load_2d_2sm(sa + q * (128 / nrep) * 128, &tmap_x, fb, kb * C::BK, row_a, pol_x);
+                // kTall: this CTA's 64 rows of the 128-row part, behind its 128 rows of the 256-row part
+                if constexpr (kTall)
+                    ptx::tma_load_2d_2sm(sa + C::A_FULL_BYTES, &tmap_xh, fb, kb * C::BK,
+                                         C::HALF_ROW0 + static_cast<int>(cta_rank) * C::HALF_ROWS, pol_x);
             }
         };
         SchedT<kDyn> sch;
@@ -1202,6 +1227,11 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
                             // advance 32 bytes of K inside the 128-byte swizzle row (+2 in 16-byte units)
                             ptx::mma<kKind, kCtaGroup>(d_tmem, adesc + 2 * k, bdesc + 2 * k, C::IDESC,
                                                        (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                            // kTall: the 128-row part on the same weight stage (M = 128, its own
+                            // A rows behind the 256-row part's, accumulator UMMA_N columns on)
+                            if constexpr (kTall)
+                                ptx::mma<kKind, kCtaGroup>(d_tmem + C::UMMA_N, adesc + (C::A_FULL_BYTES >> 4) + 2 * k,
+                                                           bdesc + 2 * k, C::IDESC_HALF, (kb > sg.kb0 || k > 0) ? 1u : 0u);
                         }
                         if constexpr (kCtaGroup == 1) {
                             ptx::mma_commit(ptx::smem_u32(&empty_bar[stage]));
@@ -1420,6 +1450,7 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
             }
             if (fused && (csplit || !contributor)) {
                 acquire_r(csplit ? mb : mb * kCtaGroup + static_cast<int>(cta_rank));
+                if constexpr (kTall) acquire_r(C::HALF_ROW0 / C::BM);  // the 128-row part's rows
                 // the CTA's last r acquisition: count it past (the last CTA resets the state)
                 const bool dp_seg = !csplit && sg.tile < p.num_dp_tiles;
                 bool last;
@@ -1606,6 +1637,64 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin>::NU
                     unit(std::integral_constant<int, 32>{}, 32 * C::chunk_a(half, i), 32 * C::chunk_b(half, i));
                 }
                 CUASM_EPI_STAMP(13 + (i > 0 ? 1 : 0));
+            }
+            if constexpr (kTall) {
+                // The 128-row part (GemmCfg kTall): TMEM lanes 0..63 hold h1 of this CTA's 64 rows
+                // (lane = row), lanes 64..127 their h3, both at columns [UMMA_N, UMMA_N + BN).  The
+                // warp of quadrant q + 2 (h3) hands each 32-column unit to the warp of quadrant q
+                // (h1, the same half) through its own, otherwise idle, TMA-store staging area
+                // ([32 rows][32 fp32], 16-byte groups XOR-swizzled by row); the pair of warps meets
+                // on named barrier 2 + (q & 1) + 2 half ("ready" after the write, "free" after the
+                // read); the h1 warp gates and stores.
+                const bool h3_warp = quad >= 2;
+                const uint32_t bar_id = 2u + (quad & 1u) + 2u * static_cast<uint32_t>(half);
+                float* xch = reinterpret_cast<float*>(smem_stg + (h3_warp ? ewarp : ewarp - 2) * C::STG_WARP_BYTES);
+                const int hrow0 = C::HALF_ROW0 + static_cast<int>(cta_rank) * C::HALF_ROWS + static_cast<int>(quad & 1u) * 32;
+                const int hrow = hrow0 + static_cast<int>(lane);
+                const float hr = hrow < p.M ? (p.use_r ? __ldcg(p.r + hrow) : 1.f) : 0.f;
+                const GateRow hg = gate_row(hr);
+                const uint32_t t_h = tmem_base + ((quad * 32) << 16) + acc * C::ACC_STRIDE + C::UMMA_N;
+                constexpr int kLastW = C::BN % 32 == 0 ? 32 : C::BN % 32;
+                if (h3_warp && lane == 0) ptx::tma_store_wait_read<0>();  // its staging area is read out
+                __syncwarp();
+                auto half_unit = [&](auto wtag, int u) {
+                    constexpr int W = decltype(wtag)::value;
+                    uint32_t v[32];
+                    ptx::tmem_ld_cols<W>(t_h + 32 * u, v);
+                    ptx::tmem_ld_wait();
+                    if (h3_warp) {
+#pragma unroll
+                        for (int q = 0; q < W / 4; ++q)
+                            *reinterpret_cast<uint4*>(xch + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        ptx::named_bar_sync(bar_id, 64);  // ready
+                        ptx::named_bar_sync(bar_id, 64);  // free: the h1 warp has read it
+                    } else {
+                        ptx::named_bar_sync(bar_id, 64);  // ready
+                        float o[32];
+#pragma unroll
+                        for (int q = 0; q < W / 4; ++q) {
+                            const uint4 w3 = *reinterpret_cast<const uint4*>(xch + lane * 32 + ((q ^ (lane & 7)) << 2));
+                            o[4 * q + 0] = silu_gate(__uint_as_float(v[4 * q + 0]), __uint_as_float(w3.x), hg);
+                            o[4 * q + 1] = silu_gate(__uint_as_float(v[4 * q + 1]), __uint_as_float(w3.y), hg);
+                            o[4 * q + 2] = silu_gate(__uint_as_float(v[4 * q + 2]), __uint_as_float(w3.z), hg);
+                            o[4 * q + 3] = silu_gate(__uint_as_float(v[4 * q + 3]), __uint_as_float(w3.w), hg);
+                        }
+                        ptx::named_bar_sync(bar_id, 64);  // free
+                        const OutMaps* maps = W == 32 ? &omaps : &omaps_h;
+                        uint8_t* stg = smem_stg + ewarp * C::STG_WARP_BYTES;
+                        if (hrow0 < p.M)
+                            store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + 32 * u,
+                                                hrow0, lane);
+                    }
+                };
+#pragma unroll 1
+                for (int u = half; u < C::NU; u += 2) {  // this pair of warps' units
+                    if (kLastW == 32 || u + 1 < C::NU)
+                        half_unit(std::integral_constant<int, 32>{}, u);
+                    else
+                        half_unit(std::integral_constant<int, kLastW>{}, u);
+                }
             }
             if (warp == 2 && lane == 0) {
                 trace_stamp(p, 11);

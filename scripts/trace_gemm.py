@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--op", default="ffn", choices=["ffn", "gemm"], help="gemm: cuasm_gemm_act (identity)")
     ap.add_argument("--scheds", default="0,1")
     ap.add_argument("--bns", default="0", help="SwiGLU tile widths (CUASM_OPT_TILE_BN), 0 = auto")
+    ap.add_argument("--talls", default="0", help="CUASM_OPT_TALL values (0 auto, 1 off, 2 on)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     wbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -37,13 +38,16 @@ def main():
         M, K, N = map(int, shp.split("x"))
         t = make_device_inputs(M, K, N, 1, dev)
         out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        for sched, bn in [(s_, b_) for s_ in map(int, a.scheds.split(",")) for b_ in map(int, a.bns.split(","))]:
+        for sched, bn, tall in [(s_, b_, t_) for s_ in map(int, a.scheds.split(",")) for b_ in map(int, a.bns.split(","))
+                                for t_ in map(int, a.talls.split(","))]:
             pdl = 1
             h = ffn.FusedFFN(dev)
             h.set_option(ffn.OPT_PDL, pdl)
             h.set_option(ffn.OPT_SCHEDULE, sched)
             h.set_option(ffn.OPT_TILE_BN, bn)
-            floor = 4 * (bn or ffn.plan_config(M, K, N)[4]) if a.op == "ffn" else 512
+            h.set_option(ffn.OPT_TALL, tall)
+            is_tall = tall == 2 or (tall == 0 and ffn.plan_config(M, K, N)[0] == "tall")
+            floor = (4 * (bn or ffn.plan_config(M, K, N)[4]) * (1.5 if is_tall else 1.0) if a.op == "ffn" else 512)
             def run():
                 if a.op == "ffn":
                     h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6, out=out)
@@ -92,7 +96,7 @@ def main():
                 rows[name] = {"min": round(rel.min().item(), 2), "med": round(rel.median().item(), 2),
                               "max": round(rel.max().item(), 2)}
             key = (f"{a.op} {shp} schedule={['auto', 'data-parallel', 'stream-k-all', 'stream-k-tail'][sched]}"
-                   f" bn={bn or 'auto'}")
+                   f" bn={bn or 'auto'}" + (f" tall={tall}" if tall else ""))
             report[key] = rows
             print(key)
             for name, r in rows.items():

@@ -123,6 +123,9 @@ def bn_frac(bn):
             0.70 if bn >= 80 else 0.62)
 
 
+TALL_FRAC = 1.07   # tall 80-wide k-block relative to a 128-wide 256-row one (csrc kTallFrac)
+
+
 def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     t_kb, fixup, hbm, pen_1sm = 0.37e-6, 10e-6, 6.5e12, 1.16
     BK = 128 // esize
@@ -130,6 +133,7 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     hbm_floor = ((2.0 if out_cols == 128 else 1.0) * N * K + M * K + M * N) * esize / hbm
     t1 = -(-M // 128) * -(-N // 128)
     t64 = -(-M // 128) * -(-N // 64)
+    tall_ok = out_cols == 128 and esize == 2 and 256 < M <= 384   # tall tiles (csrc kTallBN = 80)
     if out_cols == 128 and esize == 2 and KB >= 48 and M <= 32 and 2 * t64 <= sm_count:
         return ("1sm", False, 256, 3 if 3 * t64 <= sm_count else 2, 64)   # decode shards, 64-wide tiles
     if out_cols == 128 and KB >= 48 and M <= 32:   # decode shards: cluster split-K
@@ -174,6 +178,10 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
                 best_t, best = t_dp, (name, False, tn, 0, bn)
             if K // BK > 1 and t_sk < best_t * 0.98:
                 best_t, best = t_sk, (name, True, tn, 0, bn)
+    if tall_ok:
+        t_tall = max(hbm_floor, -(-(-(-N // 80)) // (sm_count // 2)) * KB * t_kb * TALL_FRAC)
+        if t_tall < best_t * 0.98:
+            best = ("tall", False, 256, 0, 80)
     return best
 
 
