@@ -86,6 +86,10 @@ def parse_args(argv=None):
                     help="llama7b_prefill | llama7b_decode | llama70b | sweep:M (K=4096, N=11008)")
     ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 one-SM, 2 two-SM (CTA pair)")
     ap.add_argument("--tile-bn", type=int, default=0, help="SwiGLU outputs per tile: 0 auto, 128/112/96/80/64")
+    ap.add_argument("--tune", action="store_true",
+                    help="fused FFN, bf16: run the autotuner (cuasm_ffn_tune, L2-flushed candidates) on this "
+                         "rank's shape before the warm-up and use its choice (the paper's search-then-lookup "
+                         "workflow, PAPER.md P:205-212, P:434-447)")
     ap.add_argument("--gather", action="store_true", help="all-gather the full [M,N] output every step (NCCL)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="a4 fused into the epilogue (cuasm_ffn_forward_gather): every rank's full [M,N] "
@@ -516,6 +520,15 @@ def run_cuasm(args):
             return gather_shards(layers[i][1], N)
         return None
 
+    tuned = None
+    if args.tune and op == "ffn" and wdtype == torch.bfloat16 and not (fused_gather or fused_reduce):
+        # the autotuner on layer 0's data; the other layer copies' handles import its table
+        tt0, oo0 = layers[0]
+        tplan, tus = h.tune(tt0["x"], tt0["g"], tt0["w1"], tt0["w3"], eps, warmup=10, iters=20, flush_l2=True, out=oo0)
+        table = h.tuned_export()
+        for hh in handles[1:]:
+            hh.tuned_import(table)
+        tuned = {"plan": list(tplan), "us_per_forward": round(tus, 2), "candidates": len(h.tune_log())}
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -787,6 +800,7 @@ def run_cuasm(args):
                 "plan": list(ffn.plan_config(M, K, N_l, "gemm" if op == "gemm_lrelu" else "ffn", wdtype))
                 if op in ("ffn", "gemm_lrelu") else None,
                 "tile_bn_forced": args.tile_bn or None,
+                "tuned": tuned,
                 "l2_persist_mib": args.l2_persist_mb or None,
             },
             "pct_of_peak": round(value / world / peaks["bf16_tflops"], 4),

@@ -365,6 +365,52 @@ const char* cuasm_ffn_last_error(cuasm_ffn_t h);
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k);
 
+/* The paper's autotuner and its offline-search / deploy-time-lookup workflow (PAPER.md
+ * "enumerates user-provided kernel configurations ..., measures the execution
+ * throughput on the target GPU, and greedily selects as well as caches the optimal set of
+ * kernel configurations", the mean of repeated executions after warm-up; results
+ * written "prefixed by GPU type, workload type etc., as the key to lookup", looked up at
+ * deployment instead of searched).
+ *
+ * cuasm_ffn_tune: runs the fused FFN out = SiLU(RMSNorm(x) W1^T) * (RMSNorm(x) W3^T) --
+ * arguments exactly as cuasm_ffn_forward, bf16 handles only -- under every candidate
+ * configuration of the dual GEMM for this M x K x N (the cost model's choice, each 2-SM tile
+ * width with whole tiles and a stream-K tail, the 1-SM tile, tall tiles where 256 < M <= 384,
+ * the 1-SM cluster split-K of 2..8 CTAs), in three interleaved rounds (so clock and power
+ * drift spread over all candidates): per round `warmup` untimed forwards, then `iters` timed
+ * ones -- flush_l2 = 0: back to back between one CUDA-event pair on `stream`; flush_l2 = 1:
+ * each after an L2 flush (a 2x-L2 buffer written, another read; the paper's evaluation
+ * protocol) inside its own event pair -- a candidate's time being the best round's
+ * mean per forward.  It keeps the fastest in the handle's table (replacing an entry of the
+ * same shape) and returns it in *variant /
+ * *flags (the encoding of cuasm_plan_config) and *best_us (any of them may be NULL).  From
+ * then on forwards of exactly this shape on this handle use it instead of the configuration
+ * model.  SYNCHRONOUS (waits for `stream`); writes `out` many times; packs the weights once
+ * per tile width tried (handle memory).  Errors: INVALID_ARG as for a forward, M == 0,
+ * warmup < 0, iters < 1 or flush_l2 not 0/1; UNSUPPORTED for fp32 handles; OOM if the flush
+ * buffer (4x L2, freed on return) cannot be allocated; a candidate the shape cannot run
+ * is skipped, any CUDA error aborts the search and is returned.
+ *
+ * cuasm_ffn_tuned_export: the table as text, one line per entry,
+ *   "cuasm-tuned v1 sm=<SMs> dtype=bf16 M=<M> K=<K> N=<N> variant=<v> flags=<f> us=<t> gpu=<name>\n",
+ * NUL-terminated, into buf[cap]; *needed = bytes required (incl. the NUL).  cap = 0 only
+ * queries the size; 0 < cap < *needed is INVALID_ARG (nothing written).
+ *
+ * cuasm_ffn_tuned_import: adds (or replaces, per shape) the entries of `text` whose GPU name,
+ * SM count and dtype match this handle's device; other lines (comments, other GPUs) are
+ * ignored; *accepted = entries taken.  A matching but malformed entry is INVALID_ARG (the
+ * entries before it stay imported).  cuasm_ffn_tuned_clear empties the table. */
+cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
+                              void* out, int64_t M, int64_t K, int64_t N, float eps, int warmup, int iters,
+                              int flush_l2, void* stream, int* variant, int* flags, float* best_us);
+cuasm_status_t cuasm_ffn_tuned_export(cuasm_ffn_t h, char* buf, int64_t cap, int64_t* needed);
+cuasm_status_t cuasm_ffn_tuned_import(cuasm_ffn_t h, const char* text, int* accepted);
+cuasm_status_t cuasm_ffn_tuned_clear(cuasm_ffn_t h);
+/* The last cuasm_ffn_tune's search, candidate by candidate in the order measured: *n =
+ * candidates; the first min(cap, *n) variants / flags (cuasm_plan_config encoding) / mean us
+ * per forward (-1 = the shape cannot run it) are written.  cap = 0 only queries *n. */
+cuasm_status_t cuasm_ffn_tune_log(cuasm_ffn_t h, int cap, int* n, int* variants, int* flags, float* us);
+
 /* CUASM_FFN_ABI_VERSION of the loaded library. */
 int cuasm_ffn_abi_version(void);
 

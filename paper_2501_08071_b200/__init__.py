@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
     "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_plan_config", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
+    "cuasm_ffn_tune", "cuasm_ffn_tuned_export", "cuasm_ffn_tuned_import", "cuasm_ffn_tuned_clear", "cuasm_ffn_tune_log",
 )
 
 
@@ -56,9 +57,12 @@ def plan_config(M: int, K: int, N: int, op: str = "ffn", dtype=torch.bfloat16, s
                                ctypes.byref(sk))
     if st != OK:
         raise CuasmError(st, "cuasm_plan_config: invalid arguments")
-    return (("1sm" if v.value == VARIANT_1SM else "tall" if sk.value & 4 else "2sm"), bool(sk.value & 1),
-            (128 if sk.value & 2 else 256),
-            (sk.value >> 4) & 15, sk.value >> 8)
+    return _plan_tuple(v.value, sk.value)
+
+
+def _plan_tuple(variant: int, flags: int):
+    return (("1sm" if variant == VARIANT_1SM else "tall" if flags & 4 else "2sm"), bool(flags & 1),
+            (128 if flags & 2 else 256), (flags >> 4) & 15, flags >> 8)
 
 
 def rs_layout(M: int, K: int, world: int, rank: int):
@@ -116,6 +120,13 @@ def load_library():
                                                ctypes.POINTER(ci)]
         lib.cuasm_ffn_trace_read.argtypes = [vp, vp, ctypes.POINTER(ci)]
         lib.cuasm_plan_config.argtypes = [ci, ci, i64, i64, i64, ci, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+        lib.cuasm_ffn_tune.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, ci, ci, ci, vp, ctypes.POINTER(ci),
+                                       ctypes.POINTER(ci), ctypes.POINTER(f32)]
+        lib.cuasm_ffn_tuned_export.argtypes = [vp, ctypes.c_char_p, i64, ctypes.POINTER(i64)]
+        lib.cuasm_ffn_tuned_import.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ci)]
+        lib.cuasm_ffn_tuned_clear.argtypes = [vp]
+        lib.cuasm_ffn_tune_log.argtypes = [vp, ci, ctypes.POINTER(ci), ctypes.POINTER(ci), ctypes.POINTER(ci),
+                                           ctypes.POINTER(f32)]
         lib.cuasm_ffn_destroy.argtypes = [vp]
         lib.cuasm_ffn_last_error.argtypes = [vp]
         lib.cuasm_ffn_last_error.restype = ctypes.c_char_p
@@ -262,6 +273,55 @@ class FusedFFN:
                                                w3.data_ptr(), out.data_ptr(), M, K, N, float(eps),
                                                _stream_ptr(x.device)))
         return out
+
+    def tune(self, x, rms_w, w1, w3, eps: float = 1e-6, warmup: int = 100, iters: int = 100, flush_l2: bool = True,
+             out=None):
+        """The paper's autotuner (cuasm_ffn_tune): measure every candidate
+        configuration of this shape (three interleaved rounds of `warmup` + `iters` forwards,
+        each timed forward after an L2 flush when `flush_l2`), keep the fastest for later
+        forwards of the same shape on this handle.  Synchronous.  Returns (plan tuple as
+        plan_config's, best mean us per forward)."""
+        self._validate(x, rms_w, w1, w3)
+        M, K = x.shape
+        N = w1.shape[0]
+        if w1.shape != (N, K) or w3.shape != (N, K) or rms_w.shape != (K,):
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty((M, N), dtype=self.dtype, device=x.device)
+        self._weights_changed({0: (rms_w, w1, w3)})
+        v, fl, us = ctypes.c_int(), ctypes.c_int(), ctypes.c_float()
+        self._check(self.lib.cuasm_ffn_tune(self._h, x.data_ptr(), rms_w.data_ptr(), w1.data_ptr(), w3.data_ptr(),
+                                            out.data_ptr(), M, K, N, float(eps), int(warmup), int(iters),
+                                            1 if flush_l2 else 0, _stream_ptr(x.device), ctypes.byref(v), ctypes.byref(fl),
+                                            ctypes.byref(us)))
+        return _plan_tuple(v.value, fl.value), us.value
+
+    def tuned_export(self) -> str:
+        """The tuned table as text (one "cuasm-tuned v1 ..." line per shape, keyed by GPU)."""
+        need = ctypes.c_int64()
+        self._check(self.lib.cuasm_ffn_tuned_export(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        self._check(self.lib.cuasm_ffn_tuned_export(self._h, buf, need.value, ctypes.byref(need)))
+        return buf.value.decode()
+
+    def tuned_import(self, text: str) -> int:
+        """Deploy-time lookup table: take the entries of `text` made on this GPU
+        type; returns how many were taken."""
+        n = ctypes.c_int()
+        self._check(self.lib.cuasm_ffn_tuned_import(self._h, text.encode(), ctypes.byref(n)))
+        return n.value
+
+    def tune_log(self):
+        """The last tune()'s candidates in the order measured: [(plan tuple, us or None)]."""
+        n = ctypes.c_int()
+        self._check(self.lib.cuasm_ffn_tune_log(self._h, 0, ctypes.byref(n), None, None, None))
+        cap = n.value
+        vs, fs, us = (ctypes.c_int * max(cap, 1))(), (ctypes.c_int * max(cap, 1))(), (ctypes.c_float * max(cap, 1))()
+        self._check(self.lib.cuasm_ffn_tune_log(self._h, cap, ctypes.byref(n), vs, fs, us))
+        return [(_plan_tuple(vs[i], fs[i]), None if us[i] < 0 else us[i]) for i in range(min(cap, n.value))]
+
+    def tuned_clear(self):
+        self._check(self.lib.cuasm_ffn_tuned_clear(self._h))
 
     def forward_gather(self, x, rms_w, w1, w3, dst_ptrs, ldo: int, eps: float = 1e-6, multicast: bool = False,
                        keepalive=None):

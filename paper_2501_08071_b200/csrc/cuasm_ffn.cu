@@ -67,6 +67,38 @@ struct PackedWeights {
     int tmap_rows = 0;
 };
 
+// One configuration of the dual-GEMM launch (plan_config_raw's answer, or a tuned one).
+struct Plan {
+    int variant;
+    bool stream_k;
+    int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
+    int csplit;  // cluster split-K: CTAs per tile (1-SM variant), 0 = none
+    int bn = kPackBN;  // SwiGLU outputs per tile (MMA N = 2 bn): 128, or 64..112 (2-SM bf16)
+    bool tall = false; // tall tiles (2-SM bf16, bn = kTallBN, 256 < M <= 384, whole tiles)
+};
+
+// Tall tiles (dual_gemm.cuh GemmCfg kTall): one kTallBN-output n-block over up to 384 rows.
+constexpr int kTallBN = 80;
+constexpr int64_t kTallMaxM = 384;
+
+// The flags word of cuasm_plan_config / cuasm_ffn_tune: bit 0 stream-K, bit 1 the 128-wide GEMM
+// tile, bit 2 tall tiles, bits 4..7 cluster split-K CTAs, bits 8..15 the SwiGLU outputs per tile.
+inline int plan_flags(const Plan& pl) {
+    return (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.tall ? 4 : 0) | (pl.csplit << 4) | (pl.bn << 8);
+}
+inline Plan plan_from_flags(int variant, int flags) {
+    Plan pl{variant, (flags & 1) != 0, (flags & 2) ? 128 : 256, (flags >> 4) & 15, (flags >> 8) & 0xFF};
+    pl.tall = (flags & 4) != 0;
+    return pl;
+}
+
+// A measured configuration for one problem shape (cuasm_ffn_tune / cuasm_ffn_tuned_import).
+struct TunedEntry {
+    int64_t M, K, N;
+    Plan plan;
+    float us;
+};
+
 }  // namespace
 
 struct cuasm_ffn_s {
@@ -139,6 +171,13 @@ struct cuasm_ffn_s {
     int last_variant = 0;
     int last_kernels = 0;
     EncodeTiledFn encode = nullptr;
+    // the paper's autotuner (cuasm_ffn_tune) and deploy-time lookup:
+    // measured configurations per fused-FFN shape, consulted before the cost model
+    std::string gpu_name;            // cudaDeviceProp::name: part of a tuned entry's key
+    std::vector<TunedEntry> tuned;
+    std::vector<std::pair<Plan, float>> tune_log;  // the last cuasm_ffn_tune's candidates and times (-1: skipped)
+    bool plan_forced = false;        // cuasm_ffn_tune: the candidate being measured
+    Plan plan_force{CUASM_VARIANT_2SM, false, 256, 0, kPackBN};
 };
 
 namespace {
@@ -765,18 +804,6 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
 // Constants were fitted to scripts/tune.py on a B200 (profiles/r01/tune.json):
 // t_kb = 0.37 us per k-block-tile at the power-capped clock, fixup = 10 us,
 // stream-K L2-overflow slowdown 1.32x (profiles/r01/trace_gemm.log).
-struct Plan {
-    int variant;
-    bool stream_k;
-    int tile_n;  // MMA N: 256, or 128 (GEMM + activation only)
-    int csplit;  // cluster split-K: CTAs per tile (1-SM variant), 0 = none
-    int bn = kPackBN;  // SwiGLU outputs per tile (MMA N = 2 bn): 128, or 64..112 (2-SM bf16)
-    bool tall = false; // tall tiles (2-SM bf16, bn = kTallBN, 256 < M <= 384, whole tiles)
-};
-
-// Tall tiles (dual_gemm.cuh GemmCfg kTall): one kTallBN-output n-block over up to 384 rows.
-constexpr int kTallBN = 80;
-constexpr int64_t kTallMaxM = 384;
 
 // Time of one k-block of a 2-SM SwiGLU tile of width bn relative to bn = 128, measured
 // (scripts/tune_bn.py, profiles/r02/tune_bn.json): at full size the narrower tiles run at
@@ -926,6 +953,12 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
 }
 
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
+    // the fused FFN's measured configurations (cuasm_ffn_tune) take precedence over the model
+    if (out_cols == 128) {
+        if (h->plan_forced) return h->plan_force;
+        for (const TunedEntry& t : h->tuned)
+            if (t.M == M && t.K == K && t.N == N) return t.plan;
+    }
     Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
                               out_cols == 128 ? h->tile_bn : 0, h->tall);
     // (tall tiles are a 2-SM kernel: a forced 1-SM variant takes the ordinary tiles)
@@ -1145,6 +1178,252 @@ extern "C" {
 
 int cuasm_ffn_abi_version(void) { return CUASM_FFN_ABI_VERSION; }
 
+namespace {
+bool same_plan(const Plan& a, const Plan& b) {
+    return a.variant == b.variant && a.stream_k == b.stream_k && a.tile_n == b.tile_n && a.csplit == b.csplit &&
+           a.bn == b.bn && a.tall == b.tall;
+}
+
+// The configurations cuasm_ffn_tune measures for one bf16 fused-FFN shape (the paper's
+// "user-provided kernel configurations"): the cost model's own choice first, every
+// 2-SM tile width with whole tiles and with a stream-K tail, the 1-SM 128-wide tile both
+// ways, tall tiles where they apply, and the 1-SM cluster split-K of 2..8 CTAs per tile
+// (128- and 64-output tiles) where a tile count x split fits the SMs in one wave.
+std::vector<Plan> tune_candidates(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N) {
+    std::vector<Plan> c;
+    auto add = [&](const Plan& p) {
+        for (const Plan& q : c)
+            if (same_plan(q, p)) return;
+        c.push_back(p);
+    };
+    add(plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, 128));
+    for (int bn : kTileBNs)
+        for (int sk = 0; sk < 2; ++sk) add(Plan{CUASM_VARIANT_2SM, sk == 1, 256, 0, bn});
+    for (int sk = 0; sk < 2; ++sk) add(Plan{CUASM_VARIANT_1SM, sk == 1, 256, 0, kPackBN});
+    if (M > 256 && M <= kTallMaxM) {
+        Plan t{CUASM_VARIANT_2SM, false, 256, 0, kTallBN};
+        t.tall = true;
+        add(t);
+    }
+    const int64_t KB = (K + 63) / 64;
+    for (int bn : {kPackBN, 64})
+        for (int S : {2, 3, 4, 6, 8}) {
+            const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+            if (tiles * S <= h->sm_count && KB >= 2 * S) add(Plan{CUASM_VARIANT_1SM, false, 256, S, bn});
+        }
+    return c;
+}
+}  // namespace
+
+cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
+                              void* out, int64_t M, int64_t K, int64_t N, float eps, int warmup, int iters,
+                              int flush_l2, void* stream, int* variant, int* flags, float* best_us) {
+    NvtxRange nvtx_("cuasm_ffn_tune");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "tuning: bf16 handles only");
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    if (M == 0) return fail(h, CUASM_ERR_INVALID_ARG, "tuning needs M > 0");
+    if (warmup < 0 || iters < 1 || warmup > 100000 || iters > 100000 || (flush_l2 != 0 && flush_l2 != 1))
+        return fail(h, CUASM_ERR_INVALID_ARG, "warmup must be >= 0, iters >= 1, flush_l2 0 or 1");
+    DeviceGuard dg(h);
+    if ((st = dg.status) != CUASM_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // flush_l2: a buffer of twice the L2 is written, then another read, before every timed
+    // forward (outside its event pair), so each starts with an L2 of clean, unrelated lines
+    int l2 = 0;
+    CUASM_CHECK(h, cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device), "cudaDeviceGetAttribute(L2)");
+    const int64_t fbytes = flush_l2 ? (2 * static_cast<int64_t>(l2) + 0xFFFFF) & ~int64_t(0xFFFFF) : 0;
+    void* fbuf = nullptr;
+    if (fbytes && cudaMalloc(&fbuf, 2 * fbytes) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(h, CUASM_ERR_OOM, "cudaMalloc(L2 flush buffer)");
+    }
+    const int nev = flush_l2 ? iters : 1;
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * nev), nullptr);
+    auto cleanup = [&]() {
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (fbuf) cudaFree(fbuf);
+        h->plan_forced = false;
+    };
+    for (cudaEvent_t& e : ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            cleanup();
+            return fail(h, CUASM_ERR_CUDA, "cudaEventCreate");
+        }
+    auto flush = [&]() {
+        if (!fbuf) return cudaSuccess;
+        cudaError_t e = cudaMemsetAsync(fbuf, 0, static_cast<size_t>(fbytes), s);
+        if (e == cudaSuccess) {
+            cuasm::l2_flush_read_kernel<<<2 * h->sm_count, 512, 0, s>>>(
+                reinterpret_cast<const uint4*>(static_cast<char*>(fbuf) + fbytes), fbytes / 16);
+            e = cudaGetLastError();
+        }
+        return e;
+    };
+    // candidates measured in kTuneRounds interleaved rounds (clock / power drift spreads over
+    // all of them), a candidate's time = the best of its rounds' means
+    constexpr int kTuneRounds = 3;
+    const std::vector<Plan> cands = tune_candidates(h, M, K, N);
+    std::vector<float> t_us(cands.size(), std::numeric_limits<float>::infinity());
+    std::vector<bool> skip(cands.size(), false);
+    for (int rnd = 0; rnd < kTuneRounds; ++rnd) {
+        for (size_t ci = 0; ci < cands.size(); ++ci) {
+            if (skip[ci]) continue;
+            h->plan_forced = true;
+            h->plan_force = cands[ci];
+            st = CUASM_OK;
+            for (int w = 0; w < warmup && st == CUASM_OK; ++w) st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+            cudaError_t ce = cudaSuccess;
+            if (st == CUASM_OK && !flush_l2) ce = cudaEventRecord(ev[0], s);
+            for (int i = 0; i < iters && st == CUASM_OK && ce == cudaSuccess; ++i) {
+                if (flush_l2 && (ce = flush()) == cudaSuccess) ce = cudaEventRecord(ev[2 * i], s);
+                if (ce == cudaSuccess) st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                if (flush_l2 && st == CUASM_OK && ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i + 1], s);
+            }
+            if (st == CUASM_OK && ce == cudaSuccess && !flush_l2) ce = cudaEventRecord(ev[1], s);
+            if (st == CUASM_OK && ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+            double ms = 0.0;
+            for (int i = 0; i < nev && st == CUASM_OK && ce == cudaSuccess; ++i) {
+                float m = 0.f;
+                ce = cudaEventElapsedTime(&m, ev[2 * i], ev[2 * i + 1]);
+                ms += m;
+            }
+            h->plan_forced = false;
+            if (ce != cudaSuccess) {
+                cleanup();
+                return cuda_fail(h, ce, "tuning");
+            }
+            if (st != CUASM_OK) {
+                // a configuration this shape cannot launch (rejected before any launch): skip it;
+                // anything else is a real failure
+                if (st != CUASM_ERR_UNSUPPORTED) {
+                    cleanup();
+                    return st;
+                }
+                h->err.clear();
+                skip[ci] = true;
+                continue;
+            }
+            t_us[ci] = std::min(t_us[ci], static_cast<float>(ms * 1000.0 / iters));
+        }
+    }
+    cleanup();
+    float best = std::numeric_limits<float>::infinity();
+    Plan best_plan{CUASM_VARIANT_2SM, false, 256, 0, kPackBN};
+    h->tune_log.clear();
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+        h->tune_log.emplace_back(cands[ci], skip[ci] ? -1.f : t_us[ci]);
+        if (!skip[ci] && t_us[ci] < best) {
+            best = t_us[ci];
+            best_plan = cands[ci];
+        }
+    }
+    if (!(best < std::numeric_limits<float>::infinity())) return fail(h, CUASM_ERR_UNSUPPORTED, "no configuration ran");
+    bool found = false;
+    for (TunedEntry& t : h->tuned)
+        if (t.M == M && t.K == K && t.N == N) {
+            t.plan = best_plan;
+            t.us = best;
+            found = true;
+        }
+    if (!found) h->tuned.push_back(TunedEntry{M, K, N, best_plan, best});
+    if (variant) *variant = best_plan.variant;
+    if (flags) *flags = plan_flags(best_plan);
+    if (best_us) *best_us = best;
+    return CUASM_OK;
+}
+
+// "cuasm-tuned v1 sm=<SMs> dtype=bf16 M=<M> K=<K> N=<N> variant=<v> flags=<f> us=<t> gpu=<name>\n"
+// per entry: the lookup key is the GPU name + SM count + dtype + shape (results written
+// "prefixed by GPU type, workload type etc., as the key to lookup").
+cuasm_status_t cuasm_ffn_tuned_export(cuasm_ffn_t h, char* buf, int64_t cap, int64_t* needed) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (!needed || cap < 0 || (cap > 0 && !buf)) return fail(h, CUASM_ERR_INVALID_ARG, "NULL buffer or size");
+    std::string text;
+    char line[512];
+    for (const TunedEntry& t : h->tuned) {
+        std::snprintf(line, sizeof(line),
+                      "cuasm-tuned v1 sm=%d dtype=%s M=%lld K=%lld N=%lld variant=%d flags=%d us=%.3f gpu=%s\n",
+                      h->sm_count, h->dtype == CUASM_DTYPE_BF16 ? "bf16" : "fp32", static_cast<long long>(t.M),
+                      static_cast<long long>(t.K), static_cast<long long>(t.N), t.plan.variant, plan_flags(t.plan),
+                      static_cast<double>(t.us), h->gpu_name.c_str());
+        text += line;
+    }
+    *needed = static_cast<int64_t>(text.size()) + 1;
+    if (cap < *needed) return cap == 0 ? CUASM_OK : fail(h, CUASM_ERR_INVALID_ARG, "buffer too small (%lld bytes needed)",
+                                                         static_cast<long long>(*needed));
+    std::memcpy(buf, text.c_str(), text.size() + 1);
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_tuned_import(cuasm_ffn_t h, const char* text, int* accepted) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (!text || !accepted) return fail(h, CUASM_ERR_INVALID_ARG, "NULL text or count");
+    *accepted = 0;
+    const char* p = text;
+    while (*p) {
+        const char* eol = std::strchr(p, '\n');
+        const std::string line(p, eol ? static_cast<size_t>(eol - p) : std::strlen(p));
+        p = eol ? eol + 1 : p + line.size();
+        int sm = 0, v = 0, fl = 0, pos = -1;
+        long long M = 0, K = 0, N = 0;
+        char dt[16] = {0};
+        float us = 0.f;
+        if (std::sscanf(line.c_str(), "cuasm-tuned v1 sm=%d dtype=%15s M=%lld K=%lld N=%lld variant=%d flags=%d us=%f gpu=%n",
+                        &sm, dt, &M, &K, &N, &v, &fl, &us, &pos) != 8 || pos < 0)
+            continue;  // not an entry (comments, other versions)
+        std::string gpu = line.substr(static_cast<size_t>(pos));
+        while (!gpu.empty() && (gpu.back() == '\r' || gpu.back() == ' ')) gpu.pop_back();
+        // another GPU type / SM count / dtype: not this device's entry
+        if (sm != h->sm_count || gpu != h->gpu_name || std::strcmp(dt, h->dtype == CUASM_DTYPE_BF16 ? "bf16" : "fp32") != 0)
+            continue;
+        const Plan pl = plan_from_flags(v, fl);
+        bool bn_ok = false;
+        for (int bn : kTileBNs) bn_ok |= pl.bn == bn;
+        if (M <= 0 || K <= 0 || N <= 0 || (v != CUASM_VARIANT_1SM && v != CUASM_VARIANT_2SM) || !bn_ok ||
+            pl.tile_n != 256 || (pl.csplit != 0 && (pl.csplit < 2 || pl.csplit > 8 || v != CUASM_VARIANT_1SM)) ||
+            (pl.tall && (v != CUASM_VARIANT_2SM || pl.bn != kTallBN || M <= 256 || M > kTallMaxM)) ||
+            (v == CUASM_VARIANT_1SM && pl.bn != kPackBN && pl.bn != 64 && pl.bn != 120) || (fl & ~0xFFF7) != 0)
+            return fail(h, CUASM_ERR_INVALID_ARG, "malformed tuned entry: %s", line.c_str());
+        bool found = false;
+        for (TunedEntry& t : h->tuned)
+            if (t.M == M && t.K == K && t.N == N) {
+                t.plan = pl;
+                t.us = us;
+                found = true;
+            }
+        if (!found) h->tuned.push_back(TunedEntry{M, K, N, pl, us});
+        ++*accepted;
+    }
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_tune_log(cuasm_ffn_t h, int cap, int* n, int* variants, int* flags, float* us) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (!n || cap < 0 || (cap > 0 && (!variants || !flags || !us)))
+        return fail(h, CUASM_ERR_INVALID_ARG, "NULL output arrays");
+    *n = static_cast<int>(h->tune_log.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+        variants[i] = h->tune_log[static_cast<size_t>(i)].first.variant;
+        flags[i] = plan_flags(h->tune_log[static_cast<size_t>(i)].first);
+        us[i] = h->tune_log[static_cast<size_t>(i)].second;
+    }
+    return CUASM_OK;
+}
+
+cuasm_status_t cuasm_ffn_tuned_clear(cuasm_ffn_t h) {
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    h->tuned.clear();
+    return CUASM_OK;
+}
+
 cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, int64_t N, int op, int* variant,
                                  int* stream_k) {
     if (sm_count <= 1 || (dtype != CUASM_DTYPE_BF16 && dtype != CUASM_DTYPE_FP32) || M < 0 || K <= 0 || N <= 0 ||
@@ -1152,7 +1431,7 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
         return CUASM_ERR_INVALID_ARG;
     const Plan pl = plan_config_raw(sm_count, dtype == CUASM_DTYPE_BF16 ? 2 : 4, 0, M, K, N, op == 0 ? 128 : 256);
     *variant = pl.variant;
-    *stream_k = (pl.stream_k ? 1 : 0) | (pl.tile_n == 128 ? 2 : 0) | (pl.tall ? 4 : 0) | (pl.csplit << 4) | (pl.bn << 8);
+    *stream_k = plan_flags(pl);
     return CUASM_OK;
 }
 
@@ -1179,6 +1458,7 @@ cuasm_status_t cuasm_ffn_init(cuasm_ffn_t* out, int device, cuasm_dtype_t dtype)
     h->dtype = dtype;
     h->esize = dtype == CUASM_DTYPE_BF16 ? 2 : 4;
     h->sm_count = prop.multiProcessorCount;
+    h->gpu_name = prop.name;
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);

@@ -73,3 +73,11 @@ def test_decode_roofline_is_hbm_bound():
     d = run_bench("--workload", "llama7b_decode", "--steps", "5", "--warmup", "3", "--skip-cpu-baseline",
                   "--skip-e2e", "--skip-b2b")
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["unit"] == "GB/s"
+
+
+def test_tuned_bench_line_records_the_search():
+    d = run_bench("--workload", "llama7b_decode", "--steps", "5", "--warmup", "3", "--skip-cpu-baseline",
+                  "--skip-e2e", "--skip-b2b", "--protocol-runs", "0", "--tune")
+    t = d["config"]["tuned"]
+    assert t["plan"][0] in ("1sm", "2sm", "tall") and t["us_per_forward"] > 0 and t["candidates"] >= 10
+    assert d["value"] > 0
