@@ -1683,9 +1683,14 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin, kTa
                         ptx::named_bar_sync(bar_id, 64);  // free
                         const OutMaps* maps = W == 32 ? &omaps : &omaps_h;
                         uint8_t* stg = smem_stg + ewarp * C::STG_WARP_BYTES;
-                        if (hrow0 < p.M)
-                            store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o, nb * C::OUT_COLS + 32 * u,
-                                                hrow0, lane);
+                        if (p.tma_store) {
+                            if (hrow0 < p.M)
+                                store_box_tma<1, W>(maps, p.num_dst, stg + (nst++ & 1) * 2048, o,
+                                                    nb * C::OUT_COLS + 32 * u, hrow0, lane);
+                        } else if (hrow < p.M) {
+                            // (NVLS multicast destination: 16-byte multimem stores per row)
+                            store_row32<kKind, W>(p, hrow, nb * C::OUT_COLS + 32 * u, o);
+                        }
                     }
                 };
 #pragma unroll 1

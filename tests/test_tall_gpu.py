@@ -121,3 +121,26 @@ def test_tall_full_size_sweep_shape(cuda_device, M):
     rows = sorted({0, 127, 128, 255, 256, 300, 319, 320, M - 1} & set(range(M)))
     ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
     check(out[rows], ref, f"tall full size M={M}")
+
+
+def test_tall_fused_gather_simulated_peers(cuda_device):
+    """Step a4 fused into the tall tile's epilogue (both parts): P = 3 simulated peer buffers
+    each receive every rank's columns, equal to the concatenated plain forwards."""
+    from paper_2501_08071_b200.tp import gather_destinations, shard_bounds, shard_weights
+    M, K, N, P = 300, 512, 3 * 248, 3
+    d = make_inputs(M, K, N, family="C", seed=9900, dtype="bf16")
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    bufs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda_device) for _ in range(P)]
+    shard_outs = []
+    for rank in range(P):
+        n0, _ = shard_bounds(N, rank, P)
+        w1s, w3s = shard_weights(t["w1"], t["w3"], rank, P)
+        h = _handle(cuda_device, 2)
+        dst, mc = gather_destinations([b.data_ptr() for b in bufs], n0, 2)
+        h.forward_gather(t["x"], t["g"], w1s, w3s, dst, N, 1e-6, keepalive=bufs)
+        shard_outs.append(h.forward(t["x"], t["g"], w1s, w3s, 1e-6))
+    torch.cuda.synchronize()
+    full = torch.cat(shard_outs, dim=1)
+    for q in range(P):
+        assert torch.equal(bufs[q], full), f"peer buffer {q}"
+    check(full, oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16"), "tall gather")
