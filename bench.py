@@ -73,6 +73,8 @@ EXTRA = {
     "rmsnorm_paper": ("rmsnorm", 4096, 2048, 8),
     # BASELINE.json configs[0]: tiny fp32 fused FFN (tf32 tensor cores), latency-bound
     "tiny_fp32": ("ffn", 16, 64, 128),
+    # configs[4]'s crossover region (M = 384 of the token sweep: tall tiles)
+    "crossover_m384": ("ffn", 384, 4096, 11008),
 }
 
 

@@ -13,7 +13,7 @@ timeout 900 python bench.py > $O/bench_llama7b_prefill.json 2> $O/bench.err; ech
 timeout 600 python bench.py --workload llama7b_decode > $O/bench_llama7b_decode.json 2>> $O/bench.err; echo "bench_decode=$?"
 timeout 600 python bench.py --workload llama70b --skip-cpu-baseline > $O/bench_llama70b.json 2>> $O/bench.err; echo "bench_70b=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_reference.json 2>> $O/bench.err; echo "bench_ref=$?"
-for w in llama7b_block mmleakyrelu_paper mmleakyrelu_large rmsnorm_paper fused_ff_paper tiny_fp32; do
+for w in llama7b_block mmleakyrelu_paper mmleakyrelu_large rmsnorm_paper fused_ff_paper tiny_fp32 crossover_m384; do
   timeout 600 python bench.py --workload $w --skip-cpu-baseline --skip-e2e > $O/bench_$w.json 2>> $O/bench.err; echo "bench_$w=$?"
 done
 for P in 2 4 8; do
@@ -27,15 +27,17 @@ for w in llama7b_prefill llama70b; do
   timeout 600 python bench.py --workload $w --shard-of 8 --fused-gather --skip-cpu-baseline --skip-e2e > $O/bench_${w}_shard8_fusedgather_sim.json 2>> $O/bench.err; echo "fg_$w=$?"
 done
 python scripts/show_bench.py $O/bench_*.json > $O/bench_table.txt 2>&1
+timeout 600 python scripts/tune_probe.py > $O/tune_probe.log 2>&1; echo "tune_probe=$?"
+timeout 300 python scripts/tune_tall.py --out $O/tune_tall.json > $O/tune_tall.log 2>&1; echo "tune_tall=$?"
 timeout 900 python scripts/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1; echo "sweep=$?"
 timeout 900 python scripts/sweep.py --shard-of 8 --out $O/sweep_shard8.json > $O/sweep_shard8.log 2>&1; echo "sweep8=$?"
-timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,16x4096x11008,2048x4096x1376,16x4096x1376 --json $O/trace.json > $O/trace.log 2>&1; echo "trace=$?"
+timeout 300 python scripts/trace_gemm.py --shapes 2048x4096x11008,16x4096x11008,2048x4096x1376,16x4096x1376,384x4096x11008 --json $O/trace.json > $O/trace.log 2>&1; echo "trace=$?"
 NB="--skip-cpu-baseline --skip-e2e --skip-b2b --no-graph --protocol-runs 0"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_prefill.csv \
   python bench.py --steps 5 --warmup 2 $NB > $O/ncu_launch.log 2>&1; echo "ncu_launches=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_llama7b_decode.csv \
   python bench.py --workload llama7b_decode --steps 5 --warmup 2 $NB > $O/ncu_launch_d.log 2>&1; echo "ncu_launches_d=$?"
-for spec in "prefill:llama7b_prefill:1" "decode:llama7b_decode:1" "70b:llama70b:1" "70b_shard8:llama70b:8" "prefill_shard8:llama7b_prefill:8" "decode_shard8:llama7b_decode:8" "tiny:tiny_fp32:1"; do
+for spec in "prefill:llama7b_prefill:1" "decode:llama7b_decode:1" "70b:llama70b:1" "70b_shard8:llama70b:8" "prefill_shard8:llama7b_prefill:8" "decode_shard8:llama7b_decode:8" "tiny:tiny_fp32:1" "tall:crossover_m384:1"; do
   IFS=: read name w P <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_dual_gemm -s 2 -c 1 -f -o $O/prof_gemm_$name \
     python bench.py --workload $w --shard-of $P --steps 2 --warmup 1 $NB > $O/ncu_gemm_$name.log 2>&1; echo "ncu_$name=$?"
