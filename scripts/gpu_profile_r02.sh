@@ -47,6 +47,5 @@ for spec in "prefill:llama7b_prefill:1" "decode:llama7b_decode:1" "70b:llama70b:
   gzip -f $O/ncu_raw_$name.csv
   [ "$name" = prefill ] || rm -f $O/prof_gemm_$name.ncu-rep
 done
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_memcheck.log 2>&1; echo "memcheck=$?"
-timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_synccheck.log 2>&1; echo "synccheck=$?"
-timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > $O/sanitizer_racecheck.log 2>&1; echo "racecheck=$?"
+# (compute-sanitizer runs were closed on the GPU pool late in round 2: the sanitizer evidence is
+# profiles/r02/racecheck/ and profiles/r02/evidence/sanitizer_*.log, from the same kernels minus tall tiles)
