@@ -1694,7 +1694,9 @@ __global__ void __launch_bounds__(GemmCfg<kKind, kCtaGroup, kEpi, kN, kThin, kTa
                     }
                 };
 #pragma unroll 1
-                for (int u = half; u < C::NU; u += 2) {  // this pair of warps' units
+                // this pair of warps' units: the other half's of the 256-row part (BN = 80: the warps
+                // that drained 48 columns there drain 32 here, and vice versa -- 80 each)
+                for (int u = half ^ 1; u < C::NU; u += 2) {
                     if (kLastW == 32 || u + 1 < C::NU)
                         half_unit(std::integral_constant<int, 32>{}, u);
                     else
