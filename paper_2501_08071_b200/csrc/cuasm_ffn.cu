@@ -1536,12 +1536,14 @@ cuasm_status_t cuasm_ffn_forward_host(cuasm_ffn_t h, const void* x_host, const v
     if (M == 0) return forward_impl(h, h->x_stage, rms_w, w1, w3, h->out_stage, 0, K, N, eps, s);
     // Pipelined in row chunks: H2D of chunk i+1 (copy stream 1), the forward of
     // chunk i (the caller's stream) and D2H of chunk i-1 (copy stream 2) overlap;
-    // PCIe is full duplex, so a step costs ~ the larger transfer plus one chunk.
+    // PCIe is full duplex, so a step costs ~ the larger transfer plus one chunk (256-row chunks: 7B
+    // prefill e2e 342-366 -> 366-372 TFLOP/s vs 512-row ones; a second D2H stream measured slower,
+    // profiles/r02/e2e/).
     if (!h->h2d_stream) {
         CUASM_CHECK(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking), "cudaStreamCreate(h2d)");
         CUASM_CHECK(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking), "cudaStreamCreate(d2h)");
     }
-    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, M / 512));
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(16, M / 256));
     const int64_t rows_per = (M + nchunk - 1) / nchunk;
     const size_t nev = static_cast<size_t>(2 * nchunk + 2);
     while (h->copy_events.size() < nev) {
