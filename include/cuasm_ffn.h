@@ -380,7 +380,9 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
  * drift spread over all candidates): per round `warmup` untimed forwards, then `iters` timed
  * ones -- flush_l2 = 0: back to back between one CUDA-event pair on `stream`; flush_l2 = 1:
  * each after an L2 flush (a 2x-L2 buffer written, another read; the paper's evaluation
- * protocol) inside its own event pair -- a candidate's time being the best round's
+ * protocol) inside its own event pair, as one CUDA-graph launch of the forward (captured
+ * after the warm-up; eager when `stream` is the legacy NULL stream, which cannot be captured)
+ * -- a candidate's time being the best round's
  * mean per forward.  It keeps the fastest in the handle's table (replacing an entry of the
  * same shape) and returns it in *variant /
  * *flags (the encoding of cuasm_plan_config) and *best_us (any of them may be NULL).  From

@@ -865,9 +865,24 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     }
     // (k-loops of >= 48 k-blocks: a split must save more MMA time than its partial fixup costs;
     // the paper's fused_ff shape 512 x 2048 x 512 split three ways finished its tail 5 us late)
-    if (out_cols == 128 && !narrow_forced && KB >= 48 &&
-        ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles)))
-        return Plan{CUASM_VARIANT_1SM, true, 256, 0};
+    const bool few_tiles = KB >= 48 && ((M <= 256 && tiles_1sm <= kFewTiles) || (M <= 512 && tiles_1sm <= 2 * kFewTiles));
+    // Small-M tensor-parallel shards (32 < M <= 512, few tiles), bf16: the autotuner over K = 4096 /
+    // 8192, N_l = 1376..7168, M = 48..512 (scripts/tune_grid.py, profiles/r02/tune/grid.json) beat the
+    // 1-SM stream-K tile below by 5-20% with (a) M <= 128: the cluster split-K on 64-output 1-SM tiles
+    // (pull form; 3 ways when <= 32 tiles, else 2): 48 x 4096 x 1376 21.9 -> 18.2 us, 128 x 8192 x
+    // 3584 36.5 -> 33.8; (b) 2-SM 64-output tiles split in k (stream-K) when they fill at most half the
+    // CTA pairs: 192 x 4096 x 1376 25.2 -> 21.2; (c) else 2-SM 80-output whole tiles: 256 x 4096 x
+    // 2752 28.6 -> 24.4, 512 x 4096 x 1376 28.0 -> 24.3 -- when those fit one round of the pairs;
+    // otherwise the cost model below (48 x 8192 x 7168: 2-SM 112-wide, 48.5 vs 48.4 us)
+    const bool small_m_shard = out_cols == 128 && esize == 2 && !narrow_forced && few_tiles && M > 32;
+    if (small_m_shard) {
+        if (M <= 128 && tiles_64 * 2 <= sm_count)
+            return Plan{CUASM_VARIANT_1SM, false, 256, (tiles_64 * 3 <= sm_count && tiles_64 <= kFewTiles) ? 3 : 2, 64};
+        const int64_t mblk_2sm = (M + 255) / 256;
+        if (mblk_2sm * ((N + 63) / 64) * 2 <= sm_count / 2) return Plan{CUASM_VARIANT_2SM, true, 256, 0, 64};
+        if (mblk_2sm * ((N + 79) / 80) <= sm_count / 2) return Plan{CUASM_VARIANT_2SM, false, 256, 0, 80};
+    }
+    if (out_cols == 128 && !narrow_forced && few_tiles && !small_m_shard) return Plan{CUASM_VARIANT_1SM, true, 256, 0};
     // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
     // 512 x 2048 x 512): latency-bound, and the 1-SM variant skips the cluster launch,
     // cluster barriers and 2-SM TMEM allocation -- 16.4 vs 18.3 us (GEMM mode, 128-wide
@@ -891,7 +906,9 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     } else {
         // (narrow 2-SM tiles were measured from M = 256 up; decode-sized M keeps 128 unless forced)
         for (int bn : kTileBNs)
-            if ((bn == kPackBN || (esize == 2 && (M > 128 || tile_bn_force))) &&
+            // (small-M shards past the rules above: narrow tiles from M = 33 -- 48 x 8192 x 7168:
+            // 2-SM 112-wide 49.9 us vs 1-SM 128-wide stream-K 52.0, profiles/r02/tune/grid.json)
+            if ((bn == kPackBN || (esize == 2 && (M > (small_m_shard ? 32 : 128) || tile_bn_force))) &&
                 (tile_bn_force ? bn == tile_bn_force : true))
                 cands[nc++] = Cand{256, bn};
     }
@@ -1255,13 +1272,9 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
         }
     auto flush = [&]() {
         if (!fbuf) return cudaSuccess;
-        cudaError_t e = cudaMemsetAsync(fbuf, 0, static_cast<size_t>(fbytes), s);
-        if (e == cudaSuccess) {
-            cuasm::l2_flush_read_kernel<<<2 * h->sm_count, 512, 0, s>>>(
-                reinterpret_cast<const uint4*>(static_cast<char*>(fbuf) + fbytes), fbytes / 16);
-            e = cudaGetLastError();
-        }
-        return e;
+        cuasm::l2_flush_kernel<<<2 * h->sm_count, 512, 0, s>>>(
+            static_cast<uint4*>(fbuf), reinterpret_cast<uint4*>(static_cast<char*>(fbuf) + fbytes), fbytes / 16);
+        return cudaGetLastError();
     };
     // candidates measured in kTuneRounds interleaved rounds (clock / power drift spreads over
     // all of them), a candidate's time = the best of its rounds' means
@@ -1275,13 +1288,37 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
             h->plan_forced = true;
             h->plan_force = cands[ci];
             st = CUASM_OK;
-            for (int w = 0; w < warmup && st == CUASM_OK; ++w) st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+            for (int w = 0; w < (warmup > 0 ? warmup : 1) && st == CUASM_OK; ++w)
+                st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
             cudaError_t ce = cudaSuccess;
+            // flush_l2: each timed forward is one CUDA-graph launch (captured after the warm-up, whose
+            // first forward did any packing / allocation), as bench.py times a step -- an eager
+            // launch would let PDL start the kernel under the flush's tail and hide its prologue
+            cudaGraphExec_t gexec = nullptr;
+            if (st == CUASM_OK && flush_l2 && s != nullptr) {
+                cudaGraph_t graph = nullptr;
+                if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                    const cuasm_status_t cst = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                    if (cudaStreamEndCapture(s, &graph) != cudaSuccess || cst != CUASM_OK ||
+                        cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
+                        gexec = nullptr;
+                    if (graph) cudaGraphDestroy(graph);
+                }
+                (void)cudaGetLastError();  // (capture failures fall back to eager launches)
+                h->err.clear();
+            }
             if (st == CUASM_OK && !flush_l2) ce = cudaEventRecord(ev[0], s);
             for (int i = 0; i < iters && st == CUASM_OK && ce == cudaSuccess; ++i) {
                 if (flush_l2 && (ce = flush()) == cudaSuccess) ce = cudaEventRecord(ev[2 * i], s);
-                if (ce == cudaSuccess) st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                if (ce == cudaSuccess) {
+                    if (gexec) ce = cudaGraphLaunch(gexec, s);
+                    else st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                }
                 if (flush_l2 && st == CUASM_OK && ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i + 1], s);
+            }
+            if (gexec) {
+                if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+                cudaGraphExecDestroy(gexec);
             }
             if (st == CUASM_OK && ce == cudaSuccess && !flush_l2) ce = cudaEventRecord(ev[1], s);
             if (st == CUASM_OK && ce == cudaSuccess) ce = cudaStreamSynchronize(s);

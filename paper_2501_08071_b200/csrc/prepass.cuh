@@ -143,16 +143,20 @@ __global__ void __launch_bounds__(256) ffn_rmsnorm_kernel(const T* __restrict__ 
     for (int64_t i = lane + kCache * 32; i < nvec; i += 32) orow[i] = scale_vec(__ldcg(xr + i), __ldg(g4 + i), r, T{});
 }
 
-// cuasm_ffn_tune's L2 flush (not on the hot path): read n16 16-byte words so the dirty lines a
-// preceding memset left in L2 are written back before the timed forward, not during it.
-__global__ void __launch_bounds__(512) l2_flush_read_kernel(const uint4* __restrict__ p, int64_t n16) {
+// cuasm_ffn_tune's L2 flush (not on the hot path): write n16 16-byte words of `w` through L2 (a
+// kernel, not cudaMemsetAsync, whose large fills measured no eviction), then read n16 words of
+// `r` so the written lines are cleaned before the timed forward.  The data-dependent store keeps
+// the loads alive (it fires only if the words XOR to the constant; `r` is scratch either way).
+__global__ void __launch_bounds__(512) l2_flush_kernel(uint4* __restrict__ w, uint4* __restrict__ r, int64_t n16) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    for (int64_t i = i0; i < n16; i += stride) w[i] = make_uint4(0u, 0u, 0u, 0u);
     uint32_t acc = 0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const uint4 v = p[i];
+    for (int64_t i = i0; i < n16; i += stride) {
+        const uint4 v = r[i];
         acc ^= v.x ^ v.y ^ v.z ^ v.w;
     }
-    if (acc == 0x9E3779B9u && n16 < 0) reinterpret_cast<uint32_t*>(const_cast<uint4*>(p))[0] = acc;  // never true
+    if (acc == 0x9E3779B9u) r[i0 < n16 ? i0 : 0].x = acc;
 }
 
 }  // namespace cuasm

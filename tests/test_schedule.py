@@ -143,13 +143,22 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
              2 if 2 * t1 <= sm_count and t1 <= 64 else 0)
         if S:
             return ("1sm", False, 256, S, 128)
-    if out_cols == 128 and KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64)):
+    few = KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64))
+    small_m = out_cols == 128 and esize == 2 and few and M > 32   # small-M TP shards (profiles/r02/tune/grid.json)
+    if small_m:
+        if M <= 128 and 2 * t64 <= sm_count:
+            return ("1sm", False, 256, 3 if (3 * t64 <= sm_count and t64 <= 32) else 2, 64)
+        if 2 * (-(-M // 256) * -(-N // 64)) <= sm_count // 2:
+            return ("2sm", True, 256, 0, 64)
+        if -(-M // 256) * -(-N // 80) <= sm_count // 2:
+            return ("2sm", False, 256, 0, 80)
+    if out_cols == 128 and few and not small_m:
         return ("1sm", True, 256, 0, 128)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
     if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
         return ("1sm", False, 128, 0, 128)
     best, best_t = ("2sm", False, 256, 0, 128), 1e30
     if out_cols == 128:   # SwiGLU tile widths (narrower than 128: 2-SM bf16 only)
-        cands = [(256, bn) for bn in (128, 120, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > 128)]
+        cands = [(256, bn) for bn in (128, 120, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > (32 if small_m else 128))]
     else:
         cands = [(256, 128), (128, 128)]
     for tn, bn in cands:
@@ -305,23 +314,25 @@ def test_plan_tile_width_matches_measured_best(lib_plan, shape):
 
 
 # measured (profiles/r01/csplit/ncu_ab_*.txt, profiles/r02/tune_decode_bn.log): the cluster
-# split-K wins on few-tile shards with M <= 32 and loses at M >= 64 (pull-form reduction); with
-# 64-output tiles (up to 74 of them) a split of 3 (2) beats the 128-output tile's; 65 128-wide
-# tiles: no gain
+# split-K wins on few-tile shards with M <= 32; with 64-output tiles (up to 74 of them) a split of
+# 3 (2) beats the 128-output tile's; 65 128-wide tiles: no gain.  On 128-output tiles it loses at
+# M >= 64 (pull-form reduction), but on 64-output tiles the autotuner found it best up to M = 128
+# (profiles/r02/tune/grid.json: 64 x 4096 x 1376 18.7 us vs 21.9 for the 1-SM stream-K tile)
 @pytest.mark.parametrize("M,K,N,cs,bn", [(16, 4096, 1376, 3, 64), (16, 4096, 2752, 3, 64), (16, 8192, 3584, 2, 64),
                                          (32, 4096, 1376, 3, 64), (1, 4096, 1376, 3, 64), (16, 4096, 5504, 3, 128),
                                          (32, 4096, 5504, 2, 128), (16, 4096, 6880, 2, 128),
                                          (16, 8192, 7168, 2, 128), (16, 4096, 8256, 0, 128),
-                                         (64, 4096, 1376, 0, 128), (128, 4096, 1376, 0, 128),
+                                         (64, 4096, 1376, 3, 64), (128, 4096, 1376, 3, 64),
+                                         (96, 4096, 2752, 2, 64), (128, 8192, 3584, 2, 64),
                                          (16, 4096, 11008, 0, 128)])
 def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
     assert plan_config(M, K, N)[3:] == (cs, bn)
     assert lib_plan(M, K, N)[3:] == (cs, bn)
 
 
-# every cluster split the planner picks must take the push form (dual_gemm.cuh split_k_push_fits:
+# every cluster split the planner picks at M <= 32 must take the push form (dual_gemm.cuh split_k_push_fits:
 # bf16, <= 32 rows, ceil(NU / S) * S * rc * 128 bytes of slots within the 32 KB staging area, NU =
-# 2 BN / 16 units, rc = 16 or 32 slot rows); the pull form is only reachable by forcing CUASM_OPT_CSPLIT
+# 2 BN / 16 units, rc = 16 or 32 slot rows); the pull form is what the 64-output splits at 32 < M <= 128 use
 @pytest.mark.parametrize("K", [4096, 8192])
 def test_planner_cluster_splits_take_the_push_form(K):
     for M in range(1, 33):
@@ -334,3 +345,26 @@ def test_planner_cluster_splits_take_the_push_form(K):
                 nu = 2 * bn // 16 // 2
                 assert -(-nu // S) * S * rc * 128 <= 32768, (M, N, S, bn)
                 assert -(-N // bn) * S <= 148
+
+
+# the small-M shard rules (32 < M <= 512, few tiles) against the autotuner's grid: the plan's measured
+# time is within 10% of the best candidate's at every grid shape the rules cover, and never slower
+# than the 1-SM stream-K tile they replaced (profiles/r02/tune/grid.json, L2-flushed, one B200)
+def test_small_m_shard_rules_match_the_tuned_grid():
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    grid = json.load(open(os.path.join(root, "profiles", "r02", "tune", "grid.json")))
+    checked = 0
+    for r in grid["rows"]:
+        M, K, N = r["M"], r["K"], r["N"]
+        if not 32 < M <= 512:
+            continue
+        pl = list(plan_config(M, K, N))
+        t = r["all"].get(str(pl))
+        assert t is not None, (M, K, N, pl)
+        assert t <= 1.10 * r["best_us"], (M, K, N, pl, t, r["best"], r["best_us"])
+        if r["model"] == ["1sm", True, 256, 0, 128]:   # shapes the replaced rule used to take
+            assert t <= r["model_us"] * 1.02, (M, K, N, pl, t, r["model_us"])
+        checked += 1
+    assert checked >= 30
