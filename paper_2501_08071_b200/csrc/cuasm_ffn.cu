@@ -876,6 +876,10 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // otherwise the cost model below (48 x 8192 x 7168: 2-SM 112-wide, 48.5 vs 48.4 us)
     const bool small_m_shard = out_cols == 128 && esize == 2 && !narrow_forced && few_tiles && M > 32;
     if (small_m_shard) {
+        // (<= 64 rows: a split of 2 or 4, whose partials fit the push form's staging slots --
+        // 48 x 4096 x 1376 22.5 (pull, S = 3) -> 18.5 us, profiles/r02/push64/)
+        if (M <= 64 && tiles_64 * 2 <= sm_count)
+            return Plan{CUASM_VARIANT_1SM, false, 256, tiles_64 * 4 <= sm_count ? 4 : 2, 64};
         if (M <= 128 && tiles_64 * 2 <= sm_count)
             return Plan{CUASM_VARIANT_1SM, false, 256, (tiles_64 * 3 <= sm_count && tiles_64 <= kFewTiles) ? 3 : 2, 64};
         const int64_t mblk_2sm = (M + 255) / 256;

@@ -773,11 +773,13 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
     if (ewarp == 0 && lane == 0) trace_stamp(p, 11);  // this CTA's share stored
 }
 
-// Cluster split-K, push form (bf16 output, tiles with <= 32 valid rows, whose
+// Cluster split-K, push form (bf16 output, tiles with <= 64 valid rows, whose
 // partials fit the TMA-store staging area this mode leaves unused).  The accumulator
 // is cut into units of 16 columns of chunk a + the same 16 of chunk b (8 units per
 // 256-column tile); unit u belongs to CTA u % S, so with S <= 8 every CTA owns one.
-// (a) The warp of TMEM quadrant 0 holding unit u reads it (lane = row) and writes it
+// Rows 0..31 live in TMEM lane quadrant 0, rows 32..63 in quadrant 1, each drained by
+// that quadrant's two warps (slot rows rc = 16, 32 or 64).
+// (a) The warp of the TMEM quadrant holding unit u's rows reads it (lane = row) and writes it
 // into slot [u / S][its rank] of the owner's staging area: plain shared-memory stores
 // for its own units, st.async with a transaction-count credit on the owner's barrier
 // for the others -- no copy, flag or remote read on the way; (b) the owner waits for
@@ -789,11 +791,13 @@ struct PushUnits {
     static constexpr int NUNIT = C::UMMA_N / 32;  // 16-column units (a and b halves)
 };
 
+__host__ __device__ __forceinline__ int push_slot_rows(int rows) { return rows <= 16 ? 16 : rows <= 32 ? 32 : 64; }
+
 template <class C, int kKind>
 __device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
-    if (kKind != 0 || rows > 32) return false;
+    if (kKind != 0 || rows > 64) return false;
     constexpr int NU = PushUnits<C>::NUNIT;
-    return ((NU + S - 1) / S) * S * (rows <= 16 ? 16 : 32) * 128 <= C::STG_BYTES;
+    return ((NU + S - 1) / S) * S * push_slot_rows(rows) * 128 <= C::STG_BYTES;
 }
 
 // The owner's reduction of one unit for this lane's row (split_k_push (b)): sum the
@@ -850,17 +854,18 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
     const int S = p.csplit;
     const int row0 = mb * C::TILE_M;
     const int rows = min(C::BM, p.M - row0);
-    const int rc = rows <= 16 ? 16 : 32;  // slot rows
+    const int rc = push_slot_rows(rows);  // slot rows
     const uint32_t stg_u = ptx::smem_u32(stg), rbar_u = ptx::smem_u32(rbar);
     if (!dry && ewarp == 0 && lane == 0 && static_cast<int>(part) < NU) {
         const int owned = (NU - 1 - static_cast<int>(part)) / S + 1;
         ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 128));
     }
-    if (quad != 0) return;  // every valid row lives in TMEM lane quadrant 0
-    const bool row_ok = static_cast<int>(lane) < rows;
+    if (static_cast<int>(quad) * 32 >= rows || quad >= 2) return;  // quadrants 0 (rows 0..31) and 1 (32..63)
+    const int qrow = static_cast<int>(quad) * 32;  // this quadrant's first row
+    const bool row_ok = qrow + static_cast<int>(lane) < rows;
     // reduction (b): with <= 16 rows two lanes share a row, 8 of its 16 unit columns each
     const bool pair_lanes = rows <= 16;
-    const int rrow = pair_lanes ? static_cast<int>(lane >> 1) : static_cast<int>(lane);
+    const int rrow = pair_lanes ? static_cast<int>(lane >> 1) : qrow + static_cast<int>(lane);
     const bool red_ok = rrow < rows;
     const float rr = red_ok && p.use_r ? __ldcg(p.r + row0 + rrow) : 1.f;  // early: hidden by (a)
 #if CUASM_DIAG  // experiments only: SM-cycle stamps of the phases into trace slots 12..15
@@ -875,7 +880,7 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         ptx::cluster_wait_acquire();
         cl_pending = false;
     }
-    const uint32_t t_row = tmem_base + acc * C::ACC_STRIDE;
+    const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * C::ACC_STRIDE;
     const uint32_t swz = lane & 7;
     // (a) scatter this warp's units to their owners
 #pragma unroll 1
@@ -892,7 +897,8 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         for (int h = 0; h < 2; ++h) {
             const int u = 2 * (half * C::PAIRS + i) + h;
             const uint32_t owner = static_cast<uint32_t>(u % S);
-            const uint32_t off = static_cast<uint32_t>(((u / S) * S + static_cast<int>(part)) * rc + lane) * 128;
+            const uint32_t off =
+                static_cast<uint32_t>(((u / S) * S + static_cast<int>(part)) * rc + qrow + static_cast<int>(lane)) * 128;
             if (owner == part) {
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {

@@ -146,6 +146,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     few = KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64))
     small_m = out_cols == 128 and esize == 2 and few and M > 32   # small-M TP shards (profiles/r02/tune/grid.json)
     if small_m:
+        if M <= 64 and 2 * t64 <= sm_count:   # push-form splits (2 or 4 fit its slots)
+            return ("1sm", False, 256, 4 if 4 * t64 <= sm_count else 2, 64)
         if M <= 128 and 2 * t64 <= sm_count:
             return ("1sm", False, 256, 3 if (3 * t64 <= sm_count and t64 <= 32) else 2, 64)
         if 2 * (-(-M // 256) * -(-N // 64)) <= sm_count // 2:
@@ -322,7 +324,7 @@ def test_plan_tile_width_matches_measured_best(lib_plan, shape):
                                          (32, 4096, 1376, 3, 64), (1, 4096, 1376, 3, 64), (16, 4096, 5504, 3, 128),
                                          (32, 4096, 5504, 2, 128), (16, 4096, 6880, 2, 128),
                                          (16, 8192, 7168, 2, 128), (16, 4096, 8256, 0, 128),
-                                         (64, 4096, 1376, 3, 64), (128, 4096, 1376, 3, 64),
+                                         (64, 4096, 1376, 4, 64), (48, 4096, 2752, 2, 64), (128, 4096, 1376, 3, 64),
                                          (96, 4096, 2752, 2, 64), (128, 8192, 3584, 2, 64),
                                          (16, 4096, 11008, 0, 128)])
 def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
@@ -330,18 +332,18 @@ def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
     assert lib_plan(M, K, N)[3:] == (cs, bn)
 
 
-# every cluster split the planner picks at M <= 32 must take the push form (dual_gemm.cuh split_k_push_fits:
+# every cluster split the planner picks at M <= 64 must take the push form (dual_gemm.cuh split_k_push_fits:
 # bf16, <= 32 rows, ceil(NU / S) * S * rc * 128 bytes of slots within the 32 KB staging area, NU =
-# 2 BN / 16 units, rc = 16 or 32 slot rows); the pull form is what the 64-output splits at 32 < M <= 128 use
+# 2 BN / 16 units, rc = 16, 32 or 64 slot rows); the pull form is what the 64-output splits at 64 < M <= 128 use
 @pytest.mark.parametrize("K", [4096, 8192])
 def test_planner_cluster_splits_take_the_push_form(K):
-    for M in range(1, 33):
+    for M in range(1, 65):
         for n8 in range(1, 160):
             N = 64 * n8
             pl = plan_config(M, K, N)
             S, bn = pl[3], pl[4]
             if S:
-                rc = 16 if M <= 16 else 32
+                rc = 16 if M <= 16 else 32 if M <= 32 else 64
                 nu = 2 * bn // 16 // 2
                 assert -(-nu // S) * S * rc * 128 <= 32768, (M, N, S, bn)
                 assert -(-N // bn) * S <= 148
@@ -358,7 +360,8 @@ def test_small_m_shard_rules_match_the_tuned_grid():
     checked = 0
     for r in grid["rows"]:
         M, K, N = r["M"], r["K"], r["N"]
-        if not 32 < M <= 512:
+        t1 = -(-M // 128) * -(-N // 128)
+        if not (32 < M <= 512 and ((M <= 256 and t1 <= 32) or t1 <= 64)):   # the rules' few-tile region
             continue
         pl = list(plan_config(M, K, N))
         t = r["all"].get(str(pl))
@@ -367,4 +370,4 @@ def test_small_m_shard_rules_match_the_tuned_grid():
         if r["model"] == ["1sm", True, 256, 0, 128]:   # shapes the replaced rule used to take
             assert t <= r["model_us"] * 1.02, (M, K, N, pl, t, r["model_us"])
         checked += 1
-    assert checked >= 30
+    assert checked >= 25
