@@ -876,12 +876,14 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
     // otherwise the cost model below (48 x 8192 x 7168: 2-SM 112-wide, 48.5 vs 48.4 us)
     const bool small_m_shard = out_cols == 128 && esize == 2 && !narrow_forced && few_tiles && M > 32;
     if (small_m_shard) {
-        // (<= 64 rows: a split of 2 or 4, whose partials fit the push form's staging slots --
-        // 48 x 4096 x 1376 22.5 (pull, S = 3) -> 18.5 us, profiles/r02/push64/)
-        if (M <= 64 && tiles_64 * 2 <= sm_count)
-            return Plan{CUASM_VARIANT_1SM, false, 256, tiles_64 * 4 <= sm_count ? 4 : 2, 64};
-        if (M <= 128 && tiles_64 * 2 <= sm_count)
-            return Plan{CUASM_VARIANT_1SM, false, 256, (tiles_64 * 3 <= sm_count && tiles_64 <= kFewTiles) ? 3 : 2, 64};
+        // (a split of 4, else 2: their partials fit the push form's 64 KB of slots on this tile --
+        // 48 / 96 / 128 x 4096 x 1376 22.5 / 22.5 / 22.9 (pull, S = 3) -> 18.5 / 18.9 / 20.5 us,
+        // 128 x 8192 x 3584 34.8 -> 32.8, profiles/r02/push64/; with more m-blocks while a split of 2
+        // still fits the SMs: 192 / 384 x 4096 x 1376 21.9 / 23.9 -> 20.5 / 21.6, grid.json)
+        // (3 ways where 4 do not fit and the 3-way slots do, <= 64 rows: 48 x 4096 x 2752 21.1 -> 19.9)
+        if (tiles_64 * 2 <= sm_count)
+            return Plan{CUASM_VARIANT_1SM, false, 256,
+                        tiles_64 * 4 <= sm_count ? 4 : (M <= 64 && tiles_64 * 3 <= sm_count) ? 3 : 2, 64};
         const int64_t mblk_2sm = (M + 255) / 256;
         if (mblk_2sm * ((N + 63) / 64) * 2 <= sm_count / 2) return Plan{CUASM_VARIANT_2SM, true, 256, 0, 64};
         if (mblk_2sm * ((N + 79) / 80) <= sm_count / 2) return Plan{CUASM_VARIANT_2SM, false, 256, 0, 80};

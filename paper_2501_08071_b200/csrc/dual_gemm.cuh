@@ -432,7 +432,9 @@ struct GemmCfg {
     // 7 x 32 KB 1-SM/128, 9 x 24 KB 2-SM/128)
     // bf16 output goes through TMA stores from a per-warp staging area: two 32 x 32
     // boxes (2 KB each, 64-byte swizzle) per epilogue warp
-    static constexpr int STG_WARP_BYTES = kKind == 0 ? 4096 : 0;
+    // (the 1-SM 64-output SwiGLU tile -- the decode / small-M shard tile -- reserves 8 KB per warp: the
+    // cluster split-K's push form slots for up to 128 rows with S <= 4 live here, 64 KB)
+    static constexpr int STG_WARP_BYTES = kKind == 0 ? ((kCtaGroup == 1 && kEpi == 0 && kN == 128) ? 8192 : 4096) : 0;
     static constexpr int STG_BYTES = 8 * STG_WARP_BYTES;
     static constexpr int STAGES_FIT = (232448 - BAR_BYTES - 1024 - STG_BYTES) / STAGE_BYTES;
 #ifdef CUASM_STAGE_CAP  // experiments only: cap the pipeline depth
@@ -774,11 +776,12 @@ __device__ __forceinline__ void split_k_reduce(const FfnGemmParams& p, uint32_t 
 }
 
 // Cluster split-K, push form (bf16 output, tiles with <= 64 valid rows, whose
-// partials fit the TMA-store staging area this mode leaves unused).  The accumulator
+// partials fit the TMA-store staging area this mode leaves unused; up to 128 rows on the
+// 64-output tile, whose staging area is 64 KB).  The accumulator
 // is cut into units of 16 columns of chunk a + the same 16 of chunk b (8 units per
 // 256-column tile); unit u belongs to CTA u % S, so with S <= 8 every CTA owns one.
-// Rows 0..31 live in TMEM lane quadrant 0, rows 32..63 in quadrant 1, each drained by
-// that quadrant's two warps (slot rows rc = 16, 32 or 64).
+// Rows 32q..32q+31 live in TMEM lane quadrant q, drained by that quadrant's two warps
+// (slot rows rc = 16, 32, 64 or 128).
 // (a) The warp of the TMEM quadrant holding unit u's rows reads it (lane = row) and writes it
 // into slot [u / S][its rank] of the owner's staging area: plain shared-memory stores
 // for its own units, st.async with a transaction-count credit on the owner's barrier
@@ -791,11 +794,13 @@ struct PushUnits {
     static constexpr int NUNIT = C::UMMA_N / 32;  // 16-column units (a and b halves)
 };
 
-__host__ __device__ __forceinline__ int push_slot_rows(int rows) { return rows <= 16 ? 16 : rows <= 32 ? 32 : 64; }
+__host__ __device__ __forceinline__ int push_slot_rows(int rows) {
+    return rows <= 16 ? 16 : rows <= 32 ? 32 : rows <= 64 ? 64 : 128;
+}
 
 template <class C, int kKind>
 __device__ __forceinline__ bool split_k_push_fits(int rows, int S) {
-    if (kKind != 0 || rows > 64) return false;
+    if (kKind != 0 || rows > 128) return false;
     constexpr int NU = PushUnits<C>::NUNIT;
     return ((NU + S - 1) / S) * S * push_slot_rows(rows) * 128 <= C::STG_BYTES;
 }
@@ -860,7 +865,7 @@ __device__ __forceinline__ void split_k_push(const FfnGemmParams& p, uint32_t tm
         const int owned = (NU - 1 - static_cast<int>(part)) / S + 1;
         ptx::mbar_arrive_expect_tx(rbar_u, static_cast<uint32_t>(owned * (S - 1) * rows * 128));
     }
-    if (static_cast<int>(quad) * 32 >= rows || quad >= 2) return;  // quadrants 0 (rows 0..31) and 1 (32..63)
+    if (static_cast<int>(quad) * 32 >= rows) return;  // quadrant q holds rows 32q..32q+31
     const int qrow = static_cast<int>(quad) * 32;  // this quadrant's first row
     const bool row_ok = qrow + static_cast<int>(lane) < rows;
     // reduction (b): with <= 16 rows two lanes share a row, 8 of its 16 unit columns each

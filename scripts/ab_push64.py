@@ -1,5 +1,6 @@
 """A/B of the cluster split-K at 33..64 rows (64-output 1-SM tiles, forced S): push form (new lib)
-vs pull form (old lib), L2-flushed bench-protocol step times.  python scripts/ab_push64.py LABEL"""
+vs pull form (old lib), L2-flushed bench-protocol step times.
+python scripts/ab_push64.py LABEL [MxKxN,...]"""
 import os
 import sys
 
@@ -15,7 +16,10 @@ from scripts.tune import time_cfg
 dev = torch.device("cuda:0")
 flush = bench.L2Flush(dev)
 res = {}
-for (M, K, N) in ((33, 4096, 1376), (48, 4096, 1376), (64, 4096, 1376), (64, 4096, 2752), (48, 8192, 3584)):
+SHAPES = ((33, 4096, 1376), (48, 4096, 1376), (64, 4096, 1376), (64, 4096, 2752), (48, 8192, 3584))
+if len(sys.argv) > 2:
+    SHAPES = tuple(tuple(int(v) for v in sh.split("x")) for sh in sys.argv[2].split(","))
+for (M, K, N) in SHAPES:
     t = make_device_inputs(M, K, N, 3, dev)
     out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     for S in (2, 3, 4):

@@ -146,10 +146,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
     few = KB >= 48 and ((M <= 256 and t1 <= 32) or (M <= 512 and t1 <= 64))
     small_m = out_cols == 128 and esize == 2 and few and M > 32   # small-M TP shards (profiles/r02/tune/grid.json)
     if small_m:
-        if M <= 64 and 2 * t64 <= sm_count:   # push-form splits (2 or 4 fit its slots)
-            return ("1sm", False, 256, 4 if 4 * t64 <= sm_count else 2, 64)
-        if M <= 128 and 2 * t64 <= sm_count:
-            return ("1sm", False, 256, 3 if (3 * t64 <= sm_count and t64 <= 32) else 2, 64)
+        if 2 * t64 <= sm_count:   # push-form splits (2 or 4 fit its slots)
+            return ("1sm", False, 256, 4 if 4 * t64 <= sm_count else 3 if (M <= 64 and 3 * t64 <= sm_count) else 2, 64)
         if 2 * (-(-M // 256) * -(-N // 64)) <= sm_count // 2:
             return ("2sm", True, 256, 0, 64)
         if -(-M // 256) * -(-N // 80) <= sm_count // 2:
@@ -324,7 +322,8 @@ def test_plan_tile_width_matches_measured_best(lib_plan, shape):
                                          (32, 4096, 1376, 3, 64), (1, 4096, 1376, 3, 64), (16, 4096, 5504, 3, 128),
                                          (32, 4096, 5504, 2, 128), (16, 4096, 6880, 2, 128),
                                          (16, 8192, 7168, 2, 128), (16, 4096, 8256, 0, 128),
-                                         (64, 4096, 1376, 4, 64), (48, 4096, 2752, 2, 64), (128, 4096, 1376, 3, 64),
+                                         (64, 4096, 1376, 4, 64), (48, 4096, 2752, 3, 64), (128, 4096, 1376, 4, 64),
+                                         (256, 4096, 1376, 2, 64), (384, 4096, 1376, 2, 64), (512, 4096, 1376, 0, 80),
                                          (96, 4096, 2752, 2, 64), (128, 8192, 3584, 2, 64),
                                          (16, 4096, 11008, 0, 128)])
 def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
@@ -332,20 +331,22 @@ def test_plan_cluster_split_for_decode_shards(lib_plan, M, K, N, cs, bn):
     assert lib_plan(M, K, N)[3:] == (cs, bn)
 
 
-# every cluster split the planner picks at M <= 64 must take the push form (dual_gemm.cuh split_k_push_fits:
+# every cluster split the planner picks at M <= 128 must take the push form (dual_gemm.cuh split_k_push_fits:
 # bf16, <= 32 rows, ceil(NU / S) * S * rc * 128 bytes of slots within the 32 KB staging area, NU =
-# 2 BN / 16 units, rc = 16, 32 or 64 slot rows); the pull form is what the 64-output splits at 64 < M <= 128 use
+# 2 BN / 16 units, rc = 16, 32, 64 or 128 slot rows, 64 KB of staging on the 1-SM 64-output tile); the pull
+# form is only reachable by forcing CUASM_OPT_CSPLIT
 @pytest.mark.parametrize("K", [4096, 8192])
 def test_planner_cluster_splits_take_the_push_form(K):
-    for M in range(1, 65):
+    for M in list(range(1, 129)) + [160, 192, 256, 300, 384, 448, 512]:
         for n8 in range(1, 160):
             N = 64 * n8
             pl = plan_config(M, K, N)
             S, bn = pl[3], pl[4]
             if S:
-                rc = 16 if M <= 16 else 32 if M <= 32 else 64
+                rc = 16 if M <= 16 else 32 if M <= 32 else 64 if M <= 64 else 128
                 nu = 2 * bn // 16 // 2
-                assert -(-nu // S) * S * rc * 128 <= 32768, (M, N, S, bn)
+                stg = 65536 if bn == 64 else 32768   # (the 1-SM 64-output tile's staging area is 64 KB)
+                assert -(-nu // S) * S * rc * 128 <= stg, (M, N, S, bn)
                 assert -(-N // bn) * S <= 148
 
 
