@@ -184,8 +184,9 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index: int, period_s: float = 0.005):
-        self.period = period_s
+    def __init__(self, device_index: int, period_s: float = None):
+        # (CUASM_BENCH_NVML_PERIOD_S: sampling period override, for measuring the sampler's own cost)
+        self.period = period_s if period_s is not None else float(os.environ.get("CUASM_BENCH_NVML_PERIOD_S", "0.005"))
         self.samples = []
         self.max_mhz = None
         self.ok = False
