@@ -377,7 +377,8 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
  * configuration of the dual GEMM for this M x K x N (the cost model's choice, each 2-SM tile
  * width with whole tiles and a stream-K tail, the 1-SM tile, tall tiles where 256 < M <= 384,
  * the 1-SM cluster split-K of 2..8 CTAs), in three interleaved rounds (so clock and power
- * drift spread over all candidates): per round `warmup` untimed forwards, then `iters` timed
+ * drift spread over all candidates): per round `warmup` untimed forwards (at least one: the first
+ * packs the tile width's weights and sizes the workspaces before the graph capture), then `iters` timed
  * ones -- flush_l2 = 0: back to back between one CUDA-event pair on `stream`; flush_l2 = 1:
  * each after an L2 flush (a 2x-L2 buffer written, another read; the paper's evaluation
  * protocol) inside its own event pair, as one CUDA-graph launch of the forward (captured
