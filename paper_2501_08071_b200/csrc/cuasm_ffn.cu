@@ -67,6 +67,21 @@ struct PackedWeights {
     int tmap_rows = 0;
 };
 
+// A 2-D tensor map and every argument it was encoded from.  A map is a pure function of them (no
+// memory contents), so a cached one stays valid for as long as its arguments repeat -- even if the
+// memory at `base` was freed and reallocated in between.
+struct TmapKey {
+    const void* base;
+    uint64_t dims[2], stride;
+    uint32_t box[2];
+    int dtype, swizzle, promo;
+    bool operator==(const TmapKey& o) const {
+        return base == o.base && dims[0] == o.dims[0] && dims[1] == o.dims[1] && stride == o.stride &&
+               box[0] == o.box[0] && box[1] == o.box[1] && dtype == o.dtype && swizzle == o.swizzle && promo == o.promo;
+    }
+};
+constexpr int kTmapCache = 32;  // (x, its 64-row view, out maps of a few shapes / destinations)
+
 // One configuration of the dual-GEMM launch (plan_config_raw's answer, or a tuned one).
 struct Plan {
     int variant;
@@ -171,6 +186,14 @@ struct cuasm_ffn_s {
     int last_variant = 0;
     int last_kernels = 0;
     EncodeTiledFn encode = nullptr;
+    // host-side cache of encoded tensor maps (encode_cached): an eager forward re-encodes nothing
+    // whose pointer and shape it has seen.  (An eager forward's ~18 us of host time is ~10 us of
+    // cudaLaunchKernelEx with ~2.7 KB of parameters -- three maps, two 8-map output sets -- and
+    // ~4 us of validation / plan / workspace checks; scripts/host_overhead.py.  CUDA graphs, which
+    // bench.py and serving loops use, pay none of it.)
+    TmapKey tmap_key[kTmapCache] = {};
+    CUtensorMap tmap_val[kTmapCache];
+    int tmap_next = 0;
     // the paper's autotuner (cuasm_ffn_tune) and deploy-time lookup:
     // measured configurations per fused-FFN shape, consulted before the cost model
     std::string gpu_name;            // cudaDeviceProp::name: part of a tuned entry's key
@@ -266,17 +289,37 @@ cuasm_status_t ensure_func_attr(cuasm_ffn_t h, Kernel kernel, std::atomic<uint64
     return CUASM_OK;
 }
 
+// cuTensorMapEncodeTiled of a 2-D map through the handle's cache (TmapKey).
+CUresult encode_cached(cuasm_ffn_t h, CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                       uint64_t outer, uint64_t stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                       CUtensorMapSwizzle swz, CUtensorMapL2promotion promo) {
+    const TmapKey key{base, {inner, outer}, stride_bytes, {box_inner, box_outer}, static_cast<int>(dt),
+                      static_cast<int>(swz), static_cast<int>(promo)};
+    for (int i = 0; i < kTmapCache; ++i)
+        if (h->tmap_key[i] == key && key.base != nullptr) {
+            *map = h->tmap_val[i];
+            return CUDA_SUCCESS;
+        }
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = h->encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+        h->tmap_key[h->tmap_next] = key;
+        h->tmap_val[h->tmap_next] = *map;
+        h->tmap_next = (h->tmap_next + 1) % kTmapCache;
+    }
+    return r;
+}
+
 cuasm_status_t encode_2d(cuasm_ffn_t h, CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                          uint32_t box_inner, uint32_t box_outer) {
     const CUtensorMapDataType dt =
         h->dtype == CUASM_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {inner * static_cast<uint64_t>(h->esize)};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = h->encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = encode_cached(h, map, dt, base, inner, outer, inner * static_cast<uint64_t>(h->esize), box_inner,
+                                     box_outer, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (r != CUDA_SUCCESS)
         return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d, dims %llu x %llu)", (int)r,
                     (unsigned long long)inner, (unsigned long long)outer);
@@ -528,30 +571,24 @@ cuasm_status_t launch_gemm(cuasm_ffn_t h, const EpiSpec& e, const void* x, void*
             rs_cols(N, e.rs_world, q, c0, c1);
             const int64_t kq = c1 - c0;
             if (kq == 0) continue;  // owns no columns: no tile is ever sent there
-            cuuint64_t dims[2] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(M)};
-            cuuint64_t strides[1] = {static_cast<cuuint64_t>(kq) * pes};
-            cuuint32_t box[2] = {h->rs_bf16 ? 32u : 16u, 32};  // 64-byte box rows either way
-            cuuint32_t estr[2] = {1, 1};
             void* base = static_cast<char*>(e.rs_stage[q]) + static_cast<int64_t>(e.rs_rank) * M * kq * pes;
-            CUresult r = h->encode(&omaps.m[q], h->rs_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                   2, base, dims, strides, box, estr,
-                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            // (64-byte box rows either way)
+            CUresult r = encode_cached(h, &omaps.m[q], h->rs_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                       base, static_cast<uint64_t>(kq), static_cast<uint64_t>(M),
+                                       static_cast<uint64_t>(kq) * pes, h->rs_bf16 ? 32u : 16u, 32, CU_TENSOR_MAP_SWIZZLE_64B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(stage %d) failed (CUresult %d)", q, (int)r);
         }
     }
     for (int q = 0; p.tma_store && q < p.num_dst; ++q) {
         for (int hw = 0; hw < (kHalfUnit ? 2 : 1); ++hw) {
-            cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
-            cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldo) * static_cast<cuuint64_t>(h->esize)};
-            cuuint32_t box[2] = {hw ? kNarrowW : 32u, 32};
-            cuuint32_t estr[2] = {1, 1};
-            CUresult r = h->encode(hw ? &omaps_h.m[q] : &omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.dst[q], dims,
-                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   hw ? (kNarrowW == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE)
-                                      : CU_TENSOR_MAP_SWIZZLE_64B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CUresult r = encode_cached(h, hw ? &omaps_h.m[q] : &omaps.m[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.dst[q],
+                                       static_cast<uint64_t>(N), static_cast<uint64_t>(M),
+                                       static_cast<uint64_t>(p.ldo) * static_cast<uint64_t>(h->esize), hw ? kNarrowW : 32u, 32,
+                                       hw ? (kNarrowW == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE)
+                                          : CU_TENSOR_MAP_SWIZZLE_64B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(h, CUASM_ERR_CUDA, "cuTensorMapEncodeTiled(out %d) failed (CUresult %d)", q, (int)r);
         }
