@@ -187,9 +187,10 @@ struct cuasm_ffn_s {
     int last_kernels = 0;
     EncodeTiledFn encode = nullptr;
     // host-side cache of encoded tensor maps (encode_cached): an eager forward re-encodes nothing
-    // whose pointer and shape it has seen.  (An eager forward's ~18 us of host time is ~10 us of
-    // cudaLaunchKernelEx with ~2.7 KB of parameters -- three maps, two 8-map output sets -- and
-    // ~4 us of validation / plan / workspace checks; scripts/host_overhead.py.  CUDA graphs, which
+    // whose pointer and shape it has seen.  (An eager forward costs ~7 us of host time with the GPU
+    // busy, scripts/host_queue_probe.py -- a bare cudaLaunchKernelEx with the same 2.7 KB of
+    // parameters ~2.5 us, scripts/launch_param_probe.cu; with our own kernels completing
+    // concurrently the same loop reads ~18 us, scripts/host_overhead.py.  CUDA graphs, which
     // bench.py and serving loops use, pay none of it.)
     TmapKey tmap_key[kTmapCache] = {};
     CUtensorMap tmap_val[kTmapCache];
