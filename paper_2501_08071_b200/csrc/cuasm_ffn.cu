@@ -927,15 +927,13 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
         if (mblk_2sm * ((N + 79) / 80) <= sm_count / 2) return Plan{CUASM_VARIANT_2SM, false, 256, 0, 80};
     }
     if (out_cols == 128 && !narrow_forced && few_tiles && !small_m_shard) return Plan{CUASM_VARIANT_1SM, true, 256, 0};
-    // Short k-loops that fit one wave of 1-SM tiles (e.g. the paper's mmLeakyReLu shape,
-    // 512 x 2048 x 512): latency-bound, and the 1-SM variant skips the cluster launch,
-    // cluster barriers and 2-SM TMEM allocation -- 16.4 vs 18.3 us (GEMM mode, 128-wide
-    // tiles; scripts/tune_split_gemm.py)
-    // (GEMM mode only: its 128-wide 1-SM tile does the same MMA work per SM as the 2-SM
-    // tile, whereas a SwiGLU 1-SM tile pays the 16% smem penalty -- 2048 x 2048 x 512 FFN:
-    // 1-SM 23.8 vs 2-SM 23.0 us)
-    if (KB <= 32 && out_cols != 128 && ((M + 127) / 128) * ((N + 127) / 128) <= sm_count)
-        return Plan{CUASM_VARIANT_1SM, false, 128, 0};
+    // Short k-loops whose 128-wide 2-SM tiles fit one wave of the CTA pairs (GEMM mode, e.g. the
+    // paper's mmLeakyReLu shape 512 x 2048 x 512): whole 2-SM tiles.  (Round 1 measured the 1-SM
+    // tile ahead there, 16.4 vs 18.3 us; with the round-2 kernels it is behind: 512 x 2048 x 512
+    // 20.5 vs 18.4 us, 4096 x 2048 x 512 22.6 vs 20.5 -- scripts/tune.py --op gemm,
+    // profiles/r02/tune/tune_gemm_short_k.log)
+    if (KB <= 32 && out_cols != 128 && ((M + 255) / 256) * ((N + 127) / 128) <= sm_count / 2)
+        return Plan{CUASM_VARIANT_2SM, false, 128, 0};
     Plan best{CUASM_VARIANT_2SM, false, 256, 0};
     double best_t = 1e30;
     // candidates: the GEMM mode's MMA widths 256 / 128 (128 outputs, half the k-block time

@@ -154,8 +154,8 @@ def plan_config(M, K, N, esize=2, sm_count=148, out_cols=128):
             return ("2sm", False, 256, 0, 80)
     if out_cols == 128 and few and not small_m:
         return ("1sm", True, 256, 0, 128)   # few-tile decode shapes (csrc kFewTiles / kFewTilesSplit)
-    if KB <= 32 and out_cols != 128 and t1 <= sm_count:   # GEMM mode, short k-loops, one 1-SM wave
-        return ("1sm", False, 128, 0, 128)
+    if KB <= 32 and out_cols != 128 and -(-M // 256) * -(-N // 128) <= sm_count // 2:   # GEMM mode, short k, one 2-SM wave
+        return ("2sm", False, 128, 0, 128)
     best, best_t = ("2sm", False, 256, 0, 128), 1e30
     if out_cols == 128:   # SwiGLU tile widths (narrower than 128: 2-SM bf16 only)
         cands = [(256, bn) for bn in (128, 120, 112, 96, 80, 64) if bn == 128 or (esize == 2 and M > (32 if small_m else 128))]
@@ -268,7 +268,8 @@ GEMM_MEASURED = {
     (8192, 4096, 4096): {("2sm", False, 256)},
     (2048, 11008, 4096): {("2sm", False, 256)},
     (4096, 11008, 4096): {("2sm", False, 256)},
-    (512, 2048, 512): {("2sm", False, 128), ("1sm", False, 128)},
+    (512, 2048, 512): {("2sm", False, 128), ("2sm", False, 256)},
+    (4096, 2048, 512): {("2sm", False, 128), ("2sm", False, 256)},   # (r02: 20.5 vs 1-SM 22.6 us)
     (512, 11008, 4096): {("2sm", True, 256), ("1sm", True, 256)},
 }
 
