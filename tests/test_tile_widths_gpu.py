@@ -155,11 +155,13 @@ def test_tile_bn_option_contract(cuda_device):
 # ---- the 1-SM 64-output tile with the decode paths (row replication, cluster split-K) ----
 @pytest.mark.parametrize("csplit", [1, 2, 4, 6])
 @pytest.mark.parametrize("M,K,N", [(16, 4096, 1376), (1, 1024, 200), (32, 2048, 64 * 7 + 8), (48, 1024, 520),
-                                   (33, 1024, 200), (64, 2048, 64 * 5 + 8), (64, 4096, 1376)])
+                                   (33, 1024, 200), (64, 2048, 64 * 5 + 8), (64, 4096, 1376), (65, 1024, 392),
+                                   (96, 2048, 64 * 9 + 8), (128, 4096, 1376), (300, 2048, 64 * 7 + 24)])
 def test_decode_paths_bn64(cuda_device, M, K, N, csplit):
     """BN = 64 on the 1-SM kernel: replicated decode rows (csplit 1 = off), and the
-    cluster split-K with S CTAs per tile: the push form (TMEM lane quadrants 0 and 1) for
-    <= 64 rows when its slots fit the staging area (S = 2 and 4 here), the pull form else."""
+    cluster split-K with S CTAs per tile: the push form (TMEM lane quadrant q drains rows 32q..)
+    for <= 128 rows per tile when its slots fit the 64 KB staging area (S = 2 and 4 here, 6 up to
+    32 rows), the pull form else; 300 rows = three 128-row tiles per n-block."""
     d = make_inputs(M, K, N, family="C", seed=8700 + M + K + csplit, dtype="bf16")
     h = ffn.FusedFFN(cuda_device, torch.bfloat16)
     h.set_option(ffn.OPT_TILE_BN, 64)
