@@ -42,7 +42,7 @@ def _fwd(h, t, out=None):
 
 
 @pytest.mark.parametrize("M", [257, 288, 320, 321, 352, 384])
-@pytest.mark.parametrize("K,N", [(64, 248), (512, 88), (1024, 400), (320, 8)])
+@pytest.mark.parametrize("K,N", [(64, 248), (512, 88), (1024, 400), (320, 8), (200, 168)])
 def test_forced_tall_matches_oracle(cuda_device, M, K, N):
     d = make_inputs(M, K, N, family="C", seed=9100 + M + K + N, dtype="bf16")
     t = {k: v.to(cuda_device) for k, v in d.items()}

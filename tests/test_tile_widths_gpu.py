@@ -156,7 +156,8 @@ def test_tile_bn_option_contract(cuda_device):
 @pytest.mark.parametrize("csplit", [1, 2, 4, 6])
 @pytest.mark.parametrize("M,K,N", [(16, 4096, 1376), (1, 1024, 200), (32, 2048, 64 * 7 + 8), (48, 1024, 520),
                                    (33, 1024, 200), (64, 2048, 64 * 5 + 8), (64, 4096, 1376), (65, 1024, 392),
-                                   (96, 2048, 64 * 9 + 8), (128, 4096, 1376), (300, 2048, 64 * 7 + 24)])
+                                   (96, 2048, 64 * 9 + 8), (128, 4096, 1376), (300, 2048, 64 * 7 + 24),
+                                   (100, 1000, 392)])
 def test_decode_paths_bn64(cuda_device, M, K, N, csplit):
     """BN = 64 on the 1-SM kernel: replicated decode rows (csplit 1 = off), and the
     cluster split-K with S CTAs per tile: the push form (TMEM lane quadrant q drains rows 32q..)
