@@ -118,3 +118,31 @@ def test_fp32_full_entropy_vs_fold_tf32(cuda_device, M, K, N, variant):
     torch.cuda.synchronize()
     ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_tf32")
     check(out, ref, f"fp32 family C {M}x{K}x{N} v{variant}")
+
+
+def _small_m_fuzz_shapes(n=36, seed=2026):
+    rng = np.random.default_rng(seed)
+    shapes = []
+    for _ in range(n):
+        M = int(rng.integers(33, 513))
+        K = int(rng.integers(48, 513)) * 8        # 384 .. 4096, multiples of 8 (>= 48 k-blocks only sometimes)
+        N = int(rng.integers(8, 513)) * 8         # 64 .. 4096
+        shapes.append((M, K, N))
+    return shapes
+
+
+@pytest.mark.parametrize("M,K,N", _small_m_fuzz_shapes())
+def test_small_m_planner_fuzz(cuda_device, M, K, N):
+    """Random small-M shard shapes through whatever the configuration model picks (the cluster
+    split-K push form on 64-wide tiles up to 128 rows per tile, 2-SM narrow tiles, stream-K, tall
+    tiles): sampled rows (every 128-row tile) against the oracle, bitwise run-to-run."""
+    d = make_inputs(M, K, N, family="C", seed=7700 + M + K + N, dtype="bf16")
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    t = {k: v.to(cuda_device) for k, v in d.items()}
+    out = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    again = h.forward(t["x"], t["g"], t["w1"], t["w3"], 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(out, again)
+    rows = sample_rows(M, 6, M + N)
+    ref = oracle.ffn(d["x"], d["g"], d["w1"], d["w3"], 1e-6, mode="fold_bf16", rows=rows)
+    check(out[rows], ref, f"fuzz {M}x{K}x{N} plan {ffn.plan_config(M, K, N)}")
