@@ -373,3 +373,16 @@ def test_small_m_shard_rules_match_the_tuned_grid():
             assert t <= r["model_us"] * 1.02, (M, K, N, pl, t, r["model_us"])
         checked += 1
     assert checked >= 25
+
+
+# tall tiles (257..384 rows, bf16 SwiGLU; csrc kTallBN = 80): the flags word's bit 2, decoded by the
+# binding as the variant name "tall"; the Python mirror agrees across the region's edges
+@pytest.mark.parametrize("M", [256, 257, 288, 320, 384, 385])
+def test_library_plan_tall_region(lib_plan, M):
+    pl = lib_plan(M, 4096, 11008)
+    assert pl == plan_config(M, 4096, 11008)
+    assert (pl[0] == "tall") == (256 < M <= 384)
+    if pl[0] == "tall":
+        assert pl[1:] == (False, 256, 0, 80)
+    import torch
+    assert lib_plan(M, 4096, 11008, "ffn", torch.float32)[0] != "tall"   # fp32: no tall tiles
