@@ -406,6 +406,15 @@ cuasm_status_t cuasm_plan_config(int sm_count, int dtype, int64_t M, int64_t K, 
 cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
                               void* out, int64_t M, int64_t K, int64_t N, float eps, int warmup, int iters,
                               int flush_l2, void* stream, int* variant, int* flags, float* best_us);
+/* cuasm_gemm_act_tune: the same search for the GEMM + activation op (cuasm_gemm_act: the paper's
+ * mmLeakyReLu, and the FFN block's down projection): arguments as cuasm_gemm_act plus
+ * warmup / iters / flush_l2 / outputs as above; candidates the cost model's choice and each variant
+ * x {whole tiles, stream-K} x {256, 128}-wide tiles; the winner is used by later cuasm_gemm_act
+ * calls of this M x K x N on the handle (and by block forwards whose down projection has it).  Its
+ * exported lines carry "op=gemm " before "gpu=". */
+cuasm_status_t cuasm_gemm_act_tune(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K,
+                                   int64_t N, int act, float alpha, int warmup, int iters, int flush_l2, void* stream,
+                                   int* variant, int* flags, float* best_us);
 cuasm_status_t cuasm_ffn_tuned_export(cuasm_ffn_t h, char* buf, int64_t cap, int64_t* needed);
 cuasm_status_t cuasm_ffn_tuned_import(cuasm_ffn_t h, const char* text, int* accepted);
 cuasm_status_t cuasm_ffn_tuned_clear(cuasm_ffn_t h);

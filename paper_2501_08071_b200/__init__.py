@@ -44,7 +44,7 @@ EXPORTED_SYMBOLS = (
     "cuasm_ffn_prepare", "cuasm_ffn_rms_inv",
     "cuasm_ffn_get_packed", "cuasm_ffn_invalidate_weights", "cuasm_ffn_set_option", "cuasm_ffn_last_launch",
     "cuasm_ffn_profile_read", "cuasm_ffn_trace_read", "cuasm_plan_config", "cuasm_ffn_destroy", "cuasm_ffn_last_error", "cuasm_ffn_abi_version",
-    "cuasm_ffn_tune", "cuasm_ffn_tuned_export", "cuasm_ffn_tuned_import", "cuasm_ffn_tuned_clear", "cuasm_ffn_tune_log",
+    "cuasm_ffn_tune", "cuasm_gemm_act_tune", "cuasm_ffn_tuned_export", "cuasm_ffn_tuned_import", "cuasm_ffn_tuned_clear", "cuasm_ffn_tune_log",
 )
 
 
@@ -122,6 +122,8 @@ def load_library():
         lib.cuasm_plan_config.argtypes = [ci, ci, i64, i64, i64, ci, ctypes.POINTER(ci), ctypes.POINTER(ci)]
         lib.cuasm_ffn_tune.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, f32, ci, ci, ci, vp, ctypes.POINTER(ci),
                                        ctypes.POINTER(ci), ctypes.POINTER(f32)]
+        lib.cuasm_gemm_act_tune.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, f32, ci, ci, ci, vp, ctypes.POINTER(ci),
+                                            ctypes.POINTER(ci), ctypes.POINTER(f32)]
         lib.cuasm_ffn_tuned_export.argtypes = [vp, ctypes.c_char_p, i64, ctypes.POINTER(i64)]
         lib.cuasm_ffn_tuned_import.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ci)]
         lib.cuasm_ffn_tuned_clear.argtypes = [vp]
@@ -294,6 +296,26 @@ class FusedFFN:
                                             out.data_ptr(), M, K, N, float(eps), int(warmup), int(iters),
                                             1 if flush_l2 else 0, _stream_ptr(x.device), ctypes.byref(v), ctypes.byref(fl),
                                             ctypes.byref(us)))
+        return _plan_tuple(v.value, fl.value), us.value
+
+    def tune_gemm_act(self, x, w, act: str = "identity", alpha: float = 0.0, warmup: int = 100, iters: int = 100,
+                      flush_l2: bool = True, out=None):
+        """The autotuner for the GEMM + activation op (cuasm_gemm_act_tune): x [M,K], w [N,K].
+        Returns (plan tuple as plan_config(..., "gemm")'s, best mean us per call)."""
+        self._validate(x, w)
+        M, K = x.shape
+        N = w.shape[0]
+        if w.shape[1] != K:
+            raise ValueError("shape mismatch")
+        if out is None:
+            out = torch.empty((M, N), dtype=self.dtype, device=x.device)
+        self._weights_changed({1: (w,)})
+        v, fl, us = ctypes.c_int(), ctypes.c_int(), ctypes.c_float()
+        self._check(self.lib.cuasm_gemm_act_tune(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), M, K, N,
+                                                 {"identity": ACT_IDENTITY, "leaky_relu": ACT_LEAKY_RELU}[act],
+                                                 float(alpha), int(warmup), int(iters), 1 if flush_l2 else 0,
+                                                 _stream_ptr(x.device), ctypes.byref(v), ctypes.byref(fl),
+                                                 ctypes.byref(us)))
         return _plan_tuple(v.value, fl.value), us.value
 
     def tuned_export(self) -> str:

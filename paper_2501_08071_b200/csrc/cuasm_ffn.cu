@@ -109,6 +109,7 @@ inline Plan plan_from_flags(int variant, int flags) {
 
 // A measured configuration for one problem shape (cuasm_ffn_tune / cuasm_ffn_tuned_import).
 struct TunedEntry {
+    int op;  // 0 fused FFN, 1 GEMM + activation
     int64_t M, K, N;
     Plan plan;
     float us;
@@ -200,7 +201,8 @@ struct cuasm_ffn_s {
     std::string gpu_name;            // cudaDeviceProp::name: part of a tuned entry's key
     std::vector<TunedEntry> tuned;
     std::vector<std::pair<Plan, float>> tune_log;  // the last cuasm_ffn_tune's candidates and times (-1: skipped)
-    bool plan_forced = false;        // cuasm_ffn_tune: the candidate being measured
+    bool plan_forced = false;        // cuasm_ffn_tune / cuasm_gemm_act_tune: the candidate being measured
+    int plan_force_op = 0;           // (of this op: 0 fused FFN, 1 GEMM + activation)
     Plan plan_force{CUASM_VARIANT_2SM, false, 256, 0, kPackBN};
 };
 
@@ -1012,11 +1014,12 @@ Plan plan_config_raw(int sm_count, int esize, int group_m, int64_t M, int64_t K,
 }
 
 Plan plan_config(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N, int64_t out_cols) {
-    // the fused FFN's measured configurations (cuasm_ffn_tune) take precedence over the model
-    if (out_cols == 128) {
-        if (h->plan_forced) return h->plan_force;
+    // measured configurations (cuasm_ffn_tune, cuasm_gemm_act_tune) take precedence over the model
+    {
+        const int op = out_cols == 128 ? 0 : 1;
+        if (h->plan_forced && h->plan_force_op == op) return h->plan_force;
         for (const TunedEntry& t : h->tuned)
-            if (t.M == M && t.K == K && t.N == N) return t.plan;
+            if (t.op == op && t.M == M && t.K == K && t.N == N) return t.plan;
     }
     Plan pl = plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, out_cols, out_cols == 128 ? 0 : h->tile_n,
                               out_cols == 128 ? h->tile_bn : 0, h->tall);
@@ -1274,18 +1277,16 @@ std::vector<Plan> tune_candidates(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N
 }
 }  // namespace
 
-cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
-                              void* out, int64_t M, int64_t K, int64_t N, float eps, int warmup, int iters,
-                              int flush_l2, void* stream, int* variant, int* flags, float* best_us) {
-    NvtxRange nvtx_("cuasm_ffn_tune");
-    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
-    h->err.clear();
-    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "tuning: bf16 handles only");
-    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
-    if (st != CUASM_OK) return st;
-    if (M == 0) return fail(h, CUASM_ERR_INVALID_ARG, "tuning needs M > 0");
-    if (warmup < 0 || iters < 1 || warmup > 100000 || iters > 100000 || (flush_l2 != 0 && flush_l2 != 1))
-        return fail(h, CUASM_ERR_INVALID_ARG, "warmup must be >= 0, iters >= 1, flush_l2 0 or 1");
+}  // extern "C" (the tuner's shared core follows)
+
+namespace {
+// The search loop of cuasm_ffn_tune / cuasm_gemm_act_tune: every candidate of `cands` for op `op`
+// (0 fused FFN, 1 GEMM + activation) through `fwd` (one forward under the forced plan).
+template <class Fwd>
+cuasm_status_t tune_core(cuasm_ffn_t h, int op, const std::vector<Plan>& cands, Fwd fwd, int64_t M, int64_t K,
+                         int64_t N, int warmup, int iters, int flush_l2, void* stream, int* variant, int* flags,
+                         float* best_us) {
+    cuasm_status_t st;
     DeviceGuard dg(h);
     if ((st = dg.status) != CUASM_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1321,17 +1322,16 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
     // candidates measured in kTuneRounds interleaved rounds (clock / power drift spreads over
     // all of them), a candidate's time = the best of its rounds' means
     constexpr int kTuneRounds = 3;
-    const std::vector<Plan> cands = tune_candidates(h, M, K, N);
     std::vector<float> t_us(cands.size(), std::numeric_limits<float>::infinity());
     std::vector<bool> skip(cands.size(), false);
     for (int rnd = 0; rnd < kTuneRounds; ++rnd) {
         for (size_t ci = 0; ci < cands.size(); ++ci) {
             if (skip[ci]) continue;
             h->plan_forced = true;
+            h->plan_force_op = op;
             h->plan_force = cands[ci];
             st = CUASM_OK;
-            for (int w = 0; w < (warmup > 0 ? warmup : 1) && st == CUASM_OK; ++w)
-                st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+            for (int w = 0; w < (warmup > 0 ? warmup : 1) && st == CUASM_OK; ++w) st = fwd(s);
             cudaError_t ce = cudaSuccess;
             // flush_l2: each timed forward is one CUDA-graph launch (captured after the warm-up, whose
             // first forward did any packing / allocation), as bench.py times a step -- an eager
@@ -1340,7 +1340,7 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
             if (st == CUASM_OK && flush_l2 && s != nullptr) {
                 cudaGraph_t graph = nullptr;
                 if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-                    const cuasm_status_t cst = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                    const cuasm_status_t cst = fwd(s);
                     if (cudaStreamEndCapture(s, &graph) != cudaSuccess || cst != CUASM_OK ||
                         cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
                         gexec = nullptr;
@@ -1354,7 +1354,7 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
                 if (flush_l2 && (ce = flush()) == cudaSuccess) ce = cudaEventRecord(ev[2 * i], s);
                 if (ce == cudaSuccess) {
                     if (gexec) ce = cudaGraphLaunch(gexec, s);
-                    else st = forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s);
+                    else st = fwd(s);
                 }
                 if (flush_l2 && st == CUASM_OK && ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i + 1], s);
             }
@@ -1403,16 +1403,75 @@ cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, c
     if (!(best < std::numeric_limits<float>::infinity())) return fail(h, CUASM_ERR_UNSUPPORTED, "no configuration ran");
     bool found = false;
     for (TunedEntry& t : h->tuned)
-        if (t.M == M && t.K == K && t.N == N) {
+        if (t.op == op && t.M == M && t.K == K && t.N == N) {
             t.plan = best_plan;
             t.us = best;
             found = true;
         }
-    if (!found) h->tuned.push_back(TunedEntry{M, K, N, best_plan, best});
+    if (!found) h->tuned.push_back(TunedEntry{op, M, K, N, best_plan, best});
     if (variant) *variant = best_plan.variant;
     if (flags) *flags = plan_flags(best_plan);
     if (best_us) *best_us = best;
     return CUASM_OK;
+}
+
+// GEMM + activation candidates: the cost model's choice, each variant x {whole tiles, stream-K}
+// x {256, 128}-wide tiles.
+std::vector<Plan> tune_candidates_gemm(cuasm_ffn_t h, int64_t M, int64_t K, int64_t N) {
+    std::vector<Plan> c;
+    auto add = [&](const Plan& p) {
+        for (const Plan& q : c)
+            if (same_plan(q, p)) return;
+        c.push_back(p);
+    };
+    add(plan_config_raw(h->sm_count, h->esize, h->group_m, M, K, N, 256));
+    for (int v : {CUASM_VARIANT_2SM, CUASM_VARIANT_1SM})
+        for (int sk = 0; sk < 2; ++sk)
+            for (int tn : {256, 128}) add(Plan{v, sk == 1, tn, 0, kPackBN});
+    return c;
+}
+}  // namespace
+
+extern "C" {
+
+cuasm_status_t cuasm_ffn_tune(cuasm_ffn_t h, const void* x, const void* rms_w, const void* w1, const void* w3,
+                              void* out, int64_t M, int64_t K, int64_t N, float eps, int warmup, int iters,
+                              int flush_l2, void* stream, int* variant, int* flags, float* best_us) {
+    NvtxRange nvtx_("cuasm_ffn_tune");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "tuning: bf16 handles only");
+    cuasm_status_t st = validate_forward(h, x, rms_w, w1, w3, out, M, K, N, eps);
+    if (st != CUASM_OK) return st;
+    if (M == 0) return fail(h, CUASM_ERR_INVALID_ARG, "tuning needs M > 0");
+    if (warmup < 0 || iters < 1 || warmup > 100000 || iters > 100000 || (flush_l2 != 0 && flush_l2 != 1))
+        return fail(h, CUASM_ERR_INVALID_ARG, "warmup must be >= 0, iters >= 1, flush_l2 0 or 1");
+    return tune_core(h, 0, tune_candidates(h, M, K, N),
+                     [&](cudaStream_t s) { return forward_impl(h, x, rms_w, w1, w3, out, M, K, N, eps, s); }, M, K, N,
+                     warmup, iters, flush_l2, stream, variant, flags, best_us);
+}
+
+cuasm_status_t cuasm_gemm_act_tune(cuasm_ffn_t h, const void* x, const void* w, void* out, int64_t M, int64_t K,
+                                   int64_t N, int act, float alpha, int warmup, int iters, int flush_l2, void* stream,
+                                   int* variant, int* flags, float* best_us) {
+    NvtxRange nvtx_("cuasm_gemm_act_tune");
+    if (!h) return fail(nullptr, CUASM_ERR_INVALID_ARG, "NULL handle");
+    h->err.clear();
+    if (h->dtype != CUASM_DTYPE_BF16) return fail(h, CUASM_ERR_UNSUPPORTED, "tuning: bf16 handles only");
+    cuasm_status_t st;
+    if ((st = check_common(h, K, N)) != CUASM_OK) return st;
+    if (act != CUASM_ACT_IDENTITY && act != CUASM_ACT_LEAKY_RELU)
+        return fail(h, CUASM_ERR_INVALID_ARG, "unknown activation %d", act);
+    if (!(alpha == alpha)) return fail(h, CUASM_ERR_INVALID_ARG, "alpha is NaN");
+    if (!w || !aligned16(w)) return fail(h, CUASM_ERR_INVALID_ARG, "w must be non-NULL and 16-byte aligned");
+    if (M <= 0 || M >= (int64_t(1) << 31)) return fail(h, CUASM_ERR_INVALID_ARG, "tuning needs M in [1, 2^31)");
+    if (!x || !out || !aligned16(x) || !aligned16(out))
+        return fail(h, CUASM_ERR_INVALID_ARG, "x and out must be non-NULL and 16-byte aligned");
+    if (warmup < 0 || iters < 1 || warmup > 100000 || iters > 100000 || (flush_l2 != 0 && flush_l2 != 1))
+        return fail(h, CUASM_ERR_INVALID_ARG, "warmup must be >= 0, iters >= 1, flush_l2 0 or 1");
+    return tune_core(h, 1, tune_candidates_gemm(h, M, K, N),
+                     [&](cudaStream_t s) { return gemm_act_impl(h, x, w, out, M, K, N, act, alpha, s); }, M, K, N,
+                     warmup, iters, flush_l2, stream, variant, flags, best_us);
 }
 
 // "cuasm-tuned v1 sm=<SMs> dtype=bf16 M=<M> K=<K> N=<N> variant=<v> flags=<f> us=<t> gpu=<name>\n"
@@ -1426,10 +1485,10 @@ cuasm_status_t cuasm_ffn_tuned_export(cuasm_ffn_t h, char* buf, int64_t cap, int
     char line[512];
     for (const TunedEntry& t : h->tuned) {
         std::snprintf(line, sizeof(line),
-                      "cuasm-tuned v1 sm=%d dtype=%s M=%lld K=%lld N=%lld variant=%d flags=%d us=%.3f gpu=%s\n",
+                      "cuasm-tuned v1 sm=%d dtype=%s M=%lld K=%lld N=%lld variant=%d flags=%d us=%.3f %sgpu=%s\n",
                       h->sm_count, h->dtype == CUASM_DTYPE_BF16 ? "bf16" : "fp32", static_cast<long long>(t.M),
                       static_cast<long long>(t.K), static_cast<long long>(t.N), t.plan.variant, plan_flags(t.plan),
-                      static_cast<double>(t.us), h->gpu_name.c_str());
+                      static_cast<double>(t.us), t.op == 1 ? "op=gemm " : "", h->gpu_name.c_str());
         text += line;
     }
     *needed = static_cast<int64_t>(text.size()) + 1;
@@ -1453,9 +1512,17 @@ cuasm_status_t cuasm_ffn_tuned_import(cuasm_ffn_t h, const char* text, int* acce
         long long M = 0, K = 0, N = 0;
         char dt[16] = {0};
         float us = 0.f;
-        if (std::sscanf(line.c_str(), "cuasm-tuned v1 sm=%d dtype=%15s M=%lld K=%lld N=%lld variant=%d flags=%d us=%f gpu=%n",
+        if (std::sscanf(line.c_str(), "cuasm-tuned v1 sm=%d dtype=%15s M=%lld K=%lld N=%lld variant=%d flags=%d us=%f %n",
                         &sm, dt, &M, &K, &N, &v, &fl, &us, &pos) != 8 || pos < 0)
             continue;  // not an entry (comments, other versions)
+        // optional "op=gemm " (a GEMM + activation entry, cuasm_gemm_act_tune), then "gpu=<name>"
+        int op = 0;
+        if (line.compare(static_cast<size_t>(pos), 8, "op=gemm ") == 0) {
+            op = 1;
+            pos += 8;
+        }
+        if (line.compare(static_cast<size_t>(pos), 4, "gpu=") != 0) continue;
+        pos += 4;
         std::string gpu = line.substr(static_cast<size_t>(pos));
         while (!gpu.empty() && (gpu.back() == '\r' || gpu.back() == ' ')) gpu.pop_back();
         // another GPU type / SM count / dtype: not this device's entry
@@ -1465,18 +1532,19 @@ cuasm_status_t cuasm_ffn_tuned_import(cuasm_ffn_t h, const char* text, int* acce
         bool bn_ok = false;
         for (int bn : kTileBNs) bn_ok |= pl.bn == bn;
         if (M <= 0 || K <= 0 || N <= 0 || (v != CUASM_VARIANT_1SM && v != CUASM_VARIANT_2SM) || !bn_ok ||
-            pl.tile_n != 256 || (pl.csplit != 0 && (pl.csplit < 2 || pl.csplit > 8 || v != CUASM_VARIANT_1SM)) ||
+            (pl.csplit != 0 && (pl.csplit < 2 || pl.csplit > 8 || v != CUASM_VARIANT_1SM)) ||
             (pl.tall && (v != CUASM_VARIANT_2SM || pl.bn != kTallBN || M <= 256 || M > kTallMaxM)) ||
-            (v == CUASM_VARIANT_1SM && pl.bn != kPackBN && pl.bn != 64 && pl.bn != 120) || (fl & ~0xFFF7) != 0)
+            (v == CUASM_VARIANT_1SM && pl.bn != kPackBN && pl.bn != 64 && pl.bn != 120) || (fl & ~0xFFF7) != 0 ||
+            (op == 1 && (pl.bn != kPackBN || pl.tall || pl.csplit != 0)) || (op == 0 && pl.tile_n != 256))
             return fail(h, CUASM_ERR_INVALID_ARG, "malformed tuned entry: %s", line.c_str());
         bool found = false;
         for (TunedEntry& t : h->tuned)
-            if (t.M == M && t.K == K && t.N == N) {
+            if (t.op == op && t.M == M && t.K == K && t.N == N) {
                 t.plan = pl;
                 t.us = us;
                 found = true;
             }
-        if (!found) h->tuned.push_back(TunedEntry{M, K, N, pl, us});
+        if (!found) h->tuned.push_back(TunedEntry{op, M, K, N, pl, us});
         ++*accepted;
     }
     return CUASM_OK;

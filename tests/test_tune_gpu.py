@@ -87,3 +87,28 @@ def test_tune_refuses_fp32_and_bad_arguments(cuda_device):
     h = ffn.FusedFFN(cuda_device, torch.bfloat16)
     with pytest.raises(ffn.CuasmError):
         h.tune(t["x"], t["g"], t["w1"], t["w3"], 1e-6, warmup=1, iters=0)
+
+
+@pytest.mark.parametrize("M,K,N", [(512, 2048, 512), (1024, 4096, 1024)])
+def test_gemm_act_tune_then_lookup(cuda_device, M, K, N):
+    """The GEMM + activation op's search (the paper's mmLeakyReLu): the winner is used
+    by later calls, matches the oracle, and travels in the table as an "op=gemm" line that a
+    fresh handle imports (bitwise equal output); the fused FFN's entries stay separate."""
+    d = make_inputs(M, K, N, family="C", seed=9850 + M, dtype="bf16")
+    x, w = d["x"].to(cuda_device), d["w1"].to(cuda_device)
+    h = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    plan, us = h.tune_gemm_act(x, w, "leaky_relu", 0.01, warmup=2, iters=3)
+    assert us > 0 and plan[0] in ("1sm", "2sm") and plan[2] in (128, 256)
+    out = h.gemm_act(x, w, "leaky_relu", 0.01)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_act(d["x"], d["w1"], "leaky_relu", 0.01)
+    check(out, ref, f"tuned gemm {plan}")
+    text = h.tuned_export()
+    assert f" M={M} K={K} N={N} " in text and " op=gemm gpu=" in text
+    h2 = ffn.FusedFFN(cuda_device, torch.bfloat16)
+    assert h2.tuned_import(text) == 1
+    out2 = h2.gemm_act(x, w, "leaky_relu", 0.01)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    # the same shape as a fused FFN is not affected by the GEMM entry
+    assert ffn.plan_config(M, K, N) is not None
