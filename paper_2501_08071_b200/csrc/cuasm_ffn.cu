@@ -1315,8 +1315,9 @@ cuasm_status_t tune_core(cuasm_ffn_t h, int op, const std::vector<Plan>& cands, 
         }
     auto flush = [&]() {
         if (!fbuf) return cudaSuccess;
-        cuasm::l2_flush_kernel<<<2 * h->sm_count, 512, 0, s>>>(
-            static_cast<uint4*>(fbuf), reinterpret_cast<uint4*>(static_cast<char*>(fbuf) + fbytes), fbytes / 16);
+        for (int wr = 1; wr >= 0; --wr)
+            cuasm::l2_flush_kernel<<<2 * h->sm_count, 512, 0, s>>>(
+                static_cast<uint4*>(fbuf), reinterpret_cast<uint4*>(static_cast<char*>(fbuf) + fbytes), fbytes / 16, wr);
         return cudaGetLastError();
     };
     // candidates measured in kTuneRounds interleaved rounds (clock / power drift spreads over

@@ -147,10 +147,16 @@ __global__ void __launch_bounds__(256) ffn_rmsnorm_kernel(const T* __restrict__ 
 // kernel, not cudaMemsetAsync, whose large fills measured no eviction), then read n16 words of
 // `r` so the written lines are cleaned before the timed forward.  The data-dependent store keeps
 // the loads alive (it fires only if the words XOR to the constant; `r` is scratch either way).
-__global__ void __launch_bounds__(512) l2_flush_kernel(uint4* __restrict__ w, uint4* __restrict__ r, int64_t n16) {
+// (two launches, as bench.py's flush -- a fill kernel, then a reduction over another buffer -- so the
+// timed forward follows the same kind of predecessor: `write` selects the phase)
+__global__ void __launch_bounds__(512) l2_flush_kernel(uint4* __restrict__ w, uint4* __restrict__ r, int64_t n16,
+                                                        int write) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    for (int64_t i = i0; i < n16; i += stride) w[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (write) {
+        for (int64_t i = i0; i < n16; i += stride) w[i] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
     uint32_t acc = 0;
     for (int64_t i = i0; i < n16; i += stride) {
         const uint4 v = r[i];
