@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--op", default="ffn", choices=["ffn", "gemm"], help="gemm: the GEMM + LeakyReLU op")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rows = []
@@ -31,9 +32,13 @@ def main():
         for M in (int(m) for m in a.ms.split(",")):
             t = make_device_inputs(M, K, N, 3, dev)
             h = ffn.FusedFFN(dev)
-            plan, us = h.tune(t["x"], t["g"], t["w1"], t["w3"], 1e-6, warmup=a.warmup, iters=a.iters, flush_l2=True)
+            if a.op == "ffn":
+                plan, us = h.tune(t["x"], t["g"], t["w1"], t["w3"], 1e-6, warmup=a.warmup, iters=a.iters, flush_l2=True)
+            else:
+                plan, us = h.tune_gemm_act(t["x"], t["w1"], "leaky_relu", 0.01, warmup=a.warmup, iters=a.iters,
+                                           flush_l2=True)
             log = {str(list(p)): u for p, u in h.tune_log()}
-            model = list(ffn.plan_config(M, K, N))
+            model = list(ffn.plan_config(M, K, N, a.op))
             row = {"M": M, "K": K, "N": N, "model": model, "model_us": log.get(str(model)), "best": list(plan),
                    "best_us": round(us, 2), "all": {k: (round(v, 2) if v is not None else None) for k, v in log.items()}}
             rows.append(row)
